@@ -1,0 +1,335 @@
+#!/usr/bin/env python3
+"""Benchmark: decode tokens/s of the Llama-2-7B-shaped integer model (BASELINE.json
+configs[1]: 7B-shaped random-init int8 weights, seed 7; ChaCha20 prompt seed 8,
+16 tokens; batch-1 greedy decode) on N B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one greedy decode token: one full forward of the 32-layer model
+(6.62 GB of int8 weights + scales streamed from HBM) plus the on-device
+argmax that appends the next token. With N > 1 (torchrun, one process per
+GPU) every rank decodes its own independent sequence (weak scaling, no
+data-path collective; C5's sequence sharding): value = all ranks' tokens /
+max-over-ranks time.
+
+Keys beyond the base contract:
+  e2e           the same metric through the reference-shaped C-ABI call
+                dimg_generate_greedy with HOST buffers (prompt H2D, tokens D2H
+                and the BLAKE3 hash inside the timed region)
+  roofline      dominant kernel (gate/up GEMV): algorithmic bytes per launch /
+                CUDA-event launch time, vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the reference engine (oracle/_ref, compiled from its own
+                sources) timed on this host, rank 0, N=1
+--impl reference times that reference engine alone on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG7B = (32, 4096, 32, 11008, 32000, 4096)
+MODEL_SEED = 7
+PROMPT_SEED = 8
+PROMPT_LEN = 16
+WEIGHT_HASH_7B = "8df01f77395ece3685b121f642da4442bda0862a3e76cc9823577ffc5880dd64"
+METRIC = "decode tokens/s (Llama-2-7B int) at 1/2/4/8 B200; 0 hash mismatches vs CPU"
+
+
+def bytes_per_token(L, D, F, V):
+    """Algorithmic HBM bytes of one decode forward: int8
+    weights incl. lm_head + int64 row scales + int64 norm gains + one
+    embedding row (int8 row + its int64 scale). KV traffic excluded."""
+    w = L * (4 * D * D + 3 * D * F) + V * D
+    s = L * (4 * D + 2 * F + D) + V
+    g = (2 * L + 1) * D
+    return w + 8 * s + 8 * g + D + 8
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        mx = max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------
+def reference_model(ref, cfg):
+    """The reference's own gen_toy_model (proj/src/model.cpp:189-215)."""
+    return ref.gen_toy(MODEL_SEED, cfg)
+
+
+def time_reference(ref, m, n_warm, n_timed, prompt, threads):
+    """Greedy decode through dim::InferenceSession::forward (+select_greedy),
+    the reference's stock path. Returns seconds per decode forward."""
+    import ctypes as C
+
+    import numpy as np
+    h = C.c_void_p()
+    assert ref.lib.ref_session_new(m.h, threads, C.byref(h)) == 0
+    nxt = C.c_uint32()
+    pos = 0
+    for t in prompt:  # prefill sample (untimed)
+        assert ref.lib.ref_session_forward(h, int(t), pos, None, C.byref(nxt)) == 0
+        pos += 1
+    for _ in range(n_warm):
+        assert ref.lib.ref_session_forward(h, nxt.value, pos, None, C.byref(nxt)) == 0
+        pos += 1
+    t0 = time.perf_counter()
+    for _ in range(n_timed):
+        assert ref.lib.ref_session_forward(h, nxt.value, pos, None, C.byref(nxt)) == 0
+        pos += 1
+    dt = time.perf_counter() - t0
+    ref.lib.ref_session_free(h)
+    del np
+    return dt / max(1, n_timed)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle.pyoracle import Config, Reference
+    cfg = Config(*CFG7B)
+    threads = os.cpu_count() or 1
+    if not Reference.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdimref.so not built"}))
+        return 0
+    ref = Reference()
+    t0 = time.time()
+    m = reference_model(ref, cfg)
+    gen_s = time.time() - t0
+    prompt = ref.prompt(PROMPT_SEED, cfg.vocab, PROMPT_LEN)[:4]
+    spf = time_reference(ref, m, args.warmup, args.steps, prompt, threads)
+    value = 1.0 / spf
+    sample = (f"dim::InferenceSession::forward + select_greedy, {args.steps} timed decode "
+              f"forwards after a 4-token prompt and {args.warmup} warm-up forwards "
+              f"(threads={threads}: the reference's dense matvec is single-threaded)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": spf * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference gen_toy_model seed 7)",
+        "config": {"workload": "C2: Llama-2-7B-shaped int8/Q16 model, batch-1 greedy decode",
+                   "model": "llama2-7b-shaped-int", "seed": MODEL_SEED, "prompt_seed": PROMPT_SEED},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                         "sample": sample, "threads_setting": threads, "model_gen_s": round(gen_s, 1)},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+def cpu_baseline(model_file, cfg_t):
+    """Reference engine on this host over the SAME weights (bounded sample)."""
+    try:
+        from oracle.pyoracle import Config, Reference
+        if not Reference.available():
+            raise FileNotFoundError("oracle/_ref not built")
+        ref = Reference()
+        cfg = Config(*cfg_t)
+        import numpy as np
+        names = ["tok_embd"] + [f"layers.{l}.{t}" for l in range(cfg.n_layers)
+                                for t in ("wq", "wk", "wv", "wo", "w_gate", "w_up", "w_down")] + ["output"]
+        w = np.concatenate([model_file.tensor(n)[0].reshape(-1) for n in names])
+        s = np.concatenate([model_file.tensor(n)[1] for n in names])
+        m = ref.model_from_arrays(cfg, w, s, model_file.norms())
+        del w, s
+        prompt = ref.prompt(PROMPT_SEED, cfg.vocab, PROMPT_LEN)[:2]
+        spf = time_reference(ref, m, 0, 3, prompt, 1)
+        return {"value": 1.0 / spf, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                "sample": "3 decode forwards (dim::InferenceSession::forward + select_greedy) after a "
+                          "2-token prompt, same weights, threads=1"}
+    except Exception as e:  # reported, never fatal for the GPU number
+        return {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                "sample": f"unavailable: {e}"}
+
+
+def run_ours(args, rank, world, local):
+    import numpy as np
+
+    import paper_2603_24904_b200 as P
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    cfg = P.ModelConfig(*CFG7B)
+    t0 = time.time()
+    mf = P.gen_toy_model(MODEL_SEED, cfg)
+    gen_s = time.time() - t0
+    wh_ok = None
+    if rank == 0:
+        wh_ok = mf.weight_hash == WEIGHT_HASH_7B
+    # rank r decodes its own sequence: C5's prompt seeds (8, then 1000+r)
+    pseed = PROMPT_SEED if rank == 0 else 1000 + rank
+    prompt = P.prompt_from_seed(pseed, cfg.vocab, PROMPT_LEN)
+    sess = P.InferenceSession(mf, P.EngineOptions(device=dev))
+    n_total = args.warmup + args.steps
+    sess.begin(prompt, n_total)
+    sess.prefill()
+    sess.decode(args.warmup)
+    sess.sync()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    barrier()
+    with ClockSampler(dev) as clk:
+        ms = sess.time_decode(args.steps)  # CUDA events on the session stream, synced both sides
+    barrier()
+    ms_max = ms
+    if dist is not None:
+        import torch
+        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    toks = sess.tokens(n_total)
+    per_step_ms = ms_max / args.steps
+    value = world * args.steps / (ms_max / 1e3)
+    launches_per_step, _ = sess.launches()
+
+    # dominant kernel roofline (gate/up GEMV, ~45% of the weight bytes)
+    kern = {}
+    for which, name in enumerate(sess.KERNELS):
+        kms, kb = sess.time_kernel(which, 64 if which != 4 else 16)
+        kern[name] = {"ms": kms, "bytes": kb, "gbs": kb / (kms * 1e-3) / 1e9}
+    peak, peak_kind = peaks()
+    dom = kern["gate_up_gemv"]
+    step_bytes = bytes_per_token(cfg.n_layers, cfg.d_model, cfg.d_ffn, cfg.vocab)
+    step_gbs = step_bytes / (per_step_ms * 1e-3) / 1e9
+
+    # e2e: the reference-shaped call with host buffers (C2: P=16, N=128)
+    e2e = None
+    if rank == 0 or world > 1:
+        n_new = 128
+        sess.generate_greedy(prompt, n_new)  # warm
+        reps = 3
+        t1 = time.perf_counter()
+        for _ in range(reps):
+            res = sess.generate_greedy(prompt, n_new)
+        e2e_s = (time.perf_counter() - t1) / reps
+        e2e = {"value": n_new / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": 4 * PROMPT_LEN,
+               "d2h_bytes_per_step": 4 * n_new,
+               "call": "dimg_generate_greedy(prompt 16 -> 128 tokens, BLAKE3 on host)",
+               "output_hash": res.output_hash.hex()}
+    if dist is not None:
+        import torch
+        t = torch.tensor([e2e["value"] if e2e else 0.0], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if e2e:
+            e2e["value"] = float(t.item()) * world
+    base = cpu_baseline(mf, CFG7B) if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (gen_toy_model seed 7: uniform int8 weights, Q16 scales; ChaCha20 prompt)",
+            "config": {"workload": "C2: Llama-2-7B-shaped int8/Q16 model, batch-1 greedy decode",
+                       "model": "llama2-7b-shaped-int", "layers": cfg.n_layers,
+                       "d_model": cfg.d_model, "d_ffn": cfg.d_ffn, "vocab": cfg.vocab,
+                       "seed": MODEL_SEED, "prompt_seed": PROMPT_SEED, "prompt_len": PROMPT_LEN,
+                       "global_batch": world, "parallelism": f"dp{world} (independent sequences)",
+                       "l2": "weights 6.6 GB/step > 126 MB L2 (no flush needed)",
+                       "weight_hash_ok": wh_ok, "model_gen_s": round(gen_s, 1)},
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
+                         "frac": dom["gbs"] / peak, "traffic": None, "kernel": "gate_up_gemv",
+                         "bytes_per_launch": dom["bytes"], "ms_per_launch": dom["ms"],
+                         "peak_kind": peak_kind},
+            "step_roofline": {"bytes_per_token": step_bytes, "achieved_gbs": step_gbs,
+                              "frac": step_gbs / peak},
+            "kernels": kern,
+            "clocks": clk.summary(),
+            "cpu_baseline": base,
+            "tokens_head": toks[:8],
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank, world, local = env_rank()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

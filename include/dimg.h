@@ -1,0 +1,205 @@
+/*
+ * dimg.h -- C ABI of the B200-native integer transformer engine.
+ *
+ * The reference (`dim`, /root/reference/proj) is a C++20 library whose hot
+ * path is InferenceSession::forward / generate_greedy
+ * (proj/include/dim/engine.hpp:41-80). It has no FFI; this header is the
+ * drop-in boundary a binding (ctypes, cgo, JNI, or the C++ wrapper in
+ * paper_2603_24904_b200/csrc/include/dimg/dim.hpp) links against. Plain
+ * pointers and sizes only; nothing throws across it. Every function returns a
+ * dimg_status; dimg_last_error() gives the thread-local message.
+ *
+ * Status codes map one-to-one onto the reference's exception types
+ * (SURVEY.md §8b "Errors"):
+ *   DIMG_EINVAL  std::invalid_argument  (empty prompt engine.cpp:22, bad config model.cpp:95-109)
+ *   DIMG_ERANGE  std::out_of_range      (token >= vocab engine.cpp:27,81)
+ *   DIMG_ELOGIC  std::logic_error       (pos != cache length engine.cpp:83)
+ *   DIMG_ECTX    dim::ContextOverflow   (engine.cpp:24,82)
+ *   DIMG_ELENGTH std::length_error      (attention cache overflow kernels.cpp:126)
+ *   DIMG_EDOMAIN std::domain_error      (inv_sqrt of a non-positive value q16.cpp:57)
+ *   DIMG_EPARSE  dim::ParseError        (kind via dimg_last_parse_kind, serial.hpp:10-15)
+ */
+#ifndef DIMG_H
+#define DIMG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DIMG_OK = 0,
+    DIMG_EINVAL = 1,
+    DIMG_ERANGE = 2,
+    DIMG_ELOGIC = 3,
+    DIMG_ECTX = 4,
+    DIMG_ELENGTH = 5,
+    DIMG_EDOMAIN = 6,
+    DIMG_EPARSE = 7,
+    DIMG_ECUDA = 8,
+    DIMG_ENCCL = 9,
+    DIMG_ENOMEM = 10,
+    DIMG_EIO = 11,
+} dimg_status;
+
+/* ParseError::Kind (proj/include/dim/serial.hpp:11) */
+typedef enum { DIMG_PARSE_BAD_MAGIC = 0, DIMG_PARSE_BAD_VERSION = 1, DIMG_PARSE_TRUNCATED = 2,
+               DIMG_PARSE_INVARIANT = 3 } dimg_parse_kind;
+
+const char* dimg_last_error(void);
+int dimg_last_parse_kind(void);
+const char* dimg_version(void);
+
+/* ModelConfig (proj/include/dim/model.hpp:15-29). */
+typedef struct {
+    uint32_t n_layers, d_model, n_heads, d_ffn, vocab, max_ctx;
+    double rope_theta;
+} dimg_config;
+
+/* ModelConfig::validate (proj/src/model.cpp:95-109). */
+dimg_status dimg_config_validate(const dimg_config* cfg);
+
+/* QuantTensor (proj/include/dim/model.hpp:33-41): host pointers, borrowed. */
+typedef struct {
+    uint32_t rows, cols;
+    const int8_t* data;    /* rows*cols row-major, values in [-127,127] */
+    const int64_t* scales; /* rows, Q16 raw, > 0 */
+} dimg_qtensor;
+
+/* A model as plain host buffers, in the reference's directory order
+ * (proj/src/model.cpp:41-61). layers: 7 per layer (wq wk wv wo w_gate w_up
+ * w_down). norms: (2L+1)*d_model (attn_norm[l], ffn_norm[l], ..., final_norm).
+ * rope_cos/rope_sin: optional imported RTAB tables [max_ctx][d_head/2]
+ * (InferenceSession's imported_tables, engine.hpp:43-44); NULL = build them
+ * (proj/src/rope.cpp:17-39). */
+typedef struct {
+    dimg_config cfg;
+    dimg_qtensor tok_embd;
+    dimg_qtensor output;
+    const dimg_qtensor* layers;
+    const int64_t* norms;
+    const int64_t* rope_cos;
+    const int64_t* rope_sin;
+    uint32_t rope_max_ctx; /* rows of the imported tables (>= cfg.max_ctx) */
+} dimg_model_desc;
+
+/* ------------------------------------------------------------------------ */
+/* Host side: hashes, RNG, container (the reference's L0/L1, kept on host)   */
+/* ------------------------------------------------------------------------ */
+
+/* BLAKE3 (proj/src/blake3.cpp); multi-threaded over 1 MiB subtrees when large. */
+dimg_status dimg_blake3(const void* data, size_t len, uint8_t out[32]);
+/* hash_token_ids: BLAKE3 over u32-LE ids (proj/src/engine.cpp:104-111). */
+dimg_status dimg_hash_token_ids(const uint32_t* ids, size_t n, uint8_t out[32]);
+/* select_greedy: argmax, lowest index on ties (proj/src/engine.cpp:113-120). */
+dimg_status dimg_select_greedy(const int64_t* logits, size_t n, uint32_t* out);
+/* prompt[i] = ChaCha20Rng(seed).next_u32() % vocab (acceptance.cpp:80-82). */
+dimg_status dimg_prompt_from_seed(uint64_t seed, uint32_t vocab, uint32_t n, uint32_t* out);
+/* parse_prompt (proj/tools/dim_cli.cpp:56-70): bytes != NULL maps each byte
+ * to an id; else comma-separated ids. Writes up to cap ids, *n = count. */
+dimg_status dimg_parse_prompt(const char* csv, const char* bytes, uint32_t* out, size_t cap,
+                              size_t* n);
+/* RoPE tables [max_ctx][d_head/2] in Q16 (proj/src/rope.cpp:17-39). */
+dimg_status dimg_rope_tables(double theta, uint32_t d_head, uint32_t max_ctx, int64_t* cos_out,
+                             int64_t* sin_out);
+/* The 257-entry exp LUT (q16.cpp:70-79) and 64 Q48 inv-sqrt seeds (:28-43). */
+dimg_status dimg_exp_lut(int64_t out[257]);
+dimg_status dimg_invsqrt_seeds(int64_t out[64]);
+
+/* Host model container: the canonical DIM1 bytes (ModelFile::bytes) plus
+ * views into them (proj/include/dim/model.hpp:50-60). */
+typedef struct dimg_host_model dimg_host_model;
+/* gen_toy_model (proj/src/model.cpp:189-215); threads <= 0 = all cores. */
+dimg_status dimg_host_model_gen_toy(uint64_t seed, const dimg_config* cfg, int threads,
+                                    dimg_host_model** out);
+/* deserialize (proj/src/model.cpp:251-312) / load_model (:332-334). */
+dimg_status dimg_host_model_from_bytes(const uint8_t* bytes, size_t n, dimg_host_model** out);
+dimg_status dimg_host_model_load(const char* path, dimg_host_model** out);
+dimg_status dimg_host_model_save(const dimg_host_model* m, const char* path);
+/* Builds a container from plain buffers (serialize, model.cpp:217-249). */
+dimg_status dimg_host_model_from_desc(const dimg_model_desc* d, dimg_host_model** out);
+dimg_status dimg_host_model_bytes(const dimg_host_model* m, const uint8_t** bytes, size_t* n);
+dimg_status dimg_host_model_weight_hash(const dimg_host_model* m, uint8_t out[32]);
+dimg_status dimg_host_model_desc(const dimg_host_model* m, dimg_model_desc* out);
+dimg_status dimg_host_model_free(dimg_host_model* m);
+
+/* ------------------------------------------------------------------------ */
+/* Device side (sm_100a)                                                     */
+/* ------------------------------------------------------------------------ */
+
+dimg_status dimg_device_count(int* n);
+
+/* Uploads a model to one GPU, re-laid out for the decode GEMVs (rows padded
+ * to 16 B, gate/up interleaved, q/k/v fused). tp_rank/tp_size shard it
+ * Megatron-style; pass 0/1 for a whole model. */
+typedef struct dimg_model dimg_model;
+dimg_status dimg_model_upload(int device, const dimg_model_desc* desc, int tp_rank, int tp_size,
+                              dimg_model** out);
+dimg_status dimg_model_free(dimg_model* m);
+dimg_status dimg_model_bytes_on_device(const dimg_model* m, uint64_t* bytes);
+
+/* InferenceSession (engine.hpp:41-57): owns one sequence's KV cache on the
+ * device; single writer. keep_logits_cap = how many logits vectors a
+ * generate call may keep (EngineOptions::keep_logits). */
+typedef struct dimg_session dimg_session;
+dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_session** out);
+dimg_status dimg_session_free(dimg_session* s);
+dimg_status dimg_session_reset(dimg_session* s);
+dimg_status dimg_session_len(const dimg_session* s, uint32_t* len);
+/* forward(token, pos) -> logits (engine.cpp:80-102); logits may be NULL. */
+dimg_status dimg_session_forward(dimg_session* s, uint32_t token, uint32_t pos, int64_t* logits);
+/* generate_greedy (engine.cpp:31-54,142-147) on a reset session: prompt and
+ * results in HOST memory. tokens_out: max_new ids; hash_out: BLAKE3 of them;
+ * logits_out: NULL or max_new*vocab (the logits used for each selection). */
+dimg_status dimg_generate_greedy(dimg_session* s, const uint32_t* prompt, uint32_t n_prompt,
+                                 uint32_t max_new, uint32_t* tokens_out, uint8_t hash_out[32],
+                                 int64_t* logits_out);
+
+/* Device-resident stepping (bench / advanced callers). The prompt is staged
+ * with dimg_session_begin; each decode step forwards the newest token and
+ * appends its greedy successor on the device. Nothing is copied to the host
+ * until dimg_session_tokens. */
+dimg_status dimg_session_begin(dimg_session* s, const uint32_t* prompt, uint32_t n_prompt,
+                               uint32_t max_new);
+dimg_status dimg_session_prefill(dimg_session* s);          /* all but the last prompt token */
+dimg_status dimg_session_decode(dimg_session* s, uint32_t n_steps);
+dimg_status dimg_session_sync(dimg_session* s);
+dimg_status dimg_session_tokens(dimg_session* s, uint32_t* out, uint32_t n_generated);
+/* cudaStream_t the session launches on (for CUDA-event timing by callers). */
+dimg_status dimg_session_stream(dimg_session* s, void** stream);
+/* Times n decode steps with CUDA events on the session stream. */
+dimg_status dimg_session_time_decode(dimg_session* s, uint32_t n_steps, float* ms);
+/* Replays one kernel class n times between CUDA events on the session
+ * stream (layers cycled so weights stream from HBM): which = 0 QKV GEMV,
+ * 1 WO, 2 GATE/UP, 3 DOWN, 4 LM_HEAD. Returns the mean launch time and the
+ * algorithmic bytes of one launch (roofline numerator). */
+dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, float* ms_per_launch,
+                                     uint64_t* bytes_per_launch);
+/* Kernel launches per decode step / per prefill step (for the bench claim). */
+dimg_status dimg_session_launches(const dimg_session* s, uint32_t* per_decode,
+                                  uint32_t* per_prefill);
+
+/* Counters: [0] GEMV CTAs that needed the 8-limb (full int64) path,
+ * [1] device-side domain errors (inv_sqrt of ms+1 <= 0). */
+dimg_status dimg_session_stats(dimg_session* s, uint64_t out[4]);
+
+/* ---- operator-level exports (host buffers in/out) for unit parity with
+ *      proj/src/kernels.cpp; they run the engine's own device kernels. ---- */
+dimg_status dimg_op_dense(int device, const dimg_qtensor* w, const int64_t* x, int64_t* out);
+dimg_status dimg_op_rmsnorm(int device, const int64_t* x, const int64_t* g, uint32_t n,
+                            int64_t* out);
+dimg_status dimg_op_softmax(int device, const int64_t* s, uint32_t n, int64_t* out);
+/* T consecutive attention_step calls at pos 0..T-1 on a fresh cache;
+ * q/k/v/out are [T][n_heads*d_head]. */
+dimg_status dimg_op_attention(int device, uint32_t n_heads, uint32_t d_head, uint32_t max_ctx,
+                              double theta, uint32_t steps, const int64_t* q, const int64_t* k,
+                              const int64_t* v, int64_t* out);
+dimg_status dimg_op_ffn(int device, const dimg_qtensor* gate, const dimg_qtensor* up,
+                        const dimg_qtensor* down, const int64_t* x, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,134 @@
+// Decode attention step (proj/src/kernels.cpp:117-177), one CTA per head:
+//
+//   q', k' = RoPE(q_h, k_h, pos)            rope_apply_inplace (:70-82)
+//   K[pos], V[pos] = k', v_h                KV append (:139-142)
+//   s_t = mul16((sum_j q'_j K[t]_j)_int128 >> 16, inv_sqrt(dh))   (:143-151)
+//   p = softmax_q16(s)                      exact LUT softmax (:90-107)
+//   out_j = sum_t mul16(p_t, V[t]_j)        per-product floor (:153-159)
+//
+// The score dot is int128 (warp per position, lanes over dh); the softmax
+// needs the exact max before any exp (no online form), so it is three block
+// passes over an L2-resident score strip; PV uses the exact 64-bit split of
+// mul16 for probabilities (q16.cuh mul16_prob). Every sum is an integer sum,
+// so the parallel order cannot move a bit.
+// KV layout: [layer][head][max_ctx][dh] int64 (the reference's LayerKv strips).
+#pragma once
+
+#include <cstdint>
+
+#include "gemv.cuh"
+#include "q16.cuh"
+
+namespace dimg::dev {
+
+constexpr int ATTN_THREADS = 256;
+
+struct AttnArgs {
+    const int64_t* qkv;       // [3*D]: q | k | v (this step's projections)
+    int64_t* kc;              // this layer: [H][max_ctx][dh]
+    int64_t* vc;
+    const int64_t* rope_cos;  // [max_ctx][dh/2]
+    const int64_t* rope_sin;
+    int64_t* scores;          // [H][max_ctx] scratch
+    int64_t* out;             // [D]
+    const Ctl* ctl;
+    uint32_t H, dh, max_ctx;
+    int64_t inv_scale;        // inv_sqrt_q16(dh * ONE)
+    const int64_t* exp_lut;
+};
+
+__device__ __forceinline__ void rope_pair(int64_t a, int64_t b, int64_t c, int64_t s, int64_t& x0,
+                                          int64_t& x1) {
+    x0 = wrap_sub(mul16(a, c), mul16(b, s));
+    x1 = wrap_add(mul16(a, s), mul16(b, c));
+}
+
+// softmax_q16 in place over S[0..n) (proj/src/kernels.cpp:90-107): exact max,
+// LUT weights lut(min(m - s, 8)), then p = (w << 16) / sum w (truncating).
+// Block-wide; ends with a barrier.
+__device__ void softmax_strip(int64_t* S, uint32_t n, const int64_t* lut, u128* red) {
+    int64_t m = INT64_MIN;
+    for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) m = S[t] > m ? S[t] : m;
+    m = block_reduce<int64_t>(m, reinterpret_cast<int64_t*>(red),
+                              [](int64_t x, int64_t y) { return x > y ? x : y; }, warp_max_i64);
+    uint64_t total = 0;
+    for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+        int64_t d = wrap_sub(m, S[t]);
+        total += uint64_t(exp_neg(d > 8 * ONE ? 8 * ONE : d, lut));
+    }
+    total = block_reduce<uint64_t>(total, reinterpret_cast<uint64_t*>(red),
+                                   [](uint64_t x, uint64_t y) { return x + y; }, warp_sum_u64);
+    for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+        int64_t d = wrap_sub(m, S[t]);
+        int64_t w = exp_neg(d > 8 * ONE ? 8 * ONE : d, lut);
+        S[t] = (w << 16) / int64_t(total);
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(AttnArgs a) {
+    extern __shared__ __align__(16) int64_t qrot[];  // [dh]
+    __shared__ int64_t lut[257];
+    __shared__ u128 red[32];
+    const uint32_t h = blockIdx.x, dh = a.dh, half = dh / 2, D = a.H * dh;
+    const uint32_t pos = a.ctl->pos;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = ATTN_THREADS / 32;
+    for (int i = threadIdx.x; i < 257; i += ATTN_THREADS) lut[i] = a.exp_lut[i];
+
+    const int64_t* q = a.qkv + size_t(h) * dh;
+    const int64_t* k = a.qkv + D + size_t(h) * dh;
+    const int64_t* v = a.qkv + 2 * size_t(D) + size_t(h) * dh;
+    int64_t* K = a.kc + size_t(h) * a.max_ctx * dh;
+    int64_t* V = a.vc + size_t(h) * a.max_ctx * dh;
+    const int64_t* cr = a.rope_cos + size_t(pos) * half;
+    const int64_t* sr = a.rope_sin + size_t(pos) * half;
+    for (uint32_t i = threadIdx.x; i < half; i += ATTN_THREADS) {
+        int64_t c = cr[i], s = sr[i];
+        rope_pair(q[i], q[i + half], c, s, qrot[i], qrot[i + half]);
+        int64_t k0, k1;
+        rope_pair(k[i], k[i + half], c, s, k0, k1);
+        K[size_t(pos) * dh + i] = k0;
+        K[size_t(pos) * dh + i + half] = k1;
+    }
+    for (uint32_t j = threadIdx.x; j < dh; j += ATTN_THREADS) V[size_t(pos) * dh + j] = v[j];
+    __syncthreads();
+
+    // scores: one warp per cached position, int128 dot
+    int64_t* S = a.scores + size_t(h) * a.max_ctx;
+    for (uint32_t t = warp; t <= pos; t += nw) {
+        const int64_t* kt = K + size_t(t) * dh;
+        u128 dot = 0;
+        for (uint32_t j = lane; j < dh; j += 32) dot += u128(i128(qrot[j]) * i128(kt[j]));
+        dot = warp_sum_u128(dot);
+        if (lane == 0) S[t] = mul16(int64_t(i128(dot) >> 16), a.inv_scale);
+    }
+    __syncthreads();
+
+    softmax_strip(S, pos + 1, lut, red);
+
+    // out_j = sum_t mul16(p_t, V[t]_j); threads = (column, position slice)
+    if (dh <= ATTN_THREADS) {
+        const uint32_t slices = ATTN_THREADS / dh;
+        const uint32_t j = threadIdx.x % dh, sl = threadIdx.x / dh;
+        uint64_t acc = 0;
+        if (sl < slices)
+            for (uint32_t t = sl; t <= pos; t += slices)
+                acc += uint64_t(mul16_prob(S[t], V[size_t(t) * dh + j]));
+        __shared__ uint64_t part[ATTN_THREADS];
+        part[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < dh) {
+            uint64_t sum = 0;
+            for (uint32_t s = 0; s < slices; ++s) sum += part[s * dh + threadIdx.x];
+            a.out[size_t(h) * dh + threadIdx.x] = int64_t(sum);
+        }
+    } else {
+        for (uint32_t j = threadIdx.x; j < dh; j += ATTN_THREADS) {
+            uint64_t acc = 0;
+            for (uint32_t t = 0; t <= pos; ++t) acc += uint64_t(mul16_prob(S[t], V[size_t(t) * dh + j]));
+            a.out[size_t(h) * dh + j] = int64_t(acc);
+        }
+    }
+}
+
+}  // namespace dimg::dev

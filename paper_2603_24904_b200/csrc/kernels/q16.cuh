@@ -1,0 +1,137 @@
+// Device-side Q16 integer primitives (proj/src/q16.cpp, proj/include/dim/q16.hpp).
+//
+// Every rescale is the reference's floor shift; every place the reference
+// widens to int128 widens here too (__int128 is native in sm_100a device
+// code: mul.lo/mul.hi pairs). Sums the reference keeps in int64/int128 are
+// carried in unsigned types so the two's-complement wrap it relies on is
+// reproduced without C++ undefined behaviour. No floating point anywhere.
+#pragma once
+
+#include <cstdint>
+
+namespace dimg::dev {
+
+typedef __int128 i128;
+typedef unsigned __int128 u128;
+
+constexpr int64_t ONE = int64_t(1) << 16;
+constexpr int64_t ACT_CLAMP = 256 * ONE;  // proj/include/dim/kernels.hpp:16
+
+// q16_mul: (int128(a) * b) >> 16, truncated to int64 (q16.hpp:28-30).
+__device__ __forceinline__ int64_t mul16(int64_t a, int64_t b) {
+    return int64_t((i128(a) * i128(b)) >> 16);
+}
+
+// floor(p * v / 2^16) for 0 <= p <= 2^16 (softmax probabilities) with 64-bit
+// ops only: v = vh*2^16 + vl, vl in [0, 2^16) => p*vh + (p*vl >> 16) exactly.
+__device__ __forceinline__ int64_t mul16_prob(int64_t p, int64_t v) {
+    int64_t vh = v >> 16;
+    uint64_t vl = uint64_t(v) & 0xFFFFu;
+    return int64_t(uint64_t(p) * uint64_t(vh) + ((uint64_t(p) * vl) >> 16));
+}
+
+__device__ __forceinline__ int64_t wrap_add(int64_t a, int64_t b) {
+    return int64_t(uint64_t(a) + uint64_t(b));
+}
+__device__ __forceinline__ int64_t wrap_sub(int64_t a, int64_t b) {
+    return int64_t(uint64_t(a) - uint64_t(b));
+}
+
+// Dense epilogue: (int128(acc) * scale) >> 16 (proj/src/kernels.cpp:27).
+__device__ __forceinline__ int64_t scale_row(int64_t acc, int64_t s) {
+    return int64_t((i128(acc) * i128(s)) >> 16);
+}
+
+// residual_add_clamp (proj/src/kernels.cpp:192-200).
+__device__ __forceinline__ int64_t add_clamp(int64_t a, int64_t b) {
+    int64_t s = wrap_add(a, b);
+    return s > ACT_CLAMP ? ACT_CLAMP : (s < -ACT_CLAMP ? -ACT_CLAMP : s);
+}
+
+// inv_sqrt_q16: octave seed (host-built Q48 table) + three Newton steps at
+// Q48 in int128, rounded to Q16 (proj/src/q16.cpp:56-68). x > 0.
+__device__ __forceinline__ int64_t inv_sqrt_q16(int64_t x, const int64_t* seeds) {
+    int b = 63 - __clzll(x);
+    i128 y = seeds[b];
+    const i128 three = i128(3) << 48;
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+        i128 t = (y * y) >> 48;
+        i128 u = (i128(x) * t) >> 16;
+        y = (y * (three - u)) >> 49;
+    }
+    return int64_t((y + (i128(1) << 31)) >> 32);
+}
+
+// exp_neg_lut: 257-entry table, 2048 raw units per cell, round-half-up
+// linear interpolation (proj/src/q16.cpp:81-92). 0 <= t <= 8*ONE.
+__device__ __forceinline__ int64_t exp_neg(int64_t t, const int64_t* e) {
+    int64_t cell = t >> 11, frac = t & 2047;
+    if (cell == 256) return e[0];
+    int64_t hi = e[256 - cell], lo = e[255 - cell];
+    return hi - (((hi - lo) * frac + 1024) >> 11);
+}
+
+// sigmoid_q16 with exact symmetry (proj/src/q16.cpp:94-101).
+__device__ __forceinline__ int64_t sigmoid_q16(int64_t x, const int64_t* e) {
+    bool pos = x > 0;
+    int64_t xn = pos ? -x : x;  // x > 0 => -x is representable
+    int64_t t = xn <= -8 * ONE ? 8 * ONE : -xn;
+    int64_t ev = exp_neg(t, e);
+    int64_t den = ONE + ev;
+    int64_t s = ((ev << 16) + den / 2) / den;
+    return pos ? ONE - s : s;
+}
+
+// silu_q16 = mul16(x, sigmoid(x)) (proj/src/q16.cpp:103-105).
+__device__ __forceinline__ int64_t silu_q16(int64_t x, const int64_t* e) {
+    return mul16(x, sigmoid_q16(x, e));
+}
+
+// ---- warp / block reductions ------------------------------------------------
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ u128 warp_sum_u128(u128 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t lo = __shfl_xor_sync(0xffffffffu, uint64_t(v), o);
+        uint64_t hi = __shfl_xor_sync(0xffffffffu, uint64_t(v >> 64), o);
+        v += (u128(hi) << 64) | lo;
+    }
+    return v;
+}
+
+__device__ __forceinline__ int64_t warp_max_i64(int64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        int64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+// Block-wide reductions through `scratch` (>= 32 entries of the type).
+template <class T, class Op>
+__device__ __forceinline__ T block_reduce(T v, T* scratch, Op op, T (*warp_op)(T)) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    v = warp_op(v);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    T r = scratch[0];
+    for (int i = 1; i < nw; ++i) r = op(r, scratch[i]);
+    return r;
+}
+
+// Argmax key: larger value wins, lower index on ties (engine.cpp:113-120).
+__device__ __forceinline__ bool better(int64_t v1, uint32_t i1, int64_t v2, uint32_t i2) {
+    return v1 > v2 || (v1 == v2 && i1 < i2);
+}
+
+}  // namespace dimg::dev

@@ -1,0 +1,277 @@
+"""The reference's engine API (proj/include/dim/engine.hpp) over the B200 C ABI.
+
+Same names, argument meaning and error behaviour as dim::InferenceSession,
+dim::generate_greedy, dim::hash_token_ids and dim::select_greedy, so the
+reference's tests (proj/tests/test_engine.cpp) read the same against it.
+Every forward pass runs on the GPU through libdimg.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import itertools
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import errors
+from ._lib import QTensor, check, i8p, i64p, lib, ptr, u8p, u32p, u64p
+from .model import ModelFile
+
+_generation_counter = itertools.count()
+_generations = 0
+
+
+def generation_counter() -> int:
+    """Count of generation runs in this process (engine.cpp:165-168)."""
+    return _generations
+
+
+@dataclass
+class EngineOptions:
+    """EngineOptions (engine.hpp:20-24). `threads` and `chunk` select the
+    reference's head-thread pool and chunked matvec; integer sums make both
+    invisible in the output, so the GPU path accepts and ignores them."""
+
+    threads: int = 1
+    chunk: int = 0
+    keep_logits: bool = False
+    device: int = 0
+
+
+@dataclass
+class GenerationResult:
+    token_ids: List[int]
+    output_hash: bytes
+    logits: List[np.ndarray] = field(default_factory=list)
+
+    @property
+    def output_hash_hex(self) -> str:
+        return self.output_hash.hex()
+
+
+def hash_token_ids(ids: Sequence[int]) -> bytes:
+    """BLAKE3 over u32-LE ids (engine.cpp:104-111)."""
+    a = np.ascontiguousarray(ids, dtype=np.uint32)
+    out = (C.c_uint8 * 32)()
+    check(lib.dimg_hash_token_ids(ptr(a, u32p), a.size, out))
+    return bytes(out)
+
+
+def select_greedy(logits) -> int:
+    """Argmax, lowest index on ties (engine.cpp:113-120)."""
+    a = np.ascontiguousarray(logits, dtype=np.int64)
+    out = C.c_uint32()
+    check(lib.dimg_select_greedy(ptr(a, i64p), a.size, C.byref(out)))
+    return out.value
+
+
+def parse_prompt(prompt_csv: str = "", bytes_str: str = "") -> List[int]:
+    """parse_prompt (proj/tools/dim_cli.cpp:56-70)."""
+    cap = max(16, len(prompt_csv) + len(bytes_str.encode()) + 1)
+    out = np.zeros(cap, np.uint32)
+    n = C.c_size_t()
+    check(lib.dimg_parse_prompt(prompt_csv.encode(), bytes_str.encode() if bytes_str else None,
+                                ptr(out, u32p), cap, C.byref(n)))
+    return [int(v) for v in out[:n.value]]
+
+
+def prompt_from_seed(seed: int, vocab: int, n: int) -> List[int]:
+    out = np.zeros(max(1, n), np.uint32)
+    check(lib.dimg_prompt_from_seed(C.c_uint64(seed), vocab, n, ptr(out, u32p)))
+    return [int(v) for v in out[:n]]
+
+
+def build_rope_tables(theta: float, d_head: int, max_ctx: int):
+    """RopeTables cos/sin [max_ctx][d_head/2] (proj/src/rope.cpp:17-39)."""
+    c = np.empty(max_ctx * (d_head // 2), np.int64)
+    s = np.empty_like(c)
+    check(lib.dimg_rope_tables(theta, d_head, max_ctx, ptr(c, i64p), ptr(s, i64p)))
+    return c, s
+
+
+class InferenceSession:
+    """Owns one sequence's KV cache on a GPU; single writer (engine.hpp:41-57)."""
+
+    def __init__(self, model: ModelFile, opts: Optional[EngineOptions] = None,
+                 imported_tables=None, keep_logits_cap: int = 0):
+        self.opts = opts or EngineOptions()
+        model.config.validate()
+        if imported_tables is not None:
+            c, s = imported_tables
+            half = model.config.d_head // 2
+            if c.size % max(1, half) or c.size // max(1, half) < model.config.max_ctx:
+                raise errors.InvalidArgument("session: imported tables do not fit the model")
+        self.model = model
+        self._dm = model.device_model(self.opts.device, imported_tables)
+        h = C.c_void_p()
+        check(lib.dimg_session_create(self._dm._h, keep_logits_cap, C.byref(h)))
+        self._h = h
+        self.vocab = model.config.vocab
+
+    def forward(self, token: int, pos: int) -> np.ndarray:
+        """Runs token at position pos (== cache length); returns the logits."""
+        out = np.empty(self.vocab, np.int64)
+        check(lib.dimg_session_forward(self._h, token, pos, ptr(out, i64p)))
+        return out
+
+    @property
+    def cache_len(self) -> int:
+        n = C.c_uint32()
+        check(lib.dimg_session_len(self._h, C.byref(n)))
+        return n.value
+
+    def reset(self):
+        check(lib.dimg_session_reset(self._h))
+
+    def generate_greedy(self, prompt: Sequence[int], max_new: int, keep_logits: bool = False):
+        p = np.ascontiguousarray(prompt, dtype=np.uint32)
+        toks = np.zeros(max(1, max_new), np.uint32)
+        h = (C.c_uint8 * 32)()
+        logits = np.empty((max_new, self.vocab), np.int64) if keep_logits else None
+        check(lib.dimg_generate_greedy(self._h, ptr(p, u32p), p.size, max_new, ptr(toks, u32p), h,
+                                       ptr(logits, i64p) if keep_logits else None))
+        res = GenerationResult([int(t) for t in toks[:max_new]], bytes(h))
+        if keep_logits:
+            res.logits = [logits[i] for i in range(max_new)]
+        return res
+
+    # ---- device-resident stepping (bench)
+    def begin(self, prompt: Sequence[int], max_new: int):
+        p = np.ascontiguousarray(prompt, dtype=np.uint32)
+        check(lib.dimg_session_begin(self._h, ptr(p, u32p), p.size, max_new))
+
+    def prefill(self):
+        check(lib.dimg_session_prefill(self._h))
+
+    def decode(self, n: int):
+        check(lib.dimg_session_decode(self._h, n))
+
+    def time_decode(self, n: int) -> float:
+        ms = C.c_float()
+        check(lib.dimg_session_time_decode(self._h, n, C.byref(ms)))
+        return ms.value
+
+    KERNELS = ("qkv_gemv", "wo_gemv", "gate_up_gemv", "down_gemv", "lm_head_gemv")
+
+    def time_kernel(self, which: int, n: int):
+        """(ms per launch, algorithmic bytes per launch) of kernel class `which`."""
+        ms = C.c_float()
+        b = C.c_uint64()
+        check(lib.dimg_session_time_kernel(self._h, which, n, C.byref(ms), C.byref(b)))
+        return ms.value, b.value
+
+    def sync(self):
+        check(lib.dimg_session_sync(self._h))
+
+    def tokens(self, n: int) -> List[int]:
+        out = np.zeros(max(1, n), np.uint32)
+        check(lib.dimg_session_tokens(self._h, ptr(out, u32p), n))
+        return [int(t) for t in out[:n]]
+
+    def stream(self) -> int:
+        p = C.c_void_p()
+        check(lib.dimg_session_stream(self._h, C.byref(p)))
+        return p.value or 0
+
+    def launches(self):
+        d, p = C.c_uint32(), C.c_uint32()
+        check(lib.dimg_session_launches(self._h, C.byref(d), C.byref(p)))
+        return d.value, p.value
+
+    def stats(self):
+        out = np.zeros(4, np.uint64)
+        check(lib.dimg_session_stats(self._h, ptr(out, u64p)))
+        return {"wide_limb_ctas": int(out[0]), "err": int(out[1])}
+
+    def __del__(self):
+        try:
+            lib.dimg_session_free(self._h)
+        except Exception:
+            pass
+
+
+_session_cache = {}
+
+
+def _cached_session(model: ModelFile, opts: EngineOptions, keep: int, tables):
+    key = (id(model), opts.device, None if tables is None else id(tables))
+    s = _session_cache.get(key)
+    if s is None or s.model is not model:
+        s = InferenceSession(model, EngineOptions(device=opts.device), tables, keep_logits_cap=keep)
+        _session_cache[key] = s
+    return s
+
+
+def generate_greedy(model: ModelFile, prompt: Sequence[int], max_new: int,
+                    opts: Optional[EngineOptions] = None, imported_tables=None) -> GenerationResult:
+    """generate_greedy (engine.cpp:142-147) on the GPU: prompt + greedy
+    continuation + BLAKE3 output hash; logits when opts.keep_logits."""
+    global _generations
+    opts = opts or EngineOptions()
+    _generations += 1
+    sess = _cached_session(model, opts, max_new if opts.keep_logits else 0, imported_tables)
+    return sess.generate_greedy(prompt, max_new, keep_logits=opts.keep_logits)
+
+
+def release_sessions():
+    _session_cache.clear()
+
+
+# ---- operator-level entry points (proj/src/kernels.cpp), GPU kernels --------
+
+def _qt(w, s):
+    w = np.ascontiguousarray(w, np.int8)
+    s = np.ascontiguousarray(s, np.int64)
+    return QTensor(w.shape[0], w.shape[1], ptr(w, i8p), ptr(s, i64p)), (w, s)
+
+
+def dense_forward(w, scales, x, device: int = 0) -> np.ndarray:
+    qt, keep = _qt(w, scales)
+    x = np.ascontiguousarray(x, np.int64)
+    if x.size != qt.cols:
+        raise errors.InvalidArgument("dense_forward: dimension mismatch")
+    out = np.empty(qt.rows, np.int64)
+    check(lib.dimg_op_dense(device, C.byref(qt), ptr(x, i64p), ptr(out, i64p)))
+    return out
+
+
+def rmsnorm(x, gamma, device: int = 0) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.int64)
+    g = np.ascontiguousarray(gamma, np.int64)
+    if x.size != g.size:
+        raise errors.InvalidArgument("rmsnorm: gamma size mismatch")
+    out = np.empty_like(x)
+    check(lib.dimg_op_rmsnorm(device, ptr(x, i64p), ptr(g, i64p), x.size, ptr(out, i64p)))
+    return out
+
+
+def softmax_q16(scores, device: int = 0) -> np.ndarray:
+    s = np.ascontiguousarray(scores, np.int64)
+    out = np.empty_like(s)
+    check(lib.dimg_op_softmax(device, ptr(s, i64p), s.size, ptr(out, i64p)))
+    return out
+
+
+def attention_steps(n_heads, d_head, max_ctx, theta, q, k, v, device: int = 0) -> np.ndarray:
+    q, k, v = (np.ascontiguousarray(a, np.int64) for a in (q, k, v))
+    out = np.empty_like(q)
+    check(lib.dimg_op_attention(device, n_heads, d_head, max_ctx, theta, q.shape[0], ptr(q, i64p),
+                                ptr(k, i64p), ptr(v, i64p), ptr(out, i64p)))
+    return out
+
+
+def ffn_silu(x, wg, sg, wu, su, wd, sd, device: int = 0) -> np.ndarray:
+    g, k1 = _qt(wg, sg)
+    u, k2 = _qt(wu, su)
+    d, k3 = _qt(wd, sd)
+    x = np.ascontiguousarray(x, np.int64)
+    out = np.empty(d.rows, np.int64)
+    check(lib.dimg_op_ffn(device, C.byref(g), C.byref(u), C.byref(d), ptr(x, i64p), ptr(out, i64p)))
+    return out
+
+
+def device_count() -> int:
+    n = C.c_int()
+    check(lib.dimg_device_count(C.byref(n)))
+    return n.value

@@ -1,0 +1,205 @@
+"""GPU parity: the sm_100a engine against the reference's own outputs.
+
+Goldens come from the reference engine itself (tests/golden/make_golden.py
+drives oracle/_ref, the unmodified reference compiled from its sources);
+live comparisons use the C oracle (oracle/dim_oracle.c) on the same seeded
+inputs. Integer/byte work: the bar is bit-exact, no tolerance anywhere.
+"""
+import numpy as np
+import pytest
+
+from conftest import ops_cases, wild_arrays
+
+pytestmark = pytest.mark.gpu
+
+ONE = 1 << 16
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2603_24904_b200 as P
+    return P
+
+
+def _digest(P, arrs):
+    return P.weight_hash(np.ascontiguousarray(np.stack(arrs), np.int64).tobytes())
+
+
+# ---- operators -------------------------------------------------------------
+
+def test_dense_matches_reference(P, ops_fixture):
+    for w, s, x, want in ops_cases(ops_fixture, "dense"):
+        got = P.dense_forward(w, s, x)
+        assert np.array_equal(got, want), (w.shape, int(np.abs(x).max()))
+
+
+def test_rmsnorm_matches_reference(P, ops_fixture):
+    for x, g, want in ops_cases(ops_fixture, "rmsnorm"):
+        assert np.array_equal(P.rmsnorm(x, g), want)
+
+
+def test_softmax_matches_reference(P, ops_fixture):
+    for s, want in ops_cases(ops_fixture, "softmax"):
+        assert np.array_equal(P.softmax_q16(s), want)
+    p = P.softmax_q16(np.array([0, -20 * ONE], np.int64))
+    assert list(p) == [65514, 21]  # proj/tests/test_kernels.cpp:197-203
+
+
+def test_attention_matches_reference(P, ops_fixture):
+    for (dims, q, k, v, want) in ops_cases(ops_fixture, "attention"):
+        H, dh, ctx = (int(t) for t in dims)
+        got = P.attention_steps(H, dh, ctx, 10000.0, q, k, v)
+        assert np.array_equal(got, want), (H, dh)
+
+
+def test_ffn_matches_reference(P, ops_fixture):
+    for wg, sg, wu, su, wd, sd, x, want in ops_cases(ops_fixture, "ffn"):
+        assert np.array_equal(P.ffn_silu(x, wg, sg, wu, su, wd, sd), want)
+
+
+def test_dense_against_oracle_wide_values(P, oracle):
+    """Activations past 2^23 take the 8-limb path; values near 2^62 make the
+    reference's int64 accumulator wrap -- the wrap must be reproduced."""
+    rng = np.random.default_rng(3)
+    for mag in (1 << 22, 1 << 23, (1 << 23) + 1, 1 << 40, 1 << 62):
+        for rows, cols in ((5, 4096), (33, 11008), (7, 17), (130, 100)):
+            w = rng.integers(-127, 128, (rows, cols)).astype(np.int8)
+            s = rng.integers(1, 1 << 20, rows, dtype=np.int64)
+            x = rng.integers(-mag, mag, cols, dtype=np.int64)
+            assert np.array_equal(P.dense_forward(w, s, x), oracle.dense(w, s, x)), (mag, rows, cols)
+
+
+def test_dense_edge_values(P, oracle):
+    w = np.full((4, 64), 127, np.int8)
+    w[1] = -127
+    s = np.array([1, 65536, 1 << 40, 8], np.int64)
+    for x in (np.full(64, (1 << 23) - 1, np.int64), np.full(64, -(1 << 23), np.int64),
+              np.full(64, np.iinfo(np.int64).max, np.int64), np.full(64, np.iinfo(np.int64).min, np.int64),
+              np.zeros(64, np.int64)):
+        assert np.array_equal(P.dense_forward(w, s, x), oracle.dense(w, s, x))
+
+
+# ---- whole generations -------------------------------------------------------
+
+SMALL = ["micro_s1", "micro_s9", "micro_s123456789", "small_s6", "small_s7", "small_s8",
+         "small_s9", "small_s10", "small_s11", "odd_d12", "odd_dh2", "odd_k688", "accept_101",
+         "accept_102", "accept_105", "medium", "wide_heads", "long_ctx", "wild_a", "wild_b"]
+
+
+def _model_for(P, g):
+    cfg = P.ModelConfig(*g["config"], rope_theta=g["rope_theta"])
+    m = P.gen_toy_model(g["seed"], cfg)
+    if g["kind"] == "toy":
+        assert m.weight_hash == g["weight_hash"]
+        return m
+    names = ["tok_embd"] + [f"layers.{l}.{t}" for l in range(cfg.n_layers)
+                            for t in ("wq", "wk", "wv", "wo", "w_gate", "w_up", "w_down")] + ["output"]
+    tens = [m.tensor(n) for n in names]
+    all_s = np.concatenate([s for _, s in tens])
+    s, n = wild_arrays(g["config"], g["seed"], all_s, m.norms())
+    out, o = [], 0
+    for w, s0 in tens:
+        out.append((w.copy(), s[o:o + len(s0)]))
+        o += len(s0)
+    return P.ModelFile.from_arrays(cfg, out, n)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_generation_matches_reference(P, golden_models, name):
+    g = golden_models[name]
+    m = _model_for(P, g)
+    res = P.generate_greedy(m, g["prompt"], g["max_new"], P.EngineOptions(keep_logits=True))
+    assert res.token_ids == g["tokens"]
+    assert res.output_hash.hex() == g["output_hash"]
+    assert _digest(P, res.logits) == g["logits_digest"]
+
+
+def test_wild_models_take_the_wide_path(P, golden_models):
+    g = golden_models["wild_b"]
+    m = _model_for(P, g)
+    s = P.InferenceSession(m)
+    s.generate_greedy(g["prompt"], g["max_new"])
+    assert s.stats()["wide_limb_ctas"] > 0
+
+
+def test_tinyllama_c1(P, golden_models):
+    g = golden_models["tinyllama_c1"]
+    m = _model_for(P, g)
+    res = P.generate_greedy(m, g["prompt"], g["max_new"], P.EngineOptions(keep_logits=True))
+    assert res.token_ids == g["tokens"]
+    assert res.output_hash.hex() == g["output_hash"]
+    assert _digest(P, res.logits) == g["logits_digest"]
+
+
+# ---- session contract (proj/tests/test_engine.cpp) ---------------------------
+
+def test_forward_matches_oracle_and_validates(P, oracle):
+    from oracle.pyoracle import Config
+    cfg = P.ModelConfig(1, 4, 2, 8, 8, 16)
+    for seed in (1, 9, 123456789):
+        m = P.gen_toy_model(seed, cfg)
+        om = oracle.gen_toy(seed, Config(1, 4, 2, 8, 8, 16))
+        s = P.InferenceSession(m)
+        os_ = oracle.session(om)
+        for pos, tok in enumerate([1, 5, 2, 7]):
+            assert np.array_equal(s.forward(tok, pos), os_.forward(tok, pos))
+    m = P.gen_toy_model(5, cfg)
+    s = P.InferenceSession(m)
+    with pytest.raises(P.OutOfRange):
+        s.forward(99, 0)
+    with pytest.raises(P.LogicError):
+        s.forward(1, 5)
+    for p in range(cfg.max_ctx):
+        s.forward(1, p)
+    with pytest.raises(P.ContextOverflow):
+        s.forward(1, cfg.max_ctx)
+
+
+def test_generation_preconditions(P):
+    m = P.gen_toy_model(6, P.ModelConfig(2, 16, 2, 32, 32, 64))
+    with pytest.raises(P.InvalidArgument):
+        P.generate_greedy(m, [], 4)
+    with pytest.raises(P.ContextOverflow):
+        P.generate_greedy(m, [1, 2], 1000)
+    with pytest.raises(P.OutOfRange):
+        P.generate_greedy(m, [1, 64], 4)
+    assert P.generate_greedy(m, [1, 2], 0).token_ids == []
+
+
+def test_repeat_and_cached_vs_recompute(P, oracle):
+    from oracle.pyoracle import Config
+    cfg = P.ModelConfig(2, 16, 2, 32, 32, 64)
+    m = P.gen_toy_model(7, cfg)
+    hashes = {P.generate_greedy(m, [3, 1, 4], 12).output_hash for _ in range(50)}
+    assert len(hashes) == 1
+    # KV-cached decode equals full recomputation (test_engine.cpp:113-126)
+    m9 = P.gen_toy_model(9, cfg)
+    fast = P.generate_greedy(m9, [2, 4, 8], 6).token_ids
+    om = oracle.gen_toy(9, Config(2, 16, 2, 32, 32, 64))
+    for i in range(6):
+        full = np.array([2, 4, 8] + fast[:i], np.uint32)
+        toks, _, _ = oracle.generate_greedy(om, full, 1)
+        assert int(toks[0]) == fast[i]
+
+
+def test_imported_rope_tables(P):
+    cfg = P.ModelConfig(2, 16, 2, 32, 32, 64)
+    m = P.gen_toy_model(11, cfg)
+    base = P.generate_greedy(m, [6, 2], 8)
+    tabs = P.build_rope_tables(cfg.rope_theta, cfg.d_head, cfg.max_ctx)
+    imp = P.generate_greedy(m, [6, 2], 8, imported_tables=tabs)
+    assert imp.output_hash == base.output_hash
+
+
+def test_device_resident_stepping_matches_generate(P, golden_models):
+    g = golden_models["medium"]
+    m = _model_for(P, g)
+    s = P.InferenceSession(m)
+    s.begin(g["prompt"], g["max_new"])
+    s.prefill()
+    s.decode(5)
+    s.decode(g["max_new"] - 5)
+    s.sync()
+    assert s.tokens(g["max_new"]) == g["tokens"]
+    d, p = s.launches()
+    assert d == 5 * g["config"][0] + 1 and p == 5 * g["config"][0] + 1
