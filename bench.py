@@ -298,7 +298,7 @@ def run_ours(args, rank, world, local):
                        "l2": "weights 6.6 GB/step > 126 MB L2 (no flush needed)",
                        "weight_hash_ok": wh_ok, "model_gen_s": round(gen_s, 1)},
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches_per_step,  # one persistent launch runs all K steps
             "roofline": {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
                          "frac": dom["gbs"] / peak, "traffic": None, "kernel": "gate_up_gemv",
                          "bytes_per_launch": dom["bytes"], "ms_per_launch": dom["ms"],

@@ -86,6 +86,7 @@ def _load():
         "dimg_session_launches": ([vp, u32p, u32p], C.c_int),
         "dimg_session_time_kernel": ([vp, C.c_int, C.c_uint32, C.POINTER(C.c_float), u64p], C.c_int),
         "dimg_session_stats": ([vp, u64p], C.c_int),
+        "dimg_session_trace": ([vp, C.c_uint32, u64p, C.c_uint32], C.c_int),
         "dimg_op_dense": ([C.c_int, C.POINTER(QTensor), i64p, i64p], C.c_int),
         "dimg_op_rmsnorm": ([C.c_int, i64p, i64p, C.c_uint32, i64p], C.c_int),
         "dimg_op_softmax": ([C.c_int, i64p, C.c_uint32, i64p], C.c_int),

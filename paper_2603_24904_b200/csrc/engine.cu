@@ -1,21 +1,21 @@
 // Device half of include/dimg.h: model upload (HBM layout), sessions (KV
-// cache + control block), the per-token step as a CUDA graph, and the
-// reference-shaped entry points generate_greedy / forward.
+// cache + control block) and the reference-shaped entry points
+// generate_greedy / forward.
 //
-// One decode step (InferenceSession::forward + select_greedy,
-// proj/src/engine.cpp:80-102,113-120) is 5L+1 kernels:
-//   per layer: QKV GEMV (rmsnorm prologue; layer 0 also embeds the token)
-//              -> attention step -> WO GEMV (+residual clamp)
-//              -> GATE/UP GEMV (rmsnorm prologue, silu*up epilogue)
-//              -> DOWN GEMV (+residual clamp)
-//   head:      LM_HEAD GEMV (final rmsnorm prologue, argmax epilogue that
-//              appends the next token on the device)
-// The position and the token ring live in device memory, so the same
-// instantiated graph is replayed for every token and nothing returns to the
-// host until the caller asks for the tokens.
+// Every forward step runs inside ONE cooperative launch of
+// decode_persistent_kernel (kernels/persistent.cuh): per layer the stages
+//   QKV GEMV (rmsnorm prologue; layer 0 also embeds the token)
+//   -> attention step -> WO GEMV (+residual clamp)
+//   -> GATE/UP GEMV (rmsnorm prologue, silu*up epilogue)
+//   -> DOWN GEMV (+residual clamp)
+// then the LM_HEAD GEMV with the greedy argmax, separated by grid barriers,
+// while every warp keeps streaming its next weight chunks. A whole
+// generate_greedy call (P-1 prompt steps + N decode steps) is one launch; the
+// position and the token ring live in device memory.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -27,6 +27,7 @@
 #include "host/model.hpp"
 #include "kernels/attention.cuh"
 #include "kernels/gemv.cuh"
+#include "kernels/persistent.cuh"
 
 using namespace dimg;
 using namespace dimg::dev;
@@ -51,6 +52,7 @@ struct DevCtx {
     int sm_count = 0;
     int64_t* exp_lut = nullptr;
     int64_t* seeds = nullptr;
+    int smem_optin = 0;
     Ctl* op_ctl = nullptr;  // control block for the operator-level exports
     cudaStream_t op_stream = nullptr;
 };
@@ -93,7 +95,12 @@ DevCtx& dev_ctx(int device) {
     set_gemv_attrs<EPI_ARGMAX, MODE_NORM>();
     set_gemv_attrs<EPI_RAW, MODE_PLAIN>();
     CK(cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            64 * 1024));
+                            int(attn_scratch_bytes(8192))));
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, decode_persistent_kernel));
+    c.smem_optin = int(prop.sharedMemPerBlockOptin) - int(fa.sharedSizeBytes);
+    CK(cudaFuncSetAttribute(decode_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            c.smem_optin));
     c.device = device;
     return c;
 }
@@ -120,6 +127,18 @@ struct DevBuf {
 // ---------------------------------------------------------------------------
 // Model in HBM
 // ---------------------------------------------------------------------------
+// Every dense matrix is stored "row-group blocked" for the persistent
+// kernel: rows padded to a multiple of 4, K padded to 16, then chunk
+// (group g, K-segment s) = rows 4g..4g+3 x columns [2048 s, 2048 s + w) laid
+// out contiguously, so one cp.async.bulk moves one chunk. q/k/v are one
+// matrix (3D rows); gate/up are interleaved (gate_i row 2i, up_i row 2i+1) so
+// a row group holds whole (gate, up) pairs for the silu*up epilogue.
+struct DevMat {
+    int8_t* w = nullptr;       // blocked
+    int64_t* s = nullptr;      // scales [rows]
+    uint32_t rows = 0, K = 0, Kp = 0, n_groups = 0, n_segs = 0;
+};
+
 struct dimg_model {
     int device;
     DevCtx* ctx;
@@ -127,22 +146,16 @@ struct dimg_model {
     uint32_t D, F, V, H, dh, L, Kd, Kf;
     int tp_rank, tp_size;
     struct Layer {
-        int8_t* qkv;   // [3D][Kd]: wq rows, wk rows, wv rows
-        int64_t* qkv_s;
-        int8_t* wo;    // [D][Kd]
-        int64_t* wo_s;
-        int8_t* gu;    // [2F][Kd]: gate_i at row 2i, up_i at row 2i+1
-        int64_t* gu_s;
-        int8_t* down;  // [D][Kf]
-        int64_t* down_s;
+        DevMat qkv, wo, gu, down;
         int64_t* attn_norm;
         int64_t* ffn_norm;
+        bool attn_unit, ffn_unit;  // gains all == ONE (mul16(v, ONE) == v: skipped)
     };
     std::vector<Layer> layers;
-    int8_t* embd;      // [V][D] (gathered row by row, unpadded)
+    DevMat head;
+    bool final_unit;
+    int8_t* embd;      // [V][D] row-major (one row gathered per token)
     int64_t* embd_s;
-    int8_t* out_w;     // [V][Kd]
-    int64_t* out_s;
     int64_t* final_norm;
     int64_t* rope_cos;
     int64_t* rope_sin;
@@ -168,10 +181,61 @@ T* upload(DevBuf& mem, const T* src, size_t n) {
     return d;
 }
 
+bool all_one(const int64_t* g, size_t n) {
+    for (size_t i = 0; i < n; ++i)
+        if (g[i] != kOne) return false;
+    return true;
+}
+
+// row-major [rows4][Kp] -> blocked [groups][segs][4][seg] (16-byte units)
+__global__ void blockify_kernel(const int4* __restrict__ src, int4* __restrict__ dst, uint32_t Kp,
+                                uint32_t n_groups, uint32_t n_segs) {
+    const size_t total = size_t(n_groups) * PK_ROWS * Kp / 16;
+    const uint32_t last = Kp - (n_segs - 1) * PK_SEG;
+    for (size_t o = blockIdx.x * size_t(blockDim.x) + threadIdx.x; o < total;
+         o += size_t(gridDim.x) * blockDim.x) {
+        size_t byte = o * 16;
+        size_t g = byte / (size_t(PK_ROWS) * Kp);
+        size_t in_g = byte % (size_t(PK_ROWS) * Kp);
+        uint32_t s = uint32_t(in_g / (PK_ROWS * PK_SEG));
+        uint32_t w = s + 1 < n_segs ? PK_SEG : last;
+        size_t in_s = in_g - size_t(s) * PK_ROWS * PK_SEG;
+        uint32_t r = uint32_t(in_s / w), c = uint32_t(in_s % w);
+        size_t sb = (g * PK_ROWS + r) * Kp + size_t(s) * PK_SEG + c;
+        dst[o] = src[sb / 16];
+    }
+}
+
+// Uploads one dense matrix given as `parts` row blocks (each row-major,
+// placed at row offset row0 with row stride rstride), then blockifies it.
+struct RowPart {
+    const int8_t* src;
+    uint32_t rows, row0, rstride;
+};
+
+DevMat upload_mat(dimg_model& m, uint32_t rows, uint32_t K, const std::vector<RowPart>& parts,
+                  const std::vector<int64_t>& scales, int8_t* staging) {
+    DevMat d;
+    d.rows = rows;
+    d.K = K;
+    d.Kp = pad16(K);
+    d.n_groups = (rows + PK_ROWS - 1) / PK_ROWS;
+    d.n_segs = (d.Kp + PK_SEG - 1) / PK_SEG;
+    const size_t bytes = size_t(d.n_groups) * PK_ROWS * d.Kp;
+    CK(cudaMemset(staging, 0, bytes));
+    for (const auto& p : parts) put_rows(staging, d.Kp, p.row0, p.rstride, p.src, p.rows, K);
+    d.w = m.mem.alloc<int8_t>(bytes);
+    blockify_kernel<<<1024, 256>>>(reinterpret_cast<const int4*>(staging), reinterpret_cast<int4*>(d.w),
+                                   d.Kp, d.n_groups, d.n_segs);
+    CK(cudaGetLastError());
+    d.s = upload(m.mem, scales.data(), scales.size());
+    return d;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// Session: one sequence (KV cache, control block, token ring, graphs)
+// Session: one sequence (KV cache, control block, token ring)
 // ---------------------------------------------------------------------------
 struct dimg_session {
     dimg_model* m;
@@ -181,15 +245,19 @@ struct dimg_session {
     ArgPart* parts;
     uint32_t* tokens;  // [max_ctx + 1]
     Ctl* ctl;
+    unsigned int* bar;
+    uint8_t* planes_att;   // [3][Kd] 3-limb planes of the attention output
+    uint8_t* planes_h;     // [3][Kf] 3-limb planes of the FFN hidden vector
+    uint32_t* flags;       // [2L] "needs > 3 limbs" tags (att, h) per layer
+    PkStage* stages;   // [5L + 1] device
+    std::vector<PkStage> host_stages;
+    PkStage* probe_stages = nullptr;  // [L] scratch program for time_kernel
     uint32_t keep_cap = 0;
-    uint32_t len = 0;              // host mirror of the cache length
+    uint32_t len = 0;  // host mirror of the cache length
     uint32_t n_prompt = 0, max_new = 0;
-    uint32_t gemv_blocks = 0;
-    cudaGraphExec_t g_prefill = nullptr, g_decode = nullptr;
-    uint32_t launches_decode = 0, launches_prefill = 0;
+    uint32_t grid = 0, planes_bytes = 0;
+    size_t smem = 0;
     ~dimg_session() {
-        if (g_prefill) cudaGraphExecDestroy(g_prefill);
-        if (g_decode) cudaGraphExecDestroy(g_decode);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -209,109 +277,113 @@ void launch_gemv(const GemvArgs& a, const DevCtx& c, cudaStream_t st, uint32_t g
     gemv_kernel<EPI, MODE, R_ROWS, U_3><<<grid, GEMV_THREADS, smem, st>>>(a);
 }
 
-GemvArgs base_args(const dimg_model& m, Ctl* ctl) {
-    GemvArgs a{};
-    a.ctl = ctl;
+PkStage gemv_stage(const DevMat& d, uint32_t mode, uint32_t epi, const int64_t* x, const int64_t* gamma,
+                   int64_t* y, bool gamma_unit = false) {
+    PkStage st{};
+    st.kind = SK_GEMV;
+    st.mode = mode;
+    st.epi = epi;
+    st.rows = d.rows; st.K = d.K; st.Kp = d.Kp; st.n_groups = d.n_groups; st.n_segs = d.n_segs;
+    st.W = d.w; st.scales = d.s; st.x = x; st.gamma = gamma; st.y = y;
+    st.gamma_unit = gamma_unit ? 1 : 0;
+    return st;
+}
+
+// The stage program of one forward step (proj/src/engine.cpp:85-101).
+std::vector<PkStage> step_program(const dimg_session& s) {
+    const dimg_model& m = *s.m;
+    std::vector<PkStage> p;
+    for (uint32_t l = 0; l < m.L; ++l) {
+        const auto& lw = m.layers[l];
+        uint32_t* f_att = s.flags + 2 * l;
+        uint32_t* f_h = s.flags + 2 * l + 1;
+        p.push_back(gemv_stage(lw.qkv, l == 0 ? MODE_EMBED : MODE_NORM, EPI_STORE, s.x, lw.attn_norm,
+                               s.qkv, lw.attn_unit));
+        PkStage at{};
+        at.kind = SK_ATTN;
+        at.layer = l;
+        at.out_planes = s.planes_att;
+        at.out_pitch = m.Kd;
+        at.out_flag = f_att;
+        p.push_back(at);
+        PkStage wo = gemv_stage(lw.wo, MODE_PLAIN, EPI_RESID, s.att, nullptr, s.x);
+        wo.in_planes = s.planes_att;
+        wo.in_flag = f_att;
+        p.push_back(wo);
+        PkStage gu = gemv_stage(lw.gu, MODE_NORM, EPI_SILU, s.x, lw.ffn_norm, s.h, lw.ffn_unit);
+        gu.out_planes = s.planes_h;
+        gu.out_pitch = m.Kf;
+        gu.out_flag = f_h;
+        p.push_back(gu);
+        PkStage dn = gemv_stage(lw.down, MODE_PLAIN, EPI_RESID, s.h, nullptr, s.x);
+        dn.in_planes = s.planes_h;
+        dn.in_flag = f_h;
+        p.push_back(dn);
+    }
+    p.push_back(gemv_stage(m.head, MODE_NORM, EPI_ARGMAX, s.x, m.final_norm, s.logits, m.final_unit));
+    return p;
+}
+
+PkArgs pk_args(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, uint32_t n_steps,
+               uint32_t n_prefill) {
+    const dimg_model& m = *s.m;
+    PkArgs a{};
+    a.stages = stages;
+    a.n_layer_stages = n_layer_stages;
+    a.n_steps = n_steps;
+    a.n_prefill = n_prefill;
+    a.planes_bytes = s.planes_bytes;
+    a.ctl = s.ctl;
+    a.bar = s.bar;
+    a.embd = m.embd;
+    a.embd_scales = m.embd_s;
+    a.d_model = m.D;
+    a.vocab = m.V;
+    a.tokens = s.tokens;
+    a.logits = s.logits;
+    a.parts = s.parts;
+    a.x_resid = s.x;
+    AttnArgs& t = a.attn;
+    t.qkv = s.qkv;
+    t.kc = s.kc;
+    t.vc = s.vc;
+    t.rope_cos = m.rope_cos;
+    t.rope_sin = m.rope_sin;
+    t.scores = s.scores;
+    t.out = s.att;
+    t.ctl = s.ctl;
+    t.H = m.H;
+    t.dh = m.dh;
+    t.max_ctx = m.cfg.max_ctx;
+    t.inv_scale = m.inv_scale;
+    t.exp_lut = m.ctx->exp_lut;
+    a.kv_layer_stride = size_t(m.H) * m.cfg.max_ctx * m.dh;
     a.exp_lut = m.ctx->exp_lut;
     a.seeds = m.ctx->seeds;
     return a;
 }
 
-void launch_qkv(dimg_session& s, uint32_t l) {
-    const dimg_model& m = *s.m;
-    const auto& lw = m.layers[l];
-    GemvArgs a = base_args(m, s.ctl);
-    a.W = lw.qkv; a.scales = lw.qkv_s; a.rows = 3 * m.D; a.K = m.D; a.Kp = m.Kd;
-    a.x = s.x; a.gamma = lw.attn_norm; a.y = s.qkv;
-    if (l == 0) {
-        a.embd = m.embd; a.embd_scales = m.embd_s; a.tokens = s.tokens; a.x_out = s.x;
-        launch_gemv<EPI_STORE, MODE_EMBED>(a, *m.ctx, s.stream);
-    } else {
-        launch_gemv<EPI_STORE, MODE_NORM>(a, *m.ctx, s.stream);
-    }
-}
-
-void launch_attn(dimg_session& s, uint32_t l) {
-    const dimg_model& m = *s.m;
-    AttnArgs t{};
-    t.qkv = s.qkv;
-    t.kc = s.kc + size_t(l) * m.H * m.cfg.max_ctx * m.dh;
-    t.vc = s.vc + size_t(l) * m.H * m.cfg.max_ctx * m.dh;
-    t.rope_cos = m.rope_cos; t.rope_sin = m.rope_sin;
-    t.scores = s.scores; t.out = s.att; t.ctl = s.ctl;
-    t.H = m.H; t.dh = m.dh; t.max_ctx = m.cfg.max_ctx; t.inv_scale = m.inv_scale;
-    t.exp_lut = m.ctx->exp_lut;
-    attn_decode_kernel<<<m.H, ATTN_THREADS, m.dh * sizeof(int64_t), s.stream>>>(t);
-}
-
-void launch_wo(dimg_session& s, uint32_t l) {
-    const dimg_model& m = *s.m;
-    const auto& lw = m.layers[l];
-    GemvArgs a = base_args(m, s.ctl);
-    a.W = lw.wo; a.scales = lw.wo_s; a.rows = m.D; a.K = m.D; a.Kp = m.Kd;
-    a.x = s.att; a.y = s.x;
-    launch_gemv<EPI_RESID, MODE_PLAIN>(a, *m.ctx, s.stream);
-}
-
-void launch_gate_up(dimg_session& s, uint32_t l) {
-    const dimg_model& m = *s.m;
-    const auto& lw = m.layers[l];
-    GemvArgs a = base_args(m, s.ctl);
-    a.W = lw.gu; a.scales = lw.gu_s; a.rows = 2 * m.F; a.K = m.D; a.Kp = m.Kd;
-    a.x = s.x; a.gamma = lw.ffn_norm; a.y = s.h;
-    launch_gemv<EPI_SILU, MODE_NORM>(a, *m.ctx, s.stream);
-}
-
-void launch_down(dimg_session& s, uint32_t l) {
-    const dimg_model& m = *s.m;
-    const auto& lw = m.layers[l];
-    GemvArgs a = base_args(m, s.ctl);
-    a.W = lw.down; a.scales = lw.down_s; a.rows = m.D; a.K = m.F; a.Kp = m.Kf;
-    a.x = s.h; a.y = s.x;
-    launch_gemv<EPI_RESID, MODE_PLAIN>(a, *m.ctx, s.stream);
-}
-
-void launch_head(dimg_session& s) {
-    const dimg_model& m = *s.m;
-    GemvArgs a = base_args(m, s.ctl);
-    a.W = m.out_w; a.scales = m.out_s; a.rows = m.V; a.K = m.D; a.Kp = m.Kd;
-    a.x = s.x; a.gamma = m.final_norm; a.logits = s.logits; a.parts = s.parts;
-    a.tokens_out = s.tokens;
-    launch_gemv<EPI_ARGMAX, MODE_NORM>(a, *m.ctx, s.stream, s.gemv_blocks);
-}
-
-// Enqueues one forward step; `head` adds the lm_head + greedy selection,
-// otherwise the position is just advanced (a prompt token whose logits the
-// reference computes and discards, engine.cpp:40-42).
-uint32_t enqueue_step(dimg_session& s, bool head) {
-    const dimg_model& m = *s.m;
-    for (uint32_t l = 0; l < m.L; ++l) {
-        launch_qkv(s, l);
-        launch_attn(s, l);
-        launch_wo(s, l);
-        launch_gate_up(s, l);
-        launch_down(s, l);
-    }
-    if (head) launch_head(s);
-    else advance_pos_kernel<<<1, 1, 0, s.stream>>>(s.ctl);
-    CK(cudaGetLastError());
-    return 5 * m.L + 1;
-}
-
-cudaGraphExec_t capture(dimg_session& s, bool head, uint32_t* launches) {
-    cudaGraph_t g;
-    CK(cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal));
-    try {
-        *launches = enqueue_step(s, head);
-    } catch (...) {
-        cudaStreamEndCapture(s.stream, &g);
-        throw;
-    }
-    CK(cudaStreamEndCapture(s.stream, &g));
-    cudaGraphExec_t ex;
-    CK(cudaGraphInstantiate(&ex, g, 0));
-    CK(cudaGraphDestroy(g));
-    return ex;
+void launch_pk(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, uint32_t n_steps,
+               uint32_t n_prefill, unsigned long long* trace = nullptr, uint32_t trace_cap = 0) {
+    if (n_steps == 0) return;
+    PkArgs a = pk_args(s, stages, n_layer_stages, n_steps, n_prefill);
+    a.trace = trace;
+    a.trace_cap = trace_cap;
+    static const uint32_t l2_ahead = [] {
+        const char* e = std::getenv("DIMG_L2_AHEAD");
+        return e ? uint32_t(std::atoi(e)) : 0u;
+    }();
+    static const uint32_t bar_mode = [] {
+        const char* e = std::getenv("DIMG_BAR_MODE");
+        return e ? uint32_t(std::atoi(e)) : 0u;
+    }();
+    a.l2_ahead = l2_ahead;
+    a.bar_mode = bar_mode;
+    CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned int), s.stream));
+    CK(cudaMemsetAsync(s.flags, 0, size_t(2) * s.m->L * sizeof(uint32_t), s.stream));
+    void* params[] = {&a};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(decode_persistent_kernel), dim3(s.grid),
+                                   dim3(PK_THREADS), params, s.smem, s.stream));
 }
 
 // Writes the control header (pos, logit_base, keep_cap, argmax_count, err).
@@ -324,6 +396,7 @@ void check_ctl_err(dimg_session& s) {
     uint32_t err = 0;
     CK(cudaMemcpyAsync(&err, &s.ctl->err, 4, cudaMemcpyDeviceToHost, s.stream));
     CK(cudaStreamSynchronize(s.stream));
+    if (err & 4u) fail(DIMG_ECUDA, "persistent kernel: grid barrier timed out");
     if (err & 1u) fail(DIMG_EDOMAIN, "inv_sqrt_q16: input must be positive");
 }
 
@@ -335,9 +408,10 @@ void ensure_keep(dimg_session& s, uint32_t need) {
     s.mem.ptrs.push_back(p);
     s.logits = static_cast<int64_t*>(p);
     s.keep_cap = need;
-    // the decode graph bakes the logits pointer in: recapture
-    if (s.g_decode) CK(cudaGraphExecDestroy(s.g_decode));
-    s.g_decode = capture(s, true, &s.launches_decode);
+    // the head stage's output pointer lives in the stage table
+    s.host_stages.back().y = s.logits;
+    CK(cudaMemcpy(s.stages + s.host_stages.size() - 1, &s.host_stages.back(), sizeof(PkStage),
+                  cudaMemcpyHostToDevice));
 }
 
 void check_prompt(const dimg_model& m, const uint32_t* prompt, uint32_t p, uint32_t n) {
@@ -360,13 +434,16 @@ void begin(dimg_session& s, const uint32_t* prompt, uint32_t p, uint32_t n, bool
     s.len = 0;
 }
 
+uint32_t n_layer_stages(const dimg_session& s) { return 5 * s.m->L; }
+
 void run_prefill(dimg_session& s) {
-    for (uint32_t i = 0; i + 1 < s.n_prompt; ++i) CK(cudaGraphLaunch(s.g_prefill, s.stream));
-    s.len = s.n_prompt - 1;
+    uint32_t n = s.n_prompt - 1;
+    launch_pk(s, s.stages, n_layer_stages(s), n, n);
+    s.len = n;
 }
 
 void run_decode(dimg_session& s, uint32_t steps) {
-    for (uint32_t i = 0; i < steps; ++i) CK(cudaGraphLaunch(s.g_decode, s.stream));
+    launch_pk(s, s.stages, n_layer_stages(s), steps, 0);
     s.len += steps;
 }
 
@@ -392,13 +469,19 @@ dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank,
         m->D = d->cfg.d_model; m->F = d->cfg.d_ffn; m->V = d->cfg.vocab; m->H = d->cfg.n_heads;
         m->dh = m->D / m->H; m->L = d->cfg.n_layers; m->Kd = pad16(m->D); m->Kf = pad16(m->F);
         m->tp_rank = tp_rank; m->tp_size = tp_size;
-        if (size_t(8) * std::max(m->Kd, m->Kf) > 200 * 1024)
-            fail(DIMG_EINVAL, "model_upload: d_ffn above 25600 needs the tiled-limb GEMV (not built)");
-        if (size_t(m->dh) * 8 > 64 * 1024) fail(DIMG_EINVAL, "model_upload: d_head above 8192");
         const uint32_t D = m->D, F = m->F, V = m->V;
         auto check_qt = [&](const dimg_qtensor& t, uint32_t r, uint32_t k, const char* what) {
             if (t.rows != r || t.cols != k) fail(DIMG_EINVAL, std::string("model_upload: bad shape of ") + what);
         };
+        // staging for the largest matrix (row-major, rows padded to 4)
+        size_t stage_bytes = 0;
+        auto grow = [&](uint32_t rows, uint32_t K) {
+            stage_bytes = std::max(stage_bytes, size_t((rows + 3) / 4) * 4 * pad16(K));
+        };
+        grow(3 * D, D); grow(2 * F, D); grow(D, F); grow(V, D);
+        int8_t* staging = nullptr;
+        CK(cudaMalloc(&staging, stage_bytes));
+        struct Free { int8_t* p; ~Free() { cudaFree(p); } } free_staging{staging};
         m->layers.resize(m->L);
         for (uint32_t l = 0; l < m->L; ++l) {
             const dimg_qtensor* t = d->layers + 7 * size_t(l);
@@ -406,42 +489,33 @@ dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank,
             for (int i = 0; i < 7; ++i)
                 check_qt(t[i], i < 4 ? D : (i < 6 ? F : D), i < 6 ? D : F, names[i]);
             auto& lw = m->layers[l];
-            lw.qkv = m->mem.alloc<int8_t>(size_t(3) * D * m->Kd);
-            CK(cudaMemset(lw.qkv, 0, size_t(3) * D * m->Kd));
-            for (int i = 0; i < 3; ++i) put_rows(lw.qkv, m->Kd, size_t(i) * D, 1, t[i].data, D, D);
             std::vector<int64_t> s(3 * size_t(D));
-            for (int i = 0; i < 3; ++i) std::copy(t[i].scales, t[i].scales + D, s.begin() + i * D);
-            lw.qkv_s = upload(m->mem, s.data(), s.size());
-            lw.wo = m->mem.alloc<int8_t>(size_t(D) * m->Kd);
-            CK(cudaMemset(lw.wo, 0, size_t(D) * m->Kd));
-            put_rows(lw.wo, m->Kd, 0, 1, t[3].data, D, D);
-            lw.wo_s = upload(m->mem, t[3].scales, D);
-            lw.gu = m->mem.alloc<int8_t>(size_t(2) * F * m->Kd);
-            CK(cudaMemset(lw.gu, 0, size_t(2) * F * m->Kd));
-            put_rows(lw.gu, m->Kd, 0, 2, t[4].data, F, D);
-            put_rows(lw.gu, m->Kd, 1, 2, t[5].data, F, D);
+            for (int i = 0; i < 3; ++i) std::copy(t[i].scales, t[i].scales + D, s.begin() + size_t(i) * D);
+            lw.qkv = upload_mat(*m, 3 * D, D, {{t[0].data, D, 0, 1}, {t[1].data, D, D, 1}, {t[2].data, D, 2 * D, 1}},
+                                s, staging);
+            lw.wo = upload_mat(*m, D, D, {{t[3].data, D, 0, 1}},
+                               std::vector<int64_t>(t[3].scales, t[3].scales + D), staging);
             std::vector<int64_t> gs(2 * size_t(F));
             for (uint32_t i = 0; i < F; ++i) {
                 gs[2 * i] = t[4].scales[i];
                 gs[2 * i + 1] = t[5].scales[i];
             }
-            lw.gu_s = upload(m->mem, gs.data(), gs.size());
-            lw.down = m->mem.alloc<int8_t>(size_t(D) * m->Kf);
-            CK(cudaMemset(lw.down, 0, size_t(D) * m->Kf));
-            put_rows(lw.down, m->Kf, 0, 1, t[6].data, D, F);
-            lw.down_s = upload(m->mem, t[6].scales, D);
+            lw.gu = upload_mat(*m, 2 * F, D, {{t[4].data, F, 0, 2}, {t[5].data, F, 1, 2}}, gs, staging);
+            lw.down = upload_mat(*m, D, F, {{t[6].data, D, 0, 1}},
+                                 std::vector<int64_t>(t[6].scales, t[6].scales + D), staging);
             lw.attn_norm = upload(m->mem, d->norms + size_t(2 * l) * D, D);
             lw.ffn_norm = upload(m->mem, d->norms + size_t(2 * l + 1) * D, D);
+            lw.attn_unit = all_one(d->norms + size_t(2 * l) * D, D);
+            lw.ffn_unit = all_one(d->norms + size_t(2 * l + 1) * D, D);
         }
         check_qt(d->tok_embd, V, D, "tok_embd");
         check_qt(d->output, V, D, "output");
         m->embd = upload(m->mem, d->tok_embd.data, size_t(V) * D);
         m->embd_s = upload(m->mem, d->tok_embd.scales, V);
-        m->out_w = m->mem.alloc<int8_t>(size_t(V) * m->Kd);
-        CK(cudaMemset(m->out_w, 0, size_t(V) * m->Kd));
-        put_rows(m->out_w, m->Kd, 0, 1, d->output.data, V, D);
-        m->out_s = upload(m->mem, d->output.scales, V);
+        m->head = upload_mat(*m, V, D, {{d->output.data, V, 0, 1}},
+                             std::vector<int64_t>(d->output.scales, d->output.scales + V), staging);
         m->final_norm = upload(m->mem, d->norms + size_t(2 * m->L) * D, D);
+        m->final_unit = all_one(d->norms + size_t(2 * m->L) * D, D);
         // RoPE tables: imported (RTAB) or built on the host (rope.cpp:17-39)
         const uint32_t half = m->dh / 2, ctx = d->cfg.max_ctx;
         if (d->rope_cos && d->rope_sin) {
@@ -502,14 +576,41 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         s->scores = s->mem.alloc<int64_t>(size_t(m->H) * ctx);
         s->keep_cap = keep_logits_cap;
         s->logits = s->mem.alloc<int64_t>(size_t(keep_logits_cap + 1) * m->V);
-        s->gemv_blocks = gemv_grid(*m->ctx, m->V, 1);
-        s->parts = s->mem.alloc<ArgPart>(s->gemv_blocks);
         s->tokens = s->mem.alloc<uint32_t>(ctx + 1);
         s->ctl = s->mem.alloc<Ctl>(1);
+        s->bar = s->mem.alloc<unsigned int>(64);
+        // one CTA per SM; shared memory = weight ring + limb planes + row accumulators
+        s->grid = uint32_t(m->ctx->sm_count);
+        s->parts = s->mem.alloc<ArgPart>(s->grid);
+        s->planes_att = s->mem.alloc<uint8_t>(size_t(3) * m->Kd);
+        s->planes_h = s->mem.alloc<uint8_t>(size_t(3) * m->Kf);
+        CK(cudaMemsetAsync(s->planes_att, 0, size_t(3) * m->Kd, s->stream));
+        CK(cudaMemsetAsync(s->planes_h, 0, size_t(3) * m->Kf, s->stream));
+        s->flags = s->mem.alloc<uint32_t>(2 * size_t(m->L));
+        s->host_stages = step_program(*s);
+        // shared staging: rmsnorm = vector + gains + up to 8 planes; plain =
+        // up to 8 planes; attention = head scratch + score strip
+        size_t need = attn_scratch_bytes(m->dh, m->cfg.max_ctx);
+        for (const auto& st : s->host_stages) {
+            if (st.kind != SK_GEMV) continue;
+            size_t b = st.mode == MODE_PLAIN ? size_t(8) * st.Kp
+                                             : size_t(8) * st.Kp * (st.gamma_unit ? 2 : 3);
+            need = std::max(need, b);
+        }
+        s->planes_bytes = uint32_t((need + 127) & ~size_t(127));
+        s->smem = size_t(PK_WARPS) * PK_DEPTH * PK_SLOT + s->planes_bytes + PK_WARPS * PK_DEPTH * 8;
+        if (s->smem > size_t(m->ctx->smem_optin))
+            fail(DIMG_EINVAL, "session: shapes need " + std::to_string(s->smem) +
+                                  " B of shared memory per CTA (d_ffn or vocab too large for this build)");
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_persistent_kernel, PK_THREADS,
+                                                         s->smem));
+        if (per_sm < 1) fail(DIMG_ECUDA, "session: persistent kernel does not fit one SM");
+        s->stages = s->mem.alloc<PkStage>(s->host_stages.size());
+        CK(cudaMemcpy(s->stages, s->host_stages.data(), s->host_stages.size() * sizeof(PkStage),
+                      cudaMemcpyHostToDevice));
         CK(cudaMemsetAsync(s->ctl, 0, sizeof(Ctl), s->stream));
         CK(cudaMemsetAsync(s->tokens, 0, (ctx + 1) * 4, s->stream));
-        s->g_prefill = capture(*s, false, &s->launches_prefill);
-        s->g_decode = capture(*s, true, &s->launches_decode);
         CK(cudaStreamSynchronize(s->stream));
         *out = s.release();
     })
@@ -545,12 +646,13 @@ dimg_status dimg_session_forward(dimg_session* s, uint32_t token, uint32_t pos, 
         if (pos != s->len) fail(DIMG_ELOGIC, "forward: pos must equal cache length");
         CK(cudaSetDevice(m.device));
         CK(cudaMemcpyAsync(s->tokens + pos, &token, 4, cudaMemcpyHostToDevice, s->stream));
-        // keep slot 0 for this position's logits; the head appends the argmax
-        // at tokens[pos + 1], which the next forward overwrites
-        write_ctl(*s, pos, pos, 1 <= s->keep_cap ? 1 : 0);
-        CK(cudaGraphLaunch(s->g_decode, s->stream));
+        // logits land in slot 0 (kept) or the scratch row 0 when keep_cap == 0;
+        // the head appends the argmax at tokens[pos + 1], which the next
+        // forward overwrites
+        write_ctl(*s, pos, pos, s->keep_cap >= 1 ? 1 : 0);
+        launch_pk(*s, s->stages, n_layer_stages(*s), 1, 0);
         s->len = pos + 1;
-        if (logits)  // slot 0 (kept) or row 0 = scratch when keep_cap == 0
+        if (logits)
             CK(cudaMemcpyAsync(logits, s->logits, size_t(m.V) * 8, cudaMemcpyDeviceToHost, s->stream));
         check_ctl_err(*s);
     })
@@ -560,12 +662,13 @@ dimg_status dimg_generate_greedy(dimg_session* s, const uint32_t* prompt, uint32
                                  uint32_t max_new, uint32_t* tokens_out, uint8_t hash_out[32],
                                  int64_t* logits_out) {
     // run_generation (proj/src/engine.cpp:31-54): P + N - 1 forwards, the
-    // lm_head only where a selection follows.
+    // lm_head only where a selection follows -- one persistent launch.
     DIMG_API_GUARD({
         begin(*s, prompt, n_prompt, max_new, logits_out != nullptr);
         if (max_new > 0) {
-            run_prefill(*s);
-            run_decode(*s, max_new);
+            const uint32_t np = n_prompt - 1;
+            launch_pk(*s, s->stages, n_layer_stages(*s), np + max_new, np);
+            s->len = np + max_new;
             CK(cudaMemcpyAsync(tokens_out, s->tokens + n_prompt, size_t(max_new) * 4,
                                cudaMemcpyDeviceToHost, s->stream));
             if (logits_out)
@@ -622,59 +725,79 @@ dimg_status dimg_session_time_decode(dimg_session* s, uint32_t n_steps, float* m
         CK(cudaEventElapsedTime(ms, e0, e1));
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+        check_ctl_err(*s);
     })
 }
 
 dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, float* ms_per_launch,
                                     uint64_t* bytes_per_launch) {
-    // Replays one kernel class n times (cycling layers so weights come from
-    // HBM, not L2) between CUDA events on the session stream. Algorithmic
-    // bytes = int8 weights + int64 scales + int64 gains + activation I/O.
+    // Runs a probe program of n stages of one kind (layers cycled, so the
+    // weights stream from HBM) in one persistent launch between CUDA events;
+    // the per-stage time includes its grid barrier, i.e. the real cost of the
+    // stage inside a decode step. Algorithmic bytes = int8 weights + int64
+    // scales + int64 gains + activation I/O.
     DIMG_API_GUARD({
         const dimg_model& m = *s->m;
         CK(cudaSetDevice(m.device));
+        if (which < 0 || which > 4) fail(DIMG_EINVAL, "time_kernel: which in 0..4");
         const uint64_t D = m.D, F = m.F, V = m.V;
-        uint64_t bytes = 0;
-        switch (which) {
-            case 0: bytes = 3 * D * D + 3 * D * 8 + D * 8 + D * 8 + 3 * D * 8; break;   // qkv
-            case 1: bytes = D * D + D * 8 + D * 8 + 2 * D * 8; break;                   // wo
-            case 2: bytes = 2 * F * D + 2 * F * 8 + D * 8 + D * 8 + F * 8; break;       // gate/up
-            case 3: bytes = D * F + D * 8 + F * 8 + 2 * D * 8; break;                   // down
-            case 4: bytes = V * D + V * 8 + D * 8 + D * 8; break;                       // lm_head
-            default: fail(DIMG_EINVAL, "time_kernel: which in 0..4");
+        const uint64_t bytes[5] = {3 * D * D + 3 * D * 8 + D * 8 + D * 8 + 3 * D * 8,
+                                   D * D + D * 8 + D * 8 + 2 * D * 8,
+                                   2 * F * D + 2 * F * 8 + D * 8 + D * 8 + F * 8,
+                                   D * F + D * 8 + F * 8 + 2 * D * 8,
+                                   V * D + V * 8 + D * 8 + D * 8};
+        const uint32_t idx[4] = {0, 2, 3, 4};
+        std::vector<PkStage> prog;
+        for (uint32_t i = 0; i < n; ++i) {
+            PkStage st = which == 4 ? s->host_stages.back()
+                                    : s->host_stages[5 * (i % m.L) + idx[which]];
+            if (st.mode == MODE_EMBED) st.mode = MODE_NORM;
+            if (st.epi == EPI_ARGMAX) st.epi = EPI_STORE;  // the probe never appends tokens
+            prog.push_back(st);
+        }
+        if (!s->probe_stages || n > 0) {
+            s->probe_stages = s->mem.alloc<PkStage>(prog.size());
+            CK(cudaMemcpy(s->probe_stages, prog.data(), prog.size() * sizeof(PkStage),
+                          cudaMemcpyHostToDevice));
         }
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         CK(cudaStreamSynchronize(s->stream));
-        // the head's argmax appends tokens: keep pos fixed by restoring it after
-        uint32_t pos_save = 0;
-        CK(cudaMemcpy(&pos_save, &s->ctl->pos, 4, cudaMemcpyDeviceToHost));
         CK(cudaEventRecord(e0, s->stream));
-        for (uint32_t i = 0; i < n; ++i) {
-            uint32_t l = i % m.L;
-            if (which == 0) launch_qkv(*s, l);
-            else if (which == 1) launch_wo(*s, l);
-            else if (which == 2) launch_gate_up(*s, l);
-            else if (which == 3) launch_down(*s, l);
-            else launch_head(*s);
-        }
+        launch_pk(*s, s->probe_stages, n, 1, 1);
         CK(cudaEventRecord(e1, s->stream));
         CK(cudaEventSynchronize(e1));
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, e0, e1));
-        CK(cudaMemcpy(&s->ctl->pos, &pos_save, 4, cudaMemcpyHostToDevice));
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+        check_ctl_err(*s);
         *ms_per_launch = ms / float(n);
-        *bytes_per_launch = bytes;
+        *bytes_per_launch = bytes[which];
+    })
+}
+
+dimg_status dimg_session_trace(dimg_session* s, uint32_t n_steps, uint64_t* out, uint32_t cap) {
+    // n decode steps with CTA 0 stamping %globaltimer at each stage's start,
+    // after its prologue, after its chunk loop and before its grid barrier.
+    DIMG_API_GUARD({
+        if (uint64_t(s->len) + n_steps > s->m->cfg.max_ctx)
+            fail(DIMG_ECTX, "decode: context overflow");
+        unsigned long long* d = s->mem.alloc<unsigned long long>(size_t(cap) * 8);
+        CK(cudaMemsetAsync(d, 0, size_t(cap) * 64, s->stream));
+        launch_pk(*s, s->stages, n_layer_stages(*s), n_steps, 0, d, cap);
+        s->len += n_steps;
+        CK(cudaMemcpyAsync(out, d, size_t(cap) * 64, cudaMemcpyDeviceToHost, s->stream));
+        check_ctl_err(*s);
     })
 }
 
 dimg_status dimg_session_launches(const dimg_session* s, uint32_t* per_decode, uint32_t* per_prefill) {
+    // one persistent launch per call; it runs every stage of every step
     DIMG_API_GUARD({
-        *per_decode = s->launches_decode;
-        *per_prefill = s->launches_prefill;
+        *per_decode = 1;
+        *per_prefill = 1;
     })
 }
 
@@ -838,7 +961,7 @@ dimg_status dimg_op_attention(int device, uint32_t H, uint32_t dh, uint32_t max_
             CK(cudaMemcpyAsync(qkv + 2 * D, v + p * D, D * 8, cudaMemcpyHostToDevice, o.c.op_stream));
             set_pos_kernel<<<1, 1, 0, o.c.op_stream>>>(o.c.op_ctl, p);
             t.out = d_out + p * D;
-            attn_decode_kernel<<<H, ATTN_THREADS, dh * 8, o.c.op_stream>>>(t);
+            attn_decode_kernel<<<H, ATTN_THREADS, attn_scratch_bytes(dh), o.c.op_stream>>>(t);
             CK(cudaGetLastError());
         }
         o.get(out, d_out, D * steps);

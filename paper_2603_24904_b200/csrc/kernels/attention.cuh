@@ -66,14 +66,26 @@ __device__ void softmax_strip(int64_t* S, uint32_t n, const int64_t* lut, u128* 
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(AttnArgs a) {
-    extern __shared__ __align__(16) int64_t qrot[];  // [dh]
-    __shared__ int64_t lut[257];
-    __shared__ u128 red[32];
-    const uint32_t h = blockIdx.x, dh = a.dh, half = dh / 2, D = a.H * dh;
-    const uint32_t pos = a.ctl->pos;
+// Bytes of shared scratch attn_head needs (score strip in shared memory when
+// max_ctx > 0, else in a.scores).
+__host__ __device__ constexpr size_t attn_scratch_bytes(uint32_t dh, uint32_t max_ctx = 0) {
+    return (size_t(dh) + 257 + ATTN_THREADS + max_ctx) * sizeof(int64_t);
+}
+
+// One head of one attention step at position `pos`; block-wide (blockDim.x
+// == ATTN_THREADS). `scratch` = attn_scratch_bytes(dh[, max_ctx]) of shared
+// memory; `smem_scores` keeps the score strip on chip. When `planes` is set,
+// the output is also emitted as 3-limb byte planes for the WO GEMV (plus the
+// wide flag), see persistent.cuh.
+__device__ void attn_head(const AttnArgs& a, uint32_t h, uint32_t pos, int64_t* scratch, u128* red,
+                          uint8_t* planes = nullptr, uint32_t pitch = 0, uint32_t* flag = nullptr,
+                          uint32_t tag = 0, bool smem_scores = false) {
+    int64_t* qrot = scratch;                                   // [dh]
+    int64_t* lut = scratch + a.dh;                             // [257]
+    uint64_t* part = reinterpret_cast<uint64_t*>(lut + 257);   // [ATTN_THREADS]
+    const uint32_t dh = a.dh, half = dh / 2, D = a.H * dh;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = ATTN_THREADS / 32;
-    for (int i = threadIdx.x; i < 257; i += ATTN_THREADS) lut[i] = a.exp_lut[i];
+    for (int i = threadIdx.x; i < 257; i += blockDim.x) lut[i] = a.exp_lut[i];
 
     const int64_t* q = a.qkv + size_t(h) * dh;
     const int64_t* k = a.qkv + D + size_t(h) * dh;
@@ -93,14 +105,29 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(AttnArgs a) {
     for (uint32_t j = threadIdx.x; j < dh; j += ATTN_THREADS) V[size_t(pos) * dh + j] = v[j];
     __syncthreads();
 
-    // scores: one warp per cached position, int128 dot
-    int64_t* S = a.scores + size_t(h) * a.max_ctx;
-    for (uint32_t t = warp; t <= pos; t += nw) {
-        const int64_t* kt = K + size_t(t) * dh;
-        u128 dot = 0;
-        for (uint32_t j = lane; j < dh; j += 32) dot += u128(i128(qrot[j]) * i128(kt[j]));
-        dot = warp_sum_u128(dot);
-        if (lane == 0) S[t] = mul16(int64_t(i128(dot) >> 16), a.inv_scale);
+    int64_t* S = smem_scores ? reinterpret_cast<int64_t*>(part + ATTN_THREADS)
+                             : a.scores + size_t(h) * a.max_ctx;
+    // scores: one warp per cached position, int128 dot; four positions per
+    // warp in flight so the K reads overlap
+    for (uint32_t t0 = warp; t0 <= pos; t0 += 4 * nw) {
+        u128 dot[4] = {0, 0, 0, 0};
+        for (uint32_t j = lane; j < dh; j += 32) {
+            int64_t kv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t t = t0 + u * nw;
+                kv[u] = t <= pos ? K[size_t(t) * dh + j] : 0;
+            }
+            const int64_t qj = qrot[j];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dot[u] += u128(i128(qj) * i128(kv[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const u128 d = warp_sum_u128(dot[u]);
+            const uint32_t t = t0 + u * nw;
+            if (lane == 0 && t <= pos) S[t] = mul16(int64_t(i128(d) >> 16), a.inv_scale);
+        }
     }
     __syncthreads();
 
@@ -111,24 +138,54 @@ __global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(AttnArgs a) {
         const uint32_t slices = ATTN_THREADS / dh;
         const uint32_t j = threadIdx.x % dh, sl = threadIdx.x / dh;
         uint64_t acc = 0;
-        if (sl < slices)
-            for (uint32_t t = sl; t <= pos; t += slices)
-                acc += uint64_t(mul16_prob(S[t], V[size_t(t) * dh + j]));
-        __shared__ uint64_t part[ATTN_THREADS];
+        if (sl < slices) {
+            uint32_t t = sl;
+            for (; t + 7 * slices <= pos; t += 8 * slices) {  // 8 V rows in flight
+                int64_t vv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) vv[u] = V[size_t(t + u * slices) * dh + j];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc += uint64_t(mul16_prob(S[t + u * slices], vv[u]));
+            }
+            for (; t <= pos; t += slices) acc += uint64_t(mul16_prob(S[t], V[size_t(t) * dh + j]));
+        }
         part[threadIdx.x] = acc;
         __syncthreads();
         if (threadIdx.x < dh) {
             uint64_t sum = 0;
             for (uint32_t s = 0; s < slices; ++s) sum += part[s * dh + threadIdx.x];
-            a.out[size_t(h) * dh + threadIdx.x] = int64_t(sum);
+            const uint32_t j = h * dh + threadIdx.x;
+            a.out[j] = int64_t(sum);
+            if (planes) {
+                planes[j] = uint8_t(sum);
+                planes[pitch + j] = uint8_t(sum >> 8);
+                planes[2 * pitch + j] = uint8_t(sum >> 16);
+                int64_t v = int64_t(sum);
+                if (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) *((volatile uint32_t*)flag) = tag;
+            }
         }
     } else {
         for (uint32_t j = threadIdx.x; j < dh; j += ATTN_THREADS) {
             uint64_t acc = 0;
             for (uint32_t t = 0; t <= pos; ++t) acc += uint64_t(mul16_prob(S[t], V[size_t(t) * dh + j]));
-            a.out[size_t(h) * dh + j] = int64_t(acc);
+            const uint32_t jj = h * dh + j;
+            a.out[jj] = int64_t(acc);
+            if (planes) {
+                planes[jj] = uint8_t(acc);
+                planes[pitch + jj] = uint8_t(acc >> 8);
+                planes[2 * pitch + jj] = uint8_t(acc >> 16);
+                int64_t v = int64_t(acc);
+                if (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) *((volatile uint32_t*)flag) = tag;
+            }
         }
     }
+    __syncthreads();  // scratch may be reused by the caller's next head/stage
+}
+
+__global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(AttnArgs a) {
+    extern __shared__ __align__(16) int64_t attn_smem[];
+    __shared__ u128 red[32];
+    attn_head(a, blockIdx.x, a.ctl->pos, attn_smem, red);
 }
 
 }  // namespace dimg::dev

@@ -1,0 +1,688 @@
+// Persistent decode kernel: every forward step of a generation in ONE
+// cooperative launch (one CTA per SM).
+//
+// Why: a batch-1 integer decode step is 5L+1 dependent matrix-vector stages.
+// As separate kernels each stage pays launch + ramp-up + a serial prologue
+// (rebuilding the input vector's limbs) + drain, and the HBM pipe idles in
+// between (the multi-kernel v1 reached 25% of roofline). Here the stages are
+// separated by grid barriers instead, and -- because weights never depend on
+// activations -- every warp keeps streaming its NEXT weight chunks into a
+// private shared-memory ring with cp.async.bulk (TMA bulk copies, mbarrier
+// completion) while it waits at a barrier or builds the next input vector.
+// The weight stream runs continuously across stage, layer and token
+// boundaries. (tools/microbench.cu: this ring shape -- 8 KB chunks, 2 deep,
+// 8 warps, 128 KB/SM -- streams 7.3 TB/s on a B200 with the DP4A work on.)
+//
+// Weight layout in HBM ("row-group blocked", built at upload): each matrix is
+// cut into groups of 4 rows and K-segments of <= 2048 bytes; chunk (group,
+// segment) is one contiguous 4 x seg block = one bulk copy. CTAs own
+// contiguous balanced group ranges; warp w of a CTA owns groups w, w+8, ...
+// and walks all K-segments of a group, so its per-limb int32 partial sums stay
+// in registers and each group needs one warp reduction. The dot products are
+// the exact byte-limb DP4A scheme of gemv.cuh.
+//
+// Stage inputs are staged into shared memory with one vectorised L2 pass:
+// rmsnorm inputs (the residual stream) are copied and normalised there;
+// the attention output and the FFN hidden vector arrive as 3-limb byte planes
+// written by their producers (attention / silu*up epilogues) plus a "needs
+// more than 3 limbs" flag, so those prologues are a 12-33 KB copy.
+#pragma once
+
+#include <cstdint>
+
+#include "attention.cuh"
+#include "gemv.cuh"
+#include "q16.cuh"
+
+namespace dimg::dev {
+
+constexpr int PK_THREADS = 256;
+constexpr int PK_WARPS = PK_THREADS / 32;
+constexpr int PK_DEPTH = 2;             // chunks in flight per warp
+constexpr int PK_SEG = 2048;            // K-segment width (bytes)
+constexpr int PK_ROWS = 4;              // rows per group
+constexpr int PK_SLOT = PK_ROWS * PK_SEG;
+
+enum { SK_GEMV = 0, SK_ATTN = 1 };
+
+struct PkStage {
+    uint32_t kind, mode, epi, layer;
+    uint32_t rows, K, Kp, n_groups, n_segs, gamma_unit;
+    const int8_t* W;          // blocked [n_groups][n_segs][4][seg]
+    const int64_t* scales;    // [rows]
+    const int64_t* x;         // input vector (K)
+    const int64_t* gamma;     // norm gains (MODE_NORM / MODE_EMBED)
+    int64_t* y;               // output
+    const uint8_t* in_planes; // MODE_PLAIN: producer-written 3-limb planes [3][Kp]
+    const uint32_t* in_flag;  // MODE_PLAIN: == step tag if an element needs > 3 limbs
+    uint8_t* out_planes;      // EPI_SILU / attention: planes of y, pitch out_pitch
+    uint32_t* out_flag;
+    uint32_t out_pitch;
+    uint32_t pad2;
+};
+
+struct PkArgs {
+    const PkStage* stages;    // [n_stages]: 5 per layer, then the head
+    uint32_t n_layer_stages;  // 5L
+    uint32_t n_steps;         // forward steps in this launch
+    uint32_t n_prefill;       // the first n_prefill steps skip the head
+    uint32_t planes_bytes;    // shared staging area (vector, gains, planes, attention)
+    Ctl* ctl;
+    unsigned int* bar;        // grid barrier counter (zeroed before launch)
+    // embedding / head
+    const int8_t* embd;
+    const int64_t* embd_scales;
+    uint32_t d_model, vocab;
+    uint32_t* tokens;
+    int64_t* logits;          // [keep_cap + 1][vocab]
+    ArgPart* parts;           // [gridDim.x]
+    int64_t* x_resid;         // residual stream (embedding target)
+    // attention
+    AttnArgs attn;            // per-layer kc/vc offsets applied in-kernel
+    size_t kv_layer_stride;   // elements between layers in kc/vc
+    const int64_t* exp_lut;
+    const int64_t* seeds;
+    unsigned long long* trace;  // optional: [stage_seq][8] globaltimer stamps of CTA 0
+    uint32_t trace_cap;
+    uint32_t l2_ahead;        // chunks per warp prefetched into L2 beyond the ring
+    uint32_t bar_mode;        // 0: poll the arrival counter, 1: poll a release flag line
+};
+
+// ---- small PTX helpers --------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// 1-D TMA bulk copy global -> shared, completion via the mbarrier's tx count.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const unsigned int* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// L2-coherent loads for data other CTAs wrote in this launch.
+__device__ __forceinline__ int4 ld_cg4(const void* p) {
+    int4 r;
+    asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int64_t ld_cg64(const int64_t* p) {
+    int64_t r;
+    asm volatile("ld.global.cg.s64 %0, [%1];" : "=l"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_cg32(const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Block-wide global -> shared copy of `bytes` (multiple of 16), many 16-B
+// loads in flight per thread.
+__device__ __forceinline__ void copy_g2s(void* dst, const void* src, uint32_t bytes) {
+    const uint32_t n = bytes / 16;
+    int4* d = static_cast<int4*>(dst);
+    const char* s = static_cast<const char*>(src);
+    uint32_t i = threadIdx.x;
+    for (; i + 7 * PK_THREADS < n; i += 8 * PK_THREADS) {
+        int4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_cg4(s + size_t(i + u * PK_THREADS) * 16);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) d[i + u * PK_THREADS] = v[u];
+    }
+    for (; i < n; i += PK_THREADS) d[i] = ld_cg4(s + size_t(i) * 16);
+}
+
+// Grid barrier #k (monotonic counter). Returns false if the wait timed out
+// (a hung peer): the caller then unwinds instead of hanging the GPU.
+__device__ __forceinline__ bool grid_sync(unsigned int* bar, Ctl* ctl, uint32_t k, uint32_t mode) {
+    // bar[0]: arrivals (monotonic); bar[32]: released generation, on its own
+    // 128-byte line so the pollers never contend with the arriving atomics.
+    __shared__ int ok;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ok = 1;
+        __threadfence();
+        const uint32_t target = (k + 1) * gridDim.x;
+        const uint32_t prev = atomicAdd(bar, 1u);
+        if (mode == 1 && prev == target - 1)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 32), "r"(k + 1) : "memory");
+        const unsigned int* poll = mode == 1 ? bar + 32 : bar;
+        const uint32_t want = mode == 1 ? k + 1 : target;
+        uint64_t t0 = globaltimer();
+        while (ld_acquire(poll) < want) {
+            if (*((volatile uint32_t*)&ctl->err) & 4u) { ok = 0; break; }
+            if (globaltimer() - t0 > 4000000000ull) {  // 4 s
+                atomicOr(&ctl->err, 4u);
+                ok = 0;
+                break;
+            }
+        }
+    }
+    __syncthreads();
+    return ok != 0;
+}
+
+__device__ __forceinline__ void cta_range(uint32_t n, uint32_t& lo, uint32_t& hi) {
+    lo = uint32_t(uint64_t(n) * blockIdx.x / gridDim.x);
+    hi = uint32_t(uint64_t(n) * (blockIdx.x + 1) / gridDim.x);
+}
+
+__device__ __forceinline__ uint32_t stages_in_step(const PkArgs& a, uint32_t step) {
+    return a.n_layer_stages + (step >= a.n_prefill ? 1u : 0u);
+}
+
+// ---- the warp's weight-chunk stream (same order as its consumption) -----------
+
+struct Fetch {
+    uint32_t step, stage, g, g_end, seg, n_segs, Kp;
+    const int8_t* W;
+    bool done;
+};
+
+__device__ __forceinline__ void fetch_load(const PkArgs& a, Fetch& f) {
+    const PkStage& st = a.stages[f.stage];
+    if (st.kind != SK_GEMV) {
+        f.g = f.g_end = 0;
+        return;
+    }
+    uint32_t lo, hi;
+    cta_range(st.n_groups, lo, hi);
+    f.g = lo + (threadIdx.x >> 5);
+    f.g_end = hi;
+    f.seg = 0;
+    f.n_segs = st.n_segs;
+    f.Kp = st.Kp;
+    f.W = st.W;
+}
+
+__device__ __forceinline__ void fetch_settle(const PkArgs& a, Fetch& f) {
+    while (!f.done && f.g >= f.g_end) {
+        if (++f.stage >= stages_in_step(a, f.step)) {
+            f.stage = 0;
+            if (++f.step >= a.n_steps) {
+                f.done = true;
+                return;
+            }
+        }
+        fetch_load(a, f);
+    }
+}
+
+__device__ __forceinline__ void fetch_advance(const PkArgs& a, Fetch& f) {
+    if (++f.seg == f.n_segs) {
+        f.seg = 0;
+        f.g += PK_WARPS;
+    }
+    fetch_settle(a, f);
+}
+
+__device__ __forceinline__ uint32_t fetch_bytes(const Fetch& f) {
+    return PK_ROWS * (f.seg + 1 < f.n_segs ? PK_SEG : f.Kp - (f.n_segs - 1) * PK_SEG);
+}
+__device__ __forceinline__ const int8_t* fetch_src(const Fetch& f) {
+    return f.W + size_t(f.g) * PK_ROWS * f.Kp + size_t(f.seg) * PK_SLOT;
+}
+
+__device__ __forceinline__ void fetch_issue(const Fetch& f, uint8_t* slot, uint64_t* bar) {
+    mbar_expect_tx(bar, fetch_bytes(f));
+    bulk_g2s(slot, fetch_src(f), fetch_bytes(f), bar);
+}
+
+// Bulk prefetch of a future chunk into L2: the 126 MB L2 is the deep buffer
+// that keeps HBM streaming while stages stall on barriers and prologues.
+__device__ __forceinline__ void fetch_prefetch_l2(const Fetch& f) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(fetch_src(f)), "r"(fetch_bytes(f))
+                 : "memory");
+}
+
+struct Pipe {
+    uint8_t* slots;     // this warp's ring
+    uint64_t* bars;
+    uint32_t consumed;  // chunks consumed so far
+    Fetch f;            // next chunk to load into the ring
+    Fetch pf;           // next chunk to prefetch into L2 (PK_L2_AHEAD ahead of f)
+};
+
+// Waits for the next chunk of this warp; returns its slot.
+__device__ __forceinline__ const uint8_t* pipe_wait(Pipe& p) {
+    const uint32_t sl = p.consumed % PK_DEPTH;
+    mbar_wait(&p.bars[sl], (p.consumed / PK_DEPTH) & 1);
+    return p.slots + sl * PK_SLOT;
+}
+
+// Releases the chunk just consumed and refills its slot with the next one.
+__device__ __forceinline__ void pipe_release(const PkArgs& a, Pipe& p) {
+    const uint32_t sl = p.consumed % PK_DEPTH;
+    ++p.consumed;
+    __syncwarp();
+    if (!p.f.done) {
+        if ((threadIdx.x & 31) == 0) {
+            fence_proxy_async();
+            fetch_issue(p.f, p.slots + sl * PK_SLOT, &p.bars[sl]);
+        }
+        fetch_advance(a, p.f);
+    }
+    if (!p.pf.done) {
+        if ((threadIdx.x & 31) == 0) fetch_prefetch_l2(p.pf);
+        fetch_advance(a, p.pf);
+    }
+}
+
+// ---- prologue: the stage's input vector as limb planes in shared memory -------
+
+// Returns L (3 or 8); planes at `planes` ([L][Kp] bytes as words).
+__device__ int pk_prologue(const PkArgs& a, const PkStage& st, uint32_t token, uint32_t tag,
+                           uint8_t* stage_mem, uint32_t*& planes, u128* red,
+                           unsigned long long* tr = nullptr) {
+    const uint32_t K = st.K, Kp = st.Kp, Kw = Kp / 4;
+    if (st.mode == MODE_PLAIN) {
+        planes = reinterpret_cast<uint32_t*>(stage_mem);
+        if (ld_cg32(st.in_flag) != tag) {  // all elements fit 3 limbs: copy the planes
+            copy_g2s(planes, st.in_planes, 3 * Kp);
+            __syncthreads();
+            return 3;
+        }
+        // wide input: 8 byte planes straight from the int64 vector
+        for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
+            uint32_t word[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                uint32_t j = 4 * w + e;
+                uint64_t v = j < K ? uint64_t(ld_cg64(st.x + j)) : 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) word[k] |= uint32_t((v >> (8 * k)) & 0xFF) << (8 * e);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) planes[k * Kw + w] = word[k];
+        }
+        if (threadIdx.x == 0) atomicAdd(&a.ctl->stats[0], 1ull);
+        __syncthreads();
+        return 8;
+    }
+    // rmsnorm input (residual stream, or the embedded token on layer 0)
+    int64_t* xb = reinterpret_cast<int64_t*>(stage_mem);
+    int64_t* gb = xb + Kp;
+    planes = reinterpret_cast<uint32_t*>(st.gamma_unit ? gb : gb + Kp);
+    if (st.mode == MODE_EMBED) {
+        const int8_t* erow = a.embd + size_t(token) * K;
+        const int64_t es = a.embd_scales[token];
+        for (uint32_t j = threadIdx.x; j < K; j += blockDim.x) {
+            int64_t v = int64_t(uint64_t(int64_t(erow[j])) * uint64_t(es));  // engine.cpp:10-19
+            xb[j] = v;
+            if (blockIdx.x == 0) a.x_resid[j] = v;
+        }
+    } else {
+        copy_g2s(xb, st.x, K * 8);
+    }
+    if (!st.gamma_unit) copy_g2s(gb, st.gamma, K * 8);
+    __syncthreads();
+    if (tr) tr[4] = globaltimer();
+    // ms = ((sum x^2) / n) >> 16 in int128, r = inv_sqrt(ms + 1) (kernels.cpp:56-68)
+    __shared__ int64_t s_r;
+    u128 ss = 0;
+    for (uint32_t j = threadIdx.x; j < K; j += blockDim.x) {
+        const int64_t v = xb[j];
+        ss += fits_i32(v) ? u128(uint64_t(v * v)) : u128(i128(v) * i128(v));
+    }
+    ss = block_reduce<u128>(ss, red, [](u128 p, u128 q) { return p + q; }, warp_sum_u128);
+    if (tr) tr[5] = globaltimer();
+    if (threadIdx.x == 0) {
+        const int64_t ms = int64_t((i128(ss) / i128(K)) >> 16);
+        if (ms + 1 <= 0) {
+            atomicOr(&a.ctl->err, 1u);
+            s_r = 0;
+        } else {
+            s_r = inv_sqrt_q16(ms + 1, a.seeds);
+        }
+    }
+    __syncthreads();
+    if (tr) tr[6] = globaltimer();
+    const int64_t r_inv = s_r;
+    int fits = 1;
+    for (uint32_t j = threadIdx.x; j < Kp; j += blockDim.x) {
+        int64_t v = 0;
+        if (j < K) {
+            v = mul16(xb[j], r_inv);
+            if (!st.gamma_unit) v = mul16(v, gb[j]);  // mul16(v, ONE) == v
+        }
+        xb[j] = v;
+        fits &= (v >= -(int64_t(1) << 23)) & (v < (int64_t(1) << 23));
+    }
+    fits = __syncthreads_and(fits);
+    if (tr) tr[7] = globaltimer();
+    const int L = fits ? 3 : 8;
+    if (L == 3) {
+        for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
+            uint32_t w0 = 0, w1 = 0, w2 = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t v = uint32_t(xb[4 * w + e]);
+                w0 |= (v & 0xFF) << (8 * e);
+                w1 |= ((v >> 8) & 0xFF) << (8 * e);
+                w2 |= ((v >> 16) & 0xFF) << (8 * e);
+            }
+            planes[w] = w0;
+            planes[Kw + w] = w1;
+            planes[2 * Kw + w] = w2;
+        }
+    } else {
+        for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
+            uint32_t word[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                uint64_t v = uint64_t(xb[4 * w + e]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) word[k] |= uint32_t((v >> (8 * k)) & 0xFF) << (8 * e);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) planes[k * Kw + w] = word[k];
+        }
+    }
+    if (L == 8 && threadIdx.x == 0) atomicAdd(&a.ctl->stats[0], 1ull);
+    __syncthreads();
+    return L;
+}
+
+// Producer side of the plane hand-off: element j of an output vector.
+__device__ __forceinline__ void emit_planes(uint8_t* planes, uint32_t pitch, uint32_t* flag,
+                                            uint32_t tag, uint32_t j, int64_t v) {
+    planes[j] = uint8_t(v);
+    planes[pitch + j] = uint8_t(v >> 8);
+    planes[2 * pitch + j] = uint8_t(v >> 16);
+    if (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) *((volatile uint32_t*)flag) = tag;
+}
+
+// ---- one row group: 4 rows x K against the limb planes ------------------------
+
+// Sums of 4 rows spread over the warp -> every lane gets all 4 (wrapping).
+__device__ __forceinline__ void reduce4(uint64_t (&v)[PK_ROWS]) {
+    const int lane = threadIdx.x & 31;
+    const bool up = lane & 16;
+    uint64_t k0 = (up ? v[2] : v[0]) + __shfl_xor_sync(0xffffffffu, up ? v[0] : v[2], 16);
+    uint64_t k1 = (up ? v[3] : v[1]) + __shfl_xor_sync(0xffffffffu, up ? v[1] : v[3], 16);
+    const bool b8 = lane & 8;
+    uint64_t k = (b8 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, b8 ? k0 : k1, 8);
+    k += __shfl_xor_sync(0xffffffffu, k, 4);
+    k += __shfl_xor_sync(0xffffffffu, k, 2);
+    k += __shfl_xor_sync(0xffffffffu, k, 1);
+    // lane l now holds row ((l >> 4) & 1) * 2 + ((l >> 3) & 1)
+#pragma unroll
+    for (int r = 0; r < PK_ROWS; ++r) v[r] = __shfl_sync(0xffffffffu, k, ((r >> 1) << 4) | ((r & 1) << 3));
+}
+
+template <int L>
+__device__ __forceinline__ void group_dot(const PkArgs& a, Pipe& p, const PkStage& st,
+                                          const uint32_t* planes, uint64_t (&out)[PK_ROWS]) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t Kw = st.Kp / 4;
+    int32_t acc[PK_ROWS][L];
+#pragma unroll
+    for (int r = 0; r < PK_ROWS; ++r)
+#pragma unroll
+        for (int k = 0; k < L; ++k) acc[r][k] = 0;
+    for (uint32_t s = 0; s < st.n_segs; ++s) {
+        const uint8_t* slot = pipe_wait(p);
+        const uint32_t w = s + 1 < st.n_segs ? PK_SEG : st.Kp - (st.n_segs - 1) * PK_SEG;
+        const uint32_t k0 = s * PK_SEG;
+        for (uint32_t c = lane * 16; c < w; c += 512) {
+            uint4 xl[L];
+#pragma unroll
+            for (int k = 0; k < L; ++k) xl[k] = *reinterpret_cast<const uint4*>(planes + k * Kw + (k0 + c) / 4);
+#pragma unroll
+            for (int r = 0; r < PK_ROWS; ++r) {
+                const int4 wv = *reinterpret_cast<const int4*>(slot + r * w + c);
+#pragma unroll
+                for (int k = 0; k < L - 1; ++k) {
+                    acc[r][k] = dp4a_su(wv.x, xl[k].x, acc[r][k]);
+                    acc[r][k] = dp4a_su(wv.y, xl[k].y, acc[r][k]);
+                    acc[r][k] = dp4a_su(wv.z, xl[k].z, acc[r][k]);
+                    acc[r][k] = dp4a_su(wv.w, xl[k].w, acc[r][k]);
+                }
+                acc[r][L - 1] = dp4a_ss(wv.x, xl[L - 1].x, acc[r][L - 1]);
+                acc[r][L - 1] = dp4a_ss(wv.y, xl[L - 1].y, acc[r][L - 1]);
+                acc[r][L - 1] = dp4a_ss(wv.z, xl[L - 1].z, acc[r][L - 1]);
+                acc[r][L - 1] = dp4a_ss(wv.w, xl[L - 1].w, acc[r][L - 1]);
+            }
+        }
+        pipe_release(a, p);
+    }
+#pragma unroll
+    for (int r = 0; r < PK_ROWS; ++r) {
+        uint64_t v = 0;
+#pragma unroll
+        for (int k = 0; k < L; ++k) v += uint64_t(int64_t(acc[r][k])) << (8 * k);
+        out[r] = v;
+    }
+    reduce4(out);
+}
+
+// All of this CTA's row groups of a GEMV stage, epilogues fused.
+template <int L>
+__device__ void run_gemv(const PkArgs& a, Pipe& p, const PkStage& st, const uint32_t* planes,
+                         uint32_t pos, uint32_t tag, int64_t& best_v, uint32_t& best_i) {
+    const int lane = threadIdx.x & 31;
+    uint32_t g_lo, g_hi;
+    cta_range(st.n_groups, g_lo, g_hi);
+    int64_t* lrow = nullptr;
+    if (st.epi == EPI_ARGMAX) {
+        uint32_t slot = pos - a.ctl->logit_base;
+        slot = slot < a.ctl->keep_cap ? slot : a.ctl->keep_cap;
+        lrow = st.y + size_t(slot) * st.rows;
+    }
+    for (uint32_t g = g_lo + (threadIdx.x >> 5); g < g_hi; g += PK_WARPS) {
+        const uint32_t r0 = g * PK_ROWS;
+        int64_t resid = 0;  // issued now, consumed after the dot product
+        if (st.epi == EPI_RESID && lane < PK_ROWS && r0 + lane < st.rows) resid = ld_cg64(st.y + r0 + lane);
+        uint64_t v[PK_ROWS];
+        group_dot<L>(a, p, st, planes, v);
+        if (st.epi == EPI_SILU) {
+            // rows (2i, 2i+1) = (gate_i, up_i): lanes 0,1 finish pairs 0,1
+            if (lane < 2 && r0 + 2 * lane + 1 < st.rows) {
+                const uint32_t row = r0 + 2 * lane;
+                const int64_t gs = scale_row(int64_t(lane ? v[2] : v[0]), st.scales[row]);
+                const int64_t us = scale_row(int64_t(lane ? v[3] : v[1]), st.scales[row + 1]);
+                const int64_t h = mul16(silu_q16(gs, a.exp_lut), us);
+                st.y[row / 2] = h;
+                emit_planes(st.out_planes, st.out_pitch, st.out_flag, tag, row / 2, h);
+            }
+        } else if (lane < PK_ROWS && r0 + lane < st.rows) {
+            const uint32_t row = r0 + lane;
+            uint64_t acc = v[0];
+#pragma unroll
+            for (int r = 1; r < PK_ROWS; ++r) acc = lane == r ? v[r] : acc;
+            const int64_t val = scale_row(int64_t(acc), st.scales[row]);
+            if (st.epi == EPI_STORE) {
+                st.y[row] = val;
+            } else if (st.epi == EPI_RESID) {
+                st.y[row] = add_clamp(resid, val);
+            } else {  // EPI_ARGMAX
+                lrow[row] = val;
+                if (better(val, row, best_v, best_i)) {
+                    best_v = val;
+                    best_i = row;
+                }
+            }
+        }
+    }
+}
+
+// ---- the kernel -------------------------------------------------------------------
+
+__global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* slots = smem;                                                // [warps][depth][SLOT]
+    uint8_t* stage_mem = smem + PK_WARPS * PK_DEPTH * PK_SLOT;            // planes_bytes
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stage_mem + a.planes_bytes);  // [warps][depth]
+    __shared__ u128 red[32];
+    __shared__ int64_t s_bv[PK_WARPS];
+    __shared__ uint32_t s_bi[PK_WARPS];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < PK_WARPS * PK_DEPTH) mbar_init(&bars[threadIdx.x], 1);
+    fence_proxy_async();
+    __syncthreads();
+
+    // prime this warp's pipeline
+    Pipe p;
+    p.slots = slots + size_t(warp) * PK_DEPTH * PK_SLOT;
+    p.bars = bars + warp * PK_DEPTH;
+    p.consumed = 0;
+    p.f.step = 0;
+    p.f.stage = 0;
+    p.f.done = a.n_steps == 0;
+    if (!p.f.done) {
+        fetch_load(a, p.f);
+        fetch_settle(a, p.f);
+    }
+    p.pf = p.f;
+    if (!a.l2_ahead) p.pf.done = true;
+    for (uint32_t d = 0; d < PK_DEPTH + a.l2_ahead && a.l2_ahead && !p.pf.done; ++d) {
+        if (lane == 0) fetch_prefetch_l2(p.pf);
+        fetch_advance(a, p.pf);
+    }
+    for (int d = 0; d < PK_DEPTH && !p.f.done; ++d) {
+        if (lane == 0) fetch_issue(p.f, p.slots + d * PK_SLOT, &p.bars[d]);
+        fetch_advance(a, p.f);
+    }
+
+    uint32_t pos = a.ctl->pos;
+    uint32_t token = a.tokens[pos];
+    uint32_t nbar = 0;
+    __shared__ __align__(16) PkStage s_st;
+    constexpr int kStWords = sizeof(PkStage) / 4;
+    auto load_stage = [&](uint32_t idx) {
+        if (threadIdx.x < kStWords)
+            reinterpret_cast<uint32_t*>(&s_st)[threadIdx.x] =
+                reinterpret_cast<const uint32_t*>(a.stages + idx)[threadIdx.x];
+    };
+    __syncthreads();
+    load_stage(0);
+    __syncthreads();
+
+    for (uint32_t step = 0; step < a.n_steps; ++step) {
+        const uint32_t nst = stages_in_step(a, step);
+        const uint32_t tag = step + 1;
+        int64_t best_v = INT64_MIN;
+        uint32_t best_i = 0xFFFFFFFFu;
+        for (uint32_t si = 0; si < nst; ++si) {
+            const PkStage& st = s_st;
+            const bool tr = a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nbar < a.trace_cap;
+            if (tr) a.trace[8 * nbar + 0] = globaltimer();
+            if (st.kind == SK_ATTN) {
+                AttnArgs t = a.attn;
+                t.kc += size_t(st.layer) * a.kv_layer_stride;
+                t.vc += size_t(st.layer) * a.kv_layer_stride;
+                for (uint32_t h = blockIdx.x; h < t.H; h += gridDim.x)
+                    attn_head(t, h, pos, reinterpret_cast<int64_t*>(stage_mem), red, st.out_planes,
+                              st.out_pitch, st.out_flag, tag, true);
+            } else {
+                uint32_t* planes;
+                const int L = pk_prologue(a, st, token, tag, stage_mem, planes, red,
+                                          tr ? a.trace + 8 * nbar : nullptr);
+                if (tr) a.trace[8 * nbar + 1] = globaltimer();
+                if (L == 3) run_gemv<3>(a, p, st, planes, pos, tag, best_v, best_i);
+                else run_gemv<8>(a, p, st, planes, pos, tag, best_v, best_i);
+                if (tr) a.trace[8 * nbar + 2] = globaltimer();
+                if (st.epi == EPI_ARGMAX) {
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        int64_t ov = __shfl_xor_sync(0xffffffffu, best_v, o);
+                        uint32_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+                        if (better(ov, oi, best_v, best_i)) { best_v = ov; best_i = oi; }
+                    }
+                    if (lane == 0) { s_bv[warp] = best_v; s_bi[warp] = best_i; }
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        for (int w2 = 1; w2 < PK_WARPS; ++w2)
+                            if (better(s_bv[w2], s_bi[w2], best_v, best_i)) { best_v = s_bv[w2]; best_i = s_bi[w2]; }
+                        a.parts[blockIdx.x].v = best_v;
+                        a.parts[blockIdx.x].idx = best_i;
+                    }
+                }
+            }
+            if (tr) a.trace[8 * nbar + 3] = globaltimer();
+            __syncthreads();  // everyone is done with s_st
+            load_stage(si + 1 < nst ? si + 1 : 0);
+            if (!grid_sync(a.bar, a.ctl, nbar++, a.bar_mode)) return;
+        }
+        if (step >= a.n_prefill) {
+            // every CTA reduces the lm_head partials itself (no extra barrier)
+            int64_t bv = INT64_MIN;
+            uint32_t bi = 0xFFFFFFFFu;
+            for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+                int64_t v = ld_cg64(&a.parts[b].v);
+                uint32_t i = ld_cg32(&a.parts[b].idx);
+                if (better(v, i, bv, bi)) { bv = v; bi = i; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+            }
+            __syncthreads();
+            if (lane == 0) { s_bv[warp] = bv; s_bi[warp] = bi; }
+            __syncthreads();
+            for (int w2 = 0; w2 < PK_WARPS; ++w2)
+                if (better(s_bv[w2], s_bi[w2], bv, bi)) { bv = s_bv[w2]; bi = s_bi[w2]; }
+            token = bi;
+            if (blockIdx.x == 0 && threadIdx.x == 0) a.tokens[pos + 1] = token;
+        } else {
+            token = a.tokens[pos + 1];
+        }
+        ++pos;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->pos = pos;
+}
+
+}  // namespace dimg::dev

@@ -17,8 +17,15 @@ typedef unsigned __int128 u128;
 constexpr int64_t ONE = int64_t(1) << 16;
 constexpr int64_t ACT_CLAMP = 256 * ONE;  // proj/include/dim/kernels.hpp:16
 
-// q16_mul: (int128(a) * b) >> 16, truncated to int64 (q16.hpp:28-30).
+__device__ __forceinline__ bool fits_i32(int64_t v) {
+    return ((uint64_t(v) + 0x80000000ull) >> 32) == 0;
+}
+
+// q16_mul: (int128(a) * b) >> 16, truncated to int64 (q16.hpp:28-30). When
+// both factors fit 32 bits the product fits 63 and one 64-bit multiply gives
+// the same bits.
 __device__ __forceinline__ int64_t mul16(int64_t a, int64_t b) {
+    if (fits_i32(a) && fits_i32(b)) return (a * b) >> 16;
     return int64_t((i128(a) * i128(b)) >> 16);
 }
 

@@ -161,6 +161,13 @@ class InferenceSession:
         check(lib.dimg_session_time_kernel(self._h, which, n, C.byref(ms), C.byref(b)))
         return ms.value, b.value
 
+    def trace(self, n_steps: int, cap: int):
+        """Per-stage %globaltimer stamps of CTA 0 over n decode steps: [cap, 4]
+        = (start, prologue done, chunks done, epilogue done) in ns."""
+        out = np.zeros(cap * 8, np.uint64)
+        check(lib.dimg_session_trace(self._h, n_steps, ptr(out, u64p), cap))
+        return out.reshape(cap, 8)
+
     def sync(self):
         check(lib.dimg_session_sync(self._h))
 
