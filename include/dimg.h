@@ -177,10 +177,10 @@ dimg_status dimg_session_time_decode(dimg_session* s, uint32_t n_steps, float* m
  * algorithmic bytes of one launch (roofline numerator). */
 dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, float* ms_per_launch,
                                      uint64_t* bytes_per_launch);
-/* Tracing: n decode steps; out[8*i + 0..3] = %globaltimer (ns) of CTA 0 at
+/* Tracing: n decode steps; out[12*i + 0..3] = %globaltimer (ns) of CTA 0 at
  * stage i's start, after its prologue, after its chunk loop and before its
- * grid barrier; [4..7] = rmsnorm prologue sub-steps (input staged, sum of
- * squares reduced, r computed, vector normalised). cap stages recorded. */
+ * grid barrier; [4..7] = clock64 of prologue / attention sub-steps, [8] =
+ * clock64 at the stage start. cap stages recorded. */
 dimg_status dimg_session_trace(dimg_session* s, uint32_t n_steps, uint64_t* out, uint32_t cap);
 /* Kernel launches per decode step / per prefill step (for the bench claim). */
 dimg_status dimg_session_launches(const dimg_session* s, uint32_t* per_decode,

@@ -377,8 +377,23 @@ void launch_pk(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
         const char* e = std::getenv("DIMG_BAR_MODE");
         return e ? uint32_t(std::atoi(e)) : 0u;
     }();
+    static const uint32_t debug = [] {
+        const char* e = std::getenv("DIMG_DEBUG");
+        return e ? uint32_t(std::atoi(e)) : 0u;
+    }();
+    static const uint32_t depth = [] {
+        const char* e = std::getenv("DIMG_DEPTH");
+        return e ? uint32_t(std::atoi(e)) : 0u;
+    }();
+    static const uint32_t idle_l2 = [] {
+        const char* e = std::getenv("DIMG_IDLE_L2");
+        return e ? uint32_t(std::atoi(e)) : 0u;
+    }();
     a.l2_ahead = l2_ahead;
     a.bar_mode = bar_mode;
+    a.debug = debug;
+    a.depth = depth;
+    a.idle_l2 = idle_l2;
     CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned int), s.stream));
     CK(cudaMemsetAsync(s.flags, 0, size_t(2) * s.m->L * sizeof(uint32_t), s.stream));
     void* params[] = {&a};
@@ -458,6 +473,8 @@ dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank,
                               dimg_model** out) {
     DIMG_API_GUARD({
         validate_config(d->cfg);
+        if (pad16(d->cfg.d_model) > 8192)
+            fail(DIMG_EINVAL, "model_upload: d_model above 8192");  // persistent.cuh MAXW
         if (tp_size != 1 || tp_rank != 0)
             fail(DIMG_EINVAL, "model_upload: tensor-parallel sharding is not built yet");
         DevCtx& c = dev_ctx(device);
@@ -593,8 +610,8 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         size_t need = attn_scratch_bytes(m->dh, m->cfg.max_ctx);
         for (const auto& st : s->host_stages) {
             if (st.kind != SK_GEMV) continue;
-            size_t b = st.mode == MODE_PLAIN ? size_t(8) * st.Kp
-                                             : size_t(8) * st.Kp * (st.gamma_unit ? 2 : 3);
+            // plain: up to 8 byte planes; rmsnorm: the int64 vector + up to 8 planes
+            size_t b = size_t(st.mode == MODE_PLAIN ? 8 : 16) * st.Kp;
             need = std::max(need, b);
         }
         s->planes_bytes = uint32_t((need + 127) & ~size_t(127));
@@ -784,11 +801,11 @@ dimg_status dimg_session_trace(dimg_session* s, uint32_t n_steps, uint64_t* out,
     DIMG_API_GUARD({
         if (uint64_t(s->len) + n_steps > s->m->cfg.max_ctx)
             fail(DIMG_ECTX, "decode: context overflow");
-        unsigned long long* d = s->mem.alloc<unsigned long long>(size_t(cap) * 8);
-        CK(cudaMemsetAsync(d, 0, size_t(cap) * 64, s->stream));
+        unsigned long long* d = s->mem.alloc<unsigned long long>(size_t(cap) * 12);
+        CK(cudaMemsetAsync(d, 0, size_t(cap) * 96, s->stream));
         launch_pk(*s, s->stages, n_layer_stages(*s), n_steps, 0, d, cap);
         s->len += n_steps;
-        CK(cudaMemcpyAsync(out, d, size_t(cap) * 64, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaMemcpyAsync(out, d, size_t(cap) * 96, cudaMemcpyDeviceToHost, s->stream));
         check_ctl_err(*s);
     })
 }

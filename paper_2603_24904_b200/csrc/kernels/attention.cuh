@@ -46,7 +46,7 @@ __device__ __forceinline__ void rope_pair(int64_t a, int64_t b, int64_t c, int64
 // softmax_q16 in place over S[0..n) (proj/src/kernels.cpp:90-107): exact max,
 // LUT weights lut(min(m - s, 8)), then p = (w << 16) / sum w (truncating).
 // Block-wide; ends with a barrier.
-__device__ void softmax_strip(int64_t* S, uint32_t n, const int64_t* lut, u128* red) {
+__device__ __noinline__ void softmax_strip(int64_t* S, uint32_t n, const int64_t* lut, u128* red) {
     int64_t m = INT64_MIN;
     for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) m = S[t] > m ? S[t] : m;
     m = block_reduce<int64_t>(m, reinterpret_cast<int64_t*>(red),
@@ -77,15 +77,18 @@ __host__ __device__ constexpr size_t attn_scratch_bytes(uint32_t dh, uint32_t ma
 // memory; `smem_scores` keeps the score strip on chip. When `planes` is set,
 // the output is also emitted as 3-limb byte planes for the WO GEMV (plus the
 // wide flag), see persistent.cuh.
-__device__ void attn_head(const AttnArgs& a, uint32_t h, uint32_t pos, int64_t* scratch, u128* red,
+__device__ __noinline__ void attn_head(const AttnArgs& a, uint32_t h, uint32_t pos, int64_t* scratch, u128* red,
                           uint8_t* planes = nullptr, uint32_t pitch = 0, uint32_t* flag = nullptr,
-                          uint32_t tag = 0, bool smem_scores = false) {
+                          uint32_t tag = 0, bool smem_scores = false,
+                          unsigned long long* tr = nullptr) {
     int64_t* qrot = scratch;                                   // [dh]
-    int64_t* lut = scratch + a.dh;                             // [257]
+    int64_t* lut = scratch + a.dh;                             // [257] (unless a.exp_lut is on chip)
     uint64_t* part = reinterpret_cast<uint64_t*>(lut + 257);   // [ATTN_THREADS]
     const uint32_t dh = a.dh, half = dh / 2, D = a.H * dh;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = ATTN_THREADS / 32;
-    for (int i = threadIdx.x; i < 257; i += blockDim.x) lut[i] = a.exp_lut[i];
+    if (smem_scores) lut = const_cast<int64_t*>(a.exp_lut);  // persistent kernel: already in smem
+    else
+        for (int i = threadIdx.x; i < 257; i += blockDim.x) lut[i] = a.exp_lut[i];
 
     const int64_t* q = a.qkv + size_t(h) * dh;
     const int64_t* k = a.qkv + D + size_t(h) * dh;
@@ -104,34 +107,68 @@ __device__ void attn_head(const AttnArgs& a, uint32_t h, uint32_t pos, int64_t* 
     }
     for (uint32_t j = threadIdx.x; j < dh; j += ATTN_THREADS) V[size_t(pos) * dh + j] = v[j];
     __syncthreads();
+    if (tr) tr[4] = clock64();
 
     int64_t* S = smem_scores ? reinterpret_cast<int64_t*>(part + ATTN_THREADS)
                              : a.scores + size_t(h) * a.max_ctx;
     // scores: one warp per cached position, int128 dot; four positions per
-    // warp in flight so the K reads overlap
+    // warp in flight so the K reads overlap. When every |q|, |k| < 2^27 a dot
+    // of <= 2^13 terms stays below 2^63, so plain int64 products and sums give
+    // the same int128 value; a warp-uniform check picks that fast path.
+    int q_small = 1;
+    for (uint32_t j = threadIdx.x; j < dh; j += blockDim.x) q_small &= qrot[j] < (int64_t(1) << 27) && qrot[j] > -(int64_t(1) << 27);
+    q_small = __syncthreads_and(q_small) && dh <= 512;  // 512 * 2^54 < 2^63
     for (uint32_t t0 = warp; t0 <= pos; t0 += 4 * nw) {
+        int64_t kv[4][4];
+        int small = q_small;
+        uint64_t d64[4] = {0, 0, 0, 0};
         u128 dot[4] = {0, 0, 0, 0};
-        for (uint32_t j = lane; j < dh; j += 32) {
-            int64_t kv[4];
+        for (uint32_t j0 = 0; j0 < dh; j0 += 128) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t t = t0 + u * nw;
-                kv[u] = t <= pos ? K[size_t(t) * dh + j] : 0;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint32_t j = j0 + lane + 32 * c;
+                    kv[u][c] = (t <= pos && j < dh) ? K[size_t(t) * dh + j] : 0;
+                }
             }
-            const int64_t qj = qrot[j];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) dot[u] += u128(i128(qj) * i128(kv[u]));
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    small &= kv[u][c] < (int64_t(1) << 27) && kv[u][c] > -(int64_t(1) << 27);
+            small = __all_sync(0xffffffffu, small);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t j = j0 + lane + 32 * c;
+                const int64_t qj = j < dh ? qrot[j] : 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (small) d64[u] += uint64_t(qj * kv[u][c]);
+                    else dot[u] += mul_full(qj, kv[u][c]);
+                }
+            }
         }
-#pragma unroll
+        small = __all_sync(0xffffffffu, small);
+#pragma unroll 1
         for (int u = 0; u < 4; ++u) {
-            const u128 d = warp_sum_u128(dot[u]);
             const uint32_t t = t0 + u * nw;
-            if (lane == 0 && t <= pos) S[t] = mul16(int64_t(i128(d) >> 16), a.inv_scale);
+            int64_t sc;
+            if (small) {
+                sc = int64_t(warp_sum_u64(d64[u] + uint64_t(dot[u]))) >> 16;
+            } else {
+                const u128 d = warp_sum_u128(dot[u] + u128(int64_t(d64[u])));
+                sc = int64_t(i128(d) >> 16);
+            }
+            if (lane == 0 && t <= pos) S[t] = mul16(sc, a.inv_scale);
         }
     }
     __syncthreads();
 
+    if (tr) tr[5] = clock64();
     softmax_strip(S, pos + 1, lut, red);
+    if (tr) tr[6] = clock64();
 
     // out_j = sum_t mul16(p_t, V[t]_j); threads = (column, position slice)
     if (dh <= ATTN_THREADS) {
@@ -180,6 +217,7 @@ __device__ void attn_head(const AttnArgs& a, uint32_t h, uint32_t pos, int64_t* 
         }
     }
     __syncthreads();  // scratch may be reused by the caller's next head/stage
+    if (tr) tr[7] = clock64();
 }
 
 __global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(AttnArgs a) {

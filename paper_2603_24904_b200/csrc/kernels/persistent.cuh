@@ -80,12 +80,15 @@ struct PkArgs {
     // attention
     AttnArgs attn;            // per-layer kc/vc offsets applied in-kernel
     size_t kv_layer_stride;   // elements between layers in kc/vc
-    const int64_t* exp_lut;
-    const int64_t* seeds;
+    const int64_t* exp_lut;   // repointed to a shared-memory copy inside the kernel
+    const int64_t* seeds;     // idem
     unsigned long long* trace;  // optional: [stage_seq][8] globaltimer stamps of CTA 0
     uint32_t trace_cap;
     uint32_t l2_ahead;        // chunks per warp prefetched into L2 beyond the ring
     uint32_t bar_mode;        // 0: poll the arrival counter, 1: poll a release flag line
+    uint32_t debug;
+    uint32_t depth;           // ring slots per warp (0 = PK_DEPTH)
+    uint32_t idle_l2;         // chunks per warp prefetched into L2 at each stage end
 };
 
 // ---- small PTX helpers --------------------------------------------------------
@@ -288,6 +291,7 @@ __device__ __forceinline__ void fetch_prefetch_l2(const Fetch& f) {
 struct Pipe {
     uint8_t* slots;     // this warp's ring
     uint64_t* bars;
+    uint32_t depth;     // slots in use (<= PK_DEPTH)
     uint32_t consumed;  // chunks consumed so far
     Fetch f;            // next chunk to load into the ring
     Fetch pf;           // next chunk to prefetch into L2 (PK_L2_AHEAD ahead of f)
@@ -295,14 +299,14 @@ struct Pipe {
 
 // Waits for the next chunk of this warp; returns its slot.
 __device__ __forceinline__ const uint8_t* pipe_wait(Pipe& p) {
-    const uint32_t sl = p.consumed % PK_DEPTH;
-    mbar_wait(&p.bars[sl], (p.consumed / PK_DEPTH) & 1);
+    const uint32_t sl = p.consumed % p.depth;
+    mbar_wait(&p.bars[sl], (p.consumed / p.depth) & 1);
     return p.slots + sl * PK_SLOT;
 }
 
 // Releases the chunk just consumed and refills its slot with the next one.
 __device__ __forceinline__ void pipe_release(const PkArgs& a, Pipe& p) {
-    const uint32_t sl = p.consumed % PK_DEPTH;
+    const uint32_t sl = p.consumed % p.depth;
     ++p.consumed;
     __syncwarp();
     if (!p.f.done) {
@@ -319,65 +323,77 @@ __device__ __forceinline__ void pipe_release(const PkArgs& a, Pipe& p) {
 }
 
 // ---- prologue: the stage's input vector as limb planes in shared memory -------
+// Everything here runs once per stage: it is kept compact and out of line,
+// because under a saturated HBM every instruction-cache miss is an L2 round
+// trip (ncu: 46% of prologue stalls were stall_no_inst before this).
 
-// Returns L (3 or 8); planes at `planes` ([L][Kp] bytes as words).
-__device__ int pk_prologue(const PkArgs& a, const PkStage& st, uint32_t token, uint32_t tag,
-                           uint8_t* stage_mem, uint32_t*& planes, u128* red,
-                           unsigned long long* tr = nullptr) {
-    const uint32_t K = st.K, Kp = st.Kp, Kw = Kp / 4;
-    if (st.mode == MODE_PLAIN) {
-        planes = reinterpret_cast<uint32_t*>(stage_mem);
-        if (ld_cg32(st.in_flag) != tag) {  // all elements fit 3 limbs: copy the planes
-            copy_g2s(planes, st.in_planes, 3 * Kp);
-            __syncthreads();
-            return 3;
-        }
-        // wide input: 8 byte planes straight from the int64 vector
-        for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
-            uint32_t word[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
+// Attention output / FFN hidden vector: copy the producer-written planes.
+__device__ __noinline__ int prologue_plain(const PkArgs& a, const PkStage& st, uint32_t tag,
+                                           uint32_t* planes) {
+    const uint32_t K = st.K, Kw = st.Kp / 4;
+    const uint32_t flag = ld_cg32(st.in_flag);  // same round trip as the copy
+    copy_g2s(planes, st.in_planes, 3 * st.Kp);
+    if (__syncthreads_or(flag == tag) == 0) return 3;  // every element fits 3 limbs
+    // wide input: 8 byte planes straight from the int64 vector
+#pragma unroll 1
+    for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) {
+            uint32_t word = 0;
             for (int e = 0; e < 4; ++e) {
-                uint32_t j = 4 * w + e;
-                uint64_t v = j < K ? uint64_t(ld_cg64(st.x + j)) : 0;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) word[k] |= uint32_t((v >> (8 * k)) & 0xFF) << (8 * e);
+                const uint32_t j = 4 * w + e;
+                const uint64_t v = j < K ? uint64_t(ld_cg64(st.x + j)) : 0;
+                word |= uint32_t((v >> (8 * k)) & 0xFF) << (8 * e);
             }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) planes[k * Kw + w] = word[k];
+            planes[k * Kw + w] = word;
         }
-        if (threadIdx.x == 0) atomicAdd(&a.ctl->stats[0], 1ull);
-        __syncthreads();
-        return 8;
     }
-    // rmsnorm input (residual stream, or the embedded token on layer 0)
-    int64_t* xb = reinterpret_cast<int64_t*>(stage_mem);
-    int64_t* gb = xb + Kp;
-    planes = reinterpret_cast<uint32_t*>(st.gamma_unit ? gb : gb + Kp);
-    if (st.mode == MODE_EMBED) {
+    if (threadIdx.x == 0) atomicAdd(&a.ctl->stats[0], 1ull);
+    __syncthreads();
+    return 8;
+}
+
+// rmsnorm input: the residual stream (or the embedded token on layer 0)
+// staged in shared memory, normalised there, packed into planes.
+__device__ __noinline__ int prologue_norm(const PkArgs& a, const PkStage& st, uint32_t token,
+                                          int64_t* xb, uint32_t* planes, u128* red,
+                                          unsigned long long* tr) {
+    const uint32_t K = st.K, Kw = st.Kp / 4;
+    if (st.mode == MODE_EMBED) {  // embed_token, proj/src/engine.cpp:10-19
         const int8_t* erow = a.embd + size_t(token) * K;
         const int64_t es = a.embd_scales[token];
         for (uint32_t j = threadIdx.x; j < K; j += blockDim.x) {
-            int64_t v = int64_t(uint64_t(int64_t(erow[j])) * uint64_t(es));  // engine.cpp:10-19
+            const int64_t v = int64_t(uint64_t(int64_t(erow[j])) * uint64_t(es));
             xb[j] = v;
             if (blockIdx.x == 0) a.x_resid[j] = v;
         }
     } else {
         copy_g2s(xb, st.x, K * 8);
     }
-    if (!st.gamma_unit) copy_g2s(gb, st.gamma, K * 8);
     __syncthreads();
-    if (tr) tr[4] = globaltimer();
+    if (tr) tr[4] = clock64();
     // ms = ((sum x^2) / n) >> 16 in int128, r = inv_sqrt(ms + 1) (kernels.cpp:56-68)
-    __shared__ int64_t s_r;
     u128 ss = 0;
+    int small = 1;
+#pragma unroll 4
     for (uint32_t j = threadIdx.x; j < K; j += blockDim.x) {
         const int64_t v = xb[j];
-        ss += fits_i32(v) ? u128(uint64_t(v * v)) : u128(i128(v) * i128(v));
+        if (fits_i32(v)) {
+            ss += uint64_t(int64_t(int32_t(v)) * int32_t(v));  // one IMAD.WIDE
+        } else {
+            ss += mul_full(v, v);
+            small = 0;
+        }
     }
-    ss = block_reduce<u128>(ss, red, [](u128 p, u128 q) { return p + q; }, warp_sum_u128);
-    if (tr) tr[5] = globaltimer();
+    ss = block_sum_u128(ss, red);
+    if (tr) tr[5] = clock64();
+    // one thread computes r; the others wait instead of contending for the
+    // multiplier with 255 redundant copies of the 128-bit Newton iteration
+    __shared__ int64_t s_r;
     if (threadIdx.x == 0) {
-        const int64_t ms = int64_t((i128(ss) / i128(K)) >> 16);
+        int64_t ms;
+        if ((ss >> 63) == 0) ms = int64_t((uint64_t(ss) / K) >> 16);  // usual case: one u64 divide
+        else ms = int64_t((i128(ss) / i128(K)) >> 16);
         if (ms + 1 <= 0) {
             atomicOr(&a.ctl->err, 1u);
             s_r = 0;
@@ -385,52 +401,50 @@ __device__ int pk_prologue(const PkArgs& a, const PkStage& st, uint32_t token, u
             s_r = inv_sqrt_q16(ms + 1, a.seeds);
         }
     }
-    __syncthreads();
-    if (tr) tr[6] = globaltimer();
+    small = __syncthreads_and(small);
     const int64_t r_inv = s_r;
+    if (tr) tr[6] = clock64();
+    small &= fits_i32(r_inv) & st.gamma_unit;
     int fits = 1;
-    for (uint32_t j = threadIdx.x; j < Kp; j += blockDim.x) {
-        int64_t v = 0;
-        if (j < K) {
-            v = mul16(xb[j], r_inv);
-            if (!st.gamma_unit) v = mul16(v, gb[j]);  // mul16(v, ONE) == v
+#pragma unroll 2
+    for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
+        uint32_t w0 = 0, w1 = 0, w2 = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t j = 4 * w + e;
+            int64_t v = 0;
+            if (j < K) {
+                if (small) {
+                    v = mul16_small(xb[j], r_inv);
+                } else {
+                    v = mul16(xb[j], r_inv);
+                    if (!st.gamma_unit) v = mul16(v, ld_cg64(st.gamma + j));  // mul16(v, ONE) == v
+                }
+            }
+            xb[j] = v;
+            fits &= (v >= -(int64_t(1) << 23)) & (v < (int64_t(1) << 23));
+            w0 |= uint32_t(v & 0xFF) << (8 * e);
+            w1 |= uint32_t((v >> 8) & 0xFF) << (8 * e);
+            w2 |= uint32_t((v >> 16) & 0xFF) << (8 * e);
         }
-        xb[j] = v;
-        fits &= (v >= -(int64_t(1) << 23)) & (v < (int64_t(1) << 23));
+        planes[w] = w0;
+        planes[Kw + w] = w1;
+        planes[2 * Kw + w] = w2;
     }
     fits = __syncthreads_and(fits);
-    if (tr) tr[7] = globaltimer();
-    const int L = fits ? 3 : 8;
-    if (L == 3) {
-        for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
-            uint32_t w0 = 0, w1 = 0, w2 = 0;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const uint32_t v = uint32_t(xb[4 * w + e]);
-                w0 |= (v & 0xFF) << (8 * e);
-                w1 |= ((v >> 8) & 0xFF) << (8 * e);
-                w2 |= ((v >> 16) & 0xFF) << (8 * e);
-            }
-            planes[w] = w0;
-            planes[Kw + w] = w1;
-            planes[2 * Kw + w] = w2;
+    if (tr) tr[7] = clock64();
+    if (fits) return 3;
+#pragma unroll 1
+    for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x)
+#pragma unroll 1
+        for (int k = 3; k < 8; ++k) {
+            uint32_t word = 0;
+            for (int e = 0; e < 4; ++e) word |= uint32_t((uint64_t(xb[4 * w + e]) >> (8 * k)) & 0xFF) << (8 * e);
+            planes[k * Kw + w] = word;
         }
-    } else {
-        for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
-            uint32_t word[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                uint64_t v = uint64_t(xb[4 * w + e]);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) word[k] |= uint32_t((v >> (8 * k)) & 0xFF) << (8 * e);
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) planes[k * Kw + w] = word[k];
-        }
-    }
-    if (L == 8 && threadIdx.x == 0) atomicAdd(&a.ctl->stats[0], 1ull);
+    if (threadIdx.x == 0) atomicAdd(&a.ctl->stats[0], 1ull);
     __syncthreads();
-    return L;
+    return 8;
 }
 
 // Producer side of the plane hand-off: element j of an output vector.
@@ -464,6 +478,11 @@ template <int L>
 __device__ __forceinline__ void group_dot(const PkArgs& a, Pipe& p, const PkStage& st,
                                           const uint32_t* planes, uint64_t (&out)[PK_ROWS]) {
     const int lane = threadIdx.x & 31;
+    if (a.debug & 4) {  // diagnostic: no weight streaming at all (results are garbage)
+#pragma unroll
+        for (int r = 0; r < PK_ROWS; ++r) out[r] = 0;
+        return;
+    }
     const uint32_t Kw = st.Kp / 4;
     int32_t acc[PK_ROWS][L];
 #pragma unroll
@@ -521,16 +540,21 @@ __device__ void run_gemv(const PkArgs& a, Pipe& p, const PkStage& st, const uint
     }
     for (uint32_t g = g_lo + (threadIdx.x >> 5); g < g_hi; g += PK_WARPS) {
         const uint32_t r0 = g * PK_ROWS;
-        int64_t resid = 0;  // issued now, consumed after the dot product
-        if (st.epi == EPI_RESID && lane < PK_ROWS && r0 + lane < st.rows) resid = ld_cg64(st.y + r0 + lane);
+        int64_t resid = 0, scale = 0;  // issued now, consumed after the dot product
+        if (lane < PK_ROWS && r0 + lane < st.rows) {
+            scale = st.scales[r0 + lane];
+            if (st.epi == EPI_RESID) resid = ld_cg64(st.y + r0 + lane);
+        }
         uint64_t v[PK_ROWS];
         group_dot<L>(a, p, st, planes, v);
         if (st.epi == EPI_SILU) {
             // rows (2i, 2i+1) = (gate_i, up_i): lanes 0,1 finish pairs 0,1
+            const int64_t s_g = __shfl_sync(0xffffffffu, scale, 2 * (lane & 1));
+            const int64_t s_u = __shfl_sync(0xffffffffu, scale, 2 * (lane & 1) + 1);
             if (lane < 2 && r0 + 2 * lane + 1 < st.rows) {
                 const uint32_t row = r0 + 2 * lane;
-                const int64_t gs = scale_row(int64_t(lane ? v[2] : v[0]), st.scales[row]);
-                const int64_t us = scale_row(int64_t(lane ? v[3] : v[1]), st.scales[row + 1]);
+                const int64_t gs = scale_row(int64_t(lane ? v[2] : v[0]), s_g);
+                const int64_t us = scale_row(int64_t(lane ? v[3] : v[1]), s_u);
                 const int64_t h = mul16(silu_q16(gs, a.exp_lut), us);
                 st.y[row / 2] = h;
                 emit_planes(st.out_planes, st.out_pitch, st.out_flag, tag, row / 2, h);
@@ -540,7 +564,7 @@ __device__ void run_gemv(const PkArgs& a, Pipe& p, const PkStage& st, const uint
             uint64_t acc = v[0];
 #pragma unroll
             for (int r = 1; r < PK_ROWS; ++r) acc = lane == r ? v[r] : acc;
-            const int64_t val = scale_row(int64_t(acc), st.scales[row]);
+            const int64_t val = scale_row(int64_t(acc), scale);
             if (st.epi == EPI_STORE) {
                 st.y[row] = val;
             } else if (st.epi == EPI_RESID) {
@@ -556,6 +580,13 @@ __device__ void run_gemv(const PkArgs& a, Pipe& p, const PkStage& st, const uint
     }
 }
 
+// The 8-limb instantiation only runs on out-of-range activations: out of line.
+__device__ __noinline__ void run_gemv_wide(const PkArgs& a, Pipe& p, const PkStage& st,
+                                           const uint32_t* planes, uint32_t pos, uint32_t tag,
+                                           int64_t& best_v, uint32_t& best_i) {
+    run_gemv<8>(a, p, st, planes, pos, tag, best_v, best_i);
+}
+
 // ---- the kernel -------------------------------------------------------------------
 
 __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs a) {
@@ -569,6 +600,14 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x < PK_WARPS * PK_DEPTH) mbar_init(&bars[threadIdx.x], 1);
+    // exp LUT and inv-sqrt seeds live in shared memory for the whole launch:
+    // a global load under a saturated HBM costs microseconds
+    __shared__ int64_t s_lut[257], s_seeds[64];
+    for (int i = threadIdx.x; i < 257; i += PK_THREADS) s_lut[i] = a.exp_lut[i];
+    if (threadIdx.x < 64) s_seeds[threadIdx.x] = a.seeds[threadIdx.x];
+    a.exp_lut = s_lut;
+    a.seeds = s_seeds;
+    a.attn.exp_lut = s_lut;
     fence_proxy_async();
     __syncthreads();
 
@@ -577,6 +616,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs
     p.slots = slots + size_t(warp) * PK_DEPTH * PK_SLOT;
     p.bars = bars + warp * PK_DEPTH;
     p.consumed = 0;
+    p.depth = a.depth ? min(a.depth, uint32_t(PK_DEPTH)) : PK_DEPTH;
     p.f.step = 0;
     p.f.stage = 0;
     p.f.done = a.n_steps == 0;
@@ -584,13 +624,14 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs
         fetch_load(a, p.f);
         fetch_settle(a, p.f);
     }
+    if (a.debug & 4) p.f.done = true;
     p.pf = p.f;
     if (!a.l2_ahead) p.pf.done = true;
     for (uint32_t d = 0; d < PK_DEPTH + a.l2_ahead && a.l2_ahead && !p.pf.done; ++d) {
         if (lane == 0) fetch_prefetch_l2(p.pf);
         fetch_advance(a, p.pf);
     }
-    for (int d = 0; d < PK_DEPTH && !p.f.done; ++d) {
+    for (uint32_t d = 0; d < p.depth && !p.f.done; ++d) {
         if (lane == 0) fetch_issue(p.f, p.slots + d * PK_SLOT, &p.bars[d]);
         fetch_advance(a, p.f);
     }
@@ -598,15 +639,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs
     uint32_t pos = a.ctl->pos;
     uint32_t token = a.tokens[pos];
     uint32_t nbar = 0;
-    __shared__ __align__(16) PkStage s_st;
+    __shared__ __align__(16) PkStage s_st[2];
     constexpr int kStWords = sizeof(PkStage) / 4;
-    auto load_stage = [&](uint32_t idx) {
-        if (threadIdx.x < kStWords)
-            reinterpret_cast<uint32_t*>(&s_st)[threadIdx.x] =
-                reinterpret_cast<const uint32_t*>(a.stages + idx)[threadIdx.x];
-    };
+    static_assert(kStWords <= PK_THREADS, "stage descriptor too large");
+    uint32_t cur = 0;
     __syncthreads();
-    load_stage(0);
+    if (threadIdx.x < kStWords)
+        reinterpret_cast<uint32_t*>(&s_st[0])[threadIdx.x] = reinterpret_cast<const uint32_t*>(a.stages)[threadIdx.x];
     __syncthreads();
 
     for (uint32_t step = 0; step < a.n_steps; ++step) {
@@ -615,24 +654,47 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs
         int64_t best_v = INT64_MIN;
         uint32_t best_i = 0xFFFFFFFFu;
         for (uint32_t si = 0; si < nst; ++si) {
-            const PkStage& st = s_st;
+            const PkStage& st = s_st[cur];
+            // the next stage's descriptor: loaded now, stored before the barrier
+            uint32_t next_word = 0;
+            if (threadIdx.x < kStWords)
+                next_word = reinterpret_cast<const uint32_t*>(a.stages + (si + 1 < nst ? si + 1 : 0))[threadIdx.x];
             const bool tr = a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nbar < a.trace_cap;
-            if (tr) a.trace[8 * nbar + 0] = globaltimer();
+            if (tr) a.trace[12 * nbar + 8] = clock64();
+            if (tr) a.trace[12 * nbar + 0] = globaltimer();
             if (st.kind == SK_ATTN) {
                 AttnArgs t = a.attn;
                 t.kc += size_t(st.layer) * a.kv_layer_stride;
                 t.vc += size_t(st.layer) * a.kv_layer_stride;
-                for (uint32_t h = blockIdx.x; h < t.H; h += gridDim.x)
+                for (uint32_t h = blockIdx.x; h < t.H; h += gridDim.x) {
+                    if (a.debug & 2) {  // i-cache experiment: a warm second call is what gets traced
+                        attn_head(t, h, pos, reinterpret_cast<int64_t*>(stage_mem), red, st.out_planes,
+                                  st.out_pitch, st.out_flag, tag, true, nullptr);
+                        if (tr && h == 0) a.trace[12 * nbar + 8] = clock64();
+                    }
                     attn_head(t, h, pos, reinterpret_cast<int64_t*>(stage_mem), red, st.out_planes,
-                              st.out_pitch, st.out_flag, tag, true);
+                              st.out_pitch, st.out_flag, tag, true,
+                              tr && h == 0 ? a.trace + 12 * nbar : nullptr);
+                }
             } else {
                 uint32_t* planes;
-                const int L = pk_prologue(a, st, token, tag, stage_mem, planes, red,
-                                          tr ? a.trace + 8 * nbar : nullptr);
-                if (tr) a.trace[8 * nbar + 1] = globaltimer();
+                int L;
+                if (st.mode == MODE_PLAIN) {
+                    planes = reinterpret_cast<uint32_t*>(stage_mem);
+                    L = prologue_plain(a, st, tag, planes);
+                } else {
+                    int64_t* xb = reinterpret_cast<int64_t*>(stage_mem);
+                    planes = reinterpret_cast<uint32_t*>(xb + st.Kp);
+                    if (a.debug & 1) {  // i-cache experiment
+                        prologue_norm(a, st, token, xb, planes, red, nullptr);
+                        if (tr) a.trace[12 * nbar + 8] = clock64();
+                    }
+                    L = prologue_norm(a, st, token, xb, planes, red, tr ? a.trace + 12 * nbar : nullptr);
+                }
+                if (tr) a.trace[12 * nbar + 1] = globaltimer();
                 if (L == 3) run_gemv<3>(a, p, st, planes, pos, tag, best_v, best_i);
-                else run_gemv<8>(a, p, st, planes, pos, tag, best_v, best_i);
-                if (tr) a.trace[8 * nbar + 2] = globaltimer();
+                else run_gemv_wide(a, p, st, planes, pos, tag, best_v, best_i);
+                if (tr) a.trace[12 * nbar + 2] = globaltimer();
                 if (st.epi == EPI_ARGMAX) {
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
@@ -650,9 +712,18 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs
                     }
                 }
             }
-            if (tr) a.trace[8 * nbar + 3] = globaltimer();
-            __syncthreads();  // everyone is done with s_st
-            load_stage(si + 1 < nst ? si + 1 : 0);
+            if (tr) a.trace[12 * nbar + 3] = globaltimer();
+            if (threadIdx.x < kStWords) reinterpret_cast<uint32_t*>(&s_st[cur ^ 1])[threadIdx.x] = next_word;
+            cur ^= 1;
+            // Idle-time prefetch: while this CTA waits at the barrier and runs
+            // the next prologue, HBM fills L2 with the chunks after its ring.
+            if (a.idle_l2) {
+                Fetch q = p.f;
+                for (uint32_t i = 0; i < a.idle_l2 && !q.done; ++i) {
+                    if (lane == 0) fetch_prefetch_l2(q);
+                    fetch_advance(a, q);
+                }
+            }
             if (!grid_sync(a.bar, a.ctl, nbar++, a.bar_mode)) return;
         }
         if (step >= a.n_prefill) {

@@ -21,17 +21,34 @@ __device__ __forceinline__ bool fits_i32(int64_t v) {
     return ((uint64_t(v) + 0x80000000ull) >> 32) == 0;
 }
 
-// q16_mul: (int128(a) * b) >> 16, truncated to int64 (q16.hpp:28-30). When
-// both factors fit 32 bits the product fits 63 and one 64-bit multiply gives
-// the same bits.
-__device__ __forceinline__ int64_t mul16(int64_t a, int64_t b) {
-    if (fits_i32(a) && fits_i32(b)) return (a * b) >> 16;
-    return int64_t((i128(a) * i128(b)) >> 16);
+// int64((int128(a) * b) >> k) for 0 < k < 64, exact for every input: the
+// 128-bit product is (hi, lo) = (mul.hi.s64, mul.lo.s64), and the low 64 bits
+// of the arithmetic shift are (lo >>> k) | (hi << (64 - k)). Two multiplies,
+// no branches -- compact code matters in this kernel (see persistent.cuh).
+template <int k>
+__device__ __forceinline__ int64_t mul_shr(int64_t a, int64_t b) {
+    const uint64_t lo = uint64_t(a) * uint64_t(b);
+    const uint64_t hi = uint64_t(__mul64hi(a, b));
+    return int64_t((lo >> k) | (hi << (64 - k)));
+}
+
+// Full signed 64x64 -> 128-bit product.
+__device__ __forceinline__ u128 mul_full(int64_t a, int64_t b) {
+    return (u128(uint64_t(__mul64hi(a, b))) << 64) | uint64_t(a * b);
+}
+
+// q16_mul: (int128(a) * b) >> 16, truncated to int64 (q16.hpp:28-30).
+__device__ __forceinline__ int64_t mul16(int64_t a, int64_t b) { return mul_shr<16>(a, b); }
+
+// Same value when both factors fit 32 bits (one IMAD.WIDE); callers check.
+__device__ __forceinline__ int64_t mul16_small(int64_t a, int64_t b) {
+    return (int64_t(int32_t(a)) * int32_t(b)) >> 16;
 }
 
 // floor(p * v / 2^16) for 0 <= p <= 2^16 (softmax probabilities) with 64-bit
 // ops only: v = vh*2^16 + vl, vl in [0, 2^16) => p*vh + (p*vl >> 16) exactly.
 __device__ __forceinline__ int64_t mul16_prob(int64_t p, int64_t v) {
+    if (fits_i32(v)) return (p * int64_t(int32_t(v))) >> 16;  // |p*v| < 2^48: exact
     int64_t vh = v >> 16;
     uint64_t vl = uint64_t(v) & 0xFFFFu;
     return int64_t(uint64_t(p) * uint64_t(vh) + ((uint64_t(p) * vl) >> 16));
@@ -45,9 +62,7 @@ __device__ __forceinline__ int64_t wrap_sub(int64_t a, int64_t b) {
 }
 
 // Dense epilogue: (int128(acc) * scale) >> 16 (proj/src/kernels.cpp:27).
-__device__ __forceinline__ int64_t scale_row(int64_t acc, int64_t s) {
-    return int64_t((i128(acc) * i128(s)) >> 16);
-}
+__device__ __forceinline__ int64_t scale_row(int64_t acc, int64_t s) { return mul_shr<16>(acc, s); }
 
 // residual_add_clamp (proj/src/kernels.cpp:192-200).
 __device__ __forceinline__ int64_t add_clamp(int64_t a, int64_t b) {
@@ -57,7 +72,7 @@ __device__ __forceinline__ int64_t add_clamp(int64_t a, int64_t b) {
 
 // inv_sqrt_q16: octave seed (host-built Q48 table) + three Newton steps at
 // Q48 in int128, rounded to Q16 (proj/src/q16.cpp:56-68). x > 0.
-__device__ __forceinline__ int64_t inv_sqrt_q16(int64_t x, const int64_t* seeds) {
+__device__ __noinline__ int64_t inv_sqrt_q16(int64_t x, const int64_t* seeds) {
     int b = 63 - __clzll(x);
     i128 y = seeds[b];
     const i128 three = i128(3) << 48;
@@ -134,6 +149,11 @@ __device__ __forceinline__ T block_reduce(T v, T* scratch, Op op, T (*warp_op)(T
     T r = scratch[0];
     for (int i = 1; i < nw; ++i) r = op(r, scratch[i]);
     return r;
+}
+
+// Block-wide u128 sum (all threads get it); kept out of line.
+__device__ __noinline__ u128 block_sum_u128(u128 v, u128* scratch) {
+    return block_reduce<u128>(v, scratch, [](u128 p, u128 q) { return p + q; }, warp_sum_u128);
 }
 
 // Argmax key: larger value wins, lower index on ties (engine.cpp:113-120).

@@ -164,9 +164,9 @@ class InferenceSession:
     def trace(self, n_steps: int, cap: int):
         """Per-stage %globaltimer stamps of CTA 0 over n decode steps: [cap, 4]
         = (start, prologue done, chunks done, epilogue done) in ns."""
-        out = np.zeros(cap * 8, np.uint64)
+        out = np.zeros(cap * 12, np.uint64)
         check(lib.dimg_session_trace(self._h, n_steps, ptr(out, u64p), cap))
-        return out.reshape(cap, 8)
+        return out.reshape(cap, 12)
 
     def sync(self):
         check(lib.dimg_session_sync(self._h))

@@ -23,9 +23,12 @@ for i in range(ns, 2 * ns):
     rows.setdefault(name, []).append((t[1] - t[0] if t[1] else 0, t[2] - t[1] if t[2] else 0,
                                       t[3] - (t[2] if t[2] else t[0]), nxt - t[3]))
     if t[4]:
-        sub.setdefault(name, []).append((t[4] - t[0], t[5] - t[4], t[6] - t[5], t[7] - t[6], t[1] - t[7]))
+        c = t[8]
+        ghz = 1.965e-3  # cycles per ns at max clock (approximate)
+        sub.setdefault(name, []).append(((t[4] - c) / ghz, (t[5] - t[4]) / ghz, (t[6] - t[5]) / ghz,
+                                         (t[7] - t[6]) / ghz, 0))
 print(os.environ.get("DIMG_L2_AHEAD", "0"), os.environ.get("DIMG_BAR_MODE", "0"),
-      "stage   prologue  chunks  epilogue  barrier   | copy  reduce  r  norm  pack (us)")
+      "stage   prologue  chunks  epilogue  barrier   | copy  reduce  r  norm  pack (us) [attn: rope scores softmax pv tail]")
 for k, v in rows.items():
     a = np.array(v).mean(0) / 1e3
     extra = ""
