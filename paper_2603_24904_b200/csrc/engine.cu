@@ -187,21 +187,33 @@ bool all_one(const int64_t* g, size_t n) {
     return true;
 }
 
-// row-major [rows4][Kp] -> blocked [groups][segs][4][seg] (16-byte units)
-__global__ void blockify_kernel(const int4* __restrict__ src, int4* __restrict__ dst, uint32_t Kp,
-                                uint32_t n_groups, uint32_t n_segs) {
-    const size_t total = size_t(n_groups) * PK_ROWS * Kp / 16;
+// row-major [rows4][Kp] -> blocked [groups]{[segs][4][seg], 4 int64 scales}
+// (16-byte units; persistent.cuh pk_group_bytes)
+__global__ void blockify_kernel(const int4* __restrict__ src, const int64_t* __restrict__ scales,
+                                uint32_t rows, int4* __restrict__ dst, uint32_t Kp, uint32_t n_groups,
+                                uint32_t n_segs) {
+    const size_t gbytes = pk_group_bytes(Kp);
+    const size_t total = size_t(n_groups) * gbytes / 16;
     const uint32_t last = Kp - (n_segs - 1) * PK_SEG;
     for (size_t o = blockIdx.x * size_t(blockDim.x) + threadIdx.x; o < total;
          o += size_t(gridDim.x) * blockDim.x) {
-        size_t byte = o * 16;
-        size_t g = byte / (size_t(PK_ROWS) * Kp);
-        size_t in_g = byte % (size_t(PK_ROWS) * Kp);
-        uint32_t s = uint32_t(in_g / (PK_ROWS * PK_SEG));
-        uint32_t w = s + 1 < n_segs ? PK_SEG : last;
-        size_t in_s = in_g - size_t(s) * PK_ROWS * PK_SEG;
-        uint32_t r = uint32_t(in_s / w), c = uint32_t(in_s % w);
-        size_t sb = (g * PK_ROWS + r) * Kp + size_t(s) * PK_SEG + c;
+        const size_t byte = o * 16;
+        const size_t g = byte / gbytes;
+        const size_t in_g = byte % gbytes;
+        if (in_g >= size_t(PK_ROWS) * Kp) {  // the group's scales
+            const uint32_t r = uint32_t((in_g - size_t(PK_ROWS) * Kp) / 8);
+            const uint32_t row0 = uint32_t(g) * PK_ROWS + r;
+            longlong2 v;
+            v.x = row0 < rows ? scales[row0] : 0;
+            v.y = row0 + 1 < rows ? scales[row0 + 1] : 0;
+            reinterpret_cast<longlong2*>(dst)[o] = v;
+            continue;
+        }
+        const uint32_t s = uint32_t(in_g / (PK_ROWS * PK_SEG));
+        const uint32_t w = s + 1 < n_segs ? PK_SEG : last;
+        const size_t in_s = in_g - size_t(s) * PK_ROWS * PK_SEG;
+        const uint32_t r = uint32_t(in_s / w), c = uint32_t(in_s % w);
+        const size_t sb = (g * PK_ROWS + r) * Kp + size_t(s) * PK_SEG + c;
         dst[o] = src[sb / 16];
     }
 }
@@ -224,11 +236,12 @@ DevMat upload_mat(dimg_model& m, uint32_t rows, uint32_t K, const std::vector<Ro
     const size_t bytes = size_t(d.n_groups) * PK_ROWS * d.Kp;
     CK(cudaMemset(staging, 0, bytes));
     for (const auto& p : parts) put_rows(staging, d.Kp, p.row0, p.rstride, p.src, p.rows, K);
-    d.w = m.mem.alloc<int8_t>(bytes);
-    blockify_kernel<<<1024, 256>>>(reinterpret_cast<const int4*>(staging), reinterpret_cast<int4*>(d.w),
-                                   d.Kp, d.n_groups, d.n_segs);
-    CK(cudaGetLastError());
     d.s = upload(m.mem, scales.data(), scales.size());
+    d.w = m.mem.alloc<int8_t>(size_t(d.n_groups) * pk_group_bytes(d.Kp));
+    blockify_kernel<<<1024, 256>>>(reinterpret_cast<const int4*>(staging), d.s, rows,
+                                   reinterpret_cast<int4*>(d.w), d.Kp, d.n_groups, d.n_segs);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
     return d;
 }
 
@@ -369,31 +382,7 @@ void launch_pk(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     PkArgs a = pk_args(s, stages, n_layer_stages, n_steps, n_prefill);
     a.trace = trace;
     a.trace_cap = trace_cap;
-    static const uint32_t l2_ahead = [] {
-        const char* e = std::getenv("DIMG_L2_AHEAD");
-        return e ? uint32_t(std::atoi(e)) : 0u;
-    }();
-    static const uint32_t bar_mode = [] {
-        const char* e = std::getenv("DIMG_BAR_MODE");
-        return e ? uint32_t(std::atoi(e)) : 0u;
-    }();
-    static const uint32_t debug = [] {
-        const char* e = std::getenv("DIMG_DEBUG");
-        return e ? uint32_t(std::atoi(e)) : 0u;
-    }();
-    static const uint32_t depth = [] {
-        const char* e = std::getenv("DIMG_DEPTH");
-        return e ? uint32_t(std::atoi(e)) : 0u;
-    }();
-    static const uint32_t idle_l2 = [] {
-        const char* e = std::getenv("DIMG_IDLE_L2");
-        return e ? uint32_t(std::atoi(e)) : 0u;
-    }();
-    a.l2_ahead = l2_ahead;
-    a.bar_mode = bar_mode;
-    a.debug = debug;
-    a.depth = depth;
-    a.idle_l2 = idle_l2;
+
     CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned int), s.stream));
     CK(cudaMemsetAsync(s.flags, 0, size_t(2) * s.m->L * sizeof(uint32_t), s.stream));
     void* params[] = {&a};

@@ -77,10 +77,13 @@ __host__ __device__ constexpr size_t attn_scratch_bytes(uint32_t dh, uint32_t ma
 // memory; `smem_scores` keeps the score strip on chip. When `planes` is set,
 // the output is also emitted as 3-limb byte planes for the WO GEMV (plus the
 // wide flag), see persistent.cuh.
-__device__ __noinline__ void attn_head(const AttnArgs& a, uint32_t h, uint32_t pos, int64_t* scratch, u128* red,
+__device__ __noinline__ void attn_head(const AttnArgs& a_in, uint32_t h, uint32_t pos, int64_t* scratch, u128* red,
                           uint8_t* planes = nullptr, uint32_t pitch = 0, uint32_t* flag = nullptr,
                           uint32_t tag = 0, bool smem_scores = false,
                           unsigned long long* tr = nullptr) {
+    // one copy of the arguments into registers (a_in may live in local memory,
+    // whose L1 lines the persistent kernel's grid fences invalidate)
+    const AttnArgs a = a_in;
     int64_t* qrot = scratch;                                   // [dh]
     int64_t* lut = scratch + a.dh;                             // [257] (unless a.exp_lut is on chip)
     uint64_t* part = reinterpret_cast<uint64_t*>(lut + 257);   // [ATTN_THREADS]

@@ -41,14 +41,18 @@ constexpr int PK_WARPS = PK_THREADS / 32;
 constexpr int PK_DEPTH = 2;             // chunks in flight per warp
 constexpr int PK_SEG = 2048;            // K-segment width (bytes)
 constexpr int PK_ROWS = 4;              // rows per group
-constexpr int PK_SLOT = PK_ROWS * PK_SEG;
+constexpr int PK_SCALES = PK_ROWS * 8;             // the group's 4 int64 row scales
+constexpr int PK_SLOT = PK_ROWS * PK_SEG + PK_SCALES;  // chunk bytes incl. trailing scales
+
+// Bytes of one row group in the blocked layout: 4 rows x Kp, then 4 scales.
+__host__ __device__ constexpr size_t pk_group_bytes(uint32_t Kp) { return size_t(PK_ROWS) * Kp + PK_SCALES; }
 
 enum { SK_GEMV = 0, SK_ATTN = 1 };
 
 struct PkStage {
     uint32_t kind, mode, epi, layer;
     uint32_t rows, K, Kp, n_groups, n_segs, gamma_unit;
-    const int8_t* W;          // blocked [n_groups][n_segs][4][seg]
+    const int8_t* W;          // blocked [n_groups][n_segs][4][seg] + 4 scales per group
     const int64_t* scales;    // [rows]
     const int64_t* x;         // input vector (K)
     const int64_t* gamma;     // norm gains (MODE_NORM / MODE_EMBED)
@@ -82,13 +86,16 @@ struct PkArgs {
     size_t kv_layer_stride;   // elements between layers in kc/vc
     const int64_t* exp_lut;   // repointed to a shared-memory copy inside the kernel
     const int64_t* seeds;     // idem
-    unsigned long long* trace;  // optional: [stage_seq][8] globaltimer stamps of CTA 0
+    unsigned long long* trace;  // optional: [stage_seq][12] stamps of CTA 0 (dimg_session_trace)
     uint32_t trace_cap;
-    uint32_t l2_ahead;        // chunks per warp prefetched into L2 beyond the ring
-    uint32_t bar_mode;        // 0: poll the arrival counter, 1: poll a release flag line
-    uint32_t debug;
-    uint32_t depth;           // ring slots per warp (0 = PK_DEPTH)
-    uint32_t idle_l2;         // chunks per warp prefetched into L2 at each stage end
+};
+
+// Scheduling constants, held in registers (never address kernel params or
+// shared structs from hot code: local memory goes through L1, which each
+// grid barrier's fence invalidates, turning every such read into an L2 trip).
+struct Sched {
+    const PkStage* stages;
+    uint32_t n_layer_stages, n_steps, n_prefill;
 };
 
 // ---- small PTX helpers --------------------------------------------------------
@@ -187,22 +194,16 @@ __device__ __forceinline__ void copy_g2s(void* dst, const void* src, uint32_t by
 
 // Grid barrier #k (monotonic counter). Returns false if the wait timed out
 // (a hung peer): the caller then unwinds instead of hanging the GPU.
-__device__ __forceinline__ bool grid_sync(unsigned int* bar, Ctl* ctl, uint32_t k, uint32_t mode) {
-    // bar[0]: arrivals (monotonic); bar[32]: released generation, on its own
-    // 128-byte line so the pollers never contend with the arriving atomics.
+__device__ __forceinline__ bool grid_sync(unsigned int* bar, Ctl* ctl, uint32_t k) {
     __shared__ int ok;
     __syncthreads();
     if (threadIdx.x == 0) {
         ok = 1;
         __threadfence();
+        atomicAdd(bar, 1u);
         const uint32_t target = (k + 1) * gridDim.x;
-        const uint32_t prev = atomicAdd(bar, 1u);
-        if (mode == 1 && prev == target - 1)
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 32), "r"(k + 1) : "memory");
-        const unsigned int* poll = mode == 1 ? bar + 32 : bar;
-        const uint32_t want = mode == 1 ? k + 1 : target;
         uint64_t t0 = globaltimer();
-        while (ld_acquire(poll) < want) {
+        while (ld_acquire(bar) < target) {
             if (*((volatile uint32_t*)&ctl->err) & 4u) { ok = 0; break; }
             if (globaltimer() - t0 > 4000000000ull) {  // 4 s
                 atomicOr(&ctl->err, 4u);
@@ -220,8 +221,8 @@ __device__ __forceinline__ void cta_range(uint32_t n, uint32_t& lo, uint32_t& hi
     hi = uint32_t(uint64_t(n) * (blockIdx.x + 1) / gridDim.x);
 }
 
-__device__ __forceinline__ uint32_t stages_in_step(const PkArgs& a, uint32_t step) {
-    return a.n_layer_stages + (step >= a.n_prefill ? 1u : 0u);
+__device__ __forceinline__ uint32_t stages_in_step(const Sched& sc, uint32_t step) {
+    return sc.n_layer_stages + (step >= sc.n_prefill ? 1u : 0u);
 }
 
 // ---- the warp's weight-chunk stream (same order as its consumption) -----------
@@ -232,48 +233,49 @@ struct Fetch {
     bool done;
 };
 
-__device__ __forceinline__ void fetch_load(const PkArgs& a, Fetch& f) {
-    const PkStage& st = a.stages[f.stage];
-    if (st.kind != SK_GEMV) {
+__device__ __forceinline__ void fetch_load(const Sched& sc, Fetch& f) {
+    const PkStage* st = sc.stages + f.stage;
+    if (st->kind != SK_GEMV) {
         f.g = f.g_end = 0;
         return;
     }
     uint32_t lo, hi;
-    cta_range(st.n_groups, lo, hi);
+    cta_range(st->n_groups, lo, hi);
     f.g = lo + (threadIdx.x >> 5);
     f.g_end = hi;
     f.seg = 0;
-    f.n_segs = st.n_segs;
-    f.Kp = st.Kp;
-    f.W = st.W;
+    f.n_segs = st->n_segs;
+    f.Kp = st->Kp;
+    f.W = st->W;
 }
 
-__device__ __forceinline__ void fetch_settle(const PkArgs& a, Fetch& f) {
+__device__ __forceinline__ void fetch_settle(const Sched& sc, Fetch& f) {
     while (!f.done && f.g >= f.g_end) {
-        if (++f.stage >= stages_in_step(a, f.step)) {
+        if (++f.stage >= stages_in_step(sc, f.step)) {
             f.stage = 0;
-            if (++f.step >= a.n_steps) {
+            if (++f.step >= sc.n_steps) {
                 f.done = true;
                 return;
             }
         }
-        fetch_load(a, f);
+        fetch_load(sc, f);
     }
 }
 
-__device__ __forceinline__ void fetch_advance(const PkArgs& a, Fetch& f) {
+__device__ __forceinline__ void fetch_advance(const Sched& sc, Fetch& f) {
     if (++f.seg == f.n_segs) {
         f.seg = 0;
         f.g += PK_WARPS;
     }
-    fetch_settle(a, f);
+    fetch_settle(sc, f);
 }
 
 __device__ __forceinline__ uint32_t fetch_bytes(const Fetch& f) {
-    return PK_ROWS * (f.seg + 1 < f.n_segs ? PK_SEG : f.Kp - (f.n_segs - 1) * PK_SEG);
+    return f.seg + 1 < f.n_segs ? PK_ROWS * PK_SEG
+                                : PK_ROWS * (f.Kp - (f.n_segs - 1) * PK_SEG) + PK_SCALES;
 }
 __device__ __forceinline__ const int8_t* fetch_src(const Fetch& f) {
-    return f.W + size_t(f.g) * PK_ROWS * f.Kp + size_t(f.seg) * PK_SLOT;
+    return f.W + size_t(f.g) * pk_group_bytes(f.Kp) + size_t(f.seg) * PK_ROWS * PK_SEG;
 }
 
 __device__ __forceinline__ void fetch_issue(const Fetch& f, uint8_t* slot, uint64_t* bar) {
@@ -281,32 +283,23 @@ __device__ __forceinline__ void fetch_issue(const Fetch& f, uint8_t* slot, uint6
     bulk_g2s(slot, fetch_src(f), fetch_bytes(f), bar);
 }
 
-// Bulk prefetch of a future chunk into L2: the 126 MB L2 is the deep buffer
-// that keeps HBM streaming while stages stall on barriers and prologues.
-__device__ __forceinline__ void fetch_prefetch_l2(const Fetch& f) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(fetch_src(f)), "r"(fetch_bytes(f))
-                 : "memory");
-}
-
 struct Pipe {
     uint8_t* slots;     // this warp's ring
     uint64_t* bars;
-    uint32_t depth;     // slots in use (<= PK_DEPTH)
     uint32_t consumed;  // chunks consumed so far
     Fetch f;            // next chunk to load into the ring
-    Fetch pf;           // next chunk to prefetch into L2 (PK_L2_AHEAD ahead of f)
 };
 
 // Waits for the next chunk of this warp; returns its slot.
 __device__ __forceinline__ const uint8_t* pipe_wait(Pipe& p) {
-    const uint32_t sl = p.consumed % p.depth;
-    mbar_wait(&p.bars[sl], (p.consumed / p.depth) & 1);
+    const uint32_t sl = p.consumed % PK_DEPTH;
+    mbar_wait(&p.bars[sl], (p.consumed / PK_DEPTH) & 1);
     return p.slots + sl * PK_SLOT;
 }
 
 // Releases the chunk just consumed and refills its slot with the next one.
-__device__ __forceinline__ void pipe_release(const PkArgs& a, Pipe& p) {
-    const uint32_t sl = p.consumed % p.depth;
+__device__ __forceinline__ void pipe_release(const Sched& sc, Pipe& p) {
+    const uint32_t sl = p.consumed % PK_DEPTH;
     ++p.consumed;
     __syncwarp();
     if (!p.f.done) {
@@ -314,11 +307,7 @@ __device__ __forceinline__ void pipe_release(const PkArgs& a, Pipe& p) {
             fence_proxy_async();
             fetch_issue(p.f, p.slots + sl * PK_SLOT, &p.bars[sl]);
         }
-        fetch_advance(a, p.f);
-    }
-    if (!p.pf.done) {
-        if ((threadIdx.x & 31) == 0) fetch_prefetch_l2(p.pf);
-        fetch_advance(a, p.pf);
+        fetch_advance(sc, p.f);
     }
 }
 
@@ -328,11 +317,12 @@ __device__ __forceinline__ void pipe_release(const PkArgs& a, Pipe& p) {
 // trip (ncu: 46% of prologue stalls were stall_no_inst before this).
 
 // Attention output / FFN hidden vector: copy the producer-written planes.
-__device__ __noinline__ int prologue_plain(const PkArgs& a, const PkStage& st, uint32_t tag,
-                                           uint32_t* planes) {
-    const uint32_t K = st.K, Kw = st.Kp / 4;
-    const uint32_t flag = ld_cg32(st.in_flag);  // same round trip as the copy
-    copy_g2s(planes, st.in_planes, 3 * st.Kp);
+__device__ __noinline__ int prologue_plain(uint32_t K, uint32_t Kp, const int64_t* x,
+                                           const uint8_t* in_planes, const uint32_t* in_flag,
+                                           uint32_t tag, uint32_t* planes, Ctl* ctl) {
+    const uint32_t Kw = Kp / 4;
+    const uint32_t flag = ld_cg32(in_flag);  // same round trip as the copy
+    copy_g2s(planes, in_planes, 3 * Kp);
     if (__syncthreads_or(flag == tag) == 0) return 3;  // every element fits 3 limbs
     // wide input: 8 byte planes straight from the int64 vector
 #pragma unroll 1
@@ -342,94 +332,122 @@ __device__ __noinline__ int prologue_plain(const PkArgs& a, const PkStage& st, u
             uint32_t word = 0;
             for (int e = 0; e < 4; ++e) {
                 const uint32_t j = 4 * w + e;
-                const uint64_t v = j < K ? uint64_t(ld_cg64(st.x + j)) : 0;
+                const uint64_t v = j < K ? uint64_t(ld_cg64(x + j)) : 0;
                 word |= uint32_t((v >> (8 * k)) & 0xFF) << (8 * e);
             }
             planes[k * Kw + w] = word;
         }
     }
-    if (threadIdx.x == 0) atomicAdd(&a.ctl->stats[0], 1ull);
+    if (threadIdx.x == 0) atomicAdd(&ctl->stats[0], 1ull);
     __syncthreads();
     return 8;
 }
 
 // rmsnorm input: the residual stream (or the embedded token on layer 0)
 // staged in shared memory, normalised there, packed into planes.
-__device__ __noinline__ int prologue_norm(const PkArgs& a, const PkStage& st, uint32_t token,
-                                          int64_t* xb, uint32_t* planes, u128* red,
-                                          unsigned long long* tr) {
-    const uint32_t K = st.K, Kw = st.Kp / 4;
-    if (st.mode == MODE_EMBED) {  // embed_token, proj/src/engine.cpp:10-19
-        const int8_t* erow = a.embd + size_t(token) * K;
-        const int64_t es = a.embd_scales[token];
+// erow != nullptr selects the embedding (engine.cpp:10-19).
+__device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_unit, const int64_t* x,
+                                          const int64_t* gamma, const int8_t* erow, int64_t es,
+                                          int64_t* x_resid, int64_t* xb, uint32_t* planes, u128* red,
+                                          const int64_t* seeds, Ctl* ctl, unsigned long long* tr) {
+    const uint32_t Kw = Kp / 4;
+    if (erow) {
         for (uint32_t j = threadIdx.x; j < K; j += blockDim.x) {
             const int64_t v = int64_t(uint64_t(int64_t(erow[j])) * uint64_t(es));
             xb[j] = v;
-            if (blockIdx.x == 0) a.x_resid[j] = v;
+            if (x_resid) x_resid[j] = v;
         }
     } else {
-        copy_g2s(xb, st.x, K * 8);
+        copy_g2s(xb, x, K * 8);
     }
     __syncthreads();
     if (tr) tr[4] = clock64();
-    // ms = ((sum x^2) / n) >> 16 in int128, r = inv_sqrt(ms + 1) (kernels.cpp:56-68)
-    u128 ss = 0;
+    // ms = ((sum x^2) / n) >> 16 in int128, r = inv_sqrt(ms + 1) (kernels.cpp:56-68).
+    // Squares of |x| < 2^31 are < 2^62: split into 21-bit chunks whose per-
+    // warp sums fit 32 bits, so three REDUX.SUM give the exact warp totals;
+    // any larger element goes through the 128-bit path.
+    __shared__ uint32_t s_part[PK_WARPS][3];
+    __shared__ int s_big;
+    __shared__ int64_t s_r;
+    if (threadIdx.x == 0) s_big = 0;
+    uint32_t c0 = 0, c1 = 0, c2 = 0;
+    u128 big = 0;
     int small = 1;
 #pragma unroll 4
     for (uint32_t j = threadIdx.x; j < K; j += blockDim.x) {
         const int64_t v = xb[j];
         if (fits_i32(v)) {
-            ss += uint64_t(int64_t(int32_t(v)) * int32_t(v));  // one IMAD.WIDE
+            const uint64_t q = uint64_t(int64_t(int32_t(v)) * int32_t(v));
+            c0 += uint32_t(q) & 0x1FFFFFu;
+            c1 += uint32_t(q >> 21) & 0x1FFFFFu;
+            c2 += uint32_t(q >> 42);
         } else {
-            ss += mul_full(v, v);
+            big += mul_full(v, v);
             small = 0;
         }
     }
-    ss = block_sum_u128(ss, red);
+    c0 = __reduce_add_sync(0xffffffffu, c0);
+    c1 = __reduce_add_sync(0xffffffffu, c1);
+    c2 = __reduce_add_sync(0xffffffffu, c2);
+    if ((threadIdx.x & 31) == 0) {
+        s_part[threadIdx.x >> 5][0] = c0;
+        s_part[threadIdx.x >> 5][1] = c1;
+        s_part[threadIdx.x >> 5][2] = c2;
+    }
+    if (!small) s_big = 1;
+    __syncthreads();
+    uint64_t t0 = 0, t1 = 0, t2 = 0;
+#pragma unroll
+    for (int w = 0; w < PK_WARPS; ++w) {
+        t0 += s_part[w][0];
+        t1 += s_part[w][1];
+        t2 += s_part[w][2];
+    }
+    u128 ss = u128(t0) + (u128(t1) << 21) + (u128(t2) << 42);
+    const bool any_big = s_big;
+    if (any_big) ss += block_sum_u128(big, red);  // uniform branch
     if (tr) tr[5] = clock64();
     // one thread computes r; the others wait instead of contending for the
     // multiplier with 255 redundant copies of the 128-bit Newton iteration
-    __shared__ int64_t s_r;
     if (threadIdx.x == 0) {
         int64_t ms;
         if ((ss >> 63) == 0) ms = int64_t((uint64_t(ss) / K) >> 16);  // usual case: one u64 divide
         else ms = int64_t((i128(ss) / i128(K)) >> 16);
         if (ms + 1 <= 0) {
-            atomicOr(&a.ctl->err, 1u);
+            atomicOr(&ctl->err, 1u);
             s_r = 0;
         } else {
-            s_r = inv_sqrt_q16(ms + 1, a.seeds);
+            s_r = inv_sqrt_q16(ms + 1, seeds);
         }
     }
-    small = __syncthreads_and(small);
+    __syncthreads();
     const int64_t r_inv = s_r;
     if (tr) tr[6] = clock64();
-    small &= fits_i32(r_inv) & st.gamma_unit;
+    const bool fast = !any_big && fits_i32(r_inv) && gamma_unit;
     int fits = 1;
 #pragma unroll 2
     for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
-        uint32_t w0 = 0, w1 = 0, w2 = 0;
+        uint32_t lo[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const uint32_t j = 4 * w + e;
             int64_t v = 0;
             if (j < K) {
-                if (small) {
+                if (fast) {
                     v = mul16_small(xb[j], r_inv);
                 } else {
                     v = mul16(xb[j], r_inv);
-                    if (!st.gamma_unit) v = mul16(v, ld_cg64(st.gamma + j));  // mul16(v, ONE) == v
+                    if (!gamma_unit) v = mul16(v, ld_cg64(gamma + j));  // mul16(v, ONE) == v
                 }
             }
             xb[j] = v;
-            fits &= (v >= -(int64_t(1) << 23)) & (v < (int64_t(1) << 23));
-            w0 |= uint32_t(v & 0xFF) << (8 * e);
-            w1 |= uint32_t((v >> 8) & 0xFF) << (8 * e);
-            w2 |= uint32_t((v >> 16) & 0xFF) << (8 * e);
+            fits &= uint64_t(v + (int64_t(1) << 23)) < (uint64_t(1) << 24);  // -2^23 <= v < 2^23
+            lo[e] = uint32_t(v);
         }
-        planes[w] = w0;
-        planes[Kw + w] = w1;
-        planes[2 * Kw + w] = w2;
+        // bytes 0, 1, 2 of the four elements -> one word per plane
+        planes[w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0040), __byte_perm(lo[2], lo[3], 0x0040), 0x5410);
+        planes[Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0051), __byte_perm(lo[2], lo[3], 0x0051), 0x5410);
+        planes[2 * Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0062), __byte_perm(lo[2], lo[3], 0x0062), 0x5410);
     }
     fits = __syncthreads_and(fits);
     if (tr) tr[7] = clock64();
@@ -442,7 +460,7 @@ __device__ __noinline__ int prologue_norm(const PkArgs& a, const PkStage& st, ui
             for (int e = 0; e < 4; ++e) word |= uint32_t((uint64_t(xb[4 * w + e]) >> (8 * k)) & 0xFF) << (8 * e);
             planes[k * Kw + w] = word;
         }
-    if (threadIdx.x == 0) atomicAdd(&a.ctl->stats[0], 1ull);
+    if (threadIdx.x == 0) atomicAdd(&ctl->stats[0], 1ull);
     __syncthreads();
     return 8;
 }
@@ -475,23 +493,19 @@ __device__ __forceinline__ void reduce4(uint64_t (&v)[PK_ROWS]) {
 }
 
 template <int L>
-__device__ __forceinline__ void group_dot(const PkArgs& a, Pipe& p, const PkStage& st,
-                                          const uint32_t* planes, uint64_t (&out)[PK_ROWS]) {
+__device__ __forceinline__ void group_dot(const Sched& sc, Pipe& p, uint32_t Kp, uint32_t n_segs,
+                                          const uint32_t* planes, uint64_t (&out)[PK_ROWS],
+                                          int64_t& scale) {
     const int lane = threadIdx.x & 31;
-    if (a.debug & 4) {  // diagnostic: no weight streaming at all (results are garbage)
-#pragma unroll
-        for (int r = 0; r < PK_ROWS; ++r) out[r] = 0;
-        return;
-    }
-    const uint32_t Kw = st.Kp / 4;
+    const uint32_t Kw = Kp / 4;
     int32_t acc[PK_ROWS][L];
 #pragma unroll
     for (int r = 0; r < PK_ROWS; ++r)
 #pragma unroll
         for (int k = 0; k < L; ++k) acc[r][k] = 0;
-    for (uint32_t s = 0; s < st.n_segs; ++s) {
+    for (uint32_t s = 0; s < n_segs; ++s) {
         const uint8_t* slot = pipe_wait(p);
-        const uint32_t w = s + 1 < st.n_segs ? PK_SEG : st.Kp - (st.n_segs - 1) * PK_SEG;
+        const uint32_t w = s + 1 < n_segs ? PK_SEG : Kp - (n_segs - 1) * PK_SEG;
         const uint32_t k0 = s * PK_SEG;
         for (uint32_t c = lane * 16; c < w; c += 512) {
             uint4 xl[L];
@@ -513,7 +527,9 @@ __device__ __forceinline__ void group_dot(const PkArgs& a, Pipe& p, const PkStag
                 acc[r][L - 1] = dp4a_ss(wv.w, xl[L - 1].w, acc[r][L - 1]);
             }
         }
-        pipe_release(a, p);
+        if (s + 1 == n_segs)  // lane r < 4 takes row r's scale from the chunk tail
+            scale = lane < PK_ROWS ? *reinterpret_cast<const int64_t*>(slot + PK_ROWS * w + 8 * lane) : 0;
+        pipe_release(sc, p);
     }
 #pragma unroll
     for (int r = 0; r < PK_ROWS; ++r) {
@@ -525,52 +541,54 @@ __device__ __forceinline__ void group_dot(const PkArgs& a, Pipe& p, const PkStag
     reduce4(out);
 }
 
+// Everything the GEMV loop needs, by value (registers).
+struct GemvRT {
+    uint32_t epi, rows, Kp, n_groups, n_segs, out_pitch;
+    int64_t* y;
+    uint8_t* out_planes;
+    uint32_t* out_flag;
+    int64_t* lrow;            // EPI_ARGMAX: this step's logits row
+    const int64_t* lut;
+};
+
 // All of this CTA's row groups of a GEMV stage, epilogues fused.
 template <int L>
-__device__ void run_gemv(const PkArgs& a, Pipe& p, const PkStage& st, const uint32_t* planes,
-                         uint32_t pos, uint32_t tag, int64_t& best_v, uint32_t& best_i) {
+__device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT& g_,
+                                         const uint32_t* planes, uint32_t tag, int64_t& best_v,
+                                         uint32_t& best_i) {
     const int lane = threadIdx.x & 31;
     uint32_t g_lo, g_hi;
-    cta_range(st.n_groups, g_lo, g_hi);
-    int64_t* lrow = nullptr;
-    if (st.epi == EPI_ARGMAX) {
-        uint32_t slot = pos - a.ctl->logit_base;
-        slot = slot < a.ctl->keep_cap ? slot : a.ctl->keep_cap;
-        lrow = st.y + size_t(slot) * st.rows;
-    }
+    cta_range(g_.n_groups, g_lo, g_hi);
     for (uint32_t g = g_lo + (threadIdx.x >> 5); g < g_hi; g += PK_WARPS) {
         const uint32_t r0 = g * PK_ROWS;
-        int64_t resid = 0, scale = 0;  // issued now, consumed after the dot product
-        if (lane < PK_ROWS && r0 + lane < st.rows) {
-            scale = st.scales[r0 + lane];
-            if (st.epi == EPI_RESID) resid = ld_cg64(st.y + r0 + lane);
-        }
+        int64_t resid = 0, scale = 0;  // residual issued now, consumed after the dot product
+        if (g_.epi == EPI_RESID && lane < PK_ROWS && r0 + lane < g_.rows) resid = ld_cg64(g_.y + r0 + lane);
         uint64_t v[PK_ROWS];
-        group_dot<L>(a, p, st, planes, v);
-        if (st.epi == EPI_SILU) {
+        group_dot<L>(sc, p, g_.Kp, g_.n_segs, planes, v, scale);
+        if (g_.epi == EPI_SILU) {
             // rows (2i, 2i+1) = (gate_i, up_i): lanes 0,1 finish pairs 0,1
             const int64_t s_g = __shfl_sync(0xffffffffu, scale, 2 * (lane & 1));
             const int64_t s_u = __shfl_sync(0xffffffffu, scale, 2 * (lane & 1) + 1);
-            if (lane < 2 && r0 + 2 * lane + 1 < st.rows) {
+            if (lane < 2 && r0 + 2 * lane + 1 < g_.rows) {
                 const uint32_t row = r0 + 2 * lane;
                 const int64_t gs = scale_row(int64_t(lane ? v[2] : v[0]), s_g);
                 const int64_t us = scale_row(int64_t(lane ? v[3] : v[1]), s_u);
-                const int64_t h = mul16(silu_q16(gs, a.exp_lut), us);
-                st.y[row / 2] = h;
-                emit_planes(st.out_planes, st.out_pitch, st.out_flag, tag, row / 2, h);
+                const int64_t h = mul16(silu_q16(gs, g_.lut), us);
+                g_.y[row / 2] = h;
+                emit_planes(g_.out_planes, g_.out_pitch, g_.out_flag, tag, row / 2, h);
             }
-        } else if (lane < PK_ROWS && r0 + lane < st.rows) {
+        } else if (lane < PK_ROWS && r0 + lane < g_.rows) {
             const uint32_t row = r0 + lane;
             uint64_t acc = v[0];
 #pragma unroll
             for (int r = 1; r < PK_ROWS; ++r) acc = lane == r ? v[r] : acc;
             const int64_t val = scale_row(int64_t(acc), scale);
-            if (st.epi == EPI_STORE) {
-                st.y[row] = val;
-            } else if (st.epi == EPI_RESID) {
-                st.y[row] = add_clamp(resid, val);
+            if (g_.epi == EPI_STORE) {
+                g_.y[row] = val;
+            } else if (g_.epi == EPI_RESID) {
+                g_.y[row] = add_clamp(resid, val);
             } else {  // EPI_ARGMAX
-                lrow[row] = val;
+                g_.lrow[row] = val;
                 if (better(val, row, best_v, best_i)) {
                     best_v = val;
                     best_i = row;
@@ -581,15 +599,14 @@ __device__ void run_gemv(const PkArgs& a, Pipe& p, const PkStage& st, const uint
 }
 
 // The 8-limb instantiation only runs on out-of-range activations: out of line.
-__device__ __noinline__ void run_gemv_wide(const PkArgs& a, Pipe& p, const PkStage& st,
-                                           const uint32_t* planes, uint32_t pos, uint32_t tag,
-                                           int64_t& best_v, uint32_t& best_i) {
-    run_gemv<8>(a, p, st, planes, pos, tag, best_v, best_i);
+__device__ __noinline__ void run_gemv_wide(Sched sc, Pipe& p, GemvRT g_, const uint32_t* planes,
+                                           uint32_t tag, int64_t& best_v, uint32_t& best_i) {
+    run_gemv<8>(sc, p, g_, planes, tag, best_v, best_i);
 }
 
 // ---- the kernel -------------------------------------------------------------------
 
-__global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs a) {
+__global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const PkArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* slots = smem;                                                // [warps][depth][SLOT]
     uint8_t* stage_mem = smem + PK_WARPS * PK_DEPTH * PK_SLOT;            // planes_bytes
@@ -597,17 +614,20 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs
     __shared__ u128 red[32];
     __shared__ int64_t s_bv[PK_WARPS];
     __shared__ uint32_t s_bi[PK_WARPS];
+    __shared__ __align__(16) PkStage s_st[2];
+    // exp LUT and inv-sqrt seeds live in shared memory for the whole launch
+    __shared__ int64_t s_lut[257], s_seeds[64];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Sched sc{a.stages, a.n_layer_stages, a.n_steps, a.n_prefill};
+    Ctl* const ctl = a.ctl;
     if (threadIdx.x < PK_WARPS * PK_DEPTH) mbar_init(&bars[threadIdx.x], 1);
-    // exp LUT and inv-sqrt seeds live in shared memory for the whole launch:
-    // a global load under a saturated HBM costs microseconds
-    __shared__ int64_t s_lut[257], s_seeds[64];
     for (int i = threadIdx.x; i < 257; i += PK_THREADS) s_lut[i] = a.exp_lut[i];
     if (threadIdx.x < 64) s_seeds[threadIdx.x] = a.seeds[threadIdx.x];
-    a.exp_lut = s_lut;
-    a.seeds = s_seeds;
-    a.attn.exp_lut = s_lut;
+    constexpr int kStWords = sizeof(PkStage) / 4;
+    static_assert(kStWords <= PK_THREADS, "stage descriptor too large");
+    if (threadIdx.x < kStWords)
+        reinterpret_cast<uint32_t*>(&s_st[0])[threadIdx.x] = reinterpret_cast<const uint32_t*>(sc.stages)[threadIdx.x];
     fence_proxy_async();
     __syncthreads();
 
@@ -616,85 +636,78 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs
     p.slots = slots + size_t(warp) * PK_DEPTH * PK_SLOT;
     p.bars = bars + warp * PK_DEPTH;
     p.consumed = 0;
-    p.depth = a.depth ? min(a.depth, uint32_t(PK_DEPTH)) : PK_DEPTH;
     p.f.step = 0;
     p.f.stage = 0;
-    p.f.done = a.n_steps == 0;
+    p.f.done = sc.n_steps == 0;
     if (!p.f.done) {
-        fetch_load(a, p.f);
-        fetch_settle(a, p.f);
+        fetch_load(sc, p.f);
+        fetch_settle(sc, p.f);
     }
-    if (a.debug & 4) p.f.done = true;
-    p.pf = p.f;
-    if (!a.l2_ahead) p.pf.done = true;
-    for (uint32_t d = 0; d < PK_DEPTH + a.l2_ahead && a.l2_ahead && !p.pf.done; ++d) {
-        if (lane == 0) fetch_prefetch_l2(p.pf);
-        fetch_advance(a, p.pf);
-    }
-    for (uint32_t d = 0; d < p.depth && !p.f.done; ++d) {
+    for (uint32_t d = 0; d < PK_DEPTH && !p.f.done; ++d) {
         if (lane == 0) fetch_issue(p.f, p.slots + d * PK_SLOT, &p.bars[d]);
-        fetch_advance(a, p.f);
+        fetch_advance(sc, p.f);
     }
 
-    uint32_t pos = a.ctl->pos;
+    uint32_t pos = ctl->pos;
+    const uint32_t logit_base = ctl->logit_base, keep_cap = ctl->keep_cap;
     uint32_t token = a.tokens[pos];
-    uint32_t nbar = 0;
-    __shared__ __align__(16) PkStage s_st[2];
-    constexpr int kStWords = sizeof(PkStage) / 4;
-    static_assert(kStWords <= PK_THREADS, "stage descriptor too large");
-    uint32_t cur = 0;
-    __syncthreads();
-    if (threadIdx.x < kStWords)
-        reinterpret_cast<uint32_t*>(&s_st[0])[threadIdx.x] = reinterpret_cast<const uint32_t*>(a.stages)[threadIdx.x];
-    __syncthreads();
+    uint32_t nbar = 0, cur = 0;
 
-    for (uint32_t step = 0; step < a.n_steps; ++step) {
-        const uint32_t nst = stages_in_step(a, step);
+    for (uint32_t step = 0; step < sc.n_steps; ++step) {
+        const uint32_t nst = stages_in_step(sc, step);
         const uint32_t tag = step + 1;
         int64_t best_v = INT64_MIN;
         uint32_t best_i = 0xFFFFFFFFu;
         for (uint32_t si = 0; si < nst; ++si) {
-            const PkStage& st = s_st[cur];
+            const PkStage st = s_st[cur];  // by value: registers for the whole stage
             // the next stage's descriptor: loaded now, stored before the barrier
             uint32_t next_word = 0;
             if (threadIdx.x < kStWords)
-                next_word = reinterpret_cast<const uint32_t*>(a.stages + (si + 1 < nst ? si + 1 : 0))[threadIdx.x];
-            const bool tr = a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nbar < a.trace_cap;
-            if (tr) a.trace[12 * nbar + 8] = clock64();
-            if (tr) a.trace[12 * nbar + 0] = globaltimer();
+                next_word = reinterpret_cast<const uint32_t*>(sc.stages + (si + 1 < nst ? si + 1 : 0))[threadIdx.x];
+            unsigned long long* tr =
+                a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nbar < a.trace_cap ? a.trace + 12 * nbar : nullptr;
+            if (tr) {
+                tr[8] = clock64();
+                tr[0] = globaltimer();
+            }
             if (st.kind == SK_ATTN) {
                 AttnArgs t = a.attn;
                 t.kc += size_t(st.layer) * a.kv_layer_stride;
                 t.vc += size_t(st.layer) * a.kv_layer_stride;
-                for (uint32_t h = blockIdx.x; h < t.H; h += gridDim.x) {
-                    if (a.debug & 2) {  // i-cache experiment: a warm second call is what gets traced
-                        attn_head(t, h, pos, reinterpret_cast<int64_t*>(stage_mem), red, st.out_planes,
-                                  st.out_pitch, st.out_flag, tag, true, nullptr);
-                        if (tr && h == 0) a.trace[12 * nbar + 8] = clock64();
-                    }
+                t.exp_lut = s_lut;
+                for (uint32_t h = blockIdx.x; h < t.H; h += gridDim.x)
                     attn_head(t, h, pos, reinterpret_cast<int64_t*>(stage_mem), red, st.out_planes,
-                              st.out_pitch, st.out_flag, tag, true,
-                              tr && h == 0 ? a.trace + 12 * nbar : nullptr);
-                }
+                              st.out_pitch, st.out_flag, tag, true, tr && h == 0 ? tr : nullptr);
             } else {
                 uint32_t* planes;
                 int L;
                 if (st.mode == MODE_PLAIN) {
                     planes = reinterpret_cast<uint32_t*>(stage_mem);
-                    L = prologue_plain(a, st, tag, planes);
+                    L = prologue_plain(st.K, st.Kp, st.x, st.in_planes, st.in_flag, tag, planes, ctl);
                 } else {
                     int64_t* xb = reinterpret_cast<int64_t*>(stage_mem);
                     planes = reinterpret_cast<uint32_t*>(xb + st.Kp);
-                    if (a.debug & 1) {  // i-cache experiment
-                        prologue_norm(a, st, token, xb, planes, red, nullptr);
-                        if (tr) a.trace[12 * nbar + 8] = clock64();
-                    }
-                    L = prologue_norm(a, st, token, xb, planes, red, tr ? a.trace + 12 * nbar : nullptr);
+                    const bool embed = st.mode == MODE_EMBED;
+                    L = prologue_norm(st.K, st.Kp, st.gamma_unit != 0, st.x, st.gamma,
+                                      embed ? a.embd + size_t(token) * st.K : nullptr,
+                                      embed ? a.embd_scales[token] : 0,
+                                      embed && blockIdx.x == 0 ? a.x_resid : nullptr, xb, planes, red,
+                                      s_seeds, ctl, tr);
                 }
-                if (tr) a.trace[12 * nbar + 1] = globaltimer();
-                if (L == 3) run_gemv<3>(a, p, st, planes, pos, tag, best_v, best_i);
-                else run_gemv_wide(a, p, st, planes, pos, tag, best_v, best_i);
-                if (tr) a.trace[12 * nbar + 2] = globaltimer();
+                if (tr) tr[1] = globaltimer();
+                GemvRT g_;
+                g_.epi = st.epi; g_.rows = st.rows; g_.Kp = st.Kp; g_.n_groups = st.n_groups;
+                g_.n_segs = st.n_segs; g_.out_pitch = st.out_pitch; g_.y = st.y;
+                g_.out_planes = st.out_planes; g_.out_flag = st.out_flag; g_.lut = s_lut;
+                g_.lrow = nullptr;
+                if (st.epi == EPI_ARGMAX) {
+                    uint32_t slot = pos - logit_base;
+                    slot = slot < keep_cap ? slot : keep_cap;
+                    g_.lrow = st.y + size_t(slot) * st.rows;
+                }
+                if (L == 3) run_gemv<3>(sc, p, g_, planes, tag, best_v, best_i);
+                else run_gemv_wide(sc, p, g_, planes, tag, best_v, best_i);
+                if (tr) tr[2] = globaltimer();
                 if (st.epi == EPI_ARGMAX) {
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
@@ -712,21 +725,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs
                     }
                 }
             }
-            if (tr) a.trace[12 * nbar + 3] = globaltimer();
+            if (tr) tr[3] = globaltimer();
+            __syncthreads();  // everyone has its register copy of s_st[cur]; safe to overwrite the other
             if (threadIdx.x < kStWords) reinterpret_cast<uint32_t*>(&s_st[cur ^ 1])[threadIdx.x] = next_word;
             cur ^= 1;
-            // Idle-time prefetch: while this CTA waits at the barrier and runs
-            // the next prologue, HBM fills L2 with the chunks after its ring.
-            if (a.idle_l2) {
-                Fetch q = p.f;
-                for (uint32_t i = 0; i < a.idle_l2 && !q.done; ++i) {
-                    if (lane == 0) fetch_prefetch_l2(q);
-                    fetch_advance(a, q);
-                }
-            }
-            if (!grid_sync(a.bar, a.ctl, nbar++, a.bar_mode)) return;
+            if (!grid_sync(a.bar, ctl, nbar++)) return;
         }
-        if (step >= a.n_prefill) {
+        if (step >= sc.n_prefill) {
             // every CTA reduces the lm_head partials itself (no extra barrier)
             int64_t bv = INT64_MIN;
             uint32_t bi = 0xFFFFFFFFu;
@@ -753,7 +758,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(PkArgs
         }
         ++pos;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->pos = pos;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->pos = pos;
 }
 
 }  // namespace dimg::dev
