@@ -262,6 +262,7 @@ struct dimg_session {
     uint8_t* planes_att;   // [3][Kd] 3-limb planes of the attention output
     uint8_t* planes_h;     // [3][Kf] 3-limb planes of the FFN hidden vector
     uint32_t* flags;       // [2L] "needs > 3 limbs" tags (att, h) per layer
+    unsigned long long* ssq;  // [2L] sums of squares of x after wo / after down (per layer)
     PkStage* stages;   // [5L + 1] device
     std::vector<PkStage> host_stages;
     PkStage* probe_stages = nullptr;  // [L] scratch program for time_kernel
@@ -310,30 +311,44 @@ std::vector<PkStage> step_program(const dimg_session& s) {
         const auto& lw = m.layers[l];
         uint32_t* f_att = s.flags + 2 * l;
         uint32_t* f_h = s.flags + 2 * l + 1;
-        p.push_back(gemv_stage(lw.qkv, l == 0 ? MODE_EMBED : MODE_NORM, EPI_STORE, s.x, lw.attn_norm,
-                               s.qkv, lw.attn_unit));
+        // sums of squares of x: after wo(l) -> gu(l); after down(l) -> qkv(l+1) / head
+        unsigned long long* ssq_wo = s.ssq + 2 * l;
+        unsigned long long* ssq_dn = s.ssq + 2 * l + 1;
+        unsigned long long* ssq_prev = l > 0 ? s.ssq + 2 * l - 1 : nullptr;
+        PkStage qkv = gemv_stage(lw.qkv, l == 0 ? MODE_EMBED : MODE_NORM, EPI_STORE, s.x, lw.attn_norm,
+                                 s.qkv, lw.attn_unit);
+        qkv.ssq_in = ssq_prev;
+        if (l == 0) qkv.ssq_clear = s.ssq + 2 * m.L - 1;  // consumed by the previous step's head
+        p.push_back(qkv);
         PkStage at{};
         at.kind = SK_ATTN;
         at.layer = l;
         at.out_planes = s.planes_att;
         at.out_pitch = m.Kd;
         at.out_flag = f_att;
+        at.ssq_clear = ssq_prev;
         p.push_back(at);
         PkStage wo = gemv_stage(lw.wo, MODE_PLAIN, EPI_RESID, s.att, nullptr, s.x);
         wo.in_planes = s.planes_att;
         wo.in_flag = f_att;
+        wo.ssq_out = ssq_wo;
         p.push_back(wo);
         PkStage gu = gemv_stage(lw.gu, MODE_NORM, EPI_SILU, s.x, lw.ffn_norm, s.h, lw.ffn_unit);
         gu.out_planes = s.planes_h;
         gu.out_pitch = m.Kf;
         gu.out_flag = f_h;
+        gu.ssq_in = ssq_wo;
         p.push_back(gu);
         PkStage dn = gemv_stage(lw.down, MODE_PLAIN, EPI_RESID, s.h, nullptr, s.x);
         dn.in_planes = s.planes_h;
         dn.in_flag = f_h;
+        dn.ssq_out = ssq_dn;
+        dn.ssq_clear = ssq_wo;
         p.push_back(dn);
     }
-    p.push_back(gemv_stage(m.head, MODE_NORM, EPI_ARGMAX, s.x, m.final_norm, s.logits, m.final_unit));
+    PkStage head = gemv_stage(m.head, MODE_NORM, EPI_ARGMAX, s.x, m.final_norm, s.logits, m.final_unit);
+    head.ssq_in = s.ssq + 2 * m.L - 1;
+    p.push_back(head);
     return p;
 }
 
@@ -385,6 +400,7 @@ void launch_pk(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
 
     CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned int), s.stream));
     CK(cudaMemsetAsync(s.flags, 0, size_t(2) * s.m->L * sizeof(uint32_t), s.stream));
+    CK(cudaMemsetAsync(s.ssq, 0, size_t(2) * s.m->L * sizeof(unsigned long long), s.stream));
     void* params[] = {&a};
     CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(decode_persistent_kernel), dim3(s.grid),
                                    dim3(PK_THREADS), params, s.smem, s.stream));
@@ -593,6 +609,7 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         CK(cudaMemsetAsync(s->planes_att, 0, size_t(3) * m->Kd, s->stream));
         CK(cudaMemsetAsync(s->planes_h, 0, size_t(3) * m->Kf, s->stream));
         s->flags = s->mem.alloc<uint32_t>(2 * size_t(m->L));
+        s->ssq = s->mem.alloc<unsigned long long>(2 * size_t(m->L));
         s->host_stages = step_program(*s);
         // shared staging: rmsnorm = vector + gains + up to 8 planes; plain =
         // up to 8 planes; attention = head scratch + score strip
@@ -759,6 +776,9 @@ dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, flo
                                     : s->host_stages[5 * (i % m.L) + idx[which]];
             if (st.mode == MODE_EMBED) st.mode = MODE_NORM;
             if (st.epi == EPI_ARGMAX) st.epi = EPI_STORE;  // the probe never appends tokens
+            st.ssq_in = nullptr;  // the probe has no producer stages: sums computed in place
+            st.ssq_out = nullptr;
+            st.ssq_clear = nullptr;
             prog.push_back(st);
         }
         if (!s->probe_stages || n > 0) {

@@ -63,6 +63,9 @@ struct PkStage {
     uint32_t* out_flag;
     uint32_t out_pitch;
     uint32_t pad2;
+    unsigned long long* ssq_out;  // EPI_RESID: sum of the new x^2 (exact: |x| <= 2^24 after the clamp)
+    const unsigned long long* ssq_in;  // MODE_NORM after a RESID stage: that sum (nullptr = compute it)
+    unsigned long long* ssq_clear;     // accumulator the previous stage consumed: CTA 0 re-zeroes it
 };
 
 struct PkArgs {
@@ -349,8 +352,58 @@ __device__ __noinline__ int prologue_plain(uint32_t K, uint32_t Kp, const int64_
 __device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_unit, const int64_t* x,
                                           const int64_t* gamma, const int8_t* erow, int64_t es,
                                           int64_t* x_resid, int64_t* xb, uint32_t* planes, u128* red,
-                                          const int64_t* seeds, Ctl* ctl, unsigned long long* tr) {
+                                          const int64_t* seeds, Ctl* ctl, unsigned long long* tr,
+                                          const unsigned long long* ssq_in) {
     const uint32_t Kw = Kp / 4;
+    __shared__ int64_t s_r;
+    if (ssq_in && gamma_unit) {
+        // The producer (a residual stage) already summed the squares of the
+        // clamped vector: thread 0 computes r while the copy is in flight,
+        // and every |x| <= 2^24, r <= 2^24 -> 32-bit products throughout.
+        if (threadIdx.x == 0) {
+            const uint64_t ss = uint64_t(ld_cg64(reinterpret_cast<const int64_t*>(ssq_in)));
+            const int64_t ms = int64_t((ss / K) >> 16);
+            s_r = inv_sqrt_q16(ms + 1, seeds);  // ms >= 0: ms + 1 > 0
+        }
+        copy_g2s(xb, x, K * 8);
+        __syncthreads();
+        if (tr) tr[4] = tr[5] = clock64();
+        const int64_t r_inv = s_r;
+        if (tr) tr[6] = clock64();
+        int fits = 1;
+#pragma unroll 4
+        for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
+            const int4 e01 = *reinterpret_cast<const int4*>(xb + 4 * w);
+            const int4 e23 = *reinterpret_cast<const int4*>(xb + 4 * w + 2);
+            const int32_t xs[4] = {e01.x, e01.z, e23.x, e23.z};  // low words (|x| < 2^31)
+            uint32_t lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int64_t v = 4 * w + e < K ? (int64_t(xs[e]) * int32_t(r_inv)) >> 16 : 0;
+                fits &= uint64_t(v + (int64_t(1) << 23)) < (uint64_t(1) << 24);
+                lo[e] = uint32_t(v);
+                xb[4 * w + e] = v;
+            }
+            planes[w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0040), __byte_perm(lo[2], lo[3], 0x0040), 0x5410);
+            planes[Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0051), __byte_perm(lo[2], lo[3], 0x0051), 0x5410);
+            planes[2 * Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0062), __byte_perm(lo[2], lo[3], 0x0062), 0x5410);
+        }
+        fits = __syncthreads_and(fits);
+        if (tr) tr[7] = clock64();
+        if (fits) return 3;
+        // wide (needs > 3 limbs): 8 planes from the normalised vector
+#pragma unroll 1
+        for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x)
+#pragma unroll 1
+            for (int k = 3; k < 8; ++k) {
+                uint32_t word = 0;
+                for (int e = 0; e < 4; ++e) word |= uint32_t((uint64_t(xb[4 * w + e]) >> (8 * k)) & 0xFF) << (8 * e);
+                planes[k * Kw + w] = word;
+            }
+        if (threadIdx.x == 0) atomicAdd(&ctl->stats[0], 1ull);
+        __syncthreads();
+        return 8;
+    }
     if (erow) {
         for (uint32_t j = threadIdx.x; j < K; j += blockDim.x) {
             const int64_t v = int64_t(uint64_t(int64_t(erow[j])) * uint64_t(es));
@@ -368,7 +421,6 @@ __device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_un
     // any larger element goes through the 128-bit path.
     __shared__ uint32_t s_part[PK_WARPS][3];
     __shared__ int s_big;
-    __shared__ int64_t s_r;
     if (threadIdx.x == 0) s_big = 0;
     uint32_t c0 = 0, c1 = 0, c2 = 0;
     u128 big = 0;
@@ -549,6 +601,7 @@ struct GemvRT {
     uint32_t* out_flag;
     int64_t* lrow;            // EPI_ARGMAX: this step's logits row
     const int64_t* lut;
+    unsigned long long* ssq;  // EPI_RESID: sum-of-squares accumulator
 };
 
 // All of this CTA's row groups of a GEMV stage, epilogues fused.
@@ -565,6 +618,7 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
         if (g_.epi == EPI_RESID && lane < PK_ROWS && r0 + lane < g_.rows) resid = ld_cg64(g_.y + r0 + lane);
         uint64_t v[PK_ROWS];
         group_dot<L>(sc, p, g_.Kp, g_.n_segs, planes, v, scale);
+        uint64_t sq = 0;
         if (g_.epi == EPI_SILU) {
             // rows (2i, 2i+1) = (gate_i, up_i): lanes 0,1 finish pairs 0,1
             const int64_t s_g = __shfl_sync(0xffffffffu, scale, 2 * (lane & 1));
@@ -586,7 +640,9 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
             if (g_.epi == EPI_STORE) {
                 g_.y[row] = val;
             } else if (g_.epi == EPI_RESID) {
-                g_.y[row] = add_clamp(resid, val);
+                const int64_t x = add_clamp(resid, val);
+                g_.y[row] = x;
+                sq = uint64_t(x * x);  // |x| <= 2^24: x^2 < 2^49, 8192 rows < 2^62
             } else {  // EPI_ARGMAX
                 g_.lrow[row] = val;
                 if (better(val, row, best_v, best_i)) {
@@ -594,6 +650,11 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
                     best_i = row;
                 }
             }
+        }
+        if (g_.epi == EPI_RESID && g_.ssq) {  // this group's rows -> the next rmsnorm's sum of squares
+            sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+            sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+            if (lane == 0 && sq) atomicAdd(g_.ssq, (unsigned long long)sq);
         }
     }
 }
@@ -670,6 +731,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 tr[8] = clock64();
                 tr[0] = globaltimer();
             }
+            if (st.ssq_clear && blockIdx.x == 0 && threadIdx.x == 0) *st.ssq_clear = 0;
             if (st.kind == SK_ATTN) {
                 AttnArgs t = a.attn;
                 t.kc += size_t(st.layer) * a.kv_layer_stride;
@@ -692,7 +754,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                                       embed ? a.embd + size_t(token) * st.K : nullptr,
                                       embed ? a.embd_scales[token] : 0,
                                       embed && blockIdx.x == 0 ? a.x_resid : nullptr, xb, planes, red,
-                                      s_seeds, ctl, tr);
+                                      s_seeds, ctl, tr, st.ssq_in);
                 }
                 if (tr) tr[1] = globaltimer();
                 GemvRT g_;
@@ -700,6 +762,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 g_.n_segs = st.n_segs; g_.out_pitch = st.out_pitch; g_.y = st.y;
                 g_.out_planes = st.out_planes; g_.out_flag = st.out_flag; g_.lut = s_lut;
                 g_.lrow = nullptr;
+                g_.ssq = st.ssq_out;
                 if (st.epi == EPI_ARGMAX) {
                     uint32_t slot = pos - logit_base;
                     slot = slot < keep_cap ? slot : keep_cap;
