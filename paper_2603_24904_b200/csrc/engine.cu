@@ -386,6 +386,8 @@ PkArgs pk_args(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     t.inv_scale = m.inv_scale;
     t.exp_lut = m.ctx->exp_lut;
     a.kv_layer_stride = size_t(m.H) * m.cfg.max_ctx * m.dh;
+    // CTAs per head: split the head's dims over the SMs the heads leave idle
+    a.attn_parts = std::max(1u, std::min(s.grid / m.H, std::max(1u, m.dh / 8)));
     a.exp_lut = m.ctx->exp_lut;
     a.seeds = m.ctx->seeds;
     return a;

@@ -69,29 +69,35 @@ __device__ __noinline__ void softmax_strip(int64_t* S, uint32_t n, const int64_t
 // Bytes of shared scratch attn_head needs (score strip in shared memory when
 // max_ctx > 0, else in a.scores).
 __host__ __device__ constexpr size_t attn_scratch_bytes(uint32_t dh, uint32_t max_ctx = 0) {
-    return (size_t(dh) + 257 + ATTN_THREADS + max_ctx) * sizeof(int64_t);
+    return (2 * size_t(dh) + 257 + ATTN_THREADS + max_ctx) * sizeof(int64_t);
 }
 
-// One head of one attention step at position `pos`; block-wide (blockDim.x
-// == ATTN_THREADS). `scratch` = attn_scratch_bytes(dh[, max_ctx]) of shared
-// memory; `smem_scores` keeps the score strip on chip. When `planes` is set,
+// One head of one attention step at position `pos`, or one of `nparts`
+// slices of it: every part computes all scores and the softmax (cheap,
+// redundant) and the probability-weighted V sum for its own slice of the
+// head's dimensions -- an exact split with no cross-CTA exchange. Part 0
+// writes the new K/V row. Block-wide (blockDim.x == ATTN_THREADS); `scratch`
+// = attn_scratch_bytes(dh[, max_ctx]) of shared memory; `smem_scores` keeps
+// the score strip on chip (required when nparts > 1). When `planes` is set,
 // the output is also emitted as 3-limb byte planes for the WO GEMV (plus the
 // wide flag), see persistent.cuh.
-__device__ __noinline__ void attn_head(const AttnArgs& a_in, uint32_t h, uint32_t pos, int64_t* scratch, u128* red,
-                          uint8_t* planes = nullptr, uint32_t pitch = 0, uint32_t* flag = nullptr,
-                          uint32_t tag = 0, bool smem_scores = false,
-                          unsigned long long* tr = nullptr) {
+__device__ __noinline__ void attn_head_part(const AttnArgs& a_in, uint32_t h, uint32_t part_idx,
+                                            uint32_t nparts, uint32_t pos, int64_t* scratch, u128* red,
+                                            uint8_t* planes, uint32_t pitch, uint32_t* flag, uint32_t tag,
+                                            bool smem_scores, unsigned long long* tr) {
     // one copy of the arguments into registers (a_in may live in local memory,
     // whose L1 lines the persistent kernel's grid fences invalidate)
     const AttnArgs a = a_in;
-    int64_t* qrot = scratch;                                   // [dh]
-    int64_t* lut = scratch + a.dh;                             // [257] (unless a.exp_lut is on chip)
-    uint64_t* part = reinterpret_cast<uint64_t*>(lut + 257);   // [ATTN_THREADS]
     const uint32_t dh = a.dh, half = dh / 2, D = a.H * dh;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = ATTN_THREADS / 32;
+    int64_t* qrot = scratch;                                   // [dh]
+    int64_t* krot = scratch + dh;                              // [dh] this position's key
+    int64_t* lut = scratch + 2 * dh;                           // [257] (unless a.exp_lut is on chip)
+    uint64_t* part = reinterpret_cast<uint64_t*>(lut + 257);   // [ATTN_THREADS]
     if (smem_scores) lut = const_cast<int64_t*>(a.exp_lut);  // persistent kernel: already in smem
     else
         for (int i = threadIdx.x; i < 257; i += blockDim.x) lut[i] = a.exp_lut[i];
+    int64_t* S = smem_scores ? reinterpret_cast<int64_t*>(part + ATTN_THREADS)
+                             : a.scores + size_t(h) * a.max_ctx;
 
     const int64_t* q = a.qkv + size_t(h) * dh;
     const int64_t* k = a.qkv + D + size_t(h) * dh;
@@ -100,40 +106,43 @@ __device__ __noinline__ void attn_head(const AttnArgs& a_in, uint32_t h, uint32_
     int64_t* V = a.vc + size_t(h) * a.max_ctx * dh;
     const int64_t* cr = a.rope_cos + size_t(pos) * half;
     const int64_t* sr = a.rope_sin + size_t(pos) * half;
-    for (uint32_t i = threadIdx.x; i < half; i += ATTN_THREADS) {
-        int64_t c = cr[i], s = sr[i];
+    // RoPE on q and k (rope_apply_inplace, kernels.cpp:70-82); K/V append
+    for (uint32_t i = threadIdx.x; i < half; i += blockDim.x) {
+        const int64_t c = cr[i], s = sr[i];
         rope_pair(q[i], q[i + half], c, s, qrot[i], qrot[i + half]);
-        int64_t k0, k1;
-        rope_pair(k[i], k[i + half], c, s, k0, k1);
-        K[size_t(pos) * dh + i] = k0;
-        K[size_t(pos) * dh + i + half] = k1;
+        rope_pair(k[i], k[i + half], c, s, krot[i], krot[i + half]);
+        if (part_idx == 0) {
+            K[size_t(pos) * dh + i] = krot[i];
+            K[size_t(pos) * dh + i + half] = krot[i + half];
+        }
     }
-    for (uint32_t j = threadIdx.x; j < dh; j += ATTN_THREADS) V[size_t(pos) * dh + j] = v[j];
-    __syncthreads();
+    if (part_idx == 0)
+        for (uint32_t j = threadIdx.x; j < dh; j += blockDim.x) V[size_t(pos) * dh + j] = v[j];
+    int q_small = 1;
+    for (uint32_t j = threadIdx.x; j < dh; j += blockDim.x)
+        q_small &= qrot[j] < (int64_t(1) << 27) && qrot[j] > -(int64_t(1) << 27);
+    q_small = __syncthreads_and(q_small) && dh <= 512;  // 512 * 2^54 < 2^63
     if (tr) tr[4] = clock64();
 
-    int64_t* S = smem_scores ? reinterpret_cast<int64_t*>(part + ATTN_THREADS)
-                             : a.scores + size_t(h) * a.max_ctx;
-    // scores: one warp per cached position, int128 dot; four positions per
-    // warp in flight so the K reads overlap. When every |q|, |k| < 2^27 a dot
-    // of <= 2^13 terms stays below 2^63, so plain int64 products and sums give
-    // the same int128 value; a warp-uniform check picks that fast path.
-    int q_small = 1;
-    for (uint32_t j = threadIdx.x; j < dh; j += blockDim.x) q_small &= qrot[j] < (int64_t(1) << 27) && qrot[j] > -(int64_t(1) << 27);
-    q_small = __syncthreads_and(q_small) && dh <= 512;  // 512 * 2^54 < 2^63
+    // scores (kernels.cpp:143-151): one warp per cached position, lanes over
+    // dh, four positions per warp in flight. The dot is int128 in the
+    // reference; when every |q|, |k| < 2^27 and dh <= 512 the int64 sum is
+    // exact and a warp-uniform check takes that path.
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (uint32_t t0 = warp; t0 <= pos; t0 += 4 * nw) {
-        int64_t kv[4][4];
         int small = q_small;
         uint64_t d64[4] = {0, 0, 0, 0};
         u128 dot[4] = {0, 0, 0, 0};
         for (uint32_t j0 = 0; j0 < dh; j0 += 128) {
+            int64_t kv[4][4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t t = t0 + u * nw;
+                const int64_t* kt = t == pos ? krot : K + size_t(t) * dh;  // newest key: on chip
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     const uint32_t j = j0 + lane + 32 * c;
-                    kv[u][c] = (t <= pos && j < dh) ? K[size_t(t) * dh + j] : 0;
+                    kv[u][c] = (t <= pos && j < dh) ? kt[j] : 0;
                 }
             }
 #pragma unroll
@@ -153,69 +162,68 @@ __device__ __noinline__ void attn_head(const AttnArgs& a_in, uint32_t h, uint32_
                 }
             }
         }
-        small = __all_sync(0xffffffffu, small);
 #pragma unroll 1
         for (int u = 0; u < 4; ++u) {
             const uint32_t t = t0 + u * nw;
-            int64_t sc;
-            if (small) {
-                sc = int64_t(warp_sum_u64(d64[u] + uint64_t(dot[u]))) >> 16;
-            } else {
-                const u128 d = warp_sum_u128(dot[u] + u128(int64_t(d64[u])));
-                sc = int64_t(i128(d) >> 16);
-            }
-            if (lane == 0 && t <= pos) S[t] = mul16(sc, a.inv_scale);
+            // int64 partial (exact) + 128-bit remainder, then the warp total
+            const u128 d = warp_sum_u128(dot[u] + u128(int64_t(d64[u])));
+            if (lane == 0 && t <= pos) S[t] = mul16(int64_t(i128(d) >> 16), a.inv_scale);
         }
     }
     __syncthreads();
-
     if (tr) tr[5] = clock64();
     softmax_strip(S, pos + 1, lut, red);
     if (tr) tr[6] = clock64();
 
-    // out_j = sum_t mul16(p_t, V[t]_j); threads = (column, position slice)
-    if (dh <= ATTN_THREADS) {
-        const uint32_t slices = ATTN_THREADS / dh;
-        const uint32_t j = threadIdx.x % dh, sl = threadIdx.x / dh;
+    // out_j = sum_t mul16(p_t, V[t]_j) (kernels.cpp:153-159) over this part's
+    // dims; threads = (dim, position slice); the newest V row is read from
+    // this step's projection (part 0 may not have stored it yet)
+    const uint32_t dpp = (dh + nparts - 1) / nparts;
+    const uint32_t d0 = min(dh, part_idx * dpp), d1 = min(dh, d0 + dpp), nd = d1 - d0;
+    if (nd > 0 && nd <= ATTN_THREADS) {
+        const uint32_t slices = ATTN_THREADS / nd;
+        const uint32_t jj = threadIdx.x % nd, sl = threadIdx.x / nd, j = d0 + jj;
         uint64_t acc = 0;
         if (sl < slices) {
             uint32_t t = sl;
-            for (; t + 7 * slices <= pos; t += 8 * slices) {  // 8 V rows in flight
+            for (; t + 7 * slices < pos; t += 8 * slices) {  // 8 V rows in flight
                 int64_t vv[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) vv[u] = V[size_t(t + u * slices) * dh + j];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) acc += uint64_t(mul16_prob(S[t + u * slices], vv[u]));
             }
-            for (; t <= pos; t += slices) acc += uint64_t(mul16_prob(S[t], V[size_t(t) * dh + j]));
+            for (; t <= pos; t += slices)
+                acc += uint64_t(mul16_prob(S[t], t == pos ? v[j] : V[size_t(t) * dh + j]));
         }
         part[threadIdx.x] = acc;
         __syncthreads();
-        if (threadIdx.x < dh) {
+        if (threadIdx.x < nd) {
             uint64_t sum = 0;
-            for (uint32_t s = 0; s < slices; ++s) sum += part[s * dh + threadIdx.x];
-            const uint32_t j = h * dh + threadIdx.x;
-            a.out[j] = int64_t(sum);
+            for (uint32_t s = 0; s < slices; ++s) sum += part[s * nd + threadIdx.x];
+            const uint32_t o = h * dh + d0 + threadIdx.x;
+            a.out[o] = int64_t(sum);
             if (planes) {
-                planes[j] = uint8_t(sum);
-                planes[pitch + j] = uint8_t(sum >> 8);
-                planes[2 * pitch + j] = uint8_t(sum >> 16);
-                int64_t v = int64_t(sum);
-                if (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) *((volatile uint32_t*)flag) = tag;
+                planes[o] = uint8_t(sum);
+                planes[pitch + o] = uint8_t(sum >> 8);
+                planes[2 * pitch + o] = uint8_t(sum >> 16);
+                const int64_t sv = int64_t(sum);
+                if (sv < -(int64_t(1) << 23) || sv >= (int64_t(1) << 23)) *((volatile uint32_t*)flag) = tag;
             }
         }
     } else {
-        for (uint32_t j = threadIdx.x; j < dh; j += ATTN_THREADS) {
+        for (uint32_t j = d0 + threadIdx.x; j < d1; j += blockDim.x) {
             uint64_t acc = 0;
-            for (uint32_t t = 0; t <= pos; ++t) acc += uint64_t(mul16_prob(S[t], V[size_t(t) * dh + j]));
-            const uint32_t jj = h * dh + j;
-            a.out[jj] = int64_t(acc);
+            for (uint32_t t = 0; t <= pos; ++t)
+                acc += uint64_t(mul16_prob(S[t], t == pos ? v[j] : V[size_t(t) * dh + j]));
+            const uint32_t o = h * dh + j;
+            a.out[o] = int64_t(acc);
             if (planes) {
-                planes[jj] = uint8_t(acc);
-                planes[pitch + jj] = uint8_t(acc >> 8);
-                planes[2 * pitch + jj] = uint8_t(acc >> 16);
-                int64_t v = int64_t(acc);
-                if (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) *((volatile uint32_t*)flag) = tag;
+                planes[o] = uint8_t(acc);
+                planes[pitch + o] = uint8_t(acc >> 8);
+                planes[2 * pitch + o] = uint8_t(acc >> 16);
+                const int64_t sv = int64_t(acc);
+                if (sv < -(int64_t(1) << 23) || sv >= (int64_t(1) << 23)) *((volatile uint32_t*)flag) = tag;
             }
         }
     }
@@ -226,7 +234,7 @@ __device__ __noinline__ void attn_head(const AttnArgs& a_in, uint32_t h, uint32_
 __global__ void __launch_bounds__(ATTN_THREADS) attn_decode_kernel(AttnArgs a) {
     extern __shared__ __align__(16) int64_t attn_smem[];
     __shared__ u128 red[32];
-    attn_head(a, blockIdx.x, a.ctl->pos, attn_smem, red);
+    attn_head_part(a, blockIdx.x, 0, 1, a.ctl->pos, attn_smem, red, nullptr, 0, nullptr, 0, false, nullptr);
 }
 
 }  // namespace dimg::dev

@@ -91,6 +91,7 @@ struct PkArgs {
     const int64_t* seeds;     // idem
     unsigned long long* trace;  // optional: [stage_seq][12] stamps of CTA 0 (dimg_session_trace)
     uint32_t trace_cap;
+    uint32_t attn_parts;      // CTAs per attention head (dimension slices)
 };
 
 // Scheduling constants, held in registers (never address kernel params or
@@ -737,9 +738,11 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 t.kc += size_t(st.layer) * a.kv_layer_stride;
                 t.vc += size_t(st.layer) * a.kv_layer_stride;
                 t.exp_lut = s_lut;
-                for (uint32_t h = blockIdx.x; h < t.H; h += gridDim.x)
-                    attn_head(t, h, pos, reinterpret_cast<int64_t*>(stage_mem), red, st.out_planes,
-                              st.out_pitch, st.out_flag, tag, true, tr && h == 0 ? tr : nullptr);
+                const uint32_t np = a.attn_parts;
+                for (uint32_t c = blockIdx.x; c < t.H * np; c += gridDim.x)
+                    attn_head_part(t, c / np, c % np, np, pos, reinterpret_cast<int64_t*>(stage_mem), red,
+                                   st.out_planes, st.out_pitch, st.out_flag, tag, true,
+                                   tr && c == 0 ? tr : nullptr);
             } else {
                 uint32_t* planes;
                 int L;
