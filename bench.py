@@ -90,7 +90,7 @@ class ClockSampler:
                     self.rows.append([c.strip() for c in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -252,15 +252,20 @@ def run_ours(args, rank, world, local):
     value = world * args.steps / (ms_max / 1e3)
     launches_per_step, _ = sess.launches()
 
-    # dominant kernel roofline (gate/up GEMV, ~45% of the weight bytes)
+    # per-stage probes (each stage kind replayed over the layers in one launch)
     kern = {}
     for which, name in enumerate(sess.KERNELS):
         kms, kb = sess.time_kernel(which, 64 if which != 4 else 16)
         kern[name] = {"ms": kms, "bytes": kb, "gbs": kb / (kms * 1e-3) / 1e9}
     peak, peak_kind = peaks()
-    dom = kern["gate_up_gemv"]
     step_bytes = bytes_per_token(cfg.n_layers, cfg.d_model, cfg.d_ffn, cfg.vocab)
     step_gbs = step_bytes / (per_step_ms * 1e-3) / 1e9
+    traffic = None
+    try:  # dram__bytes_read+write per decode step from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            traffic = json.load(f)["traffic_bytes_per_step"]
+    except Exception:
+        pass
 
     # e2e: the reference-shaped call with host buffers (C2: P=16, N=128)
     e2e = None
@@ -299,13 +304,15 @@ def run_ours(args, rank, world, local):
                        "weight_hash_ok": wh_ok, "model_gen_s": round(gen_s, 1)},
             "e2e": e2e,
             "gpu_launches": launches_per_step,  # one persistent launch runs all K steps
-            "roofline": {"bound": "hbm", "achieved": dom["gbs"], "peak": peak, "unit": "GB/s",
-                         "frac": dom["gbs"] / peak, "traffic": None, "kernel": "gate_up_gemv",
-                         "bytes_per_launch": dom["bytes"], "ms_per_launch": dom["ms"],
+            # dominant kernel: the persistent decode kernel (99.8% of GPU time,
+            # profiles/r01_bench_launches.csv); one decode step = 6.62 GB of
+            # algorithmic weight bytes, timed with CUDA events on its stream
+            "roofline": {"bound": "hbm", "achieved": step_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": step_gbs / peak, "traffic": traffic,
+                         "kernel": "decode_persistent_kernel (per decode step)",
+                         "bytes_per_step": step_bytes, "ms_per_step": per_step_ms,
                          "peak_kind": peak_kind},
-            "step_roofline": {"bytes_per_token": step_bytes, "achieved_gbs": step_gbs,
-                              "frac": step_gbs / peak},
-            "kernels": kern,
+            "stages": kern,
             "clocks": clk.summary(),
             "cpu_baseline": base,
             "tokens_head": toks[:8],
@@ -319,7 +326,7 @@ def run_ours(args, rank, world, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--steps", type=int, default=128)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

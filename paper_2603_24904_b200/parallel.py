@@ -1,0 +1,108 @@
+"""Partitioning of the decode path across GPUs.
+
+* Sequence sharding (C5): independent sequences are dealt to ranks; no
+  data-path collective. `sequence_shard`.
+* Tensor parallel (C4), Megatron style:
+  - column-parallel: wq/wk/wv by heads (rank r owns heads [r*H/g, (r+1)*H/g)),
+    w_gate/w_up by FFN rows, the lm_head by vocab rows;
+  - row-parallel: wo by the same head columns, w_down by the same FFN columns;
+  - after wo and after w_down the PRE-SCALE int64 accumulators are summed
+    across ranks (allreduce): `(acc * s) >> 16` is nonlinear, so the sum must
+    come first; integer addition is associative, so the result is
+    bit-identical at every g (the reference's chunk-invariance argument,
+    proj/tests/test_kernels.cpp:79-97);
+  - argmax: rank-local (max, lowest index) then a deterministic global pick.
+`TPPlan` is the single source of these slices for the host-side sharding
+(`shard_tensors`) and its tests (tests/test_parallel.py).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Tuple
+
+import numpy as np
+
+from .model import LAYER_TENSORS, ModelConfig, ModelFile
+
+
+def sequence_shard(n_seqs: int, world: int, rank: int) -> List[int]:
+    """Contiguous balanced block of sequence ids for `rank` (C5: 64 over 8)."""
+    lo = n_seqs * rank // world
+    hi = n_seqs * (rank + 1) // world
+    return list(range(lo, hi))
+
+
+def _block(n: int, parts: int, i: int) -> Tuple[int, int]:
+    return n * i // parts, n * (i + 1) // parts
+
+
+@dataclass(frozen=True)
+class TPPlan:
+    cfg: ModelConfig
+    tp: int
+    rank: int
+
+    def __post_init__(self):
+        if not (1 <= self.tp and 0 <= self.rank < self.tp):
+            raise ValueError("bad tp rank/size")
+        if self.cfg.n_heads % self.tp:
+            raise ValueError("n_heads must be divisible by the tensor-parallel degree")
+
+    @property
+    def heads(self) -> Tuple[int, int]:
+        return _block(self.cfg.n_heads, self.tp, self.rank)
+
+    @property
+    def head_cols(self) -> Tuple[int, int]:
+        """d_model columns (= q/k/v rows) owned: whole heads."""
+        h0, h1 = self.heads
+        return h0 * self.cfg.d_head, h1 * self.cfg.d_head
+
+    @property
+    def ffn(self) -> Tuple[int, int]:
+        return _block(self.cfg.d_ffn, self.tp, self.rank)
+
+    @property
+    def vocab(self) -> Tuple[int, int]:
+        return _block(self.cfg.vocab, self.tp, self.rank)
+
+    def slice_layer(self, name: str, w: np.ndarray, s: np.ndarray):
+        """The rank's part of a layer tensor (int8 weights, int64 row scales).
+        Column-parallel tensors keep their row scales; row-parallel ones keep
+        all rows (scales applied after the allreduce) and a column slice."""
+        c0, c1 = self.head_cols
+        f0, f1 = self.ffn
+        if name in ("wq", "wk", "wv"):
+            return w[c0:c1], s[c0:c1]
+        if name == "wo":
+            return w[:, c0:c1], s
+        if name in ("w_gate", "w_up"):
+            return w[f0:f1], s[f0:f1]
+        if name == "w_down":
+            return w[:, f0:f1], s
+        raise KeyError(name)
+
+    def slice_head(self, w: np.ndarray, s: np.ndarray):
+        v0, v1 = self.vocab
+        return w[v0:v1], s[v0:v1]
+
+
+def shard_tensors(model: ModelFile, plan: TPPlan):
+    """Directory-order (weights, scales) of the rank's shard, plus the
+    replicated embedding and gains."""
+    out = {"tok_embd": model.tensor("tok_embd"), "norms": model.norms()}
+    for l in range(model.config.n_layers):
+        for t in LAYER_TENSORS:
+            out[f"layers.{l}.{t}"] = plan.slice_layer(t, *model.tensor(f"layers.{l}.{t}"))
+    out["output"] = plan.slice_head(*model.tensor("output"))
+    return out
+
+
+def pick_argmax(candidates) -> int:
+    """Deterministic global argmax from per-rank (value, index) pairs:
+    largest value, lowest index on ties (proj/src/engine.cpp:113-120)."""
+    best = None
+    for v, i in candidates:
+        if best is None or v > best[0] or (v == best[0] and i < best[1]):
+            best = (v, i)
+    return int(best[1])
