@@ -177,17 +177,21 @@ dimg_status dimg_session_time_decode(dimg_session* s, uint32_t n_steps, float* m
  * algorithmic bytes of one launch (roofline numerator). */
 dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, float* ms_per_launch,
                                      uint64_t* bytes_per_launch);
-/* Tracing: n decode steps; out[12*i + 0..3] = %globaltimer (ns) of CTA 0 at
- * stage i's start, after its prologue, after its chunk loop and before its
- * grid barrier; [4..7] = clock64 of prologue / attention sub-steps, [8] =
- * clock64 at the stage start. cap stages recorded. */
+/* Tracing: n decode steps; out[DIMG_TRACE_WORDS*i + 0..3] = %globaltimer (ns)
+ * of CTA 0 at stage i's start, after its prologue, after its chunk loop and
+ * before its grid barrier; [4..7] = clock64 of prologue / attention sub-steps,
+ * [8] = clock64 at the stage start, [9..31] = finer clock64 stamps of the
+ * attention stage. cap stages recorded. */
+#define DIMG_TRACE_WORDS 32
 dimg_status dimg_session_trace(dimg_session* s, uint32_t n_steps, uint64_t* out, uint32_t cap);
 /* Kernel launches per decode step / per prefill step (for the bench claim). */
 dimg_status dimg_session_launches(const dimg_session* s, uint32_t* per_decode,
                                   uint32_t* per_prefill);
 
 /* Counters: [0] GEMV CTAs that needed the 8-limb (full int64) path,
- * [1] device-side domain errors (inv_sqrt of ms+1 <= 0). */
+ * [1] device-side error bits (1: inv_sqrt of ms+1 <= 0, 4: barrier timeout),
+ * [2] attention parts that read the int64 KV cache (a head holding values
+ * beyond int32). */
 dimg_status dimg_session_stats(dimg_session* s, uint64_t out[4]);
 
 /* ---- operator-level exports (host buffers in/out) for unit parity with

@@ -259,6 +259,9 @@ struct dimg_session {
     uint32_t* tokens;  // [max_ctx + 1]
     Ctl* ctl;
     unsigned int* bar;
+    unsigned int* hsync;   // [H] attention part counters
+    int32_t *kc32, *vc32;  // int32 mirror of the KV cache
+    uint32_t* kvwide;      // [L][H] mirror unusable (sticky per sequence)
     uint8_t* planes_att;   // [3][Kd] 3-limb planes of the attention output
     uint8_t* planes_h;     // [3][Kf] 3-limb planes of the FFN hidden vector
     uint32_t* flags;       // [2L] "needs > 3 limbs" tags (att, h) per layer
@@ -388,6 +391,10 @@ PkArgs pk_args(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     a.kv_layer_stride = size_t(m.H) * m.cfg.max_ctx * m.dh;
     // CTAs per head: split the head's dims over the SMs the heads leave idle
     a.attn_parts = std::max(1u, std::min(s.grid / m.H, std::max(1u, m.dh / 8)));
+    a.hsync = s.hsync;
+    a.kc32 = s.kc32;
+    a.vc32 = s.vc32;
+    a.kvwide = s.kvwide;
     a.exp_lut = m.ctx->exp_lut;
     a.seeds = m.ctx->seeds;
     return a;
@@ -401,6 +408,7 @@ void launch_pk(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     a.trace_cap = trace_cap;
 
     CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned int), s.stream));
+    CK(cudaMemsetAsync(s.hsync, 0, s.m->H * sizeof(unsigned int), s.stream));
     CK(cudaMemsetAsync(s.flags, 0, size_t(2) * s.m->L * sizeof(uint32_t), s.stream));
     CK(cudaMemsetAsync(s.ssq, 0, size_t(2) * s.m->L * sizeof(unsigned long long), s.stream));
     void* params[] = {&a};
@@ -603,6 +611,11 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         s->tokens = s->mem.alloc<uint32_t>(ctx + 1);
         s->ctl = s->mem.alloc<Ctl>(1);
         s->bar = s->mem.alloc<unsigned int>(64);
+        s->hsync = s->mem.alloc<unsigned int>(m->H);
+        s->kc32 = s->mem.alloc<int32_t>(kv);
+        s->vc32 = s->mem.alloc<int32_t>(kv);
+        s->kvwide = s->mem.alloc<uint32_t>(size_t(m->L) * m->H);
+        CK(cudaMemsetAsync(s->kvwide, 0, size_t(m->L) * m->H * 4, s->stream));
         // one CTA per SM; shared memory = weight ring + limb planes + row accumulators
         s->grid = uint32_t(m->ctx->sm_count);
         s->parts = s->mem.alloc<ArgPart>(s->grid);
@@ -812,11 +825,11 @@ dimg_status dimg_session_trace(dimg_session* s, uint32_t n_steps, uint64_t* out,
     DIMG_API_GUARD({
         if (uint64_t(s->len) + n_steps > s->m->cfg.max_ctx)
             fail(DIMG_ECTX, "decode: context overflow");
-        unsigned long long* d = s->mem.alloc<unsigned long long>(size_t(cap) * 12);
-        CK(cudaMemsetAsync(d, 0, size_t(cap) * 96, s->stream));
+        unsigned long long* d = s->mem.alloc<unsigned long long>(size_t(cap) * DIMG_TRACE_WORDS);
+        CK(cudaMemsetAsync(d, 0, size_t(cap) * DIMG_TRACE_WORDS * 8, s->stream));
         launch_pk(*s, s->stages, n_layer_stages(*s), n_steps, 0, d, cap);
         s->len += n_steps;
-        CK(cudaMemcpyAsync(out, d, size_t(cap) * 96, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaMemcpyAsync(out, d, size_t(cap) * DIMG_TRACE_WORDS * 8, cudaMemcpyDeviceToHost, s->stream));
         check_ctl_err(*s);
     })
 }
@@ -836,7 +849,7 @@ dimg_status dimg_session_stats(dimg_session* s, uint64_t out[4]) {
         CK(cudaStreamSynchronize(s->stream));
         out[0] = c.stats[0];
         out[1] = c.err;
-        out[2] = c.stats[2];
+        out[2] = c.stats[1];
         out[3] = c.stats[3];
     })
 }

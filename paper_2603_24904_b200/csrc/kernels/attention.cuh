@@ -46,7 +46,7 @@ __device__ __forceinline__ void rope_pair(int64_t a, int64_t b, int64_t c, int64
 // softmax_q16 in place over S[0..n) (proj/src/kernels.cpp:90-107): exact max,
 // LUT weights lut(min(m - s, 8)), then p = (w << 16) / sum w (truncating).
 // Block-wide; ends with a barrier.
-__device__ __noinline__ void softmax_strip(int64_t* S, uint32_t n, const int64_t* lut, u128* red) {
+__device__ __forceinline__ void softmax_strip_inl(int64_t* S, uint32_t n, const int64_t* lut, u128* red) {
     int64_t m = INT64_MIN;
     for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) m = S[t] > m ? S[t] : m;
     m = block_reduce<int64_t>(m, reinterpret_cast<int64_t*>(red),
@@ -66,10 +66,14 @@ __device__ __noinline__ void softmax_strip(int64_t* S, uint32_t n, const int64_t
     __syncthreads();
 }
 
+__device__ __noinline__ void softmax_strip(int64_t* S, uint32_t n, const int64_t* lut, u128* red) {
+    softmax_strip_inl(S, n, lut, red);
+}
+
 // Bytes of shared scratch attn_head needs (score strip in shared memory when
 // max_ctx > 0, else in a.scores).
 __host__ __device__ constexpr size_t attn_scratch_bytes(uint32_t dh, uint32_t max_ctx = 0) {
-    return (2 * size_t(dh) + 257 + ATTN_THREADS + max_ctx) * sizeof(int64_t);
+    return (2 * size_t(dh) + 257 + 4 * ATTN_THREADS + max_ctx) * sizeof(int64_t);
 }
 
 // One head of one attention step at position `pos`, or one of `nparts`

@@ -54,7 +54,7 @@ struct Ctl {
     uint32_t argmax_count;  // CTAs of the lm_head that finished this step
     uint32_t err;           // bit 0: inv_sqrt domain error (ms + 1 <= 0)
     uint32_t pad[3];
-    unsigned long long stats[4];  // [0] CTAs on the 8-limb path
+    unsigned long long stats[4];  // [0] CTAs on the 8-limb path, [1] attention parts on the int64 KV path
 };
 
 struct ArgPart {

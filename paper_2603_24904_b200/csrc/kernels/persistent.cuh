@@ -89,9 +89,13 @@ struct PkArgs {
     size_t kv_layer_stride;   // elements between layers in kc/vc
     const int64_t* exp_lut;   // repointed to a shared-memory copy inside the kernel
     const int64_t* seeds;     // idem
-    unsigned long long* trace;  // optional: [stage_seq][12] stamps of CTA 0 (dimg_session_trace)
+    unsigned long long* trace;  // optional: [stage_seq][32] stamps of CTA 0 (dimg_session_trace)
     uint32_t trace_cap;
-    uint32_t attn_parts;      // CTAs per attention head (dimension slices)
+    uint32_t attn_parts;      // CTAs per attention head (position blocks / dimension slices)
+    unsigned int* hsync;      // [H] per-head arrival counters of the attention parts (zeroed before launch)
+    int32_t* kc32;            // int32 mirror of kc / vc (same layout), read while kvwide is clear
+    int32_t* vc32;
+    uint32_t* kvwide;         // [L][H] some cached K/V value of the head needs more than 32 bits
 };
 
 // Scheduling constants, held in registers (never address kernel params or
@@ -666,6 +670,355 @@ __device__ __noinline__ void run_gemv_wide(Sched sc, Pipe& p, GemvRT g_, const u
     run_gemv<8>(sc, p, g_, planes, tag, best_v, best_i);
 }
 
+// ---- attention, positions split across the head's CTAs ---------------------------
+
+__device__ __forceinline__ bool below23(int64_t x) {  // |x| < 2^23
+    return uint64_t(x + (int64_t(1) << 23)) < (uint64_t(1) << 24);
+}
+
+// Exact general-case pieces of the attention step, out of line (rare, or one
+// position): int128 scores of positions [t0, t1) from the int64 cache (the
+// newest key from krot), one warp per position.
+__device__ __noinline__ void attn_scores_slow(const int64_t* K, const int64_t* qrot, const int64_t* krot,
+                                              uint32_t dh, uint32_t t0, uint32_t t1, uint32_t pos,
+                                              int64_t inv_scale, int64_t* S) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t t = t0 + warp; t < t1; t += ATTN_THREADS / 32) {
+        const int64_t* kt = t == pos ? krot : K + size_t(t) * dh;
+        u128 d = 0;
+        for (uint32_t j = lane; j < dh; j += 32) d += mul_full(qrot[j], kt[j]);
+        d = warp_sum_u128(d);
+        if (lane == 0) S[t] = mul16(int64_t(i128(d) >> 16), inv_scale);
+    }
+}
+
+// PV sums of dims [d0, d1) over all positions from the int64 cache.
+__device__ __noinline__ void attn_pv_slow(const int64_t* V, const int64_t* v, const int64_t* S, uint32_t dh,
+                                          uint32_t d0, uint32_t d1, uint32_t pos, uint64_t* out) {
+    for (uint32_t j = d0 + threadIdx.x; j < d1; j += ATTN_THREADS) {
+        uint64_t acc = 0;
+        for (uint32_t t = 0; t <= pos; ++t) acc += uint64_t(mul16_prob(S[t], t == pos ? v[j] : V[size_t(t) * dh + j]));
+        out[j - d0] = acc;
+    }
+}
+
+// RoPE of q (and, for the owner, k -> krot and the KV append) for dims past
+// what one pass of the block covers (dh > 2 * ATTN_THREADS).
+__device__ __noinline__ void attn_rope_tail(const int64_t* q, const int64_t* k, const int64_t* v,
+                                            const int64_t* cr, const int64_t* sr, uint32_t dh, bool owner,
+                                            int64_t* qrot, int64_t* krot, int64_t* K64, int64_t* V64,
+                                            int32_t* K32, int32_t* V32, int* kv_big) {
+    const uint32_t half = dh / 2;
+    for (uint32_t i = threadIdx.x + ATTN_THREADS; i < half; i += ATTN_THREADS) {
+        int64_t x0, x1;
+        rope_pair(q[i], q[i + half], cr[i], sr[i], x0, x1);
+        qrot[i] = x0;
+        qrot[i + half] = x1;
+        if (owner) {
+            rope_pair(k[i], k[i + half], cr[i], sr[i], x0, x1);
+            krot[i] = x0;
+            krot[i + half] = x1;
+            K64[i] = x0;
+            K64[i + half] = x1;
+            K32[i] = int32_t(x0);
+            K32[i + half] = int32_t(x1);
+            *kv_big |= !fits_i32(x0) || !fits_i32(x1);
+        }
+    }
+    if (owner)
+        for (uint32_t j = threadIdx.x + ATTN_THREADS; j < dh; j += ATTN_THREADS) {
+            V64[j] = v[j];
+            V32[j] = int32_t(v[j]);
+            *kv_big |= !fits_i32(v[j]);
+        }
+}
+
+// attention_step (proj/src/kernels.cpp:117-177) for head h as part `pi` of
+// `np` CTAs. Each part scores its own contiguous block of cached positions
+// (the K strip is read once per head, not once per part), publishes them to
+// the head's strip in global memory and meets the other parts at a per-head
+// counter; then every part runs the exact softmax over the whole strip in
+// shared memory and the probability-weighted V sum for its own slice of the
+// head's dimensions. Integer sums throughout: no split moves a bit.
+//
+// The cache is kept twice: int64 (the reference's values) and an int32
+// mirror that the reads use while every value of the head fits (kvwide flag
+// clear) -- half the bytes on the latency-critical path. The part owning
+// position `pos` appends both rows and maintains the flag (rewritten at
+// position 0, sticky after). The int32 rows are loaded speculatively at
+// entry, before anything else is known. This runs once per layer under a
+// saturated memory system, so the common path is kept short (instruction
+// fetches are L2 round trips too); everything else is out of line.
+// Returns false if the head's peers never arrived (ctl->err |= 4, as a barrier timeout).
+__device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint32_t h, uint32_t pi, uint32_t np,
+                                           uint32_t pos, uint32_t epoch, int64_t* scratch, u128* red,
+                                           uint8_t* planes, uint32_t pitch, uint32_t* flag, uint32_t tag,
+                                           const int64_t* lut, unsigned long long* tr) {
+#define ASTAMP(i) \
+    if (tr) tr[i] = clock64()
+    ASTAMP(9);
+    const uint32_t dh = A.attn.dh, half = dh / 2, H = A.attn.H, D = H * dh, T = pos + 1, mc = A.attn.max_ctx;
+    int64_t* qrot = scratch;                                               // [dh]
+    int64_t* krot = scratch + dh;                                          // [dh]
+    int32_t* q32 = reinterpret_cast<int32_t*>(scratch + 2 * dh);           // [dh] (257 words reserved)
+    uint64_t* part = reinterpret_cast<uint64_t*>(scratch + 2 * dh + 257);  // [4 * ATTN_THREADS]
+    int64_t* S = reinterpret_cast<int64_t*>(part + 4 * ATTN_THREADS);      // [max_ctx] score strip
+    const uint32_t t0 = T * pi / np, t1 = T * (pi + 1) / np;  // T <= max_ctx, np <= 64: 32-bit exact
+    const bool owner = pi + 1 == np;                        // t1 == T: the newest position is the last part's
+    // fast path shape: whole 4-dim quads (16-byte int32 rows), q rows within one pass
+    const bool shape_ok = (dh & 3) == 0 && dh <= 512;
+    const int64_t* q = A.attn.qkv + size_t(h) * dh;
+    const int64_t* k = A.attn.qkv + D + size_t(h) * dh;
+    const int64_t* v = A.attn.qkv + 2 * size_t(D) + size_t(h) * dh;
+    const size_t hoff = size_t(layer) * A.kv_layer_stride + size_t(h) * mc * dh;
+    int64_t* K64 = A.attn.kc + hoff;
+    int64_t* V64 = A.attn.vc + hoff;
+    int32_t* K32 = A.kc32 + hoff;
+    int32_t* V32 = A.vc32 + hoff;
+    uint32_t* wflag = A.kvwide + size_t(layer) * H + h;
+    const int64_t* cr = A.attn.rope_cos + size_t(pos) * half;
+    const int64_t* sr = A.attn.rope_sin + size_t(pos) * half;
+
+    // PV mapping: thread = (4-dim quad jq, position slice sl)
+    uint32_t dpp = (dh + np - 1) / np;
+    dpp = (dpp + 3) & ~3u;
+    const uint32_t d0 = min(dh, pi * dpp), d1 = min(dh, d0 + dpp), nd = d1 - d0, nquads = nd / 4;
+    const bool pv_shape = shape_ok && nquads > 0 && nquads <= ATTN_THREADS;
+    const uint32_t slices = pv_shape ? ATTN_THREADS / nquads : 1;
+    const uint32_t jq = pv_shape ? threadIdx.x % nquads : 0, sl = pv_shape ? threadIdx.x / nquads : ATTN_THREADS;
+    const uint32_t jv = d0 + 4 * jq;
+
+    // 1. L2 first: the head's wide flag, this step's q/k rows, the RoPE rows,
+    //    the newest V quad; then HBM, speculatively as int32: the K rows of
+    //    the first score pass and the V rows of the first PV round.
+    const bool rope_thread = threadIdx.x < half;
+    int64_t q0 = 0, q1 = 0, k0 = 0, k1 = 0, c_ = 0, s_ = 0, vnew = 0;
+    uint32_t wide_in = 0;
+    if (threadIdx.x == 0) wide_in = ld_cg32(wflag);
+    if (rope_thread) {
+        c_ = cr[threadIdx.x];
+        s_ = sr[threadIdx.x];
+        q0 = q[threadIdx.x];
+        q1 = q[threadIdx.x + half];
+        if (owner) {
+            k0 = k[threadIdx.x];
+            k1 = k[threadIdx.x + half];
+        }
+    }
+    if (owner && threadIdx.x < dh) vnew = v[threadIdx.x];
+    longlong2 vq01 = make_longlong2(0, 0), vq23 = make_longlong2(0, 0);
+    if (sl < slices) {
+        vq01 = *reinterpret_cast<const longlong2*>(v + jv);
+        vq23 = *reinterpret_cast<const longlong2*>(v + jv + 2);
+    }
+    ASTAMP(10);
+
+    const uint32_t oc = threadIdx.x >> 3, e = threadIdx.x & 7;  // scores: octet = position, lane = 4 dims
+    constexpr uint32_t NOCT = ATTN_THREADS / 8;
+    int4 ka[4], kb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint32_t j = 4 * e + 32 * u, ta = t0 + oc, tb = ta + NOCT;
+        ka[u] = (shape_ok && j < dh && ta < t1 && ta != pos) ? *reinterpret_cast<const int4*>(K32 + size_t(ta) * dh + j)
+                                                           : make_int4(0, 0, 0, 0);
+        kb[u] = (shape_ok && j < dh && tb < t1 && tb != pos) ? *reinterpret_cast<const int4*>(K32 + size_t(tb) * dh + j)
+                                                           : make_int4(0, 0, 0, 0);
+    }
+    constexpr int PV_U = 8;
+    int4 vv[PV_U];
+#pragma unroll
+    for (int u = 0; u < PV_U; ++u) {
+        const uint32_t tt = sl + u * slices;
+        vv[u] = (sl < slices && tt < pos) ? *reinterpret_cast<const int4*>(V32 + size_t(tt) * dh + jv)
+                                          : make_int4(0, 0, 0, 0);
+    }
+    ASTAMP(11);
+
+    // 2. RoPE (rope_apply_inplace, kernels.cpp:70-82) and the KV append (:139-142)
+    int q_small = 1, kv_big = 0;
+    if (rope_thread) {
+        const uint32_t i = threadIdx.x;
+        int64_t x0, x1;
+        rope_pair(q0, q1, c_, s_, x0, x1);
+        qrot[i] = x0;
+        qrot[i + half] = x1;
+        if (shape_ok) {  // q32 has room for dh <= 514
+            q32[i] = int32_t(x0);
+            q32[i + half] = int32_t(x1);
+        }
+        q_small = below23(x0) && below23(x1);
+        if (owner) {
+            rope_pair(k0, k1, c_, s_, x0, x1);
+            krot[i] = x0;
+            krot[i + half] = x1;
+            K64[size_t(pos) * dh + i] = x0;
+            K64[size_t(pos) * dh + i + half] = x1;
+            K32[size_t(pos) * dh + i] = int32_t(x0);
+            K32[size_t(pos) * dh + i + half] = int32_t(x1);
+            kv_big = !fits_i32(x0) || !fits_i32(x1);
+        }
+    }
+    if (owner && threadIdx.x < dh) {
+        V64[size_t(pos) * dh + threadIdx.x] = vnew;
+        V32[size_t(pos) * dh + threadIdx.x] = int32_t(vnew);
+        kv_big |= !fits_i32(vnew);
+    }
+    if (dh > 2 * ATTN_THREADS)
+        attn_rope_tail(q, k, v, cr, sr, dh, owner, qrot, krot, K64 + size_t(pos) * dh, V64 + size_t(pos) * dh,
+                       K32 + size_t(pos) * dh, V32 + size_t(pos) * dh, &kv_big);
+    ASTAMP(12);
+    // Block-uniform decisions. fast: every |q| < 2^23 and every cached |k|
+    // < 2^31 (flag clear), dh <= 512: the int64 score sums are exact
+    // (2^23 * 2^31 * 2^9 = 2^63). The owner's own row counts for its path.
+    q_small = __syncthreads_and(q_small);
+    const int big = __syncthreads_or(kv_big);
+    const bool wide = __syncthreads_or(wide_in != 0) || big || !shape_ok;
+    if (owner && threadIdx.x == 0 && (pos == 0 || big)) *reinterpret_cast<volatile uint32_t*>(wflag) = big ? 1u : 0u;
+    if (tr) tr[4] = clock64();
+
+    // 3. scores of this part's positions (kernels.cpp:143-151)
+    if (!wide && q_small) {
+        for (uint32_t b = t0; b < t1; b += 2 * NOCT) {
+            const uint32_t ta = b + oc, tb = ta + NOCT;
+            int64_t da = 0, db = 0;
+#pragma unroll 1
+            for (uint32_t c0 = 0; c0 < dh; c0 += 128) {
+                if (b != t0 || c0 != 0) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t j = c0 + 4 * e + 32 * u;
+                        ka[u] = (j < dh && ta < t1 && ta != pos) ? *reinterpret_cast<const int4*>(K32 + size_t(ta) * dh + j)
+                                                                 : make_int4(0, 0, 0, 0);
+                        kb[u] = (j < dh && tb < t1 && tb != pos) ? *reinterpret_cast<const int4*>(K32 + size_t(tb) * dh + j)
+                                                                 : make_int4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t j = c0 + 4 * e + 32 * u;
+                    const int4 qq = j < dh ? *reinterpret_cast<const int4*>(q32 + j) : make_int4(0, 0, 0, 0);
+                    da += int64_t(qq.x) * ka[u].x + int64_t(qq.y) * ka[u].y + int64_t(qq.z) * ka[u].z +
+                          int64_t(qq.w) * ka[u].w;
+                    db += int64_t(qq.x) * kb[u].x + int64_t(qq.y) * kb[u].y + int64_t(qq.z) * kb[u].z +
+                          int64_t(qq.w) * kb[u].w;
+                }
+            }
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                da += __shfl_xor_sync(0xffffffffu, da, o);
+                db += __shfl_xor_sync(0xffffffffu, db, o);
+            }
+            if (e == 0) {  // the newest position is scored below, exactly
+                if (ta < t1 && ta != pos) S[ta] = mul16(da >> 16, A.attn.inv_scale);
+                if (tb < t1 && tb != pos) S[tb] = mul16(db >> 16, A.attn.inv_scale);
+            }
+        }
+        if (owner) attn_scores_slow(K64, qrot, krot, dh, pos, pos + 1, pos, A.attn.inv_scale, S);
+    } else {
+        attn_scores_slow(K64, qrot, krot, dh, t0, t1, pos, A.attn.inv_scale, S);
+        if (threadIdx.x == 0 && wide) atomicAdd(&A.ctl->stats[1], 1ull);
+    }
+    ASTAMP(14);
+    if (np > 1) {
+        // publish, meet the head's other parts, gather their scores
+        int64_t* G = A.attn.scores + size_t(h) * mc;
+        __syncthreads();
+        for (uint32_t t = t0 + threadIdx.x; t < t1; t += ATTN_THREADS) G[t] = S[t];
+        __shared__ int s_ok;
+        __syncthreads();
+        ASTAMP(15);
+        if (threadIdx.x == 0) {
+            s_ok = 1;
+            __threadfence();
+            atomicAdd(A.hsync + h, 1u);
+            const uint32_t target = np * epoch;
+            const uint64_t g0 = globaltimer();
+            while (ld_acquire(A.hsync + h) < target) {
+                if (*((volatile uint32_t*)&A.ctl->err) & 4u) { s_ok = 0; break; }
+                if (globaltimer() - g0 > 4000000000ull) {
+                    atomicOr(&A.ctl->err, 4u);
+                    s_ok = 0;
+                    break;
+                }
+            }
+            ASTAMP(16);
+        }
+        __syncthreads();
+        if (!s_ok) return false;
+        for (uint32_t t = threadIdx.x; t < T; t += ATTN_THREADS)
+            if (t < t0 || t >= t1) S[t] = ld_cg64(G + t);
+        ASTAMP(17);
+    }
+    __syncthreads();
+    if (tr) tr[5] = clock64();
+    softmax_strip_inl(S, T, lut, red);
+    if (tr) tr[6] = clock64();
+
+    // 4. out_j = sum_t mul16(p_t, V[t]_j) (kernels.cpp:153-159) over this
+    //    part's dims: p < 2^17 and |v| < 2^31, so p*v is one exact 64-bit
+    //    product; the newest row (int64) comes from the projection.
+    if (!wide && pv_shape) {
+        int64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        if (sl < slices) {
+            for (uint32_t t = sl; t < pos; t += PV_U * slices) {
+                if (t != sl) {
+#pragma unroll
+                    for (int u = 0; u < PV_U; ++u) {
+                        const uint32_t tt = t + u * slices;
+                        vv[u] = tt < pos ? *reinterpret_cast<const int4*>(V32 + size_t(tt) * dh + jv) : make_int4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < PV_U; ++u) {
+                    const uint32_t tt = t + u * slices;
+                    const int64_t p = tt < pos ? S[tt] : 0;
+                    a0 += (p * vv[u].x) >> 16;
+                    a1 += (p * vv[u].y) >> 16;
+                    a2 += (p * vv[u].z) >> 16;
+                    a3 += (p * vv[u].w) >> 16;
+                }
+            }
+            if (pos % slices == sl) {  // the newest row
+                const int64_t p = S[pos];
+                a0 += mul16_prob(p, vq01.x);
+                a1 += mul16_prob(p, vq01.y);
+                a2 += mul16_prob(p, vq23.x);
+                a3 += mul16_prob(p, vq23.y);
+            }
+        }
+        part[4 * threadIdx.x + 0] = uint64_t(a0);
+        part[4 * threadIdx.x + 1] = uint64_t(a1);
+        part[4 * threadIdx.x + 2] = uint64_t(a2);
+        part[4 * threadIdx.x + 3] = uint64_t(a3);
+    } else {
+        attn_pv_slow(V64, v, S, dh, d0, d1, pos, part);
+    }
+    ASTAMP(19);
+    __syncthreads();
+    ASTAMP(20);
+    if (threadIdx.x < nd) {
+        uint64_t sum = 0;
+        if (!wide && pv_shape) {
+            const uint32_t qd = threadIdx.x >> 2, z = threadIdx.x & 3;
+            for (uint32_t s2 = 0; s2 < slices; ++s2) sum += part[4 * (s2 * nquads + qd) + z];
+        } else {
+            sum = part[threadIdx.x];
+        }
+        const uint32_t o = h * dh + d0 + threadIdx.x;
+        A.attn.out[o] = int64_t(sum);
+        planes[o] = uint8_t(sum);
+        planes[pitch + o] = uint8_t(sum >> 8);
+        planes[2 * pitch + o] = uint8_t(sum >> 16);
+        const int64_t sv = int64_t(sum);
+        if (sv < -(int64_t(1) << 23) || sv >= (int64_t(1) << 23)) *((volatile uint32_t*)flag) = tag;
+    }
+    ASTAMP(21);
+    __syncthreads();  // scratch is reused by the next head / stage
+    if (tr) tr[7] = clock64();
+    return true;
+#undef ASTAMP
+}
+
 // ---- the kernel -------------------------------------------------------------------
 
 __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const PkArgs a) {
@@ -713,7 +1066,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
     uint32_t pos = ctl->pos;
     const uint32_t logit_base = ctl->logit_base, keep_cap = ctl->keep_cap;
     uint32_t token = a.tokens[pos];
-    uint32_t nbar = 0, cur = 0;
+    uint32_t nbar = 0, cur = 0, attn_epoch = 0;
 
     for (uint32_t step = 0; step < sc.n_steps; ++step) {
         const uint32_t nst = stages_in_step(sc, step);
@@ -727,22 +1080,20 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
             if (threadIdx.x < kStWords)
                 next_word = reinterpret_cast<const uint32_t*>(sc.stages + (si + 1 < nst ? si + 1 : 0))[threadIdx.x];
             unsigned long long* tr =
-                a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nbar < a.trace_cap ? a.trace + 12 * nbar : nullptr;
+                a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nbar < a.trace_cap ? a.trace + 32 * nbar : nullptr;
             if (tr) {
                 tr[8] = clock64();
                 tr[0] = globaltimer();
             }
             if (st.ssq_clear && blockIdx.x == 0 && threadIdx.x == 0) *st.ssq_clear = 0;
             if (st.kind == SK_ATTN) {
-                AttnArgs t = a.attn;
-                t.kc += size_t(st.layer) * a.kv_layer_stride;
-                t.vc += size_t(st.layer) * a.kv_layer_stride;
-                t.exp_lut = s_lut;
                 const uint32_t np = a.attn_parts;
-                for (uint32_t c = blockIdx.x; c < t.H * np; c += gridDim.x)
-                    attn_head_part(t, c / np, c % np, np, pos, reinterpret_cast<int64_t*>(stage_mem), red,
-                                   st.out_planes, st.out_pitch, st.out_flag, tag, true,
-                                   tr && c == 0 ? tr : nullptr);
+                ++attn_epoch;
+                for (uint32_t c = blockIdx.x; c < a.attn.H * np; c += gridDim.x)
+                    if (!attn_split(a, st.layer, c / np, c % np, np, pos, attn_epoch,
+                                    reinterpret_cast<int64_t*>(stage_mem), red, st.out_planes, st.out_pitch,
+                                    st.out_flag, tag, s_lut, tr && c == 0 ? tr : nullptr))
+                        return;
             } else {
                 uint32_t* planes;
                 int L;

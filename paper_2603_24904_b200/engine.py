@@ -163,10 +163,10 @@ class InferenceSession:
 
     def trace(self, n_steps: int, cap: int):
         """Per-stage %globaltimer stamps of CTA 0 over n decode steps: [cap, 4]
-        = (start, prologue done, chunks done, epilogue done) in ns."""
-        out = np.zeros(cap * 12, np.uint64)
+        = (start, prologue done, chunks done, epilogue done) in ns, [4..31] clock64 sub-stamps."""
+        out = np.zeros(cap * 32, np.uint64)
         check(lib.dimg_session_trace(self._h, n_steps, ptr(out, u64p), cap))
-        return out.reshape(cap, 12)
+        return out.reshape(cap, 32)
 
     def sync(self):
         check(lib.dimg_session_sync(self._h))
@@ -189,7 +189,7 @@ class InferenceSession:
     def stats(self):
         out = np.zeros(4, np.uint64)
         check(lib.dimg_session_stats(self._h, ptr(out, u64p)))
-        return {"wide_limb_ctas": int(out[0]), "err": int(out[1])}
+        return {"wide_limb_ctas": int(out[0]), "err": int(out[1]), "wide_kv_ctas": int(out[2])}
 
     def __del__(self):
         try:

@@ -1,0 +1,64 @@
+"""GPU parity at the headline shape: the Llama-2-7B-shaped toy model
+(BASELINE.json north_star).
+
+* smoke7b and C2 goldens come from the REFERENCE engine itself
+  (tests/golden/make_golden_7b.py ref -> oracle/_ref); C2's output hash
+  is the one BASELINE.md quotes.
+* C4 (1024 new tokens) and the C5 sequences come from the C oracle, which
+  is pinned bit-for-bit to the reference on C1 and C2 (tests/test_oracle.py).
+"""
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2603_24904_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def model7b(P, golden_7b):
+    g = golden_7b["c2"]
+    m = P.gen_toy_model(g["seed"], P.ModelConfig(*g["config"]))
+    assert m.weight_hash == g["weight_hash"]
+    return m
+
+
+def _digest(P, arrs):
+    return P.weight_hash(np.ascontiguousarray(np.stack(arrs), np.int64).tobytes())
+
+
+@pytest.mark.parametrize("name", ["smoke7b", "c2"])
+def test_7b_matches_reference_engine(P, golden_7b, model7b, name):
+    g = golden_7b[name]
+    prompt = P.prompt_from_seed(g["prompt_seed"], g["config"][4], 16)[:g["P"]]
+    res = P.generate_greedy(model7b, prompt, g["max_new"], P.EngineOptions(keep_logits=True))
+    assert res.token_ids == g["tokens"]
+    assert res.output_hash.hex() == g["output_hash"]
+    assert _digest(P, res.logits) == g["logits_digest"]
+
+
+def test_7b_c4_long_generation(P, golden_7b, model7b):
+    g = golden_7b.get("c4")
+    if g is None:
+        pytest.skip("c4 golden not generated")
+    prompt = P.prompt_from_seed(g["prompt_seed"], g["config"][4], g["P"])
+    res = P.generate_greedy(model7b, prompt, g["max_new"])
+    assert res.token_ids == g["tokens"]
+    assert res.output_hash.hex() == g["output_hash"]
+
+
+def test_7b_c5_sequences(P, golden_7b, model7b):
+    names = sorted((k for k in golden_7b if k.startswith("c5_")), key=lambda k: int(k[3:]))
+    if not names:
+        pytest.skip("c5 goldens not generated")
+    s = P.InferenceSession(model7b)
+    for k in names:
+        g = golden_7b[k]
+        prompt = P.prompt_from_seed(g["prompt_seed"], g["config"][4], g["P"])
+        res = s.generate_greedy(prompt, g["max_new"])
+        assert res.token_ids == g["tokens"], k
+        assert res.output_hash.hex() == g["output_hash"], k

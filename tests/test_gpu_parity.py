@@ -122,6 +122,38 @@ def test_wild_models_take_the_wide_path(P, golden_models):
     assert s.stats()["wide_limb_ctas"] > 0
 
 
+def test_kv_beyond_int32_takes_the_int64_cache(P, oracle):
+    """K/V values past int32 (scaled-up wk/wv) must switch the head to the
+    int64 cache mid-sequence and still match the oracle bit for bit."""
+    from oracle.pyoracle import Config
+    cfgt = (2, 64, 2, 64, 64, 40)
+    cfg = P.ModelConfig(*cfgt)
+    base = oracle.gen_toy(21, Config(*cfgt))
+    shapes = Config(*cfgt).tensor_shapes()
+    scales = base.scales.copy()
+    boost = {1 + 7 * 0 + 2: 1 << 14, 1 + 7 * 1 + 1: 1 << 16, 1 + 7 * 1 + 2: 1 << 16}  # l0.wv, l1.wk, l1.wv
+    tens, so = [], 0
+    w_off = 0
+    for i, (r, c) in enumerate(shapes):
+        if i in boost:
+            scales[so:so + r] *= boost[i]
+        tens.append((base.weights[w_off:w_off + r * c].reshape(r, c), scales[so:so + r]))
+        so += r
+        w_off += r * c
+    om = oracle.model(Config(*cfgt), base.weights, scales, base.norms)
+    m = P.ModelFile.from_arrays(cfg, tens, base.norms)
+    prompt = [3, 9, 27, 17, 51, 25]
+    toks, h, lg = oracle.generate_greedy(om, prompt, 20, keep_logits=True)
+    s = P.InferenceSession(m, keep_logits_cap=20)
+    res = s.generate_greedy(prompt, 20, keep_logits=True)
+    assert res.token_ids == [int(t) for t in toks]
+    assert res.output_hash.hex() == h
+    assert np.array_equal(np.stack(res.logits), lg)
+    assert s.stats()["wide_kv_ctas"] > 0
+    res2 = s.generate_greedy(prompt, 20)  # a fresh sequence re-derives the flags
+    assert res2.output_hash.hex() == h
+
+
 def test_tinyllama_c1(P, golden_models):
     g = golden_models["tinyllama_c1"]
     m = _model_for(P, g)
