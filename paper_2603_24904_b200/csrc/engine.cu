@@ -95,7 +95,7 @@ DevCtx& dev_ctx(int device) {
     set_gemv_attrs<EPI_ARGMAX, MODE_NORM>();
     set_gemv_attrs<EPI_RAW, MODE_PLAIN>();
     CK(cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(attn_scratch_bytes(8192))));
+                            int(attn_op_scratch_bytes(8192))));
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, decode_persistent_kernel));
     c.smem_optin = int(prop.sharedMemPerBlockOptin) - int(fa.sharedSizeBytes);
@@ -259,7 +259,9 @@ struct dimg_session {
     uint32_t* tokens;  // [max_ctx + 1]
     Ctl* ctl;
     unsigned int* bar;
-    unsigned int* hsync;   // [H] attention part counters
+    unsigned long long* xg;  // [H][max_ctx][2] tagged score exchange words
+    unsigned long long* qkv_x;  // [3D][2] tagged q/k/v words
+    uint32_t attn_tag = 0;   // attention stages tagged so far (xg tags)
     int32_t *kc32, *vc32;  // int32 mirror of the KV cache
     uint32_t* kvwide;      // [L][H] mirror unusable (sticky per sequence)
     uint8_t* planes_att;   // [3][Kd] 3-limb planes of the attention output
@@ -322,6 +324,8 @@ std::vector<PkStage> step_program(const dimg_session& s) {
                                  s.qkv, lw.attn_unit);
         qkv.ssq_in = ssq_prev;
         if (l == 0) qkv.ssq_clear = s.ssq + 2 * m.L - 1;  // consumed by the previous step's head
+        qkv.ytag = s.qkv_x;     // q/k/v reach attention as tagged words:
+        qkv.no_barrier = 1;     // no grid barrier between the two stages
         p.push_back(qkv);
         PkStage at{};
         at.kind = SK_ATTN;
@@ -329,12 +333,12 @@ std::vector<PkStage> step_program(const dimg_session& s) {
         at.out_planes = s.planes_att;
         at.out_pitch = m.Kd;
         at.out_flag = f_att;
-        at.ssq_clear = ssq_prev;
         p.push_back(at);
         PkStage wo = gemv_stage(lw.wo, MODE_PLAIN, EPI_RESID, s.att, nullptr, s.x);
         wo.in_planes = s.planes_att;
         wo.in_flag = f_att;
         wo.ssq_out = ssq_wo;
+        wo.ssq_clear = ssq_prev;  // every CTA's qkv prologue read it before the attention barrier
         p.push_back(wo);
         PkStage gu = gemv_stage(lw.gu, MODE_NORM, EPI_SILU, s.x, lw.ffn_norm, s.h, lw.ffn_unit);
         gu.out_planes = s.planes_h;
@@ -391,7 +395,16 @@ PkArgs pk_args(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     a.kv_layer_stride = size_t(m.H) * m.cfg.max_ctx * m.dh;
     // CTAs per head: split the head's dims over the SMs the heads leave idle
     a.attn_parts = std::max(1u, std::min(s.grid / m.H, std::max(1u, m.dh / 8)));
-    a.hsync = s.hsync;
+    {
+        auto log2_or = [](uint32_t x) { return x && !(x & (x - 1)) ? int32_t(__builtin_ctz(x)) : -1; };
+        uint32_t dpp = (m.dh + a.attn_parts - 1) / a.attn_parts;
+        dpp = (dpp + 3) & ~3u;  // whole 4-dim quads
+        a.attn_dpp = dpp;
+        a.attn_np_shift = log2_or(a.attn_parts);
+        a.attn_nq_shift = log2_or(dpp / 4);
+    }
+    a.xg = s.xg;
+    a.qkv_x = s.qkv_x;
     a.kc32 = s.kc32;
     a.vc32 = s.vc32;
     a.kvwide = s.kvwide;
@@ -407,8 +420,15 @@ void launch_pk(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     a.trace = trace;
     a.trace_cap = trace_cap;
 
+    // tags of the attention score exchange: unique per attention stage, never 0
+    const uint64_t n_attn = uint64_t(n_steps) * s.m->L;
+    if (uint64_t(s.attn_tag) + n_attn + 2 > 0xFFFFFFFFull) {
+        CK(cudaMemsetAsync(s.xg, 0, size_t(s.m->H) * s.m->cfg.max_ctx * 16, s.stream));
+        s.attn_tag = 0;
+    }
+    a.tag_base = s.attn_tag;
+    s.attn_tag += uint32_t(n_attn);
     CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned int), s.stream));
-    CK(cudaMemsetAsync(s.hsync, 0, s.m->H * sizeof(unsigned int), s.stream));
     CK(cudaMemsetAsync(s.flags, 0, size_t(2) * s.m->L * sizeof(uint32_t), s.stream));
     CK(cudaMemsetAsync(s.ssq, 0, size_t(2) * s.m->L * sizeof(unsigned long long), s.stream));
     void* params[] = {&a};
@@ -611,7 +631,10 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         s->tokens = s->mem.alloc<uint32_t>(ctx + 1);
         s->ctl = s->mem.alloc<Ctl>(1);
         s->bar = s->mem.alloc<unsigned int>(64);
-        s->hsync = s->mem.alloc<unsigned int>(m->H);
+        s->xg = s->mem.alloc<unsigned long long>(size_t(m->H) * ctx * 2);
+        s->qkv_x = s->mem.alloc<unsigned long long>(size_t(3) * m->D * 2);
+        CK(cudaMemsetAsync(s->qkv_x, 0, size_t(3) * m->D * 16, s->stream));
+        CK(cudaMemsetAsync(s->xg, 0, size_t(m->H) * ctx * 16, s->stream));
         s->kc32 = s->mem.alloc<int32_t>(kv);
         s->vc32 = s->mem.alloc<int32_t>(kv);
         s->kvwide = s->mem.alloc<uint32_t>(size_t(m->L) * m->H);
@@ -794,6 +817,8 @@ dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, flo
             st.ssq_in = nullptr;  // the probe has no producer stages: sums computed in place
             st.ssq_out = nullptr;
             st.ssq_clear = nullptr;
+            st.ytag = nullptr;  // no attention stage follows
+            st.no_barrier = 0;
             prog.push_back(st);
         }
         if (!s->probe_stages || n > 0) {
@@ -1002,7 +1027,7 @@ dimg_status dimg_op_attention(int device, uint32_t H, uint32_t dh, uint32_t max_
             CK(cudaMemcpyAsync(qkv + 2 * D, v + p * D, D * 8, cudaMemcpyHostToDevice, o.c.op_stream));
             set_pos_kernel<<<1, 1, 0, o.c.op_stream>>>(o.c.op_ctl, p);
             t.out = d_out + p * D;
-            attn_decode_kernel<<<H, ATTN_THREADS, attn_scratch_bytes(dh), o.c.op_stream>>>(t);
+            attn_decode_kernel<<<H, ATTN_THREADS, attn_op_scratch_bytes(dh), o.c.op_stream>>>(t);
             CK(cudaGetLastError());
         }
         o.get(out, d_out, D * steps);

@@ -72,8 +72,11 @@ __device__ __noinline__ void softmax_strip(int64_t* S, uint32_t n, const int64_t
 
 // Bytes of shared scratch attn_head needs (score strip in shared memory when
 // max_ctx > 0, else in a.scores).
+__host__ __device__ constexpr size_t attn_op_scratch_bytes(uint32_t dh) {  // attn_head_part, strip in global
+    return (2 * size_t(dh) + 257 + ATTN_THREADS) * sizeof(int64_t);
+}
 __host__ __device__ constexpr size_t attn_scratch_bytes(uint32_t dh, uint32_t max_ctx = 0) {
-    return (2 * size_t(dh) + 257 + 4 * ATTN_THREADS + max_ctx) * sizeof(int64_t);
+    return (6 * size_t(dh) + 257 + 4 * ATTN_THREADS + max_ctx) * sizeof(int64_t);
 }
 
 // One head of one attention step at position `pos`, or one of `nparts`

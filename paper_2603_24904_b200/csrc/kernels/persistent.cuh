@@ -62,7 +62,8 @@ struct PkStage {
     uint8_t* out_planes;      // EPI_SILU / attention: planes of y, pitch out_pitch
     uint32_t* out_flag;
     uint32_t out_pitch;
-    uint32_t pad2;
+    uint32_t no_barrier;      // 1: the next stage consumes tagged words, no grid barrier after this one
+    unsigned long long* ytag; // EPI_STORE: also publish y as tagged word pairs (attention inputs)
     unsigned long long* ssq_out;  // EPI_RESID: sum of the new x^2 (exact: |x| <= 2^24 after the clamp)
     const unsigned long long* ssq_in;  // MODE_NORM after a RESID stage: that sum (nullptr = compute it)
     unsigned long long* ssq_clear;     // accumulator the previous stage consumed: CTA 0 re-zeroes it
@@ -92,7 +93,12 @@ struct PkArgs {
     unsigned long long* trace;  // optional: [stage_seq][32] stamps of CTA 0 (dimg_session_trace)
     uint32_t trace_cap;
     uint32_t attn_parts;      // CTAs per attention head (position blocks / dimension slices)
-    unsigned int* hsync;      // [H] per-head arrival counters of the attention parts (zeroed before launch)
+    uint32_t attn_dpp;        // dims per part (whole 4-dim quads)
+    int32_t attn_np_shift;    // log2(attn_parts) if a power of two, else -1
+    int32_t attn_nq_shift;    // log2(attn_dpp / 4) if a power of two, else -1
+    unsigned long long* xg;   // [H][max_ctx][2] tagged score words exchanged by a head's parts
+    unsigned long long* qkv_x;  // [3D][2] tagged q | k | v words (QKV stage -> attention)
+    uint32_t tag_base;        // attention stage k of this launch tags its words tag_base + k (never 0)
     int32_t* kc32;            // int32 mirror of kc / vc (same layout), read while kvwide is clear
     int32_t* vc32;
     uint32_t* kvwide;         // [L][H] some cached K/V value of the head needs more than 32 bits
@@ -175,6 +181,17 @@ __device__ __forceinline__ uint32_t ld_cg32(const uint32_t* p) {
     uint32_t r;
     asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
+}
+
+// Tagged-word exchange (the LL-protocol idea): every 8-byte word carries 32
+// bits of payload and a 32-bit stage tag; an aligned 8-byte access is
+// single-copy atomic, so a reader that sees the current tag sees its payload
+// -- no fence, no counter, one trip through L2.
+__device__ __forceinline__ void st_tagged2(unsigned long long* p, uint64_t a, uint64_t b) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_tagged2(const unsigned long long* p, uint64_t& a, uint64_t& b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -607,6 +624,8 @@ struct GemvRT {
     int64_t* lrow;            // EPI_ARGMAX: this step's logits row
     const int64_t* lut;
     unsigned long long* ssq;  // EPI_RESID: sum-of-squares accumulator
+    unsigned long long* ytag; // EPI_STORE: tagged word pairs of y
+    uint64_t tg;              // their tag << 32
 };
 
 // All of this CTA's row groups of a GEMV stage, epilogues fused.
@@ -644,6 +663,7 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
             const int64_t val = scale_row(int64_t(acc), scale);
             if (g_.epi == EPI_STORE) {
                 g_.y[row] = val;
+                if (g_.ytag) st_tagged2(g_.ytag + 2 * row, g_.tg | uint32_t(val), g_.tg | uint32_t(uint64_t(val) >> 32));
             } else if (g_.epi == EPI_RESID) {
                 const int64_t x = add_clamp(resid, val);
                 g_.y[row] = x;
@@ -733,6 +753,54 @@ __device__ __noinline__ void attn_rope_tail(const int64_t* q, const int64_t* k, 
         }
 }
 
+// softmax_q16 over S[0..n) in place (proj/src/kernels.cpp:90-107), the same
+// arithmetic as softmax_strip with fewer round trips: the int64 max as two
+// 32-bit REDUX steps, the weights (<= 2^16 each, n <= 2^19) summed in 32 bits
+// per warp, and the per-element division (w << 16) / total as a multiply by
+// floor((2^64 - 1) / total) plus one exact correction step.
+__device__ __forceinline__ void softmax_strip_fast(int64_t* S, uint32_t n, const int64_t* lut, u128* red) {
+    if (n > (1u << 19)) {  // the 32-bit warp sums could overflow: the plain version
+        softmax_strip_inl(S, n, lut, red);
+        return;
+    }
+    int64_t* smax = reinterpret_cast<int64_t*>(red);           // [8]
+    uint32_t* ssum = reinterpret_cast<uint32_t*>(smax + 8);    // [8]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t m = INT64_MIN;
+#pragma unroll 1
+    for (uint32_t t = threadIdx.x; t < n; t += ATTN_THREADS) m = S[t] > m ? S[t] : m;
+    const int32_t mh = __reduce_max_sync(0xffffffffu, int32_t(uint64_t(m) >> 32));
+    const uint32_t ml = __reduce_max_sync(0xffffffffu, int32_t(uint64_t(m) >> 32) == mh ? uint32_t(m) : 0u);
+    if (lane == 0) smax[warp] = int64_t((uint64_t(uint32_t(mh)) << 32) | ml);
+    __syncthreads();
+    m = smax[0];
+#pragma unroll
+    for (int w = 1; w < ATTN_THREADS / 32; ++w) m = smax[w] > m ? smax[w] : m;
+    uint32_t tot = 0;
+#pragma unroll 1
+    for (uint32_t t = threadIdx.x; t < n; t += ATTN_THREADS) {
+        const int64_t d = wrap_sub(m, S[t]);
+        const int64_t w = exp_neg(d > 8 * ONE ? 8 * ONE : d, lut);
+        S[t] = w;
+        tot += uint32_t(w);
+    }
+    tot = __reduce_add_sync(0xffffffffu, tot);
+    if (lane == 0) ssum[warp] = tot;
+    __syncthreads();
+    uint64_t total = 0;
+#pragma unroll
+    for (int w = 0; w < ATTN_THREADS / 32; ++w) total += ssum[w];
+    const uint64_t inv = ~0ull / total;
+#pragma unroll 1
+    for (uint32_t t = threadIdx.x; t < n; t += ATTN_THREADS) {
+        const uint64_t a = uint64_t(S[t]) << 16;
+        uint64_t q = __umul64hi(a, inv);  // floor(a / total) or one less
+        q += (a - q * total) >= total;
+        S[t] = int64_t(q);
+    }
+    __syncthreads();
+}
+
 // attention_step (proj/src/kernels.cpp:117-177) for head h as part `pi` of
 // `np` CTAs. Each part scores its own contiguous block of cached positions
 // (the K strip is read once per head, not once per part), publishes them to
@@ -760,16 +828,20 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
     const uint32_t dh = A.attn.dh, half = dh / 2, H = A.attn.H, D = H * dh, T = pos + 1, mc = A.attn.max_ctx;
     int64_t* qrot = scratch;                                               // [dh]
     int64_t* krot = scratch + dh;                                          // [dh]
-    int32_t* q32 = reinterpret_cast<int32_t*>(scratch + 2 * dh);           // [dh] (257 words reserved)
-    uint64_t* part = reinterpret_cast<uint64_t*>(scratch + 2 * dh + 257);  // [4 * ATTN_THREADS]
+    int32_t* q32 = reinterpret_cast<int32_t*>(scratch + 2 * dh);           // [dh]
+    int32_t* k32 = q32 + dh;                                               // [dh]
+    int64_t* qkv_s = scratch + 3 * dh;                                     // [3][dh] this step's q | k | v
+    uint64_t* part = reinterpret_cast<uint64_t*>(scratch + 6 * dh + 257);  // [4 * ATTN_THREADS]
     int64_t* S = reinterpret_cast<int64_t*>(part + 4 * ATTN_THREADS);      // [max_ctx] score strip
-    const uint32_t t0 = T * pi / np, t1 = T * (pi + 1) / np;  // T <= max_ctx, np <= 64: 32-bit exact
+    // T <= max_ctx, np <= 64: 32-bit exact; shifts when np is a power of two
+    const int nps = A.attn_np_shift;
+    const uint32_t t0 = nps >= 0 ? (T * pi) >> nps : T * pi / np, t1 = nps >= 0 ? (T * (pi + 1)) >> nps : T * (pi + 1) / np;
     const bool owner = pi + 1 == np;                        // t1 == T: the newest position is the last part's
     // fast path shape: whole 4-dim quads (16-byte int32 rows), q rows within one pass
     const bool shape_ok = (dh & 3) == 0 && dh <= 512;
-    const int64_t* q = A.attn.qkv + size_t(h) * dh;
-    const int64_t* k = A.attn.qkv + D + size_t(h) * dh;
-    const int64_t* v = A.attn.qkv + 2 * size_t(D) + size_t(h) * dh;
+    const int64_t* q = qkv_s;
+    const int64_t* k = qkv_s + dh;
+    const int64_t* v = qkv_s + 2 * dh;
     const size_t hoff = size_t(layer) * A.kv_layer_stride + size_t(h) * mc * dh;
     int64_t* K64 = A.attn.kc + hoff;
     int64_t* V64 = A.attn.vc + hoff;
@@ -780,36 +852,25 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
     const int64_t* sr = A.attn.rope_sin + size_t(pos) * half;
 
     // PV mapping: thread = (4-dim quad jq, position slice sl)
-    uint32_t dpp = (dh + np - 1) / np;
-    dpp = (dpp + 3) & ~3u;
+    const uint32_t dpp = A.attn_dpp;
     const uint32_t d0 = min(dh, pi * dpp), d1 = min(dh, d0 + dpp), nd = d1 - d0, nquads = nd / 4;
     const bool pv_shape = shape_ok && nquads > 0 && nquads <= ATTN_THREADS;
-    const uint32_t slices = pv_shape ? ATTN_THREADS / nquads : 1;
-    const uint32_t jq = pv_shape ? threadIdx.x % nquads : 0, sl = pv_shape ? threadIdx.x / nquads : ATTN_THREADS;
+    const int nqs = nquads == dpp / 4 ? A.attn_nq_shift : -1;  // the last part may be short
+    const uint32_t slices = !pv_shape ? 1 : nqs >= 0 ? ATTN_THREADS >> nqs : ATTN_THREADS / nquads;
+    const uint32_t jq = !pv_shape ? 0 : nqs >= 0 ? threadIdx.x & (nquads - 1) : threadIdx.x % nquads;
+    const uint32_t sl = !pv_shape ? ATTN_THREADS : nqs >= 0 ? threadIdx.x >> nqs : threadIdx.x / nquads;
     const uint32_t jv = d0 + 4 * jq;
 
-    // 1. L2 first: the head's wide flag, this step's q/k rows, the RoPE rows,
-    //    the newest V quad; then HBM, speculatively as int32: the K rows of
-    //    the first score pass and the V rows of the first PV round.
+    // 1. The head's wide flag and the RoPE rows (L2); then, speculatively as
+    //    int32 from HBM, the K rows of the first score pass and the V rows of
+    //    the first PV round -- none of which depends on this step's q/k/v.
     const bool rope_thread = threadIdx.x < half;
-    int64_t q0 = 0, q1 = 0, k0 = 0, k1 = 0, c_ = 0, s_ = 0, vnew = 0;
+    int64_t c_ = 0, s_ = 0;
     uint32_t wide_in = 0;
     if (threadIdx.x == 0) wide_in = ld_cg32(wflag);
     if (rope_thread) {
         c_ = cr[threadIdx.x];
         s_ = sr[threadIdx.x];
-        q0 = q[threadIdx.x];
-        q1 = q[threadIdx.x + half];
-        if (owner) {
-            k0 = k[threadIdx.x];
-            k1 = k[threadIdx.x + half];
-        }
-    }
-    if (owner && threadIdx.x < dh) vnew = v[threadIdx.x];
-    longlong2 vq01 = make_longlong2(0, 0), vq23 = make_longlong2(0, 0);
-    if (sl < slices) {
-        vq01 = *reinterpret_cast<const longlong2*>(v + jv);
-        vq23 = *reinterpret_cast<const longlong2*>(v + jv + 2);
     }
     ASTAMP(10);
 
@@ -834,27 +895,66 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
     }
     ASTAMP(11);
 
-    // 2. RoPE (rope_apply_inplace, kernels.cpp:70-82) and the KV append (:139-142)
+    // 2. This step's q/k/v rows of the head, published by the QKV stage as
+    //    tagged word pairs (no grid barrier in between): poll them into
+    //    shared memory.
+    {
+        const unsigned long long* W = A.qkv_x;
+        const uint64_t tagq = uint32_t(A.tag_base + epoch);
+        int ok = 1;
+#pragma unroll 1
+        for (uint32_t i = threadIdx.x; i < 3 * dh && ok; i += ATTN_THREADS) {
+            const uint32_t which = i / dh, j = i - which * dh;
+            const size_t row = size_t(which) * D + size_t(h) * dh + j;
+            uint64_t lo, hi;
+            uint32_t spins = 0;
+            uint64_t g0 = 0;
+            for (;;) {
+                ld_tagged2(W + 2 * row, lo, hi);
+                if ((lo >> 32) == tagq && (hi >> 32) == tagq) break;
+                if ((++spins & 1023) == 0) {
+                    const uint64_t now = globaltimer();
+                    if (!g0) g0 = now;
+                    if ((*((volatile uint32_t*)&A.ctl->err) & 4u) || now - g0 > 4000000000ull) {
+                        atomicOr(&A.ctl->err, 4u);
+                        ok = 0;
+                        break;
+                    }
+                }
+            }
+            qkv_s[i] = int64_t((hi << 32) | (lo & 0xFFFFFFFFull));
+        }
+        if (!__syncthreads_and(ok)) return false;
+    }
+    ASTAMP(13);
+
+    // 3. RoPE (rope_apply_inplace, kernels.cpp:70-82) and the KV append (:139-142)
     int q_small = 1, kv_big = 0;
+    const int64_t vnew = owner && threadIdx.x < dh ? v[threadIdx.x] : 0;
     if (rope_thread) {
         const uint32_t i = threadIdx.x;
+        const int64_t q0 = q[i], q1 = q[i + half];
         int64_t x0, x1;
         rope_pair(q0, q1, c_, s_, x0, x1);
         qrot[i] = x0;
         qrot[i + half] = x1;
-        if (shape_ok) {  // q32 has room for dh <= 514
+        if (shape_ok) {
             q32[i] = int32_t(x0);
             q32[i + half] = int32_t(x1);
         }
         q_small = below23(x0) && below23(x1);
         if (owner) {
-            rope_pair(k0, k1, c_, s_, x0, x1);
+            rope_pair(k[i], k[i + half], c_, s_, x0, x1);
             krot[i] = x0;
             krot[i + half] = x1;
             K64[size_t(pos) * dh + i] = x0;
             K64[size_t(pos) * dh + i + half] = x1;
             K32[size_t(pos) * dh + i] = int32_t(x0);
             K32[size_t(pos) * dh + i + half] = int32_t(x1);
+            if (shape_ok) {
+                k32[i] = int32_t(x0);
+                k32[i + half] = int32_t(x1);
+            }
             kv_big = !fits_i32(x0) || !fits_i32(x1);
         }
     }
@@ -876,8 +976,22 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
     if (owner && threadIdx.x == 0 && (pos == 0 || big)) *reinterpret_cast<volatile uint32_t*>(wflag) = big ? 1u : 0u;
     if (tr) tr[4] = clock64();
 
-    // 3. scores of this part's positions (kernels.cpp:143-151)
+    // 3. scores of this part's positions (kernels.cpp:143-151); the newest
+    //    key (owner only) comes from shared memory. Each score is published
+    //    at once as two tagged words for the head's other parts.
+    unsigned long long* X = A.xg + size_t(h) * mc * 2;
+    const uint32_t tagv = A.tag_base + epoch;
+    const uint64_t tg = uint64_t(tagv) << 32;
     if (!wide && q_small) {
+        if (owner && (t0 + oc == pos || t0 + oc + NOCT == pos)) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = 4 * e + 32 * u;
+                const int4 kk = j < dh ? *reinterpret_cast<const int4*>(k32 + j) : make_int4(0, 0, 0, 0);
+                if (t0 + oc == pos) ka[u] = kk;
+                else kb[u] = kk;
+            }
+        }
         for (uint32_t b = t0; b < t1; b += 2 * NOCT) {
             const uint32_t ta = b + oc, tb = ta + NOCT;
             int64_t da = 0, db = 0;
@@ -887,10 +1001,10 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const uint32_t j = c0 + 4 * e + 32 * u;
-                        ka[u] = (j < dh && ta < t1 && ta != pos) ? *reinterpret_cast<const int4*>(K32 + size_t(ta) * dh + j)
-                                                                 : make_int4(0, 0, 0, 0);
-                        kb[u] = (j < dh && tb < t1 && tb != pos) ? *reinterpret_cast<const int4*>(K32 + size_t(tb) * dh + j)
-                                                                 : make_int4(0, 0, 0, 0);
+                        const int32_t* pa = ta == pos ? k32 : K32 + size_t(ta) * dh;
+                        const int32_t* pb = tb == pos ? k32 : K32 + size_t(tb) * dh;
+                        ka[u] = (j < dh && ta < t1) ? *reinterpret_cast<const int4*>(pa + j) : make_int4(0, 0, 0, 0);
+                        kb[u] = (j < dh && tb < t1) ? *reinterpret_cast<const int4*>(pb + j) : make_int4(0, 0, 0, 0);
                     }
                 }
 #pragma unroll
@@ -908,50 +1022,60 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
                 da += __shfl_xor_sync(0xffffffffu, da, o);
                 db += __shfl_xor_sync(0xffffffffu, db, o);
             }
-            if (e == 0) {  // the newest position is scored below, exactly
-                if (ta < t1 && ta != pos) S[ta] = mul16(da >> 16, A.attn.inv_scale);
-                if (tb < t1 && tb != pos) S[tb] = mul16(db >> 16, A.attn.inv_scale);
+            if (e == 0) {
+                if (ta < t1) {
+                    const int64_t sc = mul16(da >> 16, A.attn.inv_scale);
+                    S[ta] = sc;
+                    if (np > 1) st_tagged2(X + 2 * ta, tg | uint32_t(sc), tg | uint32_t(uint64_t(sc) >> 32));
+                }
+                if (tb < t1) {
+                    const int64_t sc = mul16(db >> 16, A.attn.inv_scale);
+                    S[tb] = sc;
+                    if (np > 1) st_tagged2(X + 2 * tb, tg | uint32_t(sc), tg | uint32_t(uint64_t(sc) >> 32));
+                }
             }
         }
-        if (owner) attn_scores_slow(K64, qrot, krot, dh, pos, pos + 1, pos, A.attn.inv_scale, S);
     } else {
         attn_scores_slow(K64, qrot, krot, dh, t0, t1, pos, A.attn.inv_scale, S);
         if (threadIdx.x == 0 && wide) atomicAdd(&A.ctl->stats[1], 1ull);
+        if (np > 1) {
+            __syncthreads();
+#pragma unroll 1
+            for (uint32_t t = t0 + threadIdx.x; t < t1; t += ATTN_THREADS)
+                st_tagged2(X + 2 * t, tg | uint32_t(S[t]), tg | uint32_t(uint64_t(S[t]) >> 32));
+        }
     }
     ASTAMP(14);
     if (np > 1) {
-        // publish, meet the head's other parts, gather their scores
-        int64_t* G = A.attn.scores + size_t(h) * mc;
-        __syncthreads();
-        for (uint32_t t = t0 + threadIdx.x; t < t1; t += ATTN_THREADS) G[t] = S[t];
-        __shared__ int s_ok;
-        __syncthreads();
-        ASTAMP(15);
-        if (threadIdx.x == 0) {
-            s_ok = 1;
-            __threadfence();
-            atomicAdd(A.hsync + h, 1u);
-            const uint32_t target = np * epoch;
-            const uint64_t g0 = globaltimer();
-            while (ld_acquire(A.hsync + h) < target) {
-                if (*((volatile uint32_t*)&A.ctl->err) & 4u) { s_ok = 0; break; }
-                if (globaltimer() - g0 > 4000000000ull) {
-                    atomicOr(&A.ctl->err, 4u);
-                    s_ok = 0;
-                    break;
+        // gather the other parts' scores as their tagged words arrive
+        int ok = 1;
+#pragma unroll 1
+        for (uint32_t t = threadIdx.x; t < T && ok; t += ATTN_THREADS) {
+            if (t >= t0 && t < t1) continue;
+            uint64_t lo, hi;
+            uint32_t spins = 0;
+            uint64_t g0 = 0;
+            for (;;) {
+                ld_tagged2(X + 2 * t, lo, hi);
+                if (uint32_t(lo >> 32) == tagv && uint32_t(hi >> 32) == tagv) break;
+                if ((++spins & 1023) == 0) {
+                    const uint64_t now = globaltimer();
+                    if (!g0) g0 = now;
+                    if ((*((volatile uint32_t*)&A.ctl->err) & 4u) || now - g0 > 4000000000ull) {
+                        atomicOr(&A.ctl->err, 4u);
+                        ok = 0;
+                        break;
+                    }
                 }
             }
-            ASTAMP(16);
+            S[t] = int64_t((hi << 32) | (lo & 0xFFFFFFFFull));
         }
-        __syncthreads();
-        if (!s_ok) return false;
-        for (uint32_t t = threadIdx.x; t < T; t += ATTN_THREADS)
-            if (t < t0 || t >= t1) S[t] = ld_cg64(G + t);
         ASTAMP(17);
+        if (!__syncthreads_and(ok)) return false;
     }
     __syncthreads();
     if (tr) tr[5] = clock64();
-    softmax_strip_inl(S, T, lut, red);
+    softmax_strip_fast(S, T, lut, red);
     if (tr) tr[6] = clock64();
 
     // 4. out_j = sum_t mul16(p_t, V[t]_j) (kernels.cpp:153-159) over this
@@ -980,10 +1104,10 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
             }
             if (pos % slices == sl) {  // the newest row
                 const int64_t p = S[pos];
-                a0 += mul16_prob(p, vq01.x);
-                a1 += mul16_prob(p, vq01.y);
-                a2 += mul16_prob(p, vq23.x);
-                a3 += mul16_prob(p, vq23.y);
+                a0 += mul16_prob(p, v[jv]);
+                a1 += mul16_prob(p, v[jv + 1]);
+                a2 += mul16_prob(p, v[jv + 2]);
+                a3 += mul16_prob(p, v[jv + 3]);
             }
         }
         part[4 * threadIdx.x + 0] = uint64_t(a0);
@@ -1000,6 +1124,7 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
         uint64_t sum = 0;
         if (!wide && pv_shape) {
             const uint32_t qd = threadIdx.x >> 2, z = threadIdx.x & 3;
+#pragma unroll 4
             for (uint32_t s2 = 0; s2 < slices; ++s2) sum += part[4 * (s2 * nquads + qd) + z];
         } else {
             sum = part[threadIdx.x];
@@ -1066,7 +1191,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
     uint32_t pos = ctl->pos;
     const uint32_t logit_base = ctl->logit_base, keep_cap = ctl->keep_cap;
     uint32_t token = a.tokens[pos];
-    uint32_t nbar = 0, cur = 0, attn_epoch = 0;
+    uint32_t nbar = 0, cur = 0, attn_epoch = 0, nseq = 0;
 
     for (uint32_t step = 0; step < sc.n_steps; ++step) {
         const uint32_t nst = stages_in_step(sc, step);
@@ -1080,7 +1205,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
             if (threadIdx.x < kStWords)
                 next_word = reinterpret_cast<const uint32_t*>(sc.stages + (si + 1 < nst ? si + 1 : 0))[threadIdx.x];
             unsigned long long* tr =
-                a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nbar < a.trace_cap ? a.trace + 32 * nbar : nullptr;
+                a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nseq < a.trace_cap ? a.trace + 32 * nseq : nullptr;
+            ++nseq;
             if (tr) {
                 tr[8] = clock64();
                 tr[0] = globaltimer();
@@ -1117,6 +1243,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 g_.out_planes = st.out_planes; g_.out_flag = st.out_flag; g_.lut = s_lut;
                 g_.lrow = nullptr;
                 g_.ssq = st.ssq_out;
+                g_.ytag = st.ytag;
+                g_.tg = uint64_t(a.tag_base + attn_epoch + 1) << 32;  // the coming attention stage's tag
                 if (st.epi == EPI_ARGMAX) {
                     uint32_t slot = pos - logit_base;
                     slot = slot < keep_cap ? slot : keep_cap;
@@ -1146,7 +1274,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
             __syncthreads();  // everyone has its register copy of s_st[cur]; safe to overwrite the other
             if (threadIdx.x < kStWords) reinterpret_cast<uint32_t*>(&s_st[cur ^ 1])[threadIdx.x] = next_word;
             cur ^= 1;
-            if (!grid_sync(a.bar, ctl, nbar++)) return;
+            if (!st.no_barrier && !grid_sync(a.bar, ctl, nbar++)) return;
         }
         if (step >= sc.n_prefill) {
             // every CTA reduces the lm_head partials itself (no extra barrier)
