@@ -264,9 +264,8 @@ struct dimg_session {
     uint32_t attn_tag = 0;   // attention stages tagged so far (xg tags)
     int32_t *kc32, *vc32;  // int32 mirror of the KV cache
     uint32_t* kvwide;      // [L][H] mirror unusable (sticky per sequence)
-    uint8_t* planes_att;   // [3][Kd] 3-limb planes of the attention output
-    uint8_t* planes_h;     // [3][Kf] 3-limb planes of the FFN hidden vector
-    uint32_t* flags;       // [2L] "needs > 3 limbs" tags (att, h) per layer
+    uint32_t* words_att;   // [Kd] tagged limb words of the attention output
+    uint32_t* words_h;     // [Kf] tagged limb words of the FFN hidden vector
     unsigned long long* ssq;  // [2L] sums of squares of x after wo / after down (per layer)
     PkStage* stages;   // [5L + 1] device
     std::vector<PkStage> host_stages;
@@ -308,14 +307,20 @@ PkStage gemv_stage(const DevMat& d, uint32_t mode, uint32_t epi, const int64_t* 
     return st;
 }
 
+// Which word hand-offs run without a grid barrier (1 qkv->attention,
+// 2 attention->wo, 4 gate/up->down); DIMG_BARRIER_SKIP overrides for
+// experiments. With the barrier kept, the consumer still polls the words.
+uint32_t barrier_skip_mask() {
+    const char* v = std::getenv("DIMG_BARRIER_SKIP");
+    return v ? uint32_t(std::strtoul(v, nullptr, 0)) : 7u;
+}
+
 // The stage program of one forward step (proj/src/engine.cpp:85-101).
 std::vector<PkStage> step_program(const dimg_session& s) {
     const dimg_model& m = *s.m;
     std::vector<PkStage> p;
     for (uint32_t l = 0; l < m.L; ++l) {
         const auto& lw = m.layers[l];
-        uint32_t* f_att = s.flags + 2 * l;
-        uint32_t* f_h = s.flags + 2 * l + 1;
         // sums of squares of x: after wo(l) -> gu(l); after down(l) -> qkv(l+1) / head
         unsigned long long* ssq_wo = s.ssq + 2 * l;
         unsigned long long* ssq_dn = s.ssq + 2 * l + 1;
@@ -325,30 +330,26 @@ std::vector<PkStage> step_program(const dimg_session& s) {
         qkv.ssq_in = ssq_prev;
         if (l == 0) qkv.ssq_clear = s.ssq + 2 * m.L - 1;  // consumed by the previous step's head
         qkv.ytag = s.qkv_x;     // q/k/v reach attention as tagged words:
-        qkv.no_barrier = 1;     // no grid barrier between the two stages
+        qkv.no_barrier = (barrier_skip_mask() & 1) ? 1 : 0;  // no grid barrier between the two stages
         p.push_back(qkv);
         PkStage at{};
         at.kind = SK_ATTN;
         at.layer = l;
-        at.out_planes = s.planes_att;
-        at.out_pitch = m.Kd;
-        at.out_flag = f_att;
+        at.out_words = s.words_att;
+        at.no_barrier = (barrier_skip_mask() & 2) ? 1 : 0;  // WO polls the words
         p.push_back(at);
         PkStage wo = gemv_stage(lw.wo, MODE_PLAIN, EPI_RESID, s.att, nullptr, s.x);
-        wo.in_planes = s.planes_att;
-        wo.in_flag = f_att;
+        wo.in_words = s.words_att;
         wo.ssq_out = ssq_wo;
         wo.ssq_clear = ssq_prev;  // every CTA's qkv prologue read it before the attention barrier
         p.push_back(wo);
         PkStage gu = gemv_stage(lw.gu, MODE_NORM, EPI_SILU, s.x, lw.ffn_norm, s.h, lw.ffn_unit);
-        gu.out_planes = s.planes_h;
-        gu.out_pitch = m.Kf;
-        gu.out_flag = f_h;
+        gu.out_words = s.words_h;
+        gu.no_barrier = (barrier_skip_mask() & 4) ? 1 : 0;  // DOWN polls the words
         gu.ssq_in = ssq_wo;
         p.push_back(gu);
         PkStage dn = gemv_stage(lw.down, MODE_PLAIN, EPI_RESID, s.h, nullptr, s.x);
-        dn.in_planes = s.planes_h;
-        dn.in_flag = f_h;
+        dn.in_words = s.words_h;
         dn.ssq_out = ssq_dn;
         dn.ssq_clear = ssq_wo;
         p.push_back(dn);
@@ -429,7 +430,6 @@ void launch_pk(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     a.tag_base = s.attn_tag;
     s.attn_tag += uint32_t(n_attn);
     CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned int), s.stream));
-    CK(cudaMemsetAsync(s.flags, 0, size_t(2) * s.m->L * sizeof(uint32_t), s.stream));
     CK(cudaMemsetAsync(s.ssq, 0, size_t(2) * s.m->L * sizeof(unsigned long long), s.stream));
     void* params[] = {&a};
     CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(decode_persistent_kernel), dim3(s.grid),
@@ -642,11 +642,10 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         // one CTA per SM; shared memory = weight ring + limb planes + row accumulators
         s->grid = uint32_t(m->ctx->sm_count);
         s->parts = s->mem.alloc<ArgPart>(s->grid);
-        s->planes_att = s->mem.alloc<uint8_t>(size_t(3) * m->Kd);
-        s->planes_h = s->mem.alloc<uint8_t>(size_t(3) * m->Kf);
-        CK(cudaMemsetAsync(s->planes_att, 0, size_t(3) * m->Kd, s->stream));
-        CK(cudaMemsetAsync(s->planes_h, 0, size_t(3) * m->Kf, s->stream));
-        s->flags = s->mem.alloc<uint32_t>(2 * size_t(m->L));
+        s->words_att = s->mem.alloc<uint32_t>(m->Kd);
+        s->words_h = s->mem.alloc<uint32_t>(m->Kf);
+        CK(cudaMemsetAsync(s->words_att, 0, size_t(4) * m->Kd, s->stream));
+        CK(cudaMemsetAsync(s->words_h, 0, size_t(4) * m->Kf, s->stream));
         s->ssq = s->mem.alloc<unsigned long long>(2 * size_t(m->L));
         s->host_stages = step_program(*s);
         // shared staging: rmsnorm = vector + gains + up to 8 planes; plain =
@@ -819,6 +818,8 @@ dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, flo
             st.ssq_clear = nullptr;
             st.ytag = nullptr;  // no attention stage follows
             st.no_barrier = 0;
+            st.in_words = nullptr;  // plain inputs: planes straight from the int64 vector
+            st.out_words = nullptr;
             prog.push_back(st);
         }
         if (!s->probe_stages || n > 0) {

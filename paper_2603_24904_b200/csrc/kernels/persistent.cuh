@@ -57,11 +57,8 @@ struct PkStage {
     const int64_t* x;         // input vector (K)
     const int64_t* gamma;     // norm gains (MODE_NORM / MODE_EMBED)
     int64_t* y;               // output
-    const uint8_t* in_planes; // MODE_PLAIN: producer-written 3-limb planes [3][Kp]
-    const uint32_t* in_flag;  // MODE_PLAIN: == step tag if an element needs > 3 limbs
-    uint8_t* out_planes;      // EPI_SILU / attention: planes of y, pitch out_pitch
-    uint32_t* out_flag;
-    uint32_t out_pitch;
+    const uint32_t* in_words; // MODE_PLAIN: the input as tagged limb words (nullptr: build from x)
+    uint32_t* out_words;      // EPI_SILU / attention: publish y as tagged limb words
     uint32_t no_barrier;      // 1: the next stage consumes tagged words, no grid barrier after this one
     unsigned long long* ytag; // EPI_STORE: also publish y as tagged word pairs (attention inputs)
     unsigned long long* ssq_out;  // EPI_RESID: sum of the new x^2 (exact: |x| <= 2^24 after the clamp)
@@ -193,6 +190,26 @@ __device__ __forceinline__ void st_tagged2(unsigned long long* p, uint64_t a, ui
 __device__ __forceinline__ void ld_tagged2(const unsigned long long* p, uint64_t& a, uint64_t& b) {
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
+
+// Limb word of a MODE_PLAIN input element: bytes 0-2 = the three low limb
+// bytes, byte 3 = wide bit (needs more than 3 limbs) << 7 | 7-bit stage tag.
+__device__ __forceinline__ uint32_t limb_word(int64_t v, uint32_t tag7) {
+    const uint32_t wide = (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) ? 0x80u : 0u;
+    return (uint32_t(v) & 0xFFFFFFu) | ((wide | tag7) << 24);
+}
+__device__ __forceinline__ void st_word(uint32_t* p, uint32_t w) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(w) : "memory");
+}
+__device__ __forceinline__ uint4 ld_words4(const uint32_t* p) {
+    uint4 r;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+// 1 + (tag mod 127): consecutive uses of a word buffer always differ.
+__device__ __forceinline__ uint32_t tag7_of(uint32_t tag) { return 1u + tag % 127u; }
 
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
@@ -341,31 +358,96 @@ __device__ __forceinline__ void pipe_release(const Sched& sc, Pipe& p) {
 // because under a saturated HBM every instruction-cache miss is an L2 round
 // trip (ncu: 46% of prologue stalls were stall_no_inst before this).
 
-// Attention output / FFN hidden vector: copy the producer-written planes.
-__device__ __noinline__ int prologue_plain(uint32_t K, uint32_t Kp, const int64_t* x,
-                                           const uint8_t* in_planes, const uint32_t* in_flag,
-                                           uint32_t tag, uint32_t* planes, Ctl* ctl) {
+// Attention output / FFN hidden vector. Published by the producing stage as
+// tagged limb words with no grid barrier in between: poll every word (16-byte
+// loads) and unpack its three limb bytes into the planes. Every CTA reads
+// every word, so "some element needs more than 3 limbs" is a grid-uniform
+// decision: then (PLAIN_WIDE) all CTAs take one extra grid barrier and build
+// 8 planes from the int64 vector (planes_from_x). words == nullptr (timing
+// probes): planes straight from x.
+constexpr int PLAIN_WIDE = 9;
+
+__device__ __noinline__ int planes_from_x(uint32_t K, uint32_t Kp, const int64_t* x, uint32_t* planes, Ctl* ctl,
+                                          bool wide) {
     const uint32_t Kw = Kp / 4;
-    const uint32_t flag = ld_cg32(in_flag);  // same round trip as the copy
-    copy_g2s(planes, in_planes, 3 * Kp);
-    if (__syncthreads_or(flag == tag) == 0) return 3;  // every element fits 3 limbs
-    // wide input: 8 byte planes straight from the int64 vector
+    if (!wide) {
+        int fits = 1;
+        for (uint32_t j = threadIdx.x; j < K; j += blockDim.x) {
+            const int64_t v = ld_cg64(x + j);
+            fits &= v >= -(int64_t(1) << 23) && v < (int64_t(1) << 23);
+        }
+        wide = !__syncthreads_and(fits);
+    }
+    const int L = wide ? 8 : 3;
 #pragma unroll 1
     for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
+        uint64_t v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = 4 * w + e < K ? uint64_t(ld_cg64(x + 4 * w + e)) : 0;
 #pragma unroll 1
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < L; ++k) {
             uint32_t word = 0;
-            for (int e = 0; e < 4; ++e) {
-                const uint32_t j = 4 * w + e;
-                const uint64_t v = j < K ? uint64_t(ld_cg64(x + j)) : 0;
-                word |= uint32_t((v >> (8 * k)) & 0xFF) << (8 * e);
-            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) word |= uint32_t((v[e] >> (8 * k)) & 0xFF) << (8 * e);
             planes[k * Kw + w] = word;
         }
     }
-    if (threadIdx.x == 0) atomicAdd(&ctl->stats[0], 1ull);
+    if (L == 8 && threadIdx.x == 0) atomicAdd(&ctl->stats[0], 1ull);
     __syncthreads();
-    return 8;
+    return L;
+}
+
+__device__ __forceinline__ bool words_ready(uint4 q, uint32_t j, uint32_t K, uint32_t tag7) {
+    return (j >= K || ((q.x >> 24) & 0x7Fu) == tag7) && (j + 1 >= K || ((q.y >> 24) & 0x7Fu) == tag7) &&
+           (j + 2 >= K || ((q.z >> 24) & 0x7Fu) == tag7) && (j + 3 >= K || ((q.w >> 24) & 0x7Fu) == tag7);
+}
+
+__device__ __noinline__ int prologue_plain(uint32_t K, uint32_t Kp, const int64_t* x, const uint32_t* words,
+                                           uint32_t tag7, uint32_t* planes, Ctl* ctl) {
+    const uint32_t Kw = Kp / 4;
+    if (!words) return planes_from_x(K, Kp, x, planes, ctl, false);
+    constexpr int B = 8;  // 16-byte loads in flight per thread
+    int wide = 0, ok = 1;
+#pragma unroll 1
+    for (uint32_t w0 = threadIdx.x; w0 < Kw && ok; w0 += B * PK_THREADS) {
+        uint4 q[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const uint32_t w = w0 + b * PK_THREADS;
+            q[b] = w < Kw && 4 * w < K ? ld_words4(words + 4 * w) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const uint32_t w = w0 + b * PK_THREADS;
+            if (w >= Kw) continue;
+            uint4 v = q[b];
+            if (4 * w < K) {
+                uint32_t spins = 0;
+                uint64_t g0 = 0;
+                while (!words_ready(v, 4 * w, K, tag7)) {  // not published yet: poll this one
+                    v = ld_words4(words + 4 * w);
+                    if ((++spins & 1023) == 0) {
+                        const uint64_t now = globaltimer();
+                        if (!g0) g0 = now;
+                        if ((*((volatile uint32_t*)&ctl->err) & 4u) || now - g0 > 4000000000ull) {
+                            atomicOr(&ctl->err, 4u);
+                            ok = 0;
+                            break;
+                        }
+                    }
+                }
+                if (4 * w + 1 >= K) v.y = 0;  // padding of the last word group
+                if (4 * w + 2 >= K) v.z = 0;
+                if (4 * w + 3 >= K) v.w = 0;
+            }
+            wide |= (v.x | v.y | v.z | v.w) >> 31;
+            planes[w] = __byte_perm(__byte_perm(v.x, v.y, 0x0040), __byte_perm(v.z, v.w, 0x0040), 0x5410);
+            planes[Kw + w] = __byte_perm(__byte_perm(v.x, v.y, 0x0051), __byte_perm(v.z, v.w, 0x0051), 0x5410);
+            planes[2 * Kw + w] = __byte_perm(__byte_perm(v.x, v.y, 0x0062), __byte_perm(v.z, v.w, 0x0062), 0x5410);
+        }
+    }
+    if (!__syncthreads_and(ok)) return -1;
+    return __syncthreads_or(wide) ? PLAIN_WIDE : 3;
 }
 
 // rmsnorm input: the residual stream (or the embedded token on layer 0)
@@ -539,14 +621,6 @@ __device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_un
     return 8;
 }
 
-// Producer side of the plane hand-off: element j of an output vector.
-__device__ __forceinline__ void emit_planes(uint8_t* planes, uint32_t pitch, uint32_t* flag,
-                                            uint32_t tag, uint32_t j, int64_t v) {
-    planes[j] = uint8_t(v);
-    planes[pitch + j] = uint8_t(v >> 8);
-    planes[2 * pitch + j] = uint8_t(v >> 16);
-    if (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) *((volatile uint32_t*)flag) = tag;
-}
 
 // ---- one row group: 4 rows x K against the limb planes ------------------------
 
@@ -617,10 +691,9 @@ __device__ __forceinline__ void group_dot(const Sched& sc, Pipe& p, uint32_t Kp,
 
 // Everything the GEMV loop needs, by value (registers).
 struct GemvRT {
-    uint32_t epi, rows, Kp, n_groups, n_segs, out_pitch;
+    uint32_t epi, rows, Kp, n_groups, n_segs, tag7;
     int64_t* y;
-    uint8_t* out_planes;
-    uint32_t* out_flag;
+    uint32_t* out_words;      // EPI_SILU: tagged limb words of y
     int64_t* lrow;            // EPI_ARGMAX: this step's logits row
     const int64_t* lut;
     unsigned long long* ssq;  // EPI_RESID: sum-of-squares accumulator
@@ -653,7 +726,7 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
                 const int64_t us = scale_row(int64_t(lane ? v[3] : v[1]), s_u);
                 const int64_t h = mul16(silu_q16(gs, g_.lut), us);
                 g_.y[row / 2] = h;
-                emit_planes(g_.out_planes, g_.out_pitch, g_.out_flag, tag, row / 2, h);
+                if (g_.out_words) st_word(g_.out_words + row / 2, limb_word(h, g_.tag7));
             }
         } else if (lane < PK_ROWS && r0 + lane < g_.rows) {
             const uint32_t row = r0 + lane;
@@ -820,8 +893,7 @@ __device__ __forceinline__ void softmax_strip_fast(int64_t* S, uint32_t n, const
 // Returns false if the head's peers never arrived (ctl->err |= 4, as a barrier timeout).
 __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint32_t h, uint32_t pi, uint32_t np,
                                            uint32_t pos, uint32_t epoch, int64_t* scratch, u128* red,
-                                           uint8_t* planes, uint32_t pitch, uint32_t* flag, uint32_t tag,
-                                           const int64_t* lut, unsigned long long* tr) {
+                                           uint32_t* out_words, const int64_t* lut, unsigned long long* tr) {
 #define ASTAMP(i) \
     if (tr) tr[i] = clock64()
     ASTAMP(9);
@@ -1130,12 +1202,8 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
             sum = part[threadIdx.x];
         }
         const uint32_t o = h * dh + d0 + threadIdx.x;
-        A.attn.out[o] = int64_t(sum);
-        planes[o] = uint8_t(sum);
-        planes[pitch + o] = uint8_t(sum >> 8);
-        planes[2 * pitch + o] = uint8_t(sum >> 16);
-        const int64_t sv = int64_t(sum);
-        if (sv < -(int64_t(1) << 23) || sv >= (int64_t(1) << 23)) *((volatile uint32_t*)flag) = tag;
+        A.attn.out[o] = int64_t(sum);  // before the word: read after a grid barrier on the wide path
+        st_word(out_words + o, limb_word(int64_t(sum), tag7_of(A.tag_base + epoch)));
     }
     ASTAMP(21);
     __syncthreads();  // scratch is reused by the next head / stage
@@ -1211,36 +1279,52 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 tr[8] = clock64();
                 tr[0] = globaltimer();
             }
-            if (st.ssq_clear && blockIdx.x == 0 && threadIdx.x == 0) *st.ssq_clear = 0;
             if (st.kind == SK_ATTN) {
                 const uint32_t np = a.attn_parts;
                 ++attn_epoch;
                 for (uint32_t c = blockIdx.x; c < a.attn.H * np; c += gridDim.x)
                     if (!attn_split(a, st.layer, c / np, c % np, np, pos, attn_epoch,
-                                    reinterpret_cast<int64_t*>(stage_mem), red, st.out_planes, st.out_pitch,
-                                    st.out_flag, tag, s_lut, tr && c == 0 ? tr : nullptr))
+                                    reinterpret_cast<int64_t*>(stage_mem), red, st.out_words, s_lut,
+                                    tr && c == 0 ? tr : nullptr))
                         return;
             } else {
                 uint32_t* planes;
                 int L;
                 if (st.mode == MODE_PLAIN) {
                     planes = reinterpret_cast<uint32_t*>(stage_mem);
-                    L = prologue_plain(st.K, st.Kp, st.x, st.in_planes, st.in_flag, tag, planes, ctl);
+                    L = prologue_plain(st.K, st.Kp, st.x, st.in_words, tag7_of(a.tag_base + attn_epoch), planes, ctl);
+                    if (L < 0) return;
+                    if (L == PLAIN_WIDE) {  // grid-uniform: the int64 vector is visible after the barrier
+                        if (!grid_sync(a.bar, ctl, nbar++)) return;
+                        L = planes_from_x(st.K, st.Kp, st.x, planes, ctl, true);
+                    }
                 } else {
+                    // Stages are not always separated by grid barriers: a CTA
+                    // without rows here must not read x / the sums at all (it
+                    // could lag behind their next writers). The embedding is
+                    // written by the CTA holding group 0.
+                    uint32_t glo, ghi;
+                    cta_range(st.n_groups, glo, ghi);
                     int64_t* xb = reinterpret_cast<int64_t*>(stage_mem);
                     planes = reinterpret_cast<uint32_t*>(xb + st.Kp);
-                    const bool embed = st.mode == MODE_EMBED;
-                    L = prologue_norm(st.K, st.Kp, st.gamma_unit != 0, st.x, st.gamma,
-                                      embed ? a.embd + size_t(token) * st.K : nullptr,
-                                      embed ? a.embd_scales[token] : 0,
-                                      embed && blockIdx.x == 0 ? a.x_resid : nullptr, xb, planes, red,
-                                      s_seeds, ctl, tr, st.ssq_in);
+                    L = 3;
+                    if (glo < ghi) {
+                        const bool embed = st.mode == MODE_EMBED;
+                        L = prologue_norm(st.K, st.Kp, st.gamma_unit != 0, st.x, st.gamma,
+                                          embed ? a.embd + size_t(token) * st.K : nullptr,
+                                          embed ? a.embd_scales[token] : 0,
+                                          embed && glo == 0 ? a.x_resid : nullptr, xb, planes, red,
+                                          s_seeds, ctl, tr, st.ssq_in);
+                    }
                 }
+                // the sum the previous stages' prologues consumed: every reader
+                // is done once this stage's inputs are complete
+                if (st.ssq_clear && blockIdx.x == 0 && threadIdx.x == 0) *st.ssq_clear = 0;
                 if (tr) tr[1] = globaltimer();
                 GemvRT g_;
                 g_.epi = st.epi; g_.rows = st.rows; g_.Kp = st.Kp; g_.n_groups = st.n_groups;
-                g_.n_segs = st.n_segs; g_.out_pitch = st.out_pitch; g_.y = st.y;
-                g_.out_planes = st.out_planes; g_.out_flag = st.out_flag; g_.lut = s_lut;
+                g_.n_segs = st.n_segs; g_.tag7 = tag7_of(a.tag_base + attn_epoch); g_.y = st.y;
+                g_.out_words = st.out_words; g_.lut = s_lut;
                 g_.lrow = nullptr;
                 g_.ssq = st.ssq_out;
                 g_.ytag = st.ytag;
@@ -1274,7 +1358,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
             __syncthreads();  // everyone has its register copy of s_st[cur]; safe to overwrite the other
             if (threadIdx.x < kStWords) reinterpret_cast<uint32_t*>(&s_st[cur ^ 1])[threadIdx.x] = next_word;
             cur ^= 1;
-            if (!st.no_barrier && !grid_sync(a.bar, ctl, nbar++)) return;
+            if (st.no_barrier) __syncthreads();  // the next descriptor is complete before anyone reads it
+            else if (!grid_sync(a.bar, ctl, nbar++)) return;
         }
         if (step >= sc.n_prefill) {
             // every CTA reduces the lm_head partials itself (no extra barrier)
