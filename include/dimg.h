@@ -197,6 +197,9 @@ dimg_status dimg_session_stats(dimg_session* s, uint64_t out[4]);
 /* ---- operator-level exports (host buffers in/out) for unit parity with
  *      proj/src/kernels.cpp; they run the engine's own device kernels. ---- */
 dimg_status dimg_op_dense(int device, const dimg_qtensor* w, const int64_t* x, int64_t* out);
+/* dense_forward (proj/src/kernels.cpp:18-30) applied to T tokens x[T][cols]
+ * -> out[T][rows]: the prefill GEMM (tcgen05 kind::i8 over byte limbs). */
+dimg_status dimg_op_dense_tokens(int device, const dimg_qtensor* w, const int64_t* x, uint32_t T, int64_t* out);
 dimg_status dimg_op_rmsnorm(int device, const int64_t* x, const int64_t* g, uint32_t n,
                             int64_t* out);
 dimg_status dimg_op_softmax(int device, const int64_t* s, uint32_t n, int64_t* out);

@@ -88,6 +88,7 @@ def _load():
         "dimg_session_stats": ([vp, u64p], C.c_int),
         "dimg_session_trace": ([vp, C.c_uint32, u64p, C.c_uint32], C.c_int),
         "dimg_op_dense": ([C.c_int, C.POINTER(QTensor), i64p, i64p], C.c_int),
+        "dimg_op_dense_tokens": ([C.c_int, C.POINTER(QTensor), i64p, C.c_uint32, i64p], C.c_int),
         "dimg_op_rmsnorm": ([C.c_int, i64p, i64p, C.c_uint32, i64p], C.c_int),
         "dimg_op_softmax": ([C.c_int, i64p, C.c_uint32, i64p], C.c_int),
         "dimg_op_attention": ([C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_uint32,

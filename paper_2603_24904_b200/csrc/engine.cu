@@ -12,6 +12,8 @@
 // while every warp keeps streaming its next weight chunks. A whole
 // generate_greedy call (P-1 prompt steps + N decode steps) is one launch; the
 // position and the token ring live in device memory.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -28,6 +30,7 @@
 #include "kernels/attention.cuh"
 #include "kernels/gemv.cuh"
 #include "kernels/persistent.cuh"
+#include "kernels/tc_gemm.cuh"
 
 using namespace dimg;
 using namespace dimg::dev;
@@ -88,6 +91,7 @@ DevCtx& dev_ctx(int device) {
     CK(cudaStreamCreateWithFlags(&c.op_stream, cudaStreamNonBlocking));
     set_gemv_attrs<EPI_STORE, MODE_PLAIN>();
     set_gemv_attrs<EPI_STORE, MODE_NORM>();
+    CK(cudaFuncSetAttribute(limb_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TG_SMEM));
     set_gemv_attrs<EPI_STORE, MODE_EMBED>();
     set_gemv_attrs<EPI_RESID, MODE_PLAIN>();
     set_gemv_attrs<EPI_SILU, MODE_NORM>();
@@ -121,6 +125,60 @@ struct DevBuf {
         for (void* p : ptrs) cudaFree(p);
     }
 };
+
+// ---- tensor-core GEMM plumbing ------------------------------------------------
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (!f || q != cudaDriverEntryPointSuccess) fail(DIMG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+// 2-D byte matrix [outer][inner] with row stride `stride` bytes, read in
+// 128 x 128 boxes with the 128-byte swizzle the UMMA descriptors expect;
+// out-of-range elements read as zero.
+CUtensorMap tmap_bytes(const void* base, uint64_t inner, uint64_t outer, uint64_t stride) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {stride};
+    const cuuint32_t box[2] = {TG_BK, TG_BM};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = tmap_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box,
+                                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(DIMG_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return m;
+}
+
+// Three byte limbs of int64 rows x[t][0..K) into planes [3][rows_pad][ldp]
+// (l0, l1 unsigned, l2 signed: exact for -2^23 <= x < 2^23); *wide = 1 if
+// some element is outside that range.
+__global__ void limbs_kernel(const int64_t* __restrict__ x, uint32_t T, uint32_t K, uint32_t ldx,
+                             uint8_t* __restrict__ planes, uint32_t rows_pad, uint32_t ldp, uint32_t* wide) {
+    const size_t plane = size_t(rows_pad) * ldp;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < size_t(T) * K;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t t = uint32_t(i / K), j = uint32_t(i % K);
+        const int64_t v = x[size_t(t) * ldx + j];
+        uint8_t* p = planes + size_t(t) * ldp + j;
+        p[0] = uint8_t(v);
+        p[plane] = uint8_t(v >> 8);
+        p[2 * plane] = uint8_t(v >> 16);
+        if (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) *wide = 1;
+    }
+}
+
+void launch_limb_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs& a, cudaStream_t st) {
+    dim3 grid((a.n_out + TG_BM - 1) / TG_BM, (a.n_tok + TG_BN - 1) / TG_BN);
+    limb_gemm_kernel<<<grid, TG_THREADS, TG_SMEM, st>>>(ta, tb, a);
+    CK(cudaGetLastError());
+}
 
 }  // namespace
 
@@ -960,6 +1018,48 @@ dimg_status dimg_op_dense(int device, const dimg_qtensor* w, const int64_t* x, i
         launch_gemv<EPI_STORE, MODE_PLAIN>(a, o.c, o.c.op_stream);
         CK(cudaGetLastError());
         o.get(out, a.y, w->rows);
+    })
+}
+
+dimg_status dimg_op_dense_tokens(int device, const dimg_qtensor* w, const int64_t* x, uint32_t T, int64_t* out) {
+    // dense_forward (proj/src/kernels.cpp:18-30) for T tokens: the tensor-core
+    // limb GEMM (kind::i8); tokens with an activation beyond 3 limbs go
+    // through the exact GEMV instead.
+    DIMG_API_GUARD({
+        if (T == 0) return DIMG_OK;
+        OpScope o(device);
+        const uint32_t N = w->rows, K = w->cols, Kp = pad16(K);
+        const uint32_t Tp = (T + TG_BN - 1) / TG_BN * TG_BN;
+        int8_t* W = o.put_padded(*w, 1, N, 0);
+        int64_t* sc = o.put(w->scales, N);
+        int64_t* xd = o.put(x, size_t(T) * K);
+        uint8_t* planes = o.mem.alloc<uint8_t>(size_t(3) * Tp * Kp);
+        uint32_t* wide = o.mem.alloc<uint32_t>(1);
+        CK(cudaMemsetAsync(planes, 0, size_t(3) * Tp * Kp, o.c.op_stream));
+        CK(cudaMemsetAsync(wide, 0, 4, o.c.op_stream));
+        limbs_kernel<<<1024, 256, 0, o.c.op_stream>>>(xd, T, K, K, planes, Tp, Kp, wide);
+        CK(cudaGetLastError());
+        int64_t* y = o.mem.alloc<int64_t>(size_t(T) * N);
+        TgArgs a{};
+        a.n_out = N;
+        a.n_tok = T;
+        a.n_kblk = (K + TG_BK - 1) / TG_BK;
+        a.limb_rows = Tp;
+        a.epi = TG_STORE;
+        a.scales = sc;
+        a.y = y;
+        a.ldy = N;
+        const CUtensorMap ta = tmap_bytes(W, K, N, Kp);
+        const CUtensorMap tb = tmap_bytes(planes, K, size_t(3) * Tp, Kp);
+        launch_limb_gemm(ta, tb, a, o.c.op_stream);
+        uint32_t wide_h = 0;
+        o.get(&wide_h, wide, 1);
+        o.get(out, y, size_t(T) * N);
+        if (wide_h)
+            for (uint32_t t = 0; t < T; ++t) {
+                const dimg_status s = dimg_op_dense(device, w, x + size_t(t) * K, out + size_t(t) * N);
+                if (s != DIMG_OK) return s;
+            }
     })
 }
 

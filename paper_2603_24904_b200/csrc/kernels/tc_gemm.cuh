@@ -1,0 +1,253 @@
+// Exact int8 x int64 dense products for many tokens on the 5th-generation
+// tensor cores (tcgen05.mma kind::i8, accumulators in TMEM).
+//
+// dense_forward (proj/src/kernels.cpp:18-30) for T tokens at once:
+//   y[t][n] = ((sum_j W[n][j] * x[t][j])_int64 * s[n]) >> 16
+// with int8 W and int64 activations. Activations with |x| < 2^23 are split
+// into three byte limbs x = l0 + 2^8 l1 + 2^16 l2 (l0, l1 unsigned, l2
+// signed), so each limb product is a plain int8 x int8 GEMM with int32
+// accumulation -- exact: K * 127 * 255 < 2^31 for K <= 66000 -- and
+// acc = D0 + 2^8 D1 + 2^16 D2 is recombined exactly in int64 in the epilogue.
+// (Larger activations are detected by the producers; the engine then takes
+// the exact CUDA-core path instead.)
+//
+// One CTA computes a 128-feature x 128-token tile: the weights are the MMA
+// A operand (M = features, K-major), the three limb planes of the tokens
+// are three B operands (N = tokens, K-major) sharing one A tile per stage,
+// and the three accumulators take 3 x 128 TMEM columns. TMA loads 128-byte
+// K slices of every operand with the 128B swizzle that the UMMA smem
+// descriptors describe; a 3-stage mbarrier ring feeds the MMA warp.
+// Warp roles: 0 = TMA producer, 1 = TMEM owner + MMA issuer, 2..5 = epilogue
+// (warp w reads TMEM lane quarter w % 4, i.e. features 32 (w % 4) .. +31,
+// one feature per thread -> coalesced stores across the warp).
+#pragma once
+
+#include <cuda.h>
+
+#include <cstdint>
+
+#include "q16.cuh"
+
+namespace dimg::dev {
+
+constexpr int TG_BM = 128;      // features per tile (MMA M)
+constexpr int TG_BN = 128;      // tokens per tile (MMA N)
+constexpr int TG_BK = 128;      // K bytes per stage = one 128-byte swizzle row
+constexpr int TG_L = 3;         // activation limbs
+constexpr int TG_STAGES = 3;
+constexpr int TG_A_BYTES = TG_BM * TG_BK;
+constexpr int TG_B_BYTES = TG_BN * TG_BK;
+constexpr int TG_STAGE_BYTES = TG_A_BYTES + TG_L * TG_B_BYTES;  // 64 KB
+constexpr int TG_THREADS = 192;
+constexpr int TG_SMEM = TG_STAGES * TG_STAGE_BYTES + 1024;      // + alignment slack
+
+enum { TG_STORE = 0, TG_RESID = 1, TG_SILU = 2 };
+
+struct TgArgs {
+    uint32_t n_out;      // output features (rows of W)
+    uint32_t n_tok;      // tokens
+    uint32_t n_kblk;     // K / 128, rounded up
+    uint32_t limb_rows;  // rows of one limb plane in the B tensor map
+    uint32_t epi;
+    const int64_t* scales;  // [n_out]
+    int64_t* y;             // STORE: y[t][n]; RESID: x[t][n] updated; SILU: h[t][n / 2]
+    uint32_t ldy;           // row stride of y (elements)
+    // SILU: also the three limb planes of h for the next GEMM, [3][limb_rows_out][ldp] bytes
+    uint8_t* planes;
+    uint32_t limb_rows_out, ldp;
+    const int64_t* lut;     // exp LUT (SILU)
+    uint32_t* wide;         // set to 1 if an output needs more than 3 limbs (SILU planes)
+};
+
+// ---- PTX wrappers --------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t tg_smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void tg_mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tg_smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void tg_mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tg_smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tg_mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(tg_smem_u32(b)), "r"(parity)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ void tg_tma_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            tg_smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(tg_smem_u32(bar))
+        : "memory");
+}
+
+// K-major operand in the 128B-swizzled canonical layout: 128-byte rows,
+// 8-row core groups 1024 bytes apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t tg_desc(uint32_t smem_addr) {
+    return uint64_t((smem_addr >> 4) & 0x3FFF) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+           (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+
+// Instruction descriptor, kind::i8: D s32, A = W (s8), B = limb (u8 or s8),
+// both K-major, M = 128, N = 128.
+__host__ __device__ constexpr uint32_t tg_idesc(bool b_signed) {
+    return (2u << 4) | (1u << 7) | ((b_signed ? 1u : 0u) << 10) | (uint32_t(TG_BN >> 3) << 17) |
+           (uint32_t(TG_BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void tg_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void tg_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     tg_smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tg_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tg_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tg_ld16(uint32_t taddr, int32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tg_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ---- the kernel ---------------------------------------------------------------------
+
+__global__ void __launch_bounds__(TG_THREADS, 1)
+    limb_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const TgArgs a) {
+    extern __shared__ uint8_t tg_smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tg_smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[TG_STAGES], empty[TG_STAGES], accum_full;
+    __shared__ uint32_t tmem_slot;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t n0 = blockIdx.x * TG_BM;  // features
+    const uint32_t t0 = blockIdx.y * TG_BN;  // tokens
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TG_STAGES; ++s) {
+            tg_mbar_init(&full[s], 1);
+            tg_mbar_init(&empty[s], 1);
+        }
+        tg_mbar_init(&accum_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {  // TMEM: 3 accumulators x 128 columns (allocation rounds to 512)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         tg_smem_u32(&tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tg_fence_before();
+    __syncthreads();
+    tg_fence_after();
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer
+            for (uint32_t kb = 0; kb < a.n_kblk; ++kb) {
+                const uint32_t s = kb % TG_STAGES;
+                if (kb >= TG_STAGES) tg_mbar_wait(&empty[s], ((kb / TG_STAGES) & 1) ^ 1);
+                uint8_t* st = smem + size_t(s) * TG_STAGE_BYTES;
+                tg_mbar_expect_tx(&full[s], TG_STAGE_BYTES);
+                tg_tma_2d(st, &tmA, int32_t(kb * TG_BK), int32_t(n0), &full[s]);
+#pragma unroll
+                for (int l = 0; l < TG_L; ++l)
+                    tg_tma_2d(st + TG_A_BYTES + l * TG_B_BYTES, &tmB, int32_t(kb * TG_BK),
+                              int32_t(l * a.limb_rows + t0), &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            for (uint32_t kb = 0; kb < a.n_kblk; ++kb) {
+                const uint32_t s = kb % TG_STAGES;
+                tg_mbar_wait(&full[s], (kb / TG_STAGES) & 1);
+                tg_fence_after();
+                const uint32_t sa = tg_smem_u32(smem + size_t(s) * TG_STAGE_BYTES);
+#pragma unroll
+                for (int l = 0; l < TG_L; ++l) {
+                    const uint32_t idesc = tg_idesc(l == TG_L - 1);
+                    const uint32_t sb = sa + TG_A_BYTES + l * TG_B_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < TG_BK / 32; ++kk)  // K = 32 bytes per MMA
+                        tg_mma(tmem + l * TG_BN, tg_desc(sa + 32 * kk), tg_desc(sb + 32 * kk), idesc,
+                               (kb | kk) != 0);
+                }
+                tg_commit(&empty[s]);  // frees the stage once these MMAs have read it
+            }
+            tg_commit(&accum_full);
+        }
+    } else {
+        // epilogue: thread = feature n, columns = tokens
+        const uint32_t q = warp & 3;
+        const uint32_t n = n0 + 32 * q + lane;
+        tg_mbar_wait(&accum_full, 0);
+        tg_fence_after();
+        const bool nv = n < a.n_out;
+        const int64_t sc = nv ? a.scales[n] : 0;
+        const uint32_t tbase = tmem + ((32 * q) << 16);
+        for (uint32_t c0 = 0; c0 < TG_BN; c0 += 16) {
+            int32_t d0[16], d1[16], d2[16];
+            tg_ld16(tbase + c0, d0);
+            tg_ld16(tbase + TG_BN + c0, d1);
+            tg_ld16(tbase + 2 * TG_BN + c0, d2);
+            tg_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t t = t0 + c0 + j;
+                const int64_t acc = int64_t(d0[j]) + (int64_t(d1[j]) << 8) + (int64_t(d2[j]) << 16);
+                const int64_t val = scale_row(acc, sc);
+                if (a.epi == TG_SILU) {
+                    // rows (2i, 2i+1) = (gate_i, up_i) sit on adjacent lanes
+                    const int64_t up = __shfl_down_sync(0xffffffffu, val, 1);
+                    if (nv && !(n & 1) && t < a.n_tok) {
+                        const int64_t hv = mul16(silu_q16(val, a.lut), up);
+                        const uint32_t i = n >> 1;
+                        a.y[size_t(t) * a.ldy + i] = hv;
+                        uint8_t* p = a.planes + size_t(t) * a.ldp + i;
+                        const size_t plane = size_t(a.limb_rows_out) * a.ldp;
+                        p[0] = uint8_t(hv);
+                        p[plane] = uint8_t(hv >> 8);
+                        p[2 * plane] = uint8_t(hv >> 16);
+                        if (hv < -(int64_t(1) << 23) || hv >= (int64_t(1) << 23)) *a.wide = 1;
+                    }
+                } else if (nv && t < a.n_tok) {
+                    int64_t* yp = a.y + size_t(t) * a.ldy + n;
+                    *yp = a.epi == TG_RESID ? add_clamp(*yp, val) : val;
+                }
+            }
+        }
+        tg_fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tg_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
+}  // namespace dimg::dev

@@ -243,6 +243,18 @@ def dense_forward(w, scales, x, device: int = 0) -> np.ndarray:
     return out
 
 
+def dense_tokens(w, scales, x, device: int = 0) -> np.ndarray:
+    """dense_forward for every row of x [T, cols] -> [T, rows]: the prefill
+    GEMM on the tensor cores (exact byte-limb int8 products)."""
+    qt, keep = _qt(w, scales)
+    x = np.ascontiguousarray(x, np.int64)
+    if x.ndim != 2 or x.shape[1] != qt.cols:
+        raise errors.InvalidArgument("dense_tokens: dimension mismatch")
+    out = np.empty((x.shape[0], qt.rows), np.int64)
+    check(lib.dimg_op_dense_tokens(device, C.byref(qt), ptr(x, i64p), x.shape[0], ptr(out, i64p)))
+    return out
+
+
 def rmsnorm(x, gamma, device: int = 0) -> np.ndarray:
     x = np.ascontiguousarray(x, np.int64)
     g = np.ascontiguousarray(gamma, np.int64)

@@ -235,3 +235,29 @@ def test_device_resident_stepping_matches_generate(P, golden_models):
     assert s.tokens(g["max_new"]) == g["tokens"]
     d, p = s.launches()
     assert d == 1 and p == 1  # one persistent launch per call
+
+
+# ---- tensor-core prefill GEMM (tcgen05 kind::i8 over byte limbs) ---------------
+
+@pytest.mark.parametrize("N,K,T", [(128, 128, 128), (256, 4096, 130), (100, 300, 7), (4096, 4096, 256),
+                                   (384, 11008, 64), (33, 17, 1)])
+def test_dense_tokens_matches_oracle(P, oracle, N, K, T):
+    rng = np.random.default_rng(N * 7 + K + T)
+    w = rng.integers(-127, 128, (N, K), dtype=np.int8)
+    s = rng.integers(1, 1 << 12, N, dtype=np.int64)
+    x = rng.integers(-(1 << 23), 1 << 23, (T, K), dtype=np.int64)
+    x[0, :5] = [-(1 << 23), (1 << 23) - 1, 0, -1, 255]
+    got = P.dense_tokens(w, s, x)
+    for t in range(T):
+        assert np.array_equal(got[t], oracle.dense(w, s, x[t])), t
+
+
+def test_dense_tokens_wide_rows_fall_back_exactly(P, oracle):
+    rng = np.random.default_rng(5)
+    w = rng.integers(-127, 128, (64, 96), dtype=np.int8)
+    s = rng.integers(1, 1 << 12, 64, dtype=np.int64)
+    x = rng.integers(-(1 << 20), 1 << 20, (5, 96), dtype=np.int64)
+    x[3, 7] = 1 << 40
+    got = P.dense_tokens(w, s, x)
+    for t in range(5):
+        assert np.array_equal(got[t], oracle.dense(w, s, x[t]))
