@@ -191,7 +191,8 @@ dimg_status dimg_session_launches(const dimg_session* s, uint32_t* per_decode,
 /* Counters: [0] GEMV CTAs that needed the 8-limb (full int64) path,
  * [1] device-side error bits (1: inv_sqrt of ms+1 <= 0, 4: barrier timeout),
  * [2] attention parts that read the int64 KV cache (a head holding values
- * beyond int32). */
+ * beyond int32), [3] prompts prefilled on the tensor cores (low 32 bits) and
+ * tensor-core prefills redone on the exact decode path (high 32 bits). */
 dimg_status dimg_session_stats(dimg_session* s, uint64_t out[4]);
 
 /* ---- operator-level exports (host buffers in/out) for unit parity with

@@ -31,6 +31,7 @@
 #include "kernels/gemv.cuh"
 #include "kernels/persistent.cuh"
 #include "kernels/tc_gemm.cuh"
+#include "kernels/prefill.cuh"
 
 using namespace dimg;
 using namespace dimg::dev;
@@ -92,6 +93,19 @@ DevCtx& dev_ctx(int device) {
     set_gemv_attrs<EPI_STORE, MODE_PLAIN>();
     set_gemv_attrs<EPI_STORE, MODE_NORM>();
     CK(cudaFuncSetAttribute(limb_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TG_SMEM));
+    {
+        auto set = [&](auto kern) {
+            cudaFuncAttributes fa;
+            CK(cudaFuncGetAttributes(&fa, kern));
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(prop.sharedMemPerBlockOptin - fa.sharedSizeBytes)));
+        };
+        set(pf_attn_kernel<1>);
+        set(pf_attn_kernel<2>);
+        set(pf_attn_kernel<4>);
+        set(pf_attn_kernel<8>);
+        set(pf_attn_kernel<16>);
+    }
     set_gemv_attrs<EPI_STORE, MODE_EMBED>();
     set_gemv_attrs<EPI_RESID, MODE_PLAIN>();
     set_gemv_attrs<EPI_SILU, MODE_NORM>();
@@ -192,9 +206,11 @@ void launch_limb_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs
 // matrix (3D rows); gate/up are interleaved (gate_i row 2i, up_i row 2i+1) so
 // a row group holds whole (gate, up) pairs for the silu*up epilogue.
 struct DevMat {
-    int8_t* w = nullptr;       // blocked
+    int8_t* w = nullptr;       // blocked (decode kernel)
     int64_t* s = nullptr;      // scales [rows]
     uint32_t rows = 0, K = 0, Kp = 0, n_groups = 0, n_segs = 0;
+    int8_t* plain = nullptr;   // row-major [rows][Kp] (prefill GEMM A operand)
+    CUtensorMap tmap;          // its TMA map (128 x 128-byte boxes, 128B swizzle)
 };
 
 struct dimg_model {
@@ -295,6 +311,9 @@ DevMat upload_mat(dimg_model& m, uint32_t rows, uint32_t K, const std::vector<Ro
     CK(cudaMemset(staging, 0, bytes));
     for (const auto& p : parts) put_rows(staging, d.Kp, p.row0, p.rstride, p.src, p.rows, K);
     d.s = upload(m.mem, scales.data(), scales.size());
+    d.plain = m.mem.alloc<int8_t>(size_t(d.n_groups) * PK_ROWS * d.Kp);
+    CK(cudaMemcpy(d.plain, staging, size_t(d.n_groups) * PK_ROWS * d.Kp, cudaMemcpyDeviceToDevice));
+    d.tmap = tmap_bytes(d.plain, K, rows, d.Kp);
     d.w = m.mem.alloc<int8_t>(size_t(d.n_groups) * pk_group_bytes(d.Kp));
     blockify_kernel<<<1024, 256>>>(reinterpret_cast<const int4*>(staging), d.s, rows,
                                    reinterpret_cast<int4*>(d.w), d.Kp, d.n_groups, d.n_segs);
@@ -308,8 +327,21 @@ DevMat upload_mat(dimg_model& m, uint32_t rows, uint32_t K, const std::vector<Ro
 // ---------------------------------------------------------------------------
 // Session: one sequence (KV cache, control block, token ring)
 // ---------------------------------------------------------------------------
+// Prefill workspace: all prompt tokens through a layer at once.
+struct PrefillWs {
+    uint32_t cap = 0, cap_pad = 0;   // tokens
+    int64_t* x = nullptr;            // [cap][D] residual stream
+    int64_t* qkv = nullptr;          // [cap][3D] projections (q rotated in place)
+    uint8_t* pa = nullptr;           // [3][cap_pad][Kd] limb planes of D-wide inputs
+    uint8_t* ph = nullptr;           // [3][cap_pad][Kf] limb planes of the FFN hidden vector
+    uint32_t* wide = nullptr;        // some value needed the exact path
+    CUtensorMap tm_pa, tm_ph;
+};
+
 struct dimg_session {
     dimg_model* m;
+    PrefillWs pf;
+    uint64_t tc_prefills = 0, tc_fallbacks = 0;
     cudaStream_t stream = nullptr;
     DevBuf mem;
     int64_t *x, *qkv, *att, *h, *kc, *vc, *scores, *logits;
@@ -544,7 +576,125 @@ void begin(dimg_session& s, const uint32_t* prompt, uint32_t p, uint32_t n, bool
 
 uint32_t n_layer_stages(const dimg_session& s) { return 5 * s.m->L; }
 
+// Largest prompt the tensor-core prefill takes (the attention kernel keeps a
+// query tile's score rows in shared memory); longer prompts and shapes it
+// does not cover go through the decode kernel, one token per step.
+constexpr uint32_t kTcPrefillMaxTokens = 2560;
+
+uint32_t prefill_mode() {  // DIMG_PREFILL: 0 auto, 1 always tensor cores, 2 always decode steps
+    const char* v = std::getenv("DIMG_PREFILL");
+    return v ? uint32_t(std::strtoul(v, nullptr, 0)) : 0u;
+}
+
+bool tc_prefill_ok(const dimg_session& s, uint32_t n) {
+    const dimg_model& m = *s.m;
+    const uint32_t mode = prefill_mode();
+    if (mode == 2 || n == 0) return false;
+    if (m.dh % 4 || m.dh > 512 || m.dh / 2 > 1024 || n > kTcPrefillMaxTokens) return false;
+    if (pf_attn_smem(m.dh, n) > size_t(m.ctx->smem_optin)) return false;
+    return mode == 1 || n >= 32;
+}
+
+void ensure_prefill_ws(dimg_session& s, uint32_t n) {
+    PrefillWs& w = s.pf;
+    if (w.cap >= n) return;
+    const dimg_model& m = *s.m;
+    w.cap = std::max(n, 128u);
+    w.cap_pad = (w.cap + TG_BN - 1) / TG_BN * TG_BN;
+    w.x = s.mem.alloc<int64_t>(size_t(w.cap) * m.D);
+    w.qkv = s.mem.alloc<int64_t>(size_t(w.cap) * 3 * m.D);
+    w.pa = s.mem.alloc<uint8_t>(size_t(3) * w.cap_pad * m.Kd);
+    w.ph = s.mem.alloc<uint8_t>(size_t(3) * w.cap_pad * m.Kf);
+    CK(cudaMemset(w.pa, 0, size_t(3) * w.cap_pad * m.Kd));
+    CK(cudaMemset(w.ph, 0, size_t(3) * w.cap_pad * m.Kf));
+    if (!w.wide) w.wide = s.mem.alloc<uint32_t>(1);
+    w.tm_pa = tmap_bytes(w.pa, m.D, size_t(3) * w.cap_pad, m.Kd);
+    w.tm_ph = tmap_bytes(w.ph, m.F, size_t(3) * w.cap_pad, m.Kf);
+}
+
+template <class... A>
+void launch_pf_attn(uint32_t dh, dim3 grid, size_t smem, cudaStream_t st, A... args) {
+    const uint32_t dpl = (dh + 31) / 32;
+    if (dpl <= 1) pf_attn_kernel<1><<<grid, PA_THREADS, smem, st>>>(args...);
+    else if (dpl <= 2) pf_attn_kernel<2><<<grid, PA_THREADS, smem, st>>>(args...);
+    else if (dpl <= 4) pf_attn_kernel<4><<<grid, PA_THREADS, smem, st>>>(args...);
+    else if (dpl <= 8) pf_attn_kernel<8><<<grid, PA_THREADS, smem, st>>>(args...);
+    else pf_attn_kernel<16><<<grid, PA_THREADS, smem, st>>>(args...);
+}
+
+// Positions 0..n-1 of the prompt through every layer on the tensor cores;
+// returns false (nothing usable written) if some value needed the exact path.
+bool run_prefill_tc(dimg_session& s, uint32_t n) {
+    const dimg_model& m = *s.m;
+    ensure_prefill_ws(s, n);
+    PrefillWs& w = s.pf;
+    cudaStream_t st = s.stream;
+    const uint32_t D = m.D, dh = m.dh, H = m.H;
+    const size_t kv_layer = size_t(H) * m.cfg.max_ctx * dh;
+    CK(cudaMemsetAsync(w.wide, 0, 4, st));
+    CK(cudaMemsetAsync(s.kvwide, 0, size_t(m.L) * H * 4, st));
+    pf_embed_kernel<<<1024, 256, 0, st>>>(s.tokens, n, m.embd, m.embd_s, D, w.x);
+    auto gemm = [&](const DevMat& W, const CUtensorMap& tb, uint32_t epi, int64_t* y, uint32_t ldy) {
+        TgArgs a{};
+        a.n_out = W.rows;
+        a.n_tok = n;
+        a.n_kblk = (W.K + TG_BK - 1) / TG_BK;
+        a.limb_rows = w.cap_pad;
+        a.epi = epi;
+        a.scales = W.s;
+        a.y = y;
+        a.ldy = ldy;
+        a.planes = w.ph;
+        a.limb_rows_out = w.cap_pad;
+        a.ldp = m.Kf;
+        a.lut = m.ctx->exp_lut;
+        a.wide = w.wide;
+        launch_limb_gemm(W.tmap, tb, a, st);
+    };
+    const size_t asmem = pf_attn_smem(dh, n);
+    for (uint32_t l = 0; l < m.L; ++l) {
+        const auto& lw = m.layers[l];
+        pf_norm_limbs_kernel<<<n, 256, 0, st>>>(w.x, D, lw.attn_norm, lw.attn_unit, m.ctx->seeds, w.pa, w.cap_pad,
+                                                 m.Kd, w.wide);
+        gemm(lw.qkv, w.tm_pa, TG_STORE, w.qkv, 3 * D);
+        pf_rope_kv_kernel<<<dim3(n, H), dh / 2, 0, st>>>(w.qkv, D, dh, m.rope_cos, m.rope_sin, s.kc + l * kv_layer,
+                                                         s.vc + l * kv_layer, s.kc32 + l * kv_layer,
+                                                         s.vc32 + l * kv_layer, size_t(m.cfg.max_ctx) * dh, w.wide);
+        if (l + 1 == m.L) break;  // the last layer's output feeds only the lm_head
+        launch_pf_attn(dh, dim3(H, (n + PA_Q - 1) / PA_Q), asmem, st, w.qkv, n, D, dh, s.kc32 + l * kv_layer,
+                       s.vc32 + l * kv_layer, size_t(m.cfg.max_ctx) * dh, m.inv_scale, m.ctx->exp_lut, w.pa,
+                       w.cap_pad, m.Kd, w.wide);
+        gemm(lw.wo, w.tm_pa, TG_RESID, w.x, D);
+        pf_norm_limbs_kernel<<<n, 256, 0, st>>>(w.x, D, lw.ffn_norm, lw.ffn_unit, m.ctx->seeds, w.pa, w.cap_pad,
+                                                 m.Kd, w.wide);
+        gemm(lw.gu, w.tm_pa, TG_SILU, nullptr, 0);
+        gemm(lw.down, w.tm_ph, TG_RESID, w.x, D);
+    }
+    CK(cudaGetLastError());
+    uint32_t wide = 0;
+    CK(cudaMemcpyAsync(&wide, w.wide, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return wide == 0;
+}
+
+// The prompt's first n_prompt - 1 positions on the tensor cores when the
+// shapes allow; true if done (cache length and the kernel's position set).
+bool try_prefill_tc(dimg_session& s) {
+    const uint32_t n = s.n_prompt - 1;
+    if (!tc_prefill_ok(s, n)) return false;
+    if (!run_prefill_tc(s, n)) {
+        ++s.tc_fallbacks;
+        return false;
+    }
+    ++s.tc_prefills;
+    CK(cudaMemcpyAsync(&s.ctl->pos, &n, 4, cudaMemcpyHostToDevice, s.stream));
+    CK(cudaStreamSynchronize(s.stream));
+    s.len = n;
+    return true;
+}
+
 void run_prefill(dimg_session& s) {
+    if (try_prefill_tc(s)) return;
     uint32_t n = s.n_prompt - 1;
     launch_pk(s, s.stages, n_layer_stages(s), n, n);
     s.len = n;
@@ -785,7 +935,8 @@ dimg_status dimg_generate_greedy(dimg_session* s, const uint32_t* prompt, uint32
         begin(*s, prompt, n_prompt, max_new, logits_out != nullptr);
         if (max_new > 0) {
             const uint32_t np = n_prompt - 1;
-            launch_pk(*s, s->stages, n_layer_stages(*s), np + max_new, np);
+            if (try_prefill_tc(*s)) launch_pk(*s, s->stages, n_layer_stages(*s), max_new, 0);
+            else launch_pk(*s, s->stages, n_layer_stages(*s), np + max_new, np);
             s->len = np + max_new;
             CK(cudaMemcpyAsync(tokens_out, s->tokens + n_prompt, size_t(max_new) * 4,
                                cudaMemcpyDeviceToHost, s->stream));
@@ -934,7 +1085,7 @@ dimg_status dimg_session_stats(dimg_session* s, uint64_t out[4]) {
         out[0] = c.stats[0];
         out[1] = c.err;
         out[2] = c.stats[1];
-        out[3] = c.stats[3];
+        out[3] = (s->tc_prefills & 0xFFFFFFFFull) | (s->tc_fallbacks << 32);
     })
 }
 

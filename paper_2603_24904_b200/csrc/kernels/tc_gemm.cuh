@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
                     if (nv && !(n & 1) && t < a.n_tok) {
                         const int64_t hv = mul16(silu_q16(val, a.lut), up);
                         const uint32_t i = n >> 1;
-                        a.y[size_t(t) * a.ldy + i] = hv;
+                        if (a.y) a.y[size_t(t) * a.ldy + i] = hv;
                         uint8_t* p = a.planes + size_t(t) * a.ldp + i;
                         const size_t plane = size_t(a.limb_rows_out) * a.ldp;
                         p[0] = uint8_t(hv);

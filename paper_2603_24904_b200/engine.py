@@ -189,7 +189,8 @@ class InferenceSession:
     def stats(self):
         out = np.zeros(4, np.uint64)
         check(lib.dimg_session_stats(self._h, ptr(out, u64p)))
-        return {"wide_limb_ctas": int(out[0]), "err": int(out[1]), "wide_kv_ctas": int(out[2])}
+        return {"wide_limb_ctas": int(out[0]), "err": int(out[1]), "wide_kv_ctas": int(out[2]),
+                "tc_prefills": int(out[3]) & 0xFFFFFFFF, "tc_fallbacks": int(out[3]) >> 32}
 
     def __del__(self):
         try:

@@ -261,3 +261,37 @@ def test_dense_tokens_wide_rows_fall_back_exactly(P, oracle):
     got = P.dense_tokens(w, s, x)
     for t in range(5):
         assert np.array_equal(got[t], oracle.dense(w, s, x[t]))
+
+
+# ---- tensor-core prefill (whole prompt per layer) ------------------------------
+
+@pytest.mark.parametrize("cfg6,plen,seed", [((2, 64, 2, 64, 64, 256), 200, 3), ((2, 256, 2, 512, 300, 400), 300, 4),
+                                            ((3, 96, 3, 160, 77, 200), 40, 5)])
+def test_tensor_core_prefill_matches_oracle(P, oracle, monkeypatch, cfg6, plen, seed):
+    from oracle.pyoracle import Config
+    monkeypatch.setenv("DIMG_PREFILL", "1")
+    m = P.gen_toy_model(seed, P.ModelConfig(*cfg6))
+    om = oracle.gen_toy(seed, Config(*cfg6))
+    prompt = P.prompt_from_seed(seed + 100, cfg6[4], plen)
+    toks, h, lg = oracle.generate_greedy(om, prompt, 6, keep_logits=True)
+    s = P.InferenceSession(m, keep_logits_cap=6)
+    res = s.generate_greedy(prompt, 6, keep_logits=True)
+    assert s.stats()["tc_prefills"] == 1 and s.stats()["tc_fallbacks"] == 0
+    assert res.token_ids == [int(t) for t in toks]
+    assert res.output_hash.hex() == h
+    assert np.array_equal(np.stack(res.logits), lg)
+
+
+def test_tensor_core_prefill_falls_back_exactly(P, oracle, golden_models, monkeypatch):
+    """A model whose activations exceed 3 byte limbs: the tensor-core prefill
+    detects it and the exact decode path redoes the prompt."""
+    monkeypatch.setenv("DIMG_PREFILL", "1")
+    g = golden_models["wild_b"]
+    m = _model_for(P, g)
+    s = P.InferenceSession(m)
+    prompt = (g["prompt"] * 40)[:60]
+    res = s.generate_greedy(prompt, 5)
+    assert s.stats()["tc_fallbacks"] == 1
+    monkeypatch.setenv("DIMG_PREFILL", "2")
+    ref = P.InferenceSession(m).generate_greedy(prompt, 5)
+    assert res.token_ids == ref.token_ids and res.output_hash == ref.output_hash
