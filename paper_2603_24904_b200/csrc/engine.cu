@@ -155,13 +155,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }
 
 // 2-D byte matrix [outer][inner] with row stride `stride` bytes, read in
-// 128 x 128 boxes with the 128-byte swizzle the UMMA descriptors expect;
+// 128-byte x box_rows boxes with the 128-byte swizzle the UMMA descriptors expect;
 // out-of-range elements read as zero.
-CUtensorMap tmap_bytes(const void* base, uint64_t inner, uint64_t outer, uint64_t stride) {
+CUtensorMap tmap_bytes(const void* base, uint64_t inner, uint64_t outer, uint64_t stride, uint32_t box_rows) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {inner, outer};
     const cuuint64_t strides[1] = {stride};
-    const cuuint32_t box[2] = {TG_BK, TG_BM};
+    const cuuint32_t box[2] = {TG_BK, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = tmap_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box,
                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -189,8 +189,11 @@ __global__ void limbs_kernel(const int64_t* __restrict__ x, uint32_t T, uint32_t
 }
 
 void launch_limb_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs& a, cudaStream_t st) {
-    dim3 grid((a.n_out + TG_BM - 1) / TG_BM, (a.n_tok + TG_BN - 1) / TG_BN);
-    limb_gemm_kernel<<<grid, TG_THREADS, TG_SMEM, st>>>(ta, tb, a);
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const uint32_t tiles = ((a.n_out + TG_BM - 1) / TG_BM) * ((a.n_tok + TG_BN - 1) / TG_BN);
+    limb_gemm_kernel<<<std::min<uint32_t>(tiles, uint32_t(sms)), TG_THREADS, TG_SMEM, st>>>(ta, tb, a);
     CK(cudaGetLastError());
 }
 
@@ -313,7 +316,7 @@ DevMat upload_mat(dimg_model& m, uint32_t rows, uint32_t K, const std::vector<Ro
     d.s = upload(m.mem, scales.data(), scales.size());
     d.plain = m.mem.alloc<int8_t>(size_t(d.n_groups) * PK_ROWS * d.Kp);
     CK(cudaMemcpy(d.plain, staging, size_t(d.n_groups) * PK_ROWS * d.Kp, cudaMemcpyDeviceToDevice));
-    d.tmap = tmap_bytes(d.plain, K, rows, d.Kp);
+    d.tmap = tmap_bytes(d.plain, K, rows, d.Kp, TG_BM);
     d.w = m.mem.alloc<int8_t>(size_t(d.n_groups) * pk_group_bytes(d.Kp));
     blockify_kernel<<<1024, 256>>>(reinterpret_cast<const int4*>(staging), d.s, rows,
                                    reinterpret_cast<int4*>(d.w), d.Kp, d.n_groups, d.n_segs);
@@ -608,8 +611,8 @@ void ensure_prefill_ws(dimg_session& s, uint32_t n) {
     CK(cudaMemset(w.pa, 0, size_t(3) * w.cap_pad * m.Kd));
     CK(cudaMemset(w.ph, 0, size_t(3) * w.cap_pad * m.Kf));
     if (!w.wide) w.wide = s.mem.alloc<uint32_t>(1);
-    w.tm_pa = tmap_bytes(w.pa, m.D, size_t(3) * w.cap_pad, m.Kd);
-    w.tm_ph = tmap_bytes(w.ph, m.F, size_t(3) * w.cap_pad, m.Kf);
+    w.tm_pa = tmap_bytes(w.pa, m.D, size_t(3) * w.cap_pad, m.Kd, TG_BN);
+    w.tm_ph = tmap_bytes(w.ph, m.F, size_t(3) * w.cap_pad, m.Kf, TG_BN);
 }
 
 template <class... A>
@@ -1200,8 +1203,8 @@ dimg_status dimg_op_dense_tokens(int device, const dimg_qtensor* w, const int64_
         a.scales = sc;
         a.y = y;
         a.ldy = N;
-        const CUtensorMap ta = tmap_bytes(W, K, N, Kp);
-        const CUtensorMap tb = tmap_bytes(planes, K, size_t(3) * Tp, Kp);
+        const CUtensorMap ta = tmap_bytes(W, K, N, Kp, TG_BM);
+        const CUtensorMap tb = tmap_bytes(planes, K, size_t(3) * Tp, Kp, TG_BN);
         launch_limb_gemm(ta, tb, a, o.c.op_stream);
         uint32_t wide_h = 0;
         o.get(&wide_h, wide, 1);

@@ -11,12 +11,14 @@
 // (Larger activations are detected by the producers; the engine then takes
 // the exact CUDA-core path instead.)
 //
-// One CTA computes a 128-feature x 128-token tile: the weights are the MMA
-// A operand (M = features, K-major), the three limb planes of the tokens
-// are three B operands (N = tokens, K-major) sharing one A tile per stage,
-// and the three accumulators take 3 x 128 TMEM columns. TMA loads 128-byte
+// Tiles are 128 features x 64 tokens: the weights are the MMA A operand
+// (M = features, K-major), the three limb planes of the tokens are three B
+// operands (N = tokens, K-major) sharing one A tile per stage, and a tile's
+// three accumulators take 3 x 64 TMEM columns. The kernel is persistent (one
+// CTA per SM walks tiles round-robin) with two accumulator sets in TMEM, so
+// the epilogue of one tile overlaps the MMAs of the next. TMA loads 128-byte
 // K slices of every operand with the 128B swizzle that the UMMA smem
-// descriptors describe; a 3-stage mbarrier ring feeds the MMA warp.
+// descriptors describe; a 5-stage mbarrier ring feeds the MMA warp.
 // Warp roles: 0 = TMA producer, 1 = TMEM owner + MMA issuer, 2..5 = epilogue
 // (warp w reads TMEM lane quarter w % 4, i.e. features 32 (w % 4) .. +31,
 // one feature per thread -> coalesced stores across the warp).
@@ -31,13 +33,14 @@
 namespace dimg::dev {
 
 constexpr int TG_BM = 128;      // features per tile (MMA M)
-constexpr int TG_BN = 128;      // tokens per tile (MMA N)
+constexpr int TG_BN = 64;       // tokens per tile (MMA N)
 constexpr int TG_BK = 128;      // K bytes per stage = one 128-byte swizzle row
 constexpr int TG_L = 3;         // activation limbs
-constexpr int TG_STAGES = 3;
+constexpr int TG_STAGES = 5;
+constexpr int TG_ACC = TG_L * TG_BN;  // TMEM columns of one tile's accumulators
 constexpr int TG_A_BYTES = TG_BM * TG_BK;
 constexpr int TG_B_BYTES = TG_BN * TG_BK;
-constexpr int TG_STAGE_BYTES = TG_A_BYTES + TG_L * TG_B_BYTES;  // 64 KB
+constexpr int TG_STAGE_BYTES = TG_A_BYTES + TG_L * TG_B_BYTES;  // 40 KB
 constexpr int TG_THREADS = 192;
 constexpr int TG_SMEM = TG_STAGES * TG_STAGE_BYTES + 1024;      // + alignment slack
 
@@ -136,27 +139,35 @@ __device__ __forceinline__ void tg_ld_wait() { asm volatile("tcgen05.wait::ld.sy
 
 // ---- the kernel ---------------------------------------------------------------------
 
+__device__ __forceinline__ void tg_tile(uint32_t tile, uint32_t n_mt, uint32_t& n0, uint32_t& t0) {
+    n0 = (tile % n_mt) * TG_BM;  // feature tiles fastest: consecutive CTAs share the token tile
+    t0 = (tile / n_mt) * TG_BN;
+}
+
 __global__ void __launch_bounds__(TG_THREADS, 1)
     limb_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const TgArgs a) {
     extern __shared__ uint8_t tg_smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tg_smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) uint64_t full[TG_STAGES], empty[TG_STAGES], accum_full;
+    __shared__ __align__(8) uint64_t full[TG_STAGES], empty[TG_STAGES], acc_full[2], acc_empty[2];
     __shared__ uint32_t tmem_slot;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t n0 = blockIdx.x * TG_BM;  // features
-    const uint32_t t0 = blockIdx.y * TG_BN;  // tokens
+    const uint32_t n_mt = (a.n_out + TG_BM - 1) / TG_BM, n_tt = (a.n_tok + TG_BN - 1) / TG_BN;
+    const uint32_t n_tiles = n_mt * n_tt;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < TG_STAGES; ++s) {
             tg_mbar_init(&full[s], 1);
             tg_mbar_init(&empty[s], 1);
         }
-        tg_mbar_init(&accum_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            tg_mbar_init(&acc_full[b], 1);
+            tg_mbar_init(&acc_empty[b], 4);  // the four epilogue warps
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {  // TMEM: 3 accumulators x 128 columns (allocation rounds to 512)
+    if (warp == 1) {  // TMEM: two accumulator sets of 3 x 64 columns (allocation rounds to 512)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                          tg_smem_u32(&tmem_slot))
                      : "memory");
@@ -168,81 +179,104 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     const uint32_t tmem = tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // TMA producer
-            for (uint32_t kb = 0; kb < a.n_kblk; ++kb) {
-                const uint32_t s = kb % TG_STAGES;
-                if (kb >= TG_STAGES) tg_mbar_wait(&empty[s], ((kb / TG_STAGES) & 1) ^ 1);
-                uint8_t* st = smem + size_t(s) * TG_STAGE_BYTES;
-                tg_mbar_expect_tx(&full[s], TG_STAGE_BYTES);
-                tg_tma_2d(st, &tmA, int32_t(kb * TG_BK), int32_t(n0), &full[s]);
+        if (lane == 0) {  // TMA producer: the K slices of every tile of this CTA, in order
+            uint32_t it = 0;
+            for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                uint32_t n0, t0;
+                tg_tile(tile, n_mt, n0, t0);
+                for (uint32_t kb = 0; kb < a.n_kblk; ++kb, ++it) {
+                    const uint32_t s = it % TG_STAGES;
+                    if (it >= TG_STAGES) tg_mbar_wait(&empty[s], ((it / TG_STAGES) & 1) ^ 1);
+                    uint8_t* st = smem + size_t(s) * TG_STAGE_BYTES;
+                    tg_mbar_expect_tx(&full[s], TG_STAGE_BYTES);
+                    tg_tma_2d(st, &tmA, int32_t(kb * TG_BK), int32_t(n0), &full[s]);
 #pragma unroll
-                for (int l = 0; l < TG_L; ++l)
-                    tg_tma_2d(st + TG_A_BYTES + l * TG_B_BYTES, &tmB, int32_t(kb * TG_BK),
-                              int32_t(l * a.limb_rows + t0), &full[s]);
+                    for (int l = 0; l < TG_L; ++l)
+                        tg_tma_2d(st + TG_A_BYTES + l * TG_B_BYTES, &tmB, int32_t(kb * TG_BK),
+                                  int32_t(l * a.limb_rows + t0), &full[s]);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // MMA issuer
-            for (uint32_t kb = 0; kb < a.n_kblk; ++kb) {
-                const uint32_t s = kb % TG_STAGES;
-                tg_mbar_wait(&full[s], (kb / TG_STAGES) & 1);
+            uint32_t it = 0, j = 0;
+            for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
+                const uint32_t b = j & 1;
+                if (j >= 2) tg_mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained set b
                 tg_fence_after();
-                const uint32_t sa = tg_smem_u32(smem + size_t(s) * TG_STAGE_BYTES);
+                const uint32_t dacc = tmem + b * TG_ACC;
+                for (uint32_t kb = 0; kb < a.n_kblk; ++kb, ++it) {
+                    const uint32_t s = it % TG_STAGES;
+                    tg_mbar_wait(&full[s], (it / TG_STAGES) & 1);
+                    tg_fence_after();
+                    const uint32_t sa = tg_smem_u32(smem + size_t(s) * TG_STAGE_BYTES);
 #pragma unroll
-                for (int l = 0; l < TG_L; ++l) {
-                    const uint32_t idesc = tg_idesc(l == TG_L - 1);
-                    const uint32_t sb = sa + TG_A_BYTES + l * TG_B_BYTES;
+                    for (int l = 0; l < TG_L; ++l) {
+                        const uint32_t idesc = tg_idesc(l == TG_L - 1);
+                        const uint32_t sb = sa + TG_A_BYTES + l * TG_B_BYTES;
 #pragma unroll
-                    for (int kk = 0; kk < TG_BK / 32; ++kk)  // K = 32 bytes per MMA
-                        tg_mma(tmem + l * TG_BN, tg_desc(sa + 32 * kk), tg_desc(sb + 32 * kk), idesc,
-                               (kb | kk) != 0);
+                        for (int kk = 0; kk < TG_BK / 32; ++kk)  // K = 32 bytes per MMA
+                            tg_mma(dacc + l * TG_BN, tg_desc(sa + 32 * kk), tg_desc(sb + 32 * kk), idesc,
+                                   (kb | kk) != 0);
+                    }
+                    tg_commit(&empty[s]);  // frees the stage once these MMAs have read it
                 }
-                tg_commit(&empty[s]);  // frees the stage once these MMAs have read it
+                tg_commit(&acc_full[b]);
             }
-            tg_commit(&accum_full);
         }
     } else {
         // epilogue: thread = feature n, columns = tokens
         const uint32_t q = warp & 3;
-        const uint32_t n = n0 + 32 * q + lane;
-        tg_mbar_wait(&accum_full, 0);
-        tg_fence_after();
-        const bool nv = n < a.n_out;
-        const int64_t sc = nv ? a.scales[n] : 0;
-        const uint32_t tbase = tmem + ((32 * q) << 16);
-        for (uint32_t c0 = 0; c0 < TG_BN; c0 += 16) {
-            int32_t d0[16], d1[16], d2[16];
-            tg_ld16(tbase + c0, d0);
-            tg_ld16(tbase + TG_BN + c0, d1);
-            tg_ld16(tbase + 2 * TG_BN + c0, d2);
-            tg_ld_wait();
+        uint32_t j = 0;
+        for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
+            uint32_t n0, t0;
+            tg_tile(tile, n_mt, n0, t0);
+            const uint32_t b = j & 1;
+            const uint32_t n = n0 + 32 * q + lane;
+            const bool nv = n < a.n_out;
+            const int64_t sc = nv ? a.scales[n] : 0;
+            tg_mbar_wait(&acc_full[b], (j >> 1) & 1);
+            tg_fence_after();
+            const uint32_t tbase = tmem + ((32 * q) << 16) + b * TG_ACC;
+            for (uint32_t c0 = 0; c0 < TG_BN; c0 += 16) {
+                int32_t d0[16], d1[16], d2[16];
+                tg_ld16(tbase + c0, d0);
+                tg_ld16(tbase + TG_BN + c0, d1);
+                tg_ld16(tbase + 2 * TG_BN + c0, d2);
+                tg_ld_wait();
+                if (c0 + 16 >= TG_BN) {  // every column of set b is in registers: hand it back
+                    tg_fence_before();
+                    __syncwarp();
+                    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tg_smem_u32(&acc_empty[b])) : "memory");
+                }
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const uint32_t t = t0 + c0 + j;
-                const int64_t acc = int64_t(d0[j]) + (int64_t(d1[j]) << 8) + (int64_t(d2[j]) << 16);
-                const int64_t val = scale_row(acc, sc);
-                if (a.epi == TG_SILU) {
-                    // rows (2i, 2i+1) = (gate_i, up_i) sit on adjacent lanes
-                    const int64_t up = __shfl_down_sync(0xffffffffu, val, 1);
-                    if (nv && !(n & 1) && t < a.n_tok) {
-                        const int64_t hv = mul16(silu_q16(val, a.lut), up);
-                        const uint32_t i = n >> 1;
-                        if (a.y) a.y[size_t(t) * a.ldy + i] = hv;
-                        uint8_t* p = a.planes + size_t(t) * a.ldp + i;
-                        const size_t plane = size_t(a.limb_rows_out) * a.ldp;
-                        p[0] = uint8_t(hv);
-                        p[plane] = uint8_t(hv >> 8);
-                        p[2 * plane] = uint8_t(hv >> 16);
-                        if (hv < -(int64_t(1) << 23) || hv >= (int64_t(1) << 23)) *a.wide = 1;
+                for (int jj = 0; jj < 16; ++jj) {
+                    const uint32_t t = t0 + c0 + jj;
+                    const int64_t acc = int64_t(d0[jj]) + (int64_t(d1[jj]) << 8) + (int64_t(d2[jj]) << 16);
+                    const int64_t val = scale_row(acc, sc);
+                    if (a.epi == TG_SILU) {
+                        // rows (2i, 2i+1) = (gate_i, up_i) sit on adjacent lanes
+                        const int64_t up = __shfl_down_sync(0xffffffffu, val, 1);
+                        if (nv && !(n & 1) && t < a.n_tok) {
+                            const int64_t hv = mul16(silu_q16(val, a.lut), up);
+                            const uint32_t i = n >> 1;
+                            if (a.y) a.y[size_t(t) * a.ldy + i] = hv;
+                            uint8_t* p = a.planes + size_t(t) * a.ldp + i;
+                            const size_t plane = size_t(a.limb_rows_out) * a.ldp;
+                            p[0] = uint8_t(hv);
+                            p[plane] = uint8_t(hv >> 8);
+                            p[2 * plane] = uint8_t(hv >> 16);
+                            if (hv < -(int64_t(1) << 23) || hv >= (int64_t(1) << 23)) *a.wide = 1;
+                        }
+                    } else if (nv && t < a.n_tok) {
+                        int64_t* yp = a.y + size_t(t) * a.ldy + n;
+                        *yp = a.epi == TG_RESID ? add_clamp(*yp, val) : val;
                     }
-                } else if (nv && t < a.n_tok) {
-                    int64_t* yp = a.y + size_t(t) * a.ldy + n;
-                    *yp = a.epi == TG_RESID ? add_clamp(*yp, val) : val;
                 }
             }
         }
-        tg_fence_before();
     }
+    tg_fence_before();
     __syncthreads();
     if (warp == 1) {
         tg_fence_after();
