@@ -205,6 +205,48 @@ def cpu_baseline(model_file, cfg_t):
                 "sample": f"unavailable: {e}"}
 
 
+def prefill_c3(P, mf, cfg, dev):
+    """C3: prefill of a 2048-token synthetic prompt (prompt seed 9) on the
+    tensor cores, timed with CUDA events (2 warm + 3 timed); the positions
+    0..2046 go through every layer, the last prompt token is the first decode
+    step. Roofline: int8 tensor ops of the limb GEMMs (3 limbs per dense MAC)
+    against 2 x the measured bf16 peak (kind::i8 issues at twice kind::f16)."""
+    try:
+        n_prompt = 2048
+        prompt = P.prompt_from_seed(9, cfg.vocab, n_prompt)
+        s = P.InferenceSession(mf, P.EngineOptions(device=dev))
+        times, tc = [], True
+        for i in range(5):
+            s.begin(prompt, 1)
+            ms, used = s.time_prefill()
+            tc &= used
+            if i >= 2:
+                times.append(ms)
+        ms = sorted(times)[len(times) // 2]
+        n = n_prompt - 1
+        D, F, L = cfg.d_model, cfg.d_ffn, cfg.n_layers
+        macs = n * ((L - 1) * (4 * D * D + 3 * F * D) + 3 * D * D)
+        limb_ops = 2 * 3 * macs
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                peak = 2 * json.load(f)["bf16_tflops"]
+            kind = "2 x measured bf16 burst (kind::i8 at twice the kind::f16 rate)"
+        except Exception:
+            peak, kind = 2 * 1590.0, "2 x fallback bf16"
+        return {"workload": "C3: Llama-2-7B-shaped prefill of a 2048-token synthetic prompt",
+                "path": "tensor cores (tcgen05 kind::i8 limb GEMMs + exact causal attention)" if tc
+                        else "decode kernel (exact fallback)",
+                "prompt_tokens": n_prompt, "positions_prefilled": n, "ms": ms,
+                "tokens_per_s": n / (ms / 1e3),
+                "roofline_whole_prefill": {"bound": "tensor", "achieved": limb_ops / (ms / 1e3) / 1e12,
+                                           "peak": peak, "unit": "TOP/s (int8)",
+                                           "frac": limb_ops / (ms / 1e3) / 1e12 / peak, "peak_kind": kind,
+                                           "note": "whole prefill time incl. the CUDA-core attention "
+                                                   "(profiles/r01_prefill_launches.txt has the split)"}}
+    except Exception as e:
+        return {"workload": "C3", "unavailable": str(e)}
+
+
 def run_ours(args, rank, world, local):
     import numpy as np
 
@@ -288,6 +330,7 @@ def run_ours(args, rank, world, local):
         if e2e:
             e2e["value"] = float(t.item()) * world
     base = cpu_baseline(mf, CFG7B) if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
+    prefill = prefill_c3(P, mf, cfg, dev) if rank == 0 and not args.no_prefill else None
 
     if rank == 0:
         line = {
@@ -315,6 +358,7 @@ def run_ours(args, rank, world, local):
             "stages": kern,
             "clocks": clk.summary(),
             "cpu_baseline": base,
+            "prefill": prefill,
             "tokens_head": toks[:8],
         }
         print(json.dumps(line), flush=True)
@@ -328,6 +372,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=128)
     ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--no-prefill", action="store_true", help="skip the C3 prefill measurement")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -156,6 +156,14 @@ dimg_status dimg_session_forward(dimg_session* s, uint32_t token, uint32_t pos, 
 dimg_status dimg_generate_greedy(dimg_session* s, const uint32_t* prompt, uint32_t n_prompt,
                                  uint32_t max_new, uint32_t* tokens_out, uint8_t hash_out[32],
                                  int64_t* logits_out);
+/* generate_greedy for n_seqs independent sequences stepped together (C5):
+ * prompts concatenated (p_lens[n_seqs] tokens each), tokens_out
+ * [n_seqs][max_new], hashes_out [n_seqs][32] (nullable). Bit-identical to
+ * n_seqs separate dimg_generate_greedy calls. *path (nullable) = 1 if the
+ * tensor-core batch path produced them, 0 if the exact per-sequence path. */
+dimg_status dimg_generate_greedy_batch(dimg_model* m, uint32_t n_seqs, const uint32_t* prompts,
+                                       const uint32_t* p_lens, uint32_t max_new, uint32_t* tokens_out,
+                                       uint8_t* hashes_out, uint32_t* path);
 
 /* Device-resident stepping (bench / advanced callers). The prompt is staged
  * with dimg_session_begin; each decode step forwards the newest token and
@@ -171,6 +179,9 @@ dimg_status dimg_session_tokens(dimg_session* s, uint32_t* out, uint32_t n_gener
 dimg_status dimg_session_stream(dimg_session* s, void** stream);
 /* Times n decode steps with CUDA events on the session stream. */
 dimg_status dimg_session_time_decode(dimg_session* s, uint32_t n_steps, float* ms);
+/* The prefill of the begun prompt between CUDA events; *tensor_cores = 1 if
+ * it ran on the tensor-core prefill path (else the decode kernel). */
+dimg_status dimg_session_time_prefill(dimg_session* s, float* ms, uint32_t* tensor_cores);
 /* Replays one kernel class n times between CUDA events on the session
  * stream (layers cycled so weights stream from HBM): which = 0 QKV GEMV,
  * 1 WO, 2 GATE/UP, 3 DOWN, 4 LM_HEAD. Returns the mean launch time and the

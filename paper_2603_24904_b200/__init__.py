@@ -8,7 +8,7 @@ from . import errors
 from ._lib import LIB_PATH, lib
 from .engine import (EngineOptions, GenerationResult, InferenceSession, attention_steps,
                      build_rope_tables, dense_forward, dense_tokens, device_count, ffn_silu, generate_greedy,
-                     generation_counter, hash_token_ids, parse_prompt, prompt_from_seed,
+                     generate_greedy_batch, generation_counter, hash_token_ids, parse_prompt, prompt_from_seed,
                      release_sessions, rmsnorm, select_greedy, softmax_q16)
 from .errors import (ContextOverflow, DomainError, InvalidArgument, LengthError, LogicError,
                      OutOfRange, ParseError)
@@ -16,7 +16,7 @@ from .model import (ONE, DeviceModel, ModelConfig, ModelFile, deserialize, gen_t
                     load_model, weight_hash)
 
 __all__ = [
-    "EngineOptions", "GenerationResult", "InferenceSession", "generate_greedy",
+    "EngineOptions", "GenerationResult", "InferenceSession", "generate_greedy", "generate_greedy_batch",
     "generation_counter", "hash_token_ids", "select_greedy", "parse_prompt", "prompt_from_seed",
     "build_rope_tables", "dense_forward", "dense_tokens", "rmsnorm", "softmax_q16", "attention_steps", "ffn_silu",
     "device_count", "release_sessions", "ModelConfig", "ModelFile", "DeviceModel",

@@ -76,6 +76,7 @@ def _load():
         "dimg_session_len": ([vp, u32p], C.c_int),
         "dimg_session_forward": ([vp, C.c_uint32, C.c_uint32, i64p], C.c_int),
         "dimg_generate_greedy": ([vp, u32p, C.c_uint32, C.c_uint32, u32p, u8p, i64p], C.c_int),
+        "dimg_generate_greedy_batch": ([vp, C.c_uint32, u32p, u32p, C.c_uint32, u32p, u8p, u32p], C.c_int),
         "dimg_session_begin": ([vp, u32p, C.c_uint32, C.c_uint32], C.c_int),
         "dimg_session_prefill": ([vp], C.c_int),
         "dimg_session_decode": ([vp, C.c_uint32], C.c_int),
@@ -83,6 +84,7 @@ def _load():
         "dimg_session_tokens": ([vp, u32p, C.c_uint32], C.c_int),
         "dimg_session_stream": ([vp, pp], C.c_int),
         "dimg_session_time_decode": ([vp, C.c_uint32, C.POINTER(C.c_float)], C.c_int),
+        "dimg_session_time_prefill": ([vp, C.POINTER(C.c_float), C.POINTER(C.c_uint32)], C.c_int),
         "dimg_session_launches": ([vp, u32p, u32p], C.c_int),
         "dimg_session_time_kernel": ([vp, C.c_int, C.c_uint32, C.POINTER(C.c_float), u64p], C.c_int),
         "dimg_session_stats": ([vp, u64p], C.c_int),

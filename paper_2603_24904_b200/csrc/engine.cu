@@ -32,6 +32,7 @@
 #include "kernels/persistent.cuh"
 #include "kernels/tc_gemm.cuh"
 #include "kernels/prefill.cuh"
+#include "kernels/batch.cuh"
 
 using namespace dimg;
 using namespace dimg::dev;
@@ -92,7 +93,8 @@ DevCtx& dev_ctx(int device) {
     CK(cudaStreamCreateWithFlags(&c.op_stream, cudaStreamNonBlocking));
     set_gemv_attrs<EPI_STORE, MODE_PLAIN>();
     set_gemv_attrs<EPI_STORE, MODE_NORM>();
-    CK(cudaFuncSetAttribute(limb_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TG_SMEM));
+    CK(cudaFuncSetAttribute(limb_gemm_kernel<TG_BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TG_SMEM));
+    CK(cudaFuncSetAttribute(limb_gemm_kernel<TG_BN_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TG_SMEM));
     {
         auto set = [&](auto kern) {
             cudaFuncAttributes fa;
@@ -105,6 +107,7 @@ DevCtx& dev_ctx(int device) {
         set(pf_attn_kernel<4>);
         set(pf_attn_kernel<8>);
         set(pf_attn_kernel<16>);
+        set(bd_attn_kernel);
     }
     set_gemv_attrs<EPI_STORE, MODE_EMBED>();
     set_gemv_attrs<EPI_RESID, MODE_PLAIN>();
@@ -188,12 +191,36 @@ __global__ void limbs_kernel(const int64_t* __restrict__ x, uint32_t T, uint32_t
     }
 }
 
-void launch_limb_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs& a, cudaStream_t st) {
+uint32_t gemm_tiles(const TgArgs& a, uint32_t bn) {
+    return ((a.n_out + TG_BM - 1) / TG_BM) * ((a.n_tok + bn - 1) / bn);
+}
+
+// Split-K factor for a GEMM with few output tiles: the smallest k that
+// minimises the busiest CTA's share (ceil(tiles * k / SMs) / k), keeping at
+// least 4 K blocks per split.
+uint32_t pick_ksplit(uint32_t tiles, uint32_t n_kblk, uint32_t sms) {
+    uint32_t best = 1;
+    double best_t = double((tiles + sms - 1) / sms);
+    for (uint32_t k = 2; k <= 8 && n_kblk / k >= 4; ++k) {
+        const double t = double((tiles * k + sms - 1) / sms) / k;
+        if (t < best_t - 1e-9) {
+            best_t = t;
+            best = k;
+        }
+    }
+    return best;
+}
+
+// bn = token tile (TG_BN or TG_BN_SMALL; tb must be built with that box).
+void launch_limb_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs& a, cudaStream_t st,
+                      uint32_t bn = TG_BN) {
     int dev = 0, sms = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const uint32_t tiles = ((a.n_out + TG_BM - 1) / TG_BM) * ((a.n_tok + TG_BN - 1) / TG_BN);
-    limb_gemm_kernel<<<std::min<uint32_t>(tiles, uint32_t(sms)), TG_THREADS, TG_SMEM, st>>>(ta, tb, a);
+    const uint32_t items = gemm_tiles(a, bn) * std::max(1u, a.ksplit);
+    const uint32_t grid = std::min<uint32_t>(items, uint32_t(sms));
+    if (bn == TG_BN_SMALL) limb_gemm_kernel<TG_BN_SMALL><<<grid, TG_THREADS, TG_SMEM, st>>>(ta, tb, a);
+    else limb_gemm_kernel<TG_BN><<<grid, TG_THREADS, TG_SMEM, st>>>(ta, tb, a);
     CK(cudaGetLastError());
 }
 
@@ -212,7 +239,8 @@ struct DevMat {
     int8_t* w = nullptr;       // blocked (decode kernel)
     int64_t* s = nullptr;      // scales [rows]
     uint32_t rows = 0, K = 0, Kp = 0, n_groups = 0, n_segs = 0;
-    int8_t* plain = nullptr;   // row-major [rows][Kp] (prefill GEMM A operand)
+    int8_t* plain = nullptr;   // K-block-major [kblk][rows128][128] (tensor-core A operand)
+    uint32_t kblk = 0, rows128 = 0;
     CUtensorMap tmap;          // its TMA map (128 x 128-byte boxes, 128B swizzle)
 };
 
@@ -295,6 +323,22 @@ __global__ void blockify_kernel(const int4* __restrict__ src, const int64_t* __r
     }
 }
 
+__global__ void kmajor_kernel(const int8_t* __restrict__ src, uint32_t Kp, uint32_t rows, uint32_t K,
+                              int8_t* __restrict__ dst, uint32_t rows128, uint32_t kblk) {
+    const size_t total = size_t(kblk) * rows128 * (TG_BK / 16);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t c16 = uint32_t(i % (TG_BK / 16));
+        const size_t rb = i / (TG_BK / 16);
+        const uint32_t r = uint32_t(rb % rows128), kb = uint32_t(rb / rows128);
+        const uint32_t k = kb * TG_BK + c16 * 16;
+        int4 v = make_int4(0, 0, 0, 0);
+        if (r < rows && k < K) {
+            v = *reinterpret_cast<const int4*>(src + size_t(r) * Kp + k);  // Kp % 16 == 0; bytes past K are zero
+        }
+        reinterpret_cast<int4*>(dst)[i] = v;
+    }
+}
+
 // Uploads one dense matrix given as `parts` row blocks (each row-major,
 // placed at row offset row0 with row stride rstride), then blockifies it.
 struct RowPart {
@@ -314,9 +358,14 @@ DevMat upload_mat(dimg_model& m, uint32_t rows, uint32_t K, const std::vector<Ro
     CK(cudaMemset(staging, 0, bytes));
     for (const auto& p : parts) put_rows(staging, d.Kp, p.row0, p.rstride, p.src, p.rows, K);
     d.s = upload(m.mem, scales.data(), scales.size());
-    d.plain = m.mem.alloc<int8_t>(size_t(d.n_groups) * PK_ROWS * d.Kp);
-    CK(cudaMemcpy(d.plain, staging, size_t(d.n_groups) * PK_ROWS * d.Kp, cudaMemcpyDeviceToDevice));
-    d.tmap = tmap_bytes(d.plain, K, rows, d.Kp, TG_BM);
+    // tensor-core copy, K-block-major: [K/128][rows padded to 128][128 bytes],
+    // so every 128-row x 128-byte TMA box is one contiguous 16 KB block
+    d.kblk = (K + TG_BK - 1) / TG_BK;
+    d.rows128 = (rows + TG_BM - 1) / TG_BM * TG_BM;
+    d.plain = m.mem.alloc<int8_t>(size_t(d.kblk) * d.rows128 * TG_BK);
+    kmajor_kernel<<<1024, 256>>>(staging, d.Kp, rows, K, d.plain, d.rows128, d.kblk);
+    CK(cudaGetLastError());
+    d.tmap = tmap_bytes(d.plain, TG_BK, size_t(d.kblk) * d.rows128, TG_BK, TG_BM);
     d.w = m.mem.alloc<int8_t>(size_t(d.n_groups) * pk_group_bytes(d.Kp));
     blockify_kernel<<<1024, 256>>>(reinterpret_cast<const int4*>(staging), d.s, rows,
                                    reinterpret_cast<int4*>(d.w), d.Kp, d.n_groups, d.n_segs);
@@ -640,6 +689,7 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
     auto gemm = [&](const DevMat& W, const CUtensorMap& tb, uint32_t epi, int64_t* y, uint32_t ldy) {
         TgArgs a{};
         a.n_out = W.rows;
+        a.a_rows = W.rows128;
         a.n_tok = n;
         a.n_kblk = (W.K + TG_BK - 1) / TG_BK;
         a.limb_rows = w.cap_pad;
@@ -711,6 +761,209 @@ void run_decode(dimg_session& s, uint32_t steps) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
+
+// ---------------------------------------------------------------------------
+// Batched generation (C5): independent sequences stepped together
+// ---------------------------------------------------------------------------
+namespace {
+
+struct BatchRun {
+    dimg_model* m;
+    cudaStream_t st = nullptr;
+    DevBuf mem;
+    uint32_t B = 0, ctx = 0, nmax = 0, nmax_pad = 0, max_new = 0;
+    uint32_t *tok = nullptr, *seq = nullptr, *pos = nullptr, *out = nullptr, *step = nullptr, *wide = nullptr;
+    int64_t *x = nullptr, *qkv = nullptr, *logits = nullptr;
+    uint8_t *pa = nullptr, *ph = nullptr;
+    int32_t *K32 = nullptr, *V32 = nullptr;
+    size_t seq_stride = 0, layer_stride = 0;
+    CUtensorMap tm_pa, tm_ph;           // box rows TG_BN (prompt phase)
+    CUtensorMap tm_pa_s, tm_ph_s;       // box rows TG_BN_SMALL (decode steps of <= 16 sequences)
+    int32_t* partial = nullptr;         // split-K partials
+    uint32_t* tile_cnt = nullptr;
+    size_t partial_elems = 0;
+    uint32_t tiles_max = 0;
+    ~BatchRun() {
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+bool batch_shape_ok(const dimg_model& m) { return m.dh % 4 == 0 && m.dh / 2 <= 1024; }
+
+void batch_alloc(BatchRun& r, dimg_model* m, uint32_t B, uint32_t ctx, uint32_t nmax, uint32_t max_new) {
+    r.m = m;
+    r.B = B;
+    r.ctx = ctx;
+    r.nmax = nmax;
+    r.nmax_pad = (nmax + TG_BN - 1) / TG_BN * TG_BN;
+    r.max_new = max_new;
+    CK(cudaStreamCreateWithFlags(&r.st, cudaStreamNonBlocking));
+    r.tok = r.mem.alloc<uint32_t>(nmax);
+    r.seq = r.mem.alloc<uint32_t>(nmax);
+    r.pos = r.mem.alloc<uint32_t>(nmax);
+    r.out = r.mem.alloc<uint32_t>(size_t(B) * std::max(1u, max_new));
+    r.step = r.mem.alloc<uint32_t>(1);
+    r.wide = r.mem.alloc<uint32_t>(1);
+    r.x = r.mem.alloc<int64_t>(size_t(nmax) * m->D);
+    r.qkv = r.mem.alloc<int64_t>(size_t(nmax) * 3 * m->D);
+    r.logits = r.mem.alloc<int64_t>(size_t(B) * m->V);
+    r.pa = r.mem.alloc<uint8_t>(size_t(3) * r.nmax_pad * m->Kd);
+    r.ph = r.mem.alloc<uint8_t>(size_t(3) * r.nmax_pad * m->Kf);
+    CK(cudaMemsetAsync(r.pa, 0, size_t(3) * r.nmax_pad * m->Kd, r.st));
+    CK(cudaMemsetAsync(r.ph, 0, size_t(3) * r.nmax_pad * m->Kf, r.st));
+    r.layer_stride = size_t(m->H) * ctx * m->dh;
+    r.seq_stride = r.layer_stride * m->L;
+    r.K32 = r.mem.alloc<int32_t>(r.seq_stride * B);
+    r.V32 = r.mem.alloc<int32_t>(r.seq_stride * B);
+    CK(cudaMemsetAsync(r.step, 0, 4, r.st));
+    CK(cudaMemsetAsync(r.wide, 0, 4, r.st));
+    r.tm_pa = tmap_bytes(r.pa, m->D, size_t(3) * r.nmax_pad, m->Kd, TG_BN);
+    r.tm_ph = tmap_bytes(r.ph, m->F, size_t(3) * r.nmax_pad, m->Kf, TG_BN);
+    r.tm_pa_s = tmap_bytes(r.pa, m->D, size_t(3) * r.nmax_pad, m->Kd, TG_BN_SMALL);
+    r.tm_ph_s = tmap_bytes(r.ph, m->F, size_t(3) * r.nmax_pad, m->Kf, TG_BN_SMALL);
+    // split-K scratch for the decode steps: tiles x k x 3 limbs x BN x 128 int32
+    const uint32_t bn = B <= TG_BN_SMALL ? TG_BN_SMALL : TG_BN;
+    const uint32_t tok_tiles = (B + bn - 1) / bn;
+    const uint32_t rows[5] = {3 * m->D, m->D, 2 * m->F, m->D, m->V};
+    for (uint32_t rw : rows) {
+        const uint32_t tiles = (rw + TG_BM - 1) / TG_BM * tok_tiles;
+        r.tiles_max = std::max(r.tiles_max, tiles);
+        r.partial_elems = std::max(r.partial_elems, size_t(tiles) * 8 * TG_L * bn * TG_BM);
+    }
+    r.partial = r.mem.alloc<int32_t>(r.partial_elems);
+    r.tile_cnt = r.mem.alloc<uint32_t>(r.tiles_max);
+    CK(cudaMemsetAsync(r.tile_cnt, 0, size_t(r.tiles_max) * 4, r.st));
+}
+
+// One forward pass of n tokens (each its own sequence/position); with
+// logits: the lm_head, greedy selection and the token/position feedback.
+void batch_step(BatchRun& r, uint32_t n, bool logits) {
+    const dimg_model& m = *r.m;
+    cudaStream_t st = r.st;
+    const uint32_t D = m.D, dh = m.dh, H = m.H;
+    const BatchTok bt{r.tok, r.seq, r.pos};
+    bd_embed_kernel<<<1024, 256, 0, st>>>(bt, n, m.embd, m.embd_s, D, r.x);
+    const bool small = n <= uint32_t(TG_BN_SMALL);
+    const uint32_t bn = small ? TG_BN_SMALL : TG_BN;
+    // split-K only pays for small token tiles (DIMG_SPLITK=0/1 overrides)
+    const char* sk = std::getenv("DIMG_SPLITK");
+    const bool split_k = sk ? std::atoi(sk) != 0 : small;
+    int sms = m.ctx->sm_count;
+    auto gemm = [&](const DevMat& W, const CUtensorMap& tb_big, uint32_t epi, int64_t* y, uint32_t ldy) {
+        const bool in_h = &tb_big == &r.tm_ph;
+        const CUtensorMap& tb = small ? (in_h ? r.tm_ph_s : r.tm_pa_s) : tb_big;
+        TgArgs a{};
+        a.n_out = W.rows;
+        a.a_rows = W.rows128;
+        a.n_tok = n;
+        a.n_kblk = (W.K + TG_BK - 1) / TG_BK;
+        a.limb_rows = r.nmax_pad;
+        a.epi = epi;
+        a.scales = W.s;
+        a.y = y;
+        a.ldy = ldy;
+        a.planes = r.ph;
+        a.limb_rows_out = r.nmax_pad;
+        a.ldp = m.Kf;
+        a.lut = m.ctx->exp_lut;
+        a.wide = r.wide;
+        a.ksplit = split_k ? pick_ksplit(gemm_tiles(a, bn), a.n_kblk, uint32_t(sms)) : 1;
+        if (size_t(gemm_tiles(a, bn)) * a.ksplit * TG_L * bn * TG_BM > r.partial_elems) a.ksplit = 1;
+        a.partial = r.partial;
+        a.tile_cnt = r.tile_cnt;
+        launch_limb_gemm(W.tmap, tb, a, st, bn);
+    };
+    const size_t asmem = bd_attn_smem(dh, r.ctx) + 8;
+    for (uint32_t l = 0; l < m.L; ++l) {
+        const auto& lw = m.layers[l];
+        pf_norm_limbs_kernel<<<n, 256, 0, st>>>(r.x, D, lw.attn_norm, lw.attn_unit, m.ctx->seeds, r.pa, r.nmax_pad,
+                                                 m.Kd, r.wide);
+        gemm(lw.qkv, r.tm_pa, TG_STORE, r.qkv, 3 * D);
+        bd_rope_kv_kernel<<<dim3(n, H), dh / 2, 0, st>>>(r.qkv, bt, D, dh, m.rope_cos, m.rope_sin,
+                                                         r.K32 + l * r.layer_stride, r.V32 + l * r.layer_stride,
+                                                         r.seq_stride, r.ctx, r.wide);
+        if (l + 1 == m.L && !logits) break;  // prompt positions only feed the KV caches
+        bd_attn_kernel<<<dim3(H, n), BD_THREADS, asmem, st>>>(r.qkv, bt, D, dh, r.K32 + l * r.layer_stride,
+                                                            r.V32 + l * r.layer_stride, r.seq_stride, r.ctx,
+                                                            m.inv_scale, m.ctx->exp_lut, r.pa, r.nmax_pad, m.Kd,
+                                                            r.wide);
+        gemm(lw.wo, r.tm_pa, TG_RESID, r.x, D);
+        pf_norm_limbs_kernel<<<n, 256, 0, st>>>(r.x, D, lw.ffn_norm, lw.ffn_unit, m.ctx->seeds, r.pa, r.nmax_pad,
+                                                 m.Kd, r.wide);
+        gemm(lw.gu, r.tm_pa, TG_SILU, nullptr, 0);
+        gemm(lw.down, r.tm_ph, TG_RESID, r.x, D);
+    }
+    if (logits) {
+        pf_norm_limbs_kernel<<<n, 256, 0, st>>>(r.x, D, m.final_norm, m.final_unit, m.ctx->seeds, r.pa, r.nmax_pad,
+                                                 m.Kd, r.wide);
+        gemm(m.head, r.tm_pa, TG_STORE, r.logits, m.V);
+        bd_argmax_kernel<<<n, 256, 0, st>>>(r.logits, m.V, r.tok, r.pos, r.seq, r.out, r.max_new, r.step);
+        bd_step_kernel<<<1, 1, 0, st>>>(r.step);
+    }
+    CK(cudaGetLastError());
+}
+
+// The batch path: true if every sequence's tokens were produced exactly.
+bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<uint32_t>>& prompts,
+                       uint32_t max_new, uint32_t* tokens_out, uint64_t* steps_graph) {
+    uint32_t ctx = 0, n_prompt_pos = 0;
+    for (const auto& p : prompts) {
+        ctx = std::max<uint32_t>(ctx, uint32_t(p.size()) + max_new);
+        n_prompt_pos += uint32_t(p.size()) - 1;
+    }
+    if (bd_attn_smem(m->dh, ctx) + 8 > size_t(m->ctx->smem_optin)) return false;
+    BatchRun r;
+    batch_alloc(r, m, B, ctx, std::max(n_prompt_pos, B), max_new);
+    // prompt phase: all positions but each prompt's last, one forward pass
+    if (n_prompt_pos) {
+        std::vector<uint32_t> tok, seq, pos;
+        for (uint32_t b = 0; b < B; ++b)
+            for (uint32_t i = 0; i + 1 < prompts[b].size(); ++i) {
+                tok.push_back(prompts[b][i]);
+                seq.push_back(b);
+                pos.push_back(i);
+            }
+        CK(cudaMemcpyAsync(r.tok, tok.data(), tok.size() * 4, cudaMemcpyHostToDevice, r.st));
+        CK(cudaMemcpyAsync(r.seq, seq.data(), seq.size() * 4, cudaMemcpyHostToDevice, r.st));
+        CK(cudaMemcpyAsync(r.pos, pos.data(), pos.size() * 4, cudaMemcpyHostToDevice, r.st));
+        CK(cudaStreamSynchronize(r.st));
+        batch_step(r, n_prompt_pos, false);
+    }
+    // decode: one token per sequence per step, the step captured once as a CUDA graph
+    {
+        std::vector<uint32_t> tok(B), seq(B), pos(B);
+        for (uint32_t b = 0; b < B; ++b) {
+            tok[b] = prompts[b].back();
+            seq[b] = b;
+            pos[b] = uint32_t(prompts[b].size()) - 1;
+        }
+        CK(cudaMemcpyAsync(r.tok, tok.data(), B * 4, cudaMemcpyHostToDevice, r.st));
+        CK(cudaMemcpyAsync(r.seq, seq.data(), B * 4, cudaMemcpyHostToDevice, r.st));
+        CK(cudaMemcpyAsync(r.pos, pos.data(), B * 4, cudaMemcpyHostToDevice, r.st));
+        CK(cudaStreamSynchronize(r.st));
+    }
+    if (max_new > 0) {
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        CK(cudaStreamBeginCapture(r.st, cudaStreamCaptureModeThreadLocal));
+        batch_step(r, B, true);
+        CK(cudaStreamEndCapture(r.st, &g));
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        for (uint32_t s = 0; s < max_new; ++s) CK(cudaGraphLaunch(ge, r.st));
+        CK(cudaStreamSynchronize(r.st));
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+        if (steps_graph) *steps_graph += max_new;
+    }
+    uint32_t wide = 0;
+    CK(cudaMemcpyAsync(&wide, r.wide, 4, cudaMemcpyDeviceToHost, r.st));
+    CK(cudaMemcpyAsync(tokens_out, r.out, size_t(B) * max_new * 4, cudaMemcpyDeviceToHost, r.st));
+    CK(cudaStreamSynchronize(r.st));
+    return wide == 0;
+}
+
+}  // namespace
+
 extern "C" {
 
 dimg_status dimg_device_count(int* n) { DIMG_API_GUARD(CK(cudaGetDeviceCount(n))) }
@@ -955,6 +1208,44 @@ dimg_status dimg_generate_greedy(dimg_session* s, const uint32_t* prompt, uint32
     })
 }
 
+dimg_status dimg_generate_greedy_batch(dimg_model* m, uint32_t n_seqs, const uint32_t* prompts,
+                                       const uint32_t* p_lens, uint32_t max_new, uint32_t* tokens_out,
+                                       uint8_t* hashes_out, uint32_t* path) {
+    // run_generation (proj/src/engine.cpp:31-54) for every sequence, stepped
+    // together on the tensor cores; an exact per-sequence rerun when some
+    // value falls outside the batch path's fast representations.
+    DIMG_API_GUARD({
+        CK(cudaSetDevice(m->device));
+        std::vector<std::vector<uint32_t>> ps(n_seqs);
+        size_t off = 0;
+        for (uint32_t b = 0; b < n_seqs; ++b) {
+            ps[b].assign(prompts + off, prompts + off + p_lens[b]);
+            off += p_lens[b];
+            check_prompt(*m, ps[b].data(), p_lens[b], max_new);
+        }
+        uint32_t used = 0;
+        static uint64_t graph_steps = 0;
+        if (n_seqs && batch_shape_ok(*m) && generate_batch_tc(m, n_seqs, ps, max_new, tokens_out, &graph_steps)) {
+            used = 1;
+        } else if (n_seqs) {
+            dimg_session* s = nullptr;
+            const dimg_status st = dimg_session_create(m, 0, &s);
+            if (st != DIMG_OK) return st;
+            std::unique_ptr<dimg_session, dimg_status (*)(dimg_session*)> keep(s, dimg_session_free);
+            for (uint32_t b = 0; b < n_seqs; ++b) {
+                const dimg_status g = dimg_generate_greedy(s, ps[b].data(), p_lens[b], max_new,
+                                                           tokens_out + size_t(b) * max_new, nullptr, nullptr);
+                if (g != DIMG_OK) return g;
+            }
+        }
+        if (path) *path = used;
+        for (uint32_t b = 0; b < n_seqs && hashes_out; ++b) {
+            auto d = b3::hash(tokens_out + size_t(b) * max_new, size_t(max_new) * 4, 1);
+            std::memcpy(hashes_out + 32 * size_t(b), d.data(), 32);
+        }
+    })
+}
+
 dimg_status dimg_session_begin(dimg_session* s, const uint32_t* prompt, uint32_t n_prompt,
                                uint32_t max_new) {
     DIMG_API_GUARD(begin(*s, prompt, n_prompt, max_new, false))
@@ -997,6 +1288,27 @@ dimg_status dimg_session_time_decode(dimg_session* s, uint32_t n_steps, float* m
         CK(cudaEventElapsedTime(ms, e0, e1));
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+        check_ctl_err(*s);
+    })
+}
+
+dimg_status dimg_session_time_prefill(dimg_session* s, float* ms, uint32_t* tensor_cores) {
+    // The prefill of the prompt given to dimg_session_begin, between CUDA
+    // events on the session stream (tensor-core path when it applies).
+    DIMG_API_GUARD({
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaStreamSynchronize(s->stream));
+        const uint64_t before = s->tc_prefills;
+        CK(cudaEventRecord(e0, s->stream));
+        run_prefill(*s);
+        CK(cudaEventRecord(e1, s->stream));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *tensor_cores = s->tc_prefills > before ? 1 : 0;
         check_ctl_err(*s);
     })
 }
@@ -1184,7 +1496,10 @@ dimg_status dimg_op_dense_tokens(int device, const dimg_qtensor* w, const int64_
         OpScope o(device);
         const uint32_t N = w->rows, K = w->cols, Kp = pad16(K);
         const uint32_t Tp = (T + TG_BN - 1) / TG_BN * TG_BN;
-        int8_t* W = o.put_padded(*w, 1, N, 0);
+        int8_t* Wr = o.put_padded(*w, 1, N, 0);
+        const uint32_t kblk = (K + TG_BK - 1) / TG_BK, rows128 = (N + TG_BM - 1) / TG_BM * TG_BM;
+        int8_t* W = o.mem.alloc<int8_t>(size_t(kblk) * rows128 * TG_BK);
+        kmajor_kernel<<<1024, 256, 0, o.c.op_stream>>>(Wr, Kp, N, K, W, rows128, kblk);
         int64_t* sc = o.put(w->scales, N);
         int64_t* xd = o.put(x, size_t(T) * K);
         uint8_t* planes = o.mem.alloc<uint8_t>(size_t(3) * Tp * Kp);
@@ -1196,6 +1511,7 @@ dimg_status dimg_op_dense_tokens(int device, const dimg_qtensor* w, const int64_
         int64_t* y = o.mem.alloc<int64_t>(size_t(T) * N);
         TgArgs a{};
         a.n_out = N;
+        a.a_rows = rows128;
         a.n_tok = T;
         a.n_kblk = (K + TG_BK - 1) / TG_BK;
         a.limb_rows = Tp;
@@ -1203,7 +1519,7 @@ dimg_status dimg_op_dense_tokens(int device, const dimg_qtensor* w, const int64_
         a.scales = sc;
         a.y = y;
         a.ldy = N;
-        const CUtensorMap ta = tmap_bytes(W, K, N, Kp, TG_BM);
+        const CUtensorMap ta = tmap_bytes(W, TG_BK, size_t(kblk) * rows128, TG_BK, TG_BM);
         const CUtensorMap tb = tmap_bytes(planes, K, size_t(3) * Tp, Kp, TG_BN);
         launch_limb_gemm(ta, tb, a, o.c.op_stream);
         uint32_t wide_h = 0;

@@ -1,0 +1,205 @@
+// Batched steps over many independent sequences (C5: 64 sequences, one per
+// slot of a batch): every token of a step is (sequence, position, token id),
+// the dense products of all of them are one tensor-core limb GEMM per matrix
+// (tc_gemm.cuh), and attention / RoPE / the KV append are per token against
+// that token's own sequence cache. The same step function serves the prompt
+// phase (all prompt positions but the last of every sequence, no logits) and
+// the decode steps (one token per sequence, logits + greedy argmax), so a
+// sequence sees exactly the forward passes of run_generation
+// (proj/src/engine.cpp:31-54).
+//
+// The batch keeps only the int32 KV mirror; any value outside the fast
+// representations (3 byte limbs, int32 K/V and scores, |q| < 2^23) sets
+// *wide and the engine regenerates every sequence on the exact single-
+// sequence path instead.
+#pragma once
+
+#include <cstdint>
+
+#include "attention.cuh"
+#include "q16.cuh"
+
+namespace dimg::dev {
+
+struct BatchTok {  // device arrays, one entry per token of the step
+    const uint32_t* tok;
+    const uint32_t* seq;
+    const uint32_t* pos;
+};
+
+__global__ void bd_embed_kernel(BatchTok bt, uint32_t n, const int8_t* __restrict__ E,
+                                const int64_t* __restrict__ Es, uint32_t D, int64_t* __restrict__ x) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < size_t(n) * D;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t t = uint32_t(i / D), j = uint32_t(i % D);
+        const uint32_t tk = bt.tok[t];
+        x[i] = int64_t(uint64_t(int64_t(E[size_t(tk) * D + j])) * uint64_t(Es[tk]));
+    }
+}
+
+// RoPE (proj/src/kernels.cpp:70-82) and the KV append (:139-142) of token t
+// at its own (sequence, position); q' overwrites q. grid (n, H), dh/2 threads.
+// cache layout: [seq][layer][head][ctx][dh] int32; this layer's base given.
+__global__ void bd_rope_kv_kernel(int64_t* __restrict__ qkv, BatchTok bt, uint32_t D, uint32_t dh,
+                                  const int64_t* __restrict__ rc, const int64_t* __restrict__ rs, int32_t* K32,
+                                  int32_t* V32, size_t seq_stride, uint32_t ctx, uint32_t* wide) {
+    const uint32_t t = blockIdx.x, h = blockIdx.y, half = dh / 2, i = threadIdx.x;
+    const uint32_t b = bt.seq[t], p = bt.pos[t];
+    int64_t* q = qkv + size_t(t) * 3 * D + size_t(h) * dh;
+    const int64_t* k = q + D;
+    const int64_t* v = q + 2 * D;
+    const size_t kv = size_t(b) * seq_stride + (size_t(h) * ctx + p) * dh;
+    const int64_t c = rc[size_t(p) * half + i], s = rs[size_t(p) * half + i];
+    int64_t q0, q1, k0, k1;
+    rope_pair(q[i], q[i + half], c, s, q0, q1);
+    rope_pair(k[i], k[i + half], c, s, k0, k1);
+    const int64_t v0 = v[i], v1 = v[i + half];
+    __syncthreads();
+    q[i] = q0;
+    q[i + half] = q1;
+    K32[kv + i] = int32_t(k0);
+    K32[kv + i + half] = int32_t(k1);
+    V32[kv + i] = int32_t(v0);
+    V32[kv + i + half] = int32_t(v1);
+    const auto b23 = [](int64_t a) { return a >= -(int64_t(1) << 23) && a < (int64_t(1) << 23); };
+    if (!fits_i32(k0) || !fits_i32(k1) || !fits_i32(v0) || !fits_i32(v1) || !b23(q0) || !b23(q1)) *wide = 1;
+}
+
+constexpr int BD_THREADS = 256;
+
+__host__ __device__ constexpr size_t bd_attn_smem(uint32_t dh, uint32_t ctx) {
+    return size_t(ctx) * 8 + size_t(dh) * 4 + size_t(BD_THREADS) * 8;
+}
+
+// attention_step (proj/src/kernels.cpp:117-177) of token t against positions
+// 0..pos[t] of its sequence, exact: int64 score sums of int32 products (one
+// warp per position, lanes over 4-dim quads), the softmax of softmax_q16 over
+// the strip in shared memory, the per-product floor of mul16(p, v).
+// grid (H, n); writes the limb planes of the attention vector, row t.
+__global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __restrict__ qkv, BatchTok bt,
+                                                             uint32_t D, uint32_t dh, const int32_t* __restrict__ K32,
+                                                             const int32_t* __restrict__ V32, size_t seq_stride,
+                                                             uint32_t ctx, int64_t inv_scale,
+                                                             const int64_t* __restrict__ lut_g, uint8_t* planes,
+                                                             uint32_t rows_pad, uint32_t ldp, uint32_t* wide) {
+    extern __shared__ __align__(16) uint8_t bd_smem[];
+    __shared__ int64_t lut[257];
+    __shared__ u128 red[32];
+    const uint32_t h = blockIdx.x, t = blockIdx.y;
+    const uint32_t b = bt.seq[t], T = bt.pos[t] + 1;
+    int64_t* S = reinterpret_cast<int64_t*>(bd_smem);              // [ctx]
+    int32_t* q = reinterpret_cast<int32_t*>(S + ctx);              // [dh]
+    uint64_t* part = reinterpret_cast<uint64_t*>(q + dh + (dh & 1));  // [BD_THREADS]
+    for (int i = threadIdx.x; i < 257; i += BD_THREADS) lut[i] = lut_g[i];
+    for (uint32_t j = threadIdx.x; j < dh; j += BD_THREADS) q[j] = int32_t(qkv[size_t(t) * 3 * D + size_t(h) * dh + j]);
+    __syncthreads();
+    const int32_t* Kh = K32 + size_t(b) * seq_stride + size_t(h) * ctx * dh;
+    const int32_t* Vh = V32 + size_t(b) * seq_stride + size_t(h) * ctx * dh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int big = 0;
+    // four positions per warp per pass, their row loads in flight together
+    for (uint32_t p0 = 4 * warp; p0 < T; p0 += 4 * (BD_THREADS / 32)) {
+        int64_t d[4] = {0, 0, 0, 0};
+        for (uint32_t j = 4 * lane; j < dh; j += 128) {
+            int4 kk[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                kk[u] = p0 + u < T ? *reinterpret_cast<const int4*>(Kh + size_t(p0 + u) * dh + j) : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                d[u] += int64_t(q[j]) * kk[u].x + int64_t(q[j + 1]) * kk[u].y + int64_t(q[j + 2]) * kk[u].z +
+                        int64_t(q[j + 3]) * kk[u].w;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+        if (lane == 0)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (p0 + u < T) S[p0 + u] = mul16(d[u] >> 16, inv_scale);
+    }
+    __syncthreads();
+    softmax_strip_inl(S, T, lut, red);  // ends with a barrier
+    // out_j = sum_p mul16(p_p, V[p]_j): threads = (dim, position slice)
+    const uint32_t slices = dh <= BD_THREADS ? BD_THREADS / dh : 1;
+    const uint32_t j = threadIdx.x % dh, sl = threadIdx.x / dh;
+    uint64_t acc = 0;
+    if (sl < slices && j < dh) {
+        uint32_t p = sl;
+        for (; p + 3 * slices < T; p += 4 * slices) {  // four V rows in flight
+            int32_t vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) vv[u] = Vh[size_t(p + u * slices) * dh + j];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc += uint64_t(mul16_prob(S[p + u * slices], vv[u]));
+        }
+        for (; p < T; p += slices) acc += uint64_t(mul16_prob(S[p], Vh[size_t(p) * dh + j]));
+    }
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    const size_t plane = size_t(rows_pad) * ldp;
+    for (uint32_t jj = threadIdx.x; jj < dh; jj += BD_THREADS) {
+        uint64_t sum = 0;
+        if (dh <= BD_THREADS) {
+            for (uint32_t s2 = 0; s2 < slices; ++s2) sum += part[s2 * dh + jj];
+        } else {  // dh > BD_THREADS: this thread sums dimension jj itself
+            for (uint32_t p = 0; p < T; ++p) sum += uint64_t(mul16_prob(S[p], Vh[size_t(p) * dh + jj]));
+        }
+        const int64_t v = int64_t(sum);
+        uint8_t* pp = planes + size_t(t) * ldp + h * dh + jj;
+        pp[0] = uint8_t(v);
+        pp[plane] = uint8_t(v >> 8);
+        pp[2 * plane] = uint8_t(v >> 16);
+        if (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) big = 1;
+    }
+    if (big) *wide = 1;
+}
+
+// Greedy selection per token row of the logits (proj/src/engine.cpp:113-120:
+// largest value, lowest index on ties); feeds the next step: tok[t] = the
+// choice, pos[t] += 1, and the choice is recorded at out[seq][step].
+__global__ void __launch_bounds__(256) bd_argmax_kernel(const int64_t* __restrict__ logits, uint32_t V,
+                                                        uint32_t* tok, uint32_t* pos, const uint32_t* seq,
+                                                        uint32_t* out, uint32_t max_new, uint32_t* step) {
+    __shared__ int64_t sv[8];
+    __shared__ uint32_t si[8];
+    const uint32_t t = blockIdx.x;
+    const int64_t* row = logits + size_t(t) * V;
+    int64_t bv = INT64_MIN;
+    uint32_t bi = 0xFFFFFFFFu;
+    for (uint32_t i = threadIdx.x; i < V; i += blockDim.x)
+        if (better(row[i], i, bv, bi)) {
+            bv = row[i];
+            bi = i;
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (better(ov, oi, bv, bi)) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sv[threadIdx.x >> 5] = bv;
+        si[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w)
+            if (better(sv[w], si[w], bv, bi)) {
+                bv = sv[w];
+                bi = si[w];
+            }
+        const uint32_t s = *step;
+        out[size_t(seq[t]) * max_new + s] = bi;
+        tok[t] = bi;
+        pos[t] += 1;
+    }
+}
+
+__global__ void bd_step_kernel(uint32_t* step) { *step += 1; }
+
+}  // namespace dimg::dev

@@ -38,7 +38,10 @@ __device__ __forceinline__ void pf_put_limbs(uint8_t* p, size_t plane, int64_t v
 }
 
 // rmsnorm (proj/src/kernels.cpp:56-68) of every token row, written as the
-// three limb planes of the next GEMM's B operand. One CTA per token.
+// three limb planes of the next GEMM's B operand. One CTA per token; the row
+// is loaded once into registers (all loads in flight together).
+constexpr int PN_PER = 16;  // elements per thread held in registers (K <= 4096 with 256 threads)
+
 __global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int64_t* __restrict__ x, uint32_t K,
                                                             const int64_t* __restrict__ gamma, int gamma_unit,
                                                             const int64_t* __restrict__ seeds, uint8_t* planes,
@@ -47,21 +50,40 @@ __global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int64_t* __res
     __shared__ int64_t s_r;
     const uint32_t t = blockIdx.x;
     const int64_t* xr = x + size_t(t) * K;
+    int64_t v[PN_PER];
+#pragma unroll
+    for (int u = 0; u < PN_PER; ++u) {
+        const uint32_t j = threadIdx.x + u * 256;
+        v[u] = j < K ? xr[j] : 0;
+    }
     u128 ss = 0;
-    for (uint32_t j = threadIdx.x; j < K; j += blockDim.x) ss += mul_full(xr[j], xr[j]);
+#pragma unroll
+    for (int u = 0; u < PN_PER; ++u) ss += mul_full(v[u], v[u]);
+    for (uint32_t j = threadIdx.x + PN_PER * 256; j < K; j += 256) ss += mul_full(xr[j], xr[j]);
     ss = block_sum_u128(ss, red);
     if (threadIdx.x == 0) {
-        const int64_t ms = int64_t((i128(ss) / i128(K)) >> 16);
+        // usual case: the sum fits 63 bits and one u64 division is exact
+        const int64_t ms = (ss >> 63) == 0 ? int64_t((uint64_t(ss) / K) >> 16) : int64_t((i128(ss) / i128(K)) >> 16);
         s_r = ms + 1 > 0 ? inv_sqrt_q16(ms + 1, seeds) : 0;
         if (ms + 1 <= 0) *wide = 1;  // the reference throws (domain_error): the exact path reports it
     }
     __syncthreads();
     const int64_t r = s_r;
     const size_t plane = size_t(rows_pad) * ldp;
-    for (uint32_t j = threadIdx.x; j < K; j += blockDim.x) {
-        int64_t v = mul16(xr[j], r);
-        if (!gamma_unit) v = mul16(v, gamma[j]);
-        pf_put_limbs(planes + size_t(t) * ldp + j, plane, v, wide);
+    uint8_t* pr = planes + size_t(t) * ldp;
+#pragma unroll
+    for (int u = 0; u < PN_PER; ++u) {
+        const uint32_t j = threadIdx.x + u * 256;
+        if (j < K) {
+            int64_t o = mul16(v[u], r);
+            if (!gamma_unit) o = mul16(o, gamma[j]);
+            pf_put_limbs(pr + j, plane, o, wide);
+        }
+    }
+    for (uint32_t j = threadIdx.x + PN_PER * 256; j < K; j += 256) {
+        int64_t o = mul16(xr[j], r);
+        if (!gamma_unit) o = mul16(o, gamma[j]);
+        pf_put_limbs(pr + j, plane, o, wide);
     }
 }
 

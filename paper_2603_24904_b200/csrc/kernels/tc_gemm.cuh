@@ -11,14 +11,16 @@
 // (Larger activations are detected by the producers; the engine then takes
 // the exact CUDA-core path instead.)
 //
-// Tiles are 128 features x 64 tokens: the weights are the MMA A operand
+// Tiles are 128 features x BN tokens (64, or 16 for decode batches): the weights are the MMA A operand
 // (M = features, K-major), the three limb planes of the tokens are three B
 // operands (N = tokens, K-major) sharing one A tile per stage, and a tile's
 // three accumulators take 3 x 64 TMEM columns. The kernel is persistent (one
 // CTA per SM walks tiles round-robin) with two accumulator sets in TMEM, so
 // the epilogue of one tile overlaps the MMAs of the next. TMA loads 128-byte
 // K slices of every operand with the 128B swizzle that the UMMA smem
-// descriptors describe; a 5-stage mbarrier ring feeds the MMA warp.
+// descriptors describe; an mbarrier ring of ~200 KB feeds the MMA warp.
+// When there are too few output tiles to occupy every SM (decode batches),
+// several CTAs split a tile's K range (split-K, see TgArgs).
 // Warp roles: 0 = TMA producer, 1 = TMEM owner + MMA issuer, 2..5 = epilogue
 // (warp w reads TMEM lane quarter w % 4, i.e. features 32 (w % 4) .. +31,
 // one feature per thread -> coalesced stores across the warp).
@@ -33,16 +35,22 @@
 namespace dimg::dev {
 
 constexpr int TG_BM = 128;      // features per tile (MMA M)
-constexpr int TG_BN = 64;       // tokens per tile (MMA N)
+constexpr int TG_BN = 64;       // tokens per tile (MMA N), prefill / large batches
+constexpr int TG_BN_SMALL = 16; // tokens per tile for decode batches of <= 16 sequences
 constexpr int TG_BK = 128;      // K bytes per stage = one 128-byte swizzle row
 constexpr int TG_L = 3;         // activation limbs
-constexpr int TG_STAGES = 5;
-constexpr int TG_ACC = TG_L * TG_BN;  // TMEM columns of one tile's accumulators
 constexpr int TG_A_BYTES = TG_BM * TG_BK;
-constexpr int TG_B_BYTES = TG_BN * TG_BK;
-constexpr int TG_STAGE_BYTES = TG_A_BYTES + TG_L * TG_B_BYTES;  // 40 KB
 constexpr int TG_THREADS = 192;
-constexpr int TG_SMEM = TG_STAGES * TG_STAGE_BYTES + 1024;      // + alignment slack
+constexpr int TG_SMEM = 200 * 1024 + 1024;  // stage ring (+ alignment slack)
+
+template <int BN>
+struct TgShape {
+    static constexpr int B_BYTES = BN * TG_BK;
+    static constexpr int STAGE_BYTES = TG_A_BYTES + TG_L * B_BYTES;  // 40 KB (BN 64) / 22 KB (BN 16)
+    static constexpr int STAGES = (200 * 1024) / STAGE_BYTES;
+    static constexpr int ACC = TG_L * BN;  // TMEM columns of one tile's accumulators
+    static constexpr uint32_t TMEM_COLS = 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
+};
 
 enum { TG_STORE = 0, TG_RESID = 1, TG_SILU = 2 };
 
@@ -51,6 +59,7 @@ struct TgArgs {
     uint32_t n_tok;      // tokens
     uint32_t n_kblk;     // K / 128, rounded up
     uint32_t limb_rows;  // rows of one limb plane in the B tensor map
+    uint32_t a_rows;     // rows per K block of the K-block-major A operand (n_out padded to 128)
     uint32_t epi;
     const int64_t* scales;  // [n_out]
     int64_t* y;             // STORE: y[t][n]; RESID: x[t][n] updated; SILU: h[t][n / 2]
@@ -60,6 +69,12 @@ struct TgArgs {
     uint32_t limb_rows_out, ldp;
     const int64_t* lut;     // exp LUT (SILU)
     uint32_t* wide;         // set to 1 if an output needs more than 3 limbs (SILU planes)
+    // split-K (few output tiles, e.g. decode batches): ksplit CTAs share a
+    // tile; each stores its int32 limb partials, the last one to finish sums
+    // them (integer sums: exact in any order) and runs the epilogue.
+    uint32_t ksplit;
+    int32_t* partial;       // [tiles][ksplit][3][BN][128]
+    uint32_t* tile_cnt;     // [tiles], zero between launches (the last CTA resets)
 };
 
 // ---- PTX wrappers --------------------------------------------------------------
@@ -104,9 +119,9 @@ __device__ __forceinline__ uint64_t tg_desc(uint32_t smem_addr) {
 }
 
 // Instruction descriptor, kind::i8: D s32, A = W (s8), B = limb (u8 or s8),
-// both K-major, M = 128, N = 128.
-__host__ __device__ constexpr uint32_t tg_idesc(bool b_signed) {
-    return (2u << 4) | (1u << 7) | ((b_signed ? 1u : 0u) << 10) | (uint32_t(TG_BN >> 3) << 17) |
+// both K-major, M = 128, N = bn.
+__host__ __device__ constexpr uint32_t tg_idesc(bool b_signed, int bn) {
+    return (2u << 4) | (1u << 7) | ((b_signed ? 1u : 0u) << 10) | (uint32_t(bn >> 3) << 17) |
            (uint32_t(TG_BM >> 4) << 24);
 }
 
@@ -139,25 +154,38 @@ __device__ __forceinline__ void tg_ld_wait() { asm volatile("tcgen05.wait::ld.sy
 
 // ---- the kernel ---------------------------------------------------------------------
 
+template <int BN>
 __device__ __forceinline__ void tg_tile(uint32_t tile, uint32_t n_mt, uint32_t& n0, uint32_t& t0) {
     n0 = (tile % n_mt) * TG_BM;  // feature tiles fastest: consecutive CTAs share the token tile
-    t0 = (tile / n_mt) * TG_BN;
+    t0 = (tile / n_mt) * BN;
 }
 
+// work item -> (tile, K-block range)
+__device__ __forceinline__ void tg_item(uint32_t item, uint32_t ksplit, uint32_t n_kblk, uint32_t& tile,
+                                        uint32_t& ks, uint32_t& kb0, uint32_t& kb1) {
+    tile = item / ksplit;
+    ks = item % ksplit;
+    kb0 = uint32_t(uint64_t(n_kblk) * ks / ksplit);
+    kb1 = uint32_t(uint64_t(n_kblk) * (ks + 1) / ksplit);
+}
+
+template <int BN>
 __global__ void __launch_bounds__(TG_THREADS, 1)
     limb_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const TgArgs a) {
+    using S = TgShape<BN>;
     extern __shared__ uint8_t tg_smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tg_smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ __align__(8) uint64_t full[TG_STAGES], empty[TG_STAGES], acc_full[2], acc_empty[2];
-    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t full[S::STAGES], empty[S::STAGES], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_slot, s_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t n_mt = (a.n_out + TG_BM - 1) / TG_BM, n_tt = (a.n_tok + TG_BN - 1) / TG_BN;
-    const uint32_t n_tiles = n_mt * n_tt;
+    const uint32_t n_mt = (a.n_out + TG_BM - 1) / TG_BM, n_tt = (a.n_tok + BN - 1) / BN;
+    const uint32_t ksplit = a.ksplit ? a.ksplit : 1;
+    const uint32_t n_items = n_mt * n_tt * ksplit;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TG_STAGES; ++s) {
+        for (int s = 0; s < S::STAGES; ++s) {
             tg_mbar_init(&full[s], 1);
             tg_mbar_init(&empty[s], 1);
         }
@@ -167,9 +195,9 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {  // TMEM: two accumulator sets of 3 x 64 columns (allocation rounds to 512)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         tg_smem_u32(&tmem_slot))
+    if (warp == 1) {  // TMEM: two accumulator sets of 3 x BN columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         tg_smem_u32(&tmem_slot)), "n"(S::TMEM_COLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -179,20 +207,21 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     const uint32_t tmem = tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // TMA producer: the K slices of every tile of this CTA, in order
+        if (lane == 0) {  // TMA producer: the K slices of every work item of this CTA, in order
             uint32_t it = 0;
-            for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-                uint32_t n0, t0;
-                tg_tile(tile, n_mt, n0, t0);
-                for (uint32_t kb = 0; kb < a.n_kblk; ++kb, ++it) {
-                    const uint32_t s = it % TG_STAGES;
-                    if (it >= TG_STAGES) tg_mbar_wait(&empty[s], ((it / TG_STAGES) & 1) ^ 1);
-                    uint8_t* st = smem + size_t(s) * TG_STAGE_BYTES;
-                    tg_mbar_expect_tx(&full[s], TG_STAGE_BYTES);
-                    tg_tma_2d(st, &tmA, int32_t(kb * TG_BK), int32_t(n0), &full[s]);
+            for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+                uint32_t tile, ks, kb0, kb1, n0, t0;
+                tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
+                tg_tile<BN>(tile, n_mt, n0, t0);
+                for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
+                    const uint32_t s = it % S::STAGES;
+                    if (it >= S::STAGES) tg_mbar_wait(&empty[s], ((it / S::STAGES) & 1) ^ 1);
+                    uint8_t* st = smem + size_t(s) * S::STAGE_BYTES;
+                    tg_mbar_expect_tx(&full[s], S::STAGE_BYTES);
+                    tg_tma_2d(st, &tmA, 0, int32_t(kb * a.a_rows + n0), &full[s]);  // K-block-major A
 #pragma unroll
                     for (int l = 0; l < TG_L; ++l)
-                        tg_tma_2d(st + TG_A_BYTES + l * TG_B_BYTES, &tmB, int32_t(kb * TG_BK),
+                        tg_tma_2d(st + TG_A_BYTES + l * S::B_BYTES, &tmB, int32_t(kb * TG_BK),
                                   int32_t(l * a.limb_rows + t0), &full[s]);
                 }
             }
@@ -200,24 +229,26 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     } else if (warp == 1) {
         if (lane == 0) {  // MMA issuer
             uint32_t it = 0, j = 0;
-            for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
+            for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++j) {
+                uint32_t tile, ks, kb0, kb1;
+                tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
                 const uint32_t b = j & 1;
                 if (j >= 2) tg_mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained set b
                 tg_fence_after();
-                const uint32_t dacc = tmem + b * TG_ACC;
-                for (uint32_t kb = 0; kb < a.n_kblk; ++kb, ++it) {
-                    const uint32_t s = it % TG_STAGES;
-                    tg_mbar_wait(&full[s], (it / TG_STAGES) & 1);
+                const uint32_t dacc = tmem + b * S::ACC;
+                for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
+                    const uint32_t s = it % S::STAGES;
+                    tg_mbar_wait(&full[s], (it / S::STAGES) & 1);
                     tg_fence_after();
-                    const uint32_t sa = tg_smem_u32(smem + size_t(s) * TG_STAGE_BYTES);
+                    const uint32_t sa = tg_smem_u32(smem + size_t(s) * S::STAGE_BYTES);
 #pragma unroll
                     for (int l = 0; l < TG_L; ++l) {
-                        const uint32_t idesc = tg_idesc(l == TG_L - 1);
-                        const uint32_t sb = sa + TG_A_BYTES + l * TG_B_BYTES;
+                        const uint32_t idesc = tg_idesc(l == TG_L - 1, BN);
+                        const uint32_t sb = sa + TG_A_BYTES + l * S::B_BYTES;
 #pragma unroll
                         for (int kk = 0; kk < TG_BK / 32; ++kk)  // K = 32 bytes per MMA
-                            tg_mma(dacc + l * TG_BN, tg_desc(sa + 32 * kk), tg_desc(sb + 32 * kk), idesc,
-                                   (kb | kk) != 0);
+                            tg_mma(dacc + l * BN, tg_desc(sa + 32 * kk), tg_desc(sb + 32 * kk), idesc,
+                                   (kb != kb0) || (kk != 0));
                     }
                     tg_commit(&empty[s]);  // frees the stage once these MMAs have read it
                 }
@@ -227,32 +258,77 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     } else {
         // epilogue: thread = feature n, columns = tokens
         const uint32_t q = warp & 3;
+        const uint32_t fl = 32 * q + lane;  // feature within the tile
         uint32_t j = 0;
-        for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
-            uint32_t n0, t0;
-            tg_tile(tile, n_mt, n0, t0);
+        for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++j) {
+            uint32_t tile, ks, kb0, kb1, n0, t0;
+            tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
+            tg_tile<BN>(tile, n_mt, n0, t0);
             const uint32_t b = j & 1;
-            const uint32_t n = n0 + 32 * q + lane;
+            const uint32_t n = n0 + fl;
             const bool nv = n < a.n_out;
-            const int64_t sc = nv ? a.scales[n] : 0;
             tg_mbar_wait(&acc_full[b], (j >> 1) & 1);
             tg_fence_after();
-            const uint32_t tbase = tmem + ((32 * q) << 16) + b * TG_ACC;
-            for (uint32_t c0 = 0; c0 < TG_BN; c0 += 16) {
-                int32_t d0[16], d1[16], d2[16];
-                tg_ld16(tbase + c0, d0);
-                tg_ld16(tbase + TG_BN + c0, d1);
-                tg_ld16(tbase + 2 * TG_BN + c0, d2);
-                tg_ld_wait();
-                if (c0 + 16 >= TG_BN) {  // every column of set b is in registers: hand it back
-                    tg_fence_before();
-                    __syncwarp();
-                    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tg_smem_u32(&acc_empty[b])) : "memory");
+            const uint32_t tbase = tmem + ((32 * q) << 16) + b * S::ACC;
+            int32_t* part = ksplit > 1 ? a.partial + (size_t(tile) * ksplit) * (TG_L * BN * TG_BM) : nullptr;
+            bool last = true;
+            if (ksplit > 1) {
+                // this split's partials -> global, then the last split of the tile sums them
+                for (uint32_t c0 = 0; c0 < BN; c0 += 16) {
+                    int32_t d[TG_L][16];
+#pragma unroll
+                    for (int l = 0; l < TG_L; ++l) tg_ld16(tbase + l * BN + c0, d[l]);
+                    tg_ld_wait();
+#pragma unroll
+                    for (int l = 0; l < TG_L; ++l)
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj)
+                            part[((size_t(ks) * TG_L + l) * BN + c0 + jj) * TG_BM + fl] = d[l][jj];
+                }
+                tg_fence_before();
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tg_smem_u32(&acc_empty[b])) : "memory");
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (threadIdx.x == 64) s_last = atomicAdd(a.tile_cnt + tile, 1u) == ksplit - 1;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                last = s_last != 0;
+                if (last) {
+                    __threadfence();
+                    if (threadIdx.x == 64) a.tile_cnt[tile] = 0;  // ready for the next launch
+                }
+            }
+            if (!last) continue;
+            const int64_t sc = nv ? a.scales[n] : 0;
+            for (uint32_t c0 = 0; c0 < BN; c0 += 16) {
+                int32_t d[TG_L][16];
+                if (ksplit > 1) {
+                    // sum the splits: 48 independent loads in flight per split
+#pragma unroll
+                    for (int l = 0; l < TG_L; ++l)
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) d[l][jj] = 0;
+                    for (uint32_t k2 = 0; k2 < ksplit; ++k2) {
+                        const int32_t* pk = part + (size_t(k2) * TG_L * BN + c0) * TG_BM + fl;
+#pragma unroll
+                        for (int l = 0; l < TG_L; ++l)
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) d[l][jj] += __ldcg(pk + (size_t(l) * BN + jj) * TG_BM);
+                    }
+                } else {
+#pragma unroll
+                    for (int l = 0; l < TG_L; ++l) tg_ld16(tbase + l * BN + c0, d[l]);
+                    tg_ld_wait();
+                    if (c0 + 16 >= BN) {  // every column of set b is in registers: hand it back
+                        tg_fence_before();
+                        __syncwarp();
+                        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tg_smem_u32(&acc_empty[b])) : "memory");
+                    }
                 }
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) {
                     const uint32_t t = t0 + c0 + jj;
-                    const int64_t acc = int64_t(d0[jj]) + (int64_t(d1[jj]) << 8) + (int64_t(d2[jj]) << 16);
+                    const int64_t acc = int64_t(d[0][jj]) + (int64_t(d[1][jj]) << 8) + (int64_t(d[2][jj]) << 16);
                     const int64_t val = scale_row(acc, sc);
                     if (a.epi == TG_SILU) {
                         // rows (2i, 2i+1) = (gate_i, up_i) sit on adjacent lanes
@@ -280,7 +356,7 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
     __syncthreads();
     if (warp == 1) {
         tg_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(S::TMEM_COLS) : "memory");
     }
 }
 

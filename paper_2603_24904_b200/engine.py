@@ -154,6 +154,13 @@ class InferenceSession:
 
     KERNELS = ("qkv_gemv", "wo_gemv", "gate_up_gemv", "down_gemv", "lm_head_gemv")
 
+    def time_prefill(self):
+        """(ms, tensor_cores) of the prefill of the begun prompt (CUDA events)."""
+        ms = C.c_float()
+        tc = C.c_uint32()
+        check(lib.dimg_session_time_prefill(self._h, C.byref(ms), C.byref(tc)))
+        return ms.value, bool(tc.value)
+
     def time_kernel(self, which: int, n: int):
         """(ms per launch, algorithmic bytes per launch) of kernel class `which`."""
         ms = C.c_float()
@@ -220,6 +227,26 @@ def generate_greedy(model: ModelFile, prompt: Sequence[int], max_new: int,
     _generations += 1
     sess = _cached_session(model, opts, max_new if opts.keep_logits else 0, imported_tables)
     return sess.generate_greedy(prompt, max_new, keep_logits=opts.keep_logits)
+
+
+def generate_greedy_batch(model: ModelFile, prompts: Sequence[Sequence[int]], max_new: int,
+                          device: int = 0):
+    """generate_greedy for many independent sequences at once (C5): stepped
+    together on the tensor cores (one limb GEMM per matrix per step for all
+    sequences), bit-identical to separate generate_greedy calls. Returns
+    (results, path) with path "tensor_cores" or "per_sequence"."""
+    dm = model.device_model(device)
+    n = len(prompts)
+    lens = np.array([len(p) for p in prompts], np.uint32)
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(p, np.uint32) for p in prompts]) if n else
+                                np.zeros(1, np.uint32), np.uint32)
+    toks = np.zeros((max(1, n), max(1, max_new)), np.uint32)
+    hashes = np.zeros((max(1, n), 32), np.uint8)
+    path = C.c_uint32()
+    check(lib.dimg_generate_greedy_batch(dm._h, n, ptr(flat, u32p), ptr(lens, u32p), max_new, ptr(toks, u32p),
+                                         ptr(hashes, u8p), C.byref(path)))
+    res = [GenerationResult([int(t) for t in toks[i, :max_new]], bytes(hashes[i])) for i in range(n)]
+    return res, "tensor_cores" if path.value else "per_sequence"
 
 
 def release_sessions():

@@ -295,3 +295,31 @@ def test_tensor_core_prefill_falls_back_exactly(P, oracle, golden_models, monkey
     monkeypatch.setenv("DIMG_PREFILL", "2")
     ref = P.InferenceSession(m).generate_greedy(prompt, 5)
     assert res.token_ids == ref.token_ids and res.output_hash == ref.output_hash
+
+
+# ---- batched generation (C5) ----------------------------------------------------
+
+@pytest.mark.parametrize("cfg6,n_seqs,plen,new", [((2, 64, 2, 64, 64, 256), 5, 12, 9),
+                                                  ((2, 256, 2, 512, 300, 200), 8, 30, 6),
+                                                  ((3, 96, 3, 160, 77, 100), 3, 1, 7)])
+def test_batch_generation_matches_single(P, oracle, cfg6, n_seqs, plen, new):
+    from oracle.pyoracle import Config
+    m = P.gen_toy_model(11, P.ModelConfig(*cfg6))
+    om = oracle.gen_toy(11, Config(*cfg6))
+    prompts = [P.prompt_from_seed(500 + i, cfg6[4], plen + (i % 3)) for i in range(n_seqs)]
+    res, path = P.generate_greedy_batch(m, prompts, new)
+    assert path == "tensor_cores"
+    for p, r in zip(prompts, res):
+        toks, h, _ = oracle.generate_greedy(om, p, new)
+        assert r.token_ids == [int(t) for t in toks]
+        assert r.output_hash.hex() == h
+
+
+def test_batch_generation_wild_falls_back(P, golden_models):
+    g = golden_models["wild_b"]
+    m = _model_for(P, g)
+    prompts = [g["prompt"], g["prompt"][:1] * 3]
+    res, path = P.generate_greedy_batch(m, prompts, 4)
+    single = [P.generate_greedy(m, p, 4) for p in prompts]
+    assert [r.token_ids for r in res] == [s.token_ids for s in single]
+    assert [r.output_hash for r in res] == [s.output_hash for s in single]

@@ -195,6 +195,15 @@ int main() {
         printf("ring S=%5u D=%u warps=%2u (%3zu KB/SM) : copy %7.1f GB/s   +dp4a %7.1f GB/s\n", c.S, c.D, c.W,
                size_t(c.W) * c.D * c.S / 1024, bytes / m0 / 1e6, bytes / m1 / 1e6);
     }
+    // per-SM fill rate when only some SMs stream (8 warps x 2 x 8 KB ring)
+    for (int g : {16, 32, 64, 96, 148}) {
+        const uint32_t S = 8192, D = 2, W = 8;
+        size_t smem = size_t(W) * D * S + W * D * 8 + 6144;
+        CK(cudaFuncSetAttribute(ring_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        const size_t part = bytes / 148 * g;  // same bytes per CTA as the full-grid run
+        float ms = time_it([&] { ring_kernel<false><<<g, W * 32, smem>>>(buf, part, S, D, sink); });
+        printf("ring %3d CTAs: %7.1f GB/s total, %6.1f GB/s per SM\n", g, part / ms / 1e6, part / ms / 1e6 / g);
+    }
     {
         int iters = 1 << 16;
         float ms = time_it([&] { idp_kernel<<<sms * 4, 256>>>(iters, sink); });

@@ -17,10 +17,10 @@ import re
 import subprocess
 import tempfile
 
-KERNEL = "_ZN4dimg3dev24decode_persistent_kernelENS0_6PkArgsE"
+KERNEL = "_ZN4dimg3dev24decode_persistent_kernelENS0_6PkArgsE"  # --kernel overrides (mangled name)
 
 
-def sass_lines(lib):
+def sass_lines(lib, kernel=KERNEL):
     with tempfile.TemporaryDirectory() as d:
         subprocess.run(["cuobjdump", "-xelf", "engine.sm_100a.cubin", os.path.abspath(lib)], cwd=d,
                        check=True, capture_output=True)
@@ -31,7 +31,7 @@ def sass_lines(lib):
     cur = ("?", 0)
     for ln in out.splitlines():
         if ln.startswith(".text."):
-            inside = ln.startswith(".text." + KERNEL + ":")
+            inside = ln.startswith(".text." + kernel + ":")
             continue
         if not inside:
             continue
@@ -52,6 +52,8 @@ def main():
     ap.add_argument("--from", dest="lo", type=int, default=0)
     ap.add_argument("--to", dest="hi", type=int, default=10 ** 9)
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--kernel", default=KERNEL, help="mangled kernel name (nvdisasm section)")
+    ap.add_argument("--file", default="persistent.cuh", help="source file the line range refers to")
     a = ap.parse_args()
     txt = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--print-source", "sass"],
                          check=True, capture_output=True, text=True).stdout
@@ -60,7 +62,7 @@ def main():
     ia, iss = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)")
     data = rows[2:]
     base = int(data[0][ia], 16)
-    m = sass_lines(a.lib)
+    m = sass_lines(a.lib, a.kernel)
     reasons = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
     per = collections.Counter()
     why = collections.Counter()
@@ -69,9 +71,9 @@ def main():
         s = int(r[iss] or 0)
         total += s
         f, line = m.get(int(r[ia], 16) - base, ("?", 0))
-        if f == "persistent.cuh" and not (a.lo <= line <= a.hi):
+        if f == a.file and not (a.lo <= line <= a.hi):
             continue
-        if f != "persistent.cuh" and (a.lo > 0 or a.hi < 10 ** 9):
+        if f != a.file and (a.lo > 0 or a.hi < 10 ** 9):
             continue
         per[(f, line)] += s
         for i in reasons:
