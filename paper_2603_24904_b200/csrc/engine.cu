@@ -244,7 +244,10 @@ struct DevMat {
     CUtensorMap tmap;          // its TMA map (128 x 128-byte boxes, 128B swizzle)
 };
 
+struct BatchCache;  // batched-generation buffers + captured step graph (see below)
+
 struct dimg_model {
+    std::shared_ptr<BatchCache> batch;  // declared first: released after the weights' users
     int device;
     DevCtx* ctx;
     dimg_config cfg;
@@ -790,6 +793,18 @@ struct BatchRun {
 
 bool batch_shape_ok(const dimg_model& m) { return m.dh % 4 == 0 && m.dh / 2 <= 1024; }
 
+}  // namespace
+
+struct BatchCache {
+    BatchRun r;
+    cudaGraphExec_t ge = nullptr;  // the captured decode step (depends only on r's buffers and B)
+    ~BatchCache() {
+        if (ge) cudaGraphExecDestroy(ge);
+    }
+};
+
+namespace {
+
 void batch_alloc(BatchRun& r, dimg_model* m, uint32_t B, uint32_t ctx, uint32_t nmax, uint32_t max_new) {
     r.m = m;
     r.B = B;
@@ -912,8 +927,20 @@ bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<
         n_prompt_pos += uint32_t(p.size()) - 1;
     }
     if (bd_attn_smem(m->dh, ctx) + 8 > size_t(m->ctx->smem_optin)) return false;
-    BatchRun r;
-    batch_alloc(r, m, B, ctx, std::max(n_prompt_pos, B), max_new);
+    // buffers (and the captured step graph) are kept on the model and reused
+    // while the batch fits them
+    const uint32_t nmax = std::max(n_prompt_pos, B);
+    if (!m->batch || m->batch->r.B != B || m->batch->r.ctx < ctx || m->batch->r.nmax < nmax ||
+        m->batch->r.max_new < std::max(1u, max_new)) {
+        m->batch.reset();
+        auto c = std::make_shared<BatchCache>();
+        batch_alloc(c->r, m, B, std::max(ctx, 64u), nmax, std::max(max_new, 128u));
+        m->batch = c;
+    }
+    BatchCache& c = *m->batch;
+    BatchRun& r = c.r;
+    CK(cudaMemsetAsync(r.step, 0, 4, r.st));
+    CK(cudaMemsetAsync(r.wide, 0, 4, r.st));
     // prompt phase: all positions but each prompt's last, one forward pass
     if (n_prompt_pos) {
         std::vector<uint32_t> tok, seq, pos;
@@ -926,7 +953,6 @@ bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<
         CK(cudaMemcpyAsync(r.tok, tok.data(), tok.size() * 4, cudaMemcpyHostToDevice, r.st));
         CK(cudaMemcpyAsync(r.seq, seq.data(), seq.size() * 4, cudaMemcpyHostToDevice, r.st));
         CK(cudaMemcpyAsync(r.pos, pos.data(), pos.size() * 4, cudaMemcpyHostToDevice, r.st));
-        CK(cudaStreamSynchronize(r.st));
         batch_step(r, n_prompt_pos, false);
     }
     // decode: one token per sequence per step, the step captured once as a CUDA graph
@@ -943,21 +969,22 @@ bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<
         CK(cudaStreamSynchronize(r.st));
     }
     if (max_new > 0) {
-        cudaGraph_t g = nullptr;
-        cudaGraphExec_t ge = nullptr;
-        CK(cudaStreamBeginCapture(r.st, cudaStreamCaptureModeThreadLocal));
-        batch_step(r, B, true);
-        CK(cudaStreamEndCapture(r.st, &g));
-        CK(cudaGraphInstantiate(&ge, g, 0));
-        for (uint32_t s = 0; s < max_new; ++s) CK(cudaGraphLaunch(ge, r.st));
-        CK(cudaStreamSynchronize(r.st));
-        cudaGraphExecDestroy(ge);
-        cudaGraphDestroy(g);
+        if (!c.ge) {
+            cudaGraph_t g = nullptr;
+            CK(cudaStreamBeginCapture(r.st, cudaStreamCaptureModeThreadLocal));
+            batch_step(r, B, true);
+            CK(cudaStreamEndCapture(r.st, &g));
+            CK(cudaGraphInstantiate(&c.ge, g, 0));
+            cudaGraphDestroy(g);
+        }
+        for (uint32_t s = 0; s < max_new; ++s) CK(cudaGraphLaunch(c.ge, r.st));
         if (steps_graph) *steps_graph += max_new;
     }
     uint32_t wide = 0;
     CK(cudaMemcpyAsync(&wide, r.wide, 4, cudaMemcpyDeviceToHost, r.st));
-    CK(cudaMemcpyAsync(tokens_out, r.out, size_t(B) * max_new * 4, cudaMemcpyDeviceToHost, r.st));
+    if (max_new > 0)
+        CK(cudaMemcpy2DAsync(tokens_out, size_t(max_new) * 4, r.out, size_t(r.max_new) * 4, size_t(max_new) * 4, B,
+                             cudaMemcpyDeviceToHost, r.st));
     CK(cudaStreamSynchronize(r.st));
     return wide == 0;
 }

@@ -62,3 +62,34 @@ def test_7b_c5_sequences(P, golden_7b, model7b):
         res = s.generate_greedy(prompt, g["max_new"])
         assert res.token_ids == g["tokens"], k
         assert res.output_hash.hex() == g["output_hash"], k
+
+
+def test_7b_c5_batch_on_tensor_cores(P, golden_7b, model7b):
+    """C5: the sequences generated together (tensor-core batch path), each
+    stream and hash identical to the oracle's single-sequence goldens."""
+    names = sorted((k for k in golden_7b if k.startswith("c5_")), key=lambda k: int(k[3:]))[:8]
+    if not names:
+        pytest.skip("c5 goldens not generated")
+    gs = [golden_7b[k] for k in names]
+    prompts = [P.prompt_from_seed(g["prompt_seed"], g["config"][4], g["P"]) for g in gs]
+    res, path = P.generate_greedy_batch(model7b, prompts, gs[0]["max_new"])
+    assert path == "tensor_cores"
+    for g, r in zip(gs, res):
+        assert r.token_ids == g["tokens"]
+        assert r.output_hash.hex() == g["output_hash"]
+
+
+def test_7b_c3_prefill_on_tensor_cores(P, golden_7b, model7b):
+    """C3: a 2048-token prompt prefilled on the tensor cores, then 8 greedy
+    tokens; tokens, hash and the kept logits equal the oracle's."""
+    g = golden_7b.get("c3")
+    if g is None:
+        pytest.skip("c3 golden not generated")
+    prompt = P.prompt_from_seed(g["prompt_seed"], g["config"][4], g["P"])
+    s = P.InferenceSession(model7b, keep_logits_cap=g["max_new"])
+    res = s.generate_greedy(prompt, g["max_new"], keep_logits=True)
+    assert s.stats()["tc_prefills"] == 1
+    assert res.token_ids == g["tokens"]
+    assert res.output_hash.hex() == g["output_hash"]
+    if g.get("logits_digest"):
+        assert _digest(P, res.logits) == g["logits_digest"]
