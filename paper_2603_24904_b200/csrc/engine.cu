@@ -400,6 +400,7 @@ struct dimg_session {
     cudaStream_t stream = nullptr;
     DevBuf mem;
     int64_t *x, *qkv, *att, *h, *kc, *vc, *scores, *logits;
+    int32_t* x32;  // [Kd] the residual stream as int32 (written by the residual epilogues)
     ArgPart* parts;
     uint32_t* tokens;  // [max_ctx + 1]
     Ctl* ctl;
@@ -418,7 +419,8 @@ struct dimg_session {
     uint32_t keep_cap = 0;
     uint32_t len = 0;  // host mirror of the cache length
     uint32_t n_prompt = 0, max_new = 0;
-    uint32_t grid = 0, planes_bytes = 0;
+    uint32_t grid = 0, planes_bytes = 0, ring_depth = 2, wide_stride = 0;
+    uint32_t* wide_planes = nullptr;
     size_t smem = 0;
     ~dimg_session() {
         if (stream) cudaStreamDestroy(stream);
@@ -473,6 +475,7 @@ std::vector<PkStage> step_program(const dimg_session& s) {
         PkStage qkv = gemv_stage(lw.qkv, l == 0 ? MODE_EMBED : MODE_NORM, EPI_STORE, s.x, lw.attn_norm,
                                  s.qkv, lw.attn_unit);
         qkv.ssq_in = ssq_prev;
+        qkv.x32_in = l > 0 ? s.x32 : nullptr;
         if (l == 0) qkv.ssq_clear = s.ssq + 2 * m.L - 1;  // consumed by the previous step's head
         qkv.ytag = s.qkv_x;     // q/k/v reach attention as tagged words:
         qkv.no_barrier = (barrier_skip_mask() & 1) ? 1 : 0;  // no grid barrier between the two stages
@@ -486,21 +489,25 @@ std::vector<PkStage> step_program(const dimg_session& s) {
         PkStage wo = gemv_stage(lw.wo, MODE_PLAIN, EPI_RESID, s.att, nullptr, s.x);
         wo.in_words = s.words_att;
         wo.ssq_out = ssq_wo;
+        wo.x32_out = s.x32;
         wo.ssq_clear = ssq_prev;  // every CTA's qkv prologue read it before the attention barrier
         p.push_back(wo);
         PkStage gu = gemv_stage(lw.gu, MODE_NORM, EPI_SILU, s.x, lw.ffn_norm, s.h, lw.ffn_unit);
         gu.out_words = s.words_h;
         gu.no_barrier = (barrier_skip_mask() & 4) ? 1 : 0;  // DOWN polls the words
         gu.ssq_in = ssq_wo;
+        gu.x32_in = s.x32;
         p.push_back(gu);
         PkStage dn = gemv_stage(lw.down, MODE_PLAIN, EPI_RESID, s.h, nullptr, s.x);
         dn.in_words = s.words_h;
         dn.ssq_out = ssq_dn;
+        dn.x32_out = s.x32;
         dn.ssq_clear = ssq_wo;
         p.push_back(dn);
     }
     PkStage head = gemv_stage(m.head, MODE_NORM, EPI_ARGMAX, s.x, m.final_norm, s.logits, m.final_unit);
     head.ssq_in = s.ssq + 2 * m.L - 1;
+    head.x32_in = s.x32;
     p.push_back(head);
     return p;
 }
@@ -514,6 +521,9 @@ PkArgs pk_args(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     a.n_steps = n_steps;
     a.n_prefill = n_prefill;
     a.planes_bytes = s.planes_bytes;
+    a.ring_depth = s.ring_depth;
+    a.wide_planes = s.wide_planes;
+    a.wide_stride = s.wide_stride;
     a.ctl = s.ctl;
     a.bar = s.bar;
     a.embd = m.embd;
@@ -1110,6 +1120,8 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
         const size_t ctx = m->cfg.max_ctx;
         s->x = s->mem.alloc<int64_t>(m->D);
+        s->x32 = s->mem.alloc<int32_t>(m->Kd);
+        CK(cudaMemsetAsync(s->x32, 0, size_t(m->Kd) * 4, s->stream));
         s->qkv = s->mem.alloc<int64_t>(3 * size_t(m->D));
         s->att = s->mem.alloc<int64_t>(m->D);
         s->h = s->mem.alloc<int64_t>(m->F);
@@ -1139,20 +1151,31 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         CK(cudaMemsetAsync(s->words_h, 0, size_t(4) * m->Kf, s->stream));
         s->ssq = s->mem.alloc<unsigned long long>(2 * size_t(m->L));
         s->host_stages = step_program(*s);
-        // shared staging: rmsnorm = vector + gains + up to 8 planes; plain =
-        // up to 8 planes; attention = head scratch + score strip
+        // shared staging: rmsnorm = the int64 vector + 3 planes (11 Kp bytes);
+        // plain = 3 planes; attention = head scratch + score strip. 8-limb
+        // planes (out-of-range inputs) live in a global per-CTA scratch. The
+        // rest of shared memory is the weight ring: as many 4 KB slots per
+        // warp as fit (up to PK_MAX_DEPTH).
         size_t need = attn_scratch_bytes(m->dh, m->cfg.max_ctx);
+        uint32_t kp_max = 0;
         for (const auto& st : s->host_stages) {
             if (st.kind != SK_GEMV) continue;
-            // plain: up to 8 byte planes; rmsnorm: the int64 vector + up to 8 planes
-            size_t b = size_t(st.mode == MODE_PLAIN ? 8 : 16) * st.Kp;
+            size_t b = size_t(st.mode == MODE_PLAIN ? 3 : 11) * st.Kp;
             need = std::max(need, b);
+            kp_max = std::max(kp_max, st.Kp);
         }
         s->planes_bytes = uint32_t((need + 127) & ~size_t(127));
-        s->smem = size_t(PK_WARPS) * PK_DEPTH * PK_SLOT + s->planes_bytes + PK_WARPS * PK_DEPTH * 8;
-        if (s->smem > size_t(m->ctx->smem_optin))
-            fail(DIMG_EINVAL, "session: shapes need " + std::to_string(s->smem) +
-                                  " B of shared memory per CTA (d_ffn or vocab too large for this build)");
+        const size_t bars = size_t(PK_WARPS) * PK_MAX_DEPTH * 8;
+        const size_t avail = size_t(m->ctx->smem_optin) > s->planes_bytes + bars
+                                 ? size_t(m->ctx->smem_optin) - s->planes_bytes - bars
+                                 : 0;
+        s->ring_depth = uint32_t(std::min<size_t>(PK_MAX_DEPTH, avail / (size_t(PK_WARPS) * PK_SLOT)));
+        if (s->ring_depth < 2)
+            fail(DIMG_EINVAL, "session: shapes need " + std::to_string(s->planes_bytes) +
+                                  " B of shared staging per CTA (d_ffn or max_ctx too large for this build)");
+        s->smem = size_t(PK_WARPS) * s->ring_depth * PK_SLOT + s->planes_bytes + size_t(PK_WARPS) * s->ring_depth * 8;
+        s->wide_stride = 2 * kp_max;  // 8 planes x Kp/4 words
+        s->wide_planes = s->mem.alloc<uint32_t>(size_t(s->grid) * s->wide_stride);
         int per_sm = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_persistent_kernel, PK_THREADS,
                                                          s->smem));
@@ -1370,6 +1393,8 @@ dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, flo
             st.ytag = nullptr;  // no attention stage follows
             st.no_barrier = 0;
             st.in_words = nullptr;  // plain inputs: planes straight from the int64 vector
+            st.x32_in = nullptr;
+            st.x32_out = nullptr;
             st.out_words = nullptr;
             prog.push_back(st);
         }

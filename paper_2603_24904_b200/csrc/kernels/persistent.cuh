@@ -38,8 +38,8 @@ namespace dimg::dev {
 
 constexpr int PK_THREADS = 256;
 constexpr int PK_WARPS = PK_THREADS / 32;
-constexpr int PK_DEPTH = 2;             // chunks in flight per warp
-constexpr int PK_SEG = 2048;            // K-segment width (bytes)
+constexpr int PK_MAX_DEPTH = 6;         // chunks in flight per warp (runtime depth <= this)
+constexpr int PK_SEG = 1536;            // K-segment width (bytes)
 constexpr int PK_ROWS = 4;              // rows per group
 constexpr int PK_SCALES = PK_ROWS * 8;             // the group's 4 int64 row scales
 constexpr int PK_SLOT = PK_ROWS * PK_SEG + PK_SCALES;  // chunk bytes incl. trailing scales
@@ -60,6 +60,8 @@ struct PkStage {
     const uint32_t* in_words; // MODE_PLAIN: the input as tagged limb words (nullptr: build from x)
     uint32_t* out_words;      // EPI_SILU / attention: publish y as tagged limb words
     uint32_t no_barrier;      // 1: the next stage consumes tagged words, no grid barrier after this one
+    int32_t* x32_out;         // EPI_RESID: the clamped x also as int32 (|x| <= 2^24)
+    const int32_t* x32_in;    // MODE_NORM after a RESID stage: read that copy (16 KB, not 32)
     unsigned long long* ytag; // EPI_STORE: also publish y as tagged word pairs (attention inputs)
     unsigned long long* ssq_out;  // EPI_RESID: sum of the new x^2 (exact: |x| <= 2^24 after the clamp)
     const unsigned long long* ssq_in;  // MODE_NORM after a RESID stage: that sum (nullptr = compute it)
@@ -71,7 +73,10 @@ struct PkArgs {
     uint32_t n_layer_stages;  // 5L
     uint32_t n_steps;         // forward steps in this launch
     uint32_t n_prefill;       // the first n_prefill steps skip the head
-    uint32_t planes_bytes;    // shared staging area (vector, gains, planes, attention)
+    uint32_t planes_bytes;    // shared staging area (vector, 3 limb planes, attention)
+    uint32_t ring_depth;      // weight-ring slots per warp (2 .. PK_MAX_DEPTH)
+    uint32_t* wide_planes;    // [grid][wide_stride] words: 8-limb planes of out-of-range inputs
+    uint32_t wide_stride;
     Ctl* ctl;
     unsigned int* bar;        // grid barrier counter (zeroed before launch)
     // embedding / head
@@ -328,21 +333,25 @@ __device__ __forceinline__ void fetch_issue(const Fetch& f, uint8_t* slot, uint6
 struct Pipe {
     uint8_t* slots;     // this warp's ring
     uint64_t* bars;
-    uint32_t consumed;  // chunks consumed so far
+    uint32_t slot;      // slot of the next chunk to consume
+    uint32_t phase;     // its mbarrier parity
+    uint32_t depth;     // slots in the ring (runtime: what shared memory allows)
     Fetch f;            // next chunk to load into the ring
 };
 
 // Waits for the next chunk of this warp; returns its slot.
 __device__ __forceinline__ const uint8_t* pipe_wait(Pipe& p) {
-    const uint32_t sl = p.consumed % PK_DEPTH;
-    mbar_wait(&p.bars[sl], (p.consumed / PK_DEPTH) & 1);
-    return p.slots + sl * PK_SLOT;
+    mbar_wait(&p.bars[p.slot], p.phase);
+    return p.slots + p.slot * PK_SLOT;
 }
 
 // Releases the chunk just consumed and refills its slot with the next one.
 __device__ __forceinline__ void pipe_release(const Sched& sc, Pipe& p) {
-    const uint32_t sl = p.consumed % PK_DEPTH;
-    ++p.consumed;
+    const uint32_t sl = p.slot;
+    if (++p.slot == p.depth) {
+        p.slot = 0;
+        p.phase ^= 1;
+    }
     __syncwarp();
     if (!p.f.done) {
         if ((threadIdx.x & 31) == 0) {
@@ -367,8 +376,10 @@ __device__ __forceinline__ void pipe_release(const Sched& sc, Pipe& p) {
 // probes): planes straight from x.
 constexpr int PLAIN_WIDE = 9;
 
-__device__ __noinline__ int planes_from_x(uint32_t K, uint32_t Kp, const int64_t* x, uint32_t* planes, Ctl* ctl,
-                                          bool wide) {
+// 8-limb planes go to the CTA's global scratch (wplanes): shared memory only
+// holds the usual 3.
+__device__ __noinline__ int planes_from_x(uint32_t K, uint32_t Kp, const int64_t* x, uint32_t* splanes,
+                                          uint32_t* wplanes, Ctl* ctl, bool wide) {
     const uint32_t Kw = Kp / 4;
     if (!wide) {
         int fits = 1;
@@ -379,6 +390,7 @@ __device__ __noinline__ int planes_from_x(uint32_t K, uint32_t Kp, const int64_t
         wide = !__syncthreads_and(fits);
     }
     const int L = wide ? 8 : 3;
+    uint32_t* planes = wide ? wplanes : splanes;
 #pragma unroll 1
     for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
         uint64_t v[4];
@@ -403,9 +415,9 @@ __device__ __forceinline__ bool words_ready(uint4 q, uint32_t j, uint32_t K, uin
 }
 
 __device__ __noinline__ int prologue_plain(uint32_t K, uint32_t Kp, const int64_t* x, const uint32_t* words,
-                                           uint32_t tag7, uint32_t* planes, Ctl* ctl) {
+                                           uint32_t tag7, uint32_t* planes, uint32_t* wplanes, Ctl* ctl) {
     const uint32_t Kw = Kp / 4;
-    if (!words) return planes_from_x(K, Kp, x, planes, ctl, false);
+    if (!words) return planes_from_x(K, Kp, x, planes, wplanes, ctl, false);
     constexpr int B = 8;  // 16-byte loads in flight per thread
     int wide = 0, ok = 1;
 #pragma unroll 1
@@ -455,21 +467,23 @@ __device__ __noinline__ int prologue_plain(uint32_t K, uint32_t Kp, const int64_
 // erow != nullptr selects the embedding (engine.cpp:10-19).
 __device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_unit, const int64_t* x,
                                           const int64_t* gamma, const int8_t* erow, int64_t es,
-                                          int64_t* x_resid, int64_t* xb, uint32_t* planes, u128* red,
-                                          const int64_t* seeds, Ctl* ctl, unsigned long long* tr,
-                                          const unsigned long long* ssq_in) {
+                                          int64_t* x_resid, int64_t* xb, uint32_t* planes, uint32_t* wplanes,
+                                          u128* red, const int64_t* seeds, Ctl* ctl, unsigned long long* tr,
+                                          const unsigned long long* ssq_in, const int32_t* x32) {
     const uint32_t Kw = Kp / 4;
     __shared__ int64_t s_r;
-    if (ssq_in && gamma_unit) {
+    if (ssq_in && gamma_unit && x32) {
         // The producer (a residual stage) already summed the squares of the
-        // clamped vector: thread 0 computes r while the copy is in flight,
-        // and every |x| <= 2^24, r <= 2^24 -> 32-bit products throughout.
+        // clamped vector and wrote it as int32 too (|x| <= 2^24): thread 0
+        // computes r while the 4-byte copy is in flight; r <= 2^24, so the
+        // products are 32 x 32 bits throughout.
         if (threadIdx.x == 0) {
             const uint64_t ss = uint64_t(ld_cg64(reinterpret_cast<const int64_t*>(ssq_in)));
             const int64_t ms = int64_t((ss / K) >> 16);
             s_r = inv_sqrt_q16(ms + 1, seeds);  // ms >= 0: ms + 1 > 0
         }
-        copy_g2s(xb, x, K * 8);
+        int32_t* xs32 = reinterpret_cast<int32_t*>(xb);
+        copy_g2s(xs32, x32, Kp * 4);
         __syncthreads();
         if (tr) tr[4] = tr[5] = clock64();
         const int64_t r_inv = s_r;
@@ -477,16 +491,14 @@ __device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_un
         int fits = 1;
 #pragma unroll 4
         for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
-            const int4 e01 = *reinterpret_cast<const int4*>(xb + 4 * w);
-            const int4 e23 = *reinterpret_cast<const int4*>(xb + 4 * w + 2);
-            const int32_t xs[4] = {e01.x, e01.z, e23.x, e23.z};  // low words (|x| < 2^31)
+            const int4 e4 = *reinterpret_cast<const int4*>(xs32 + 4 * w);
+            const int32_t xs[4] = {e4.x, e4.y, e4.z, e4.w};
             uint32_t lo[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int64_t v = 4 * w + e < K ? (int64_t(xs[e]) * int32_t(r_inv)) >> 16 : 0;
                 fits &= uint64_t(v + (int64_t(1) << 23)) < (uint64_t(1) << 24);
                 lo[e] = uint32_t(v);
-                xb[4 * w + e] = v;
             }
             planes[w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0040), __byte_perm(lo[2], lo[3], 0x0040), 0x5410);
             planes[Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0051), __byte_perm(lo[2], lo[3], 0x0051), 0x5410);
@@ -495,14 +507,19 @@ __device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_un
         fits = __syncthreads_and(fits);
         if (tr) tr[7] = clock64();
         if (fits) return 3;
-        // wide (needs > 3 limbs): 8 planes from the normalised vector
+        // wide (needs > 3 limbs): 8 planes of the normalised vector into the
+        // global scratch, recomputed from the global int32 copy (rare)
 #pragma unroll 1
         for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x)
 #pragma unroll 1
-            for (int k = 3; k < 8; ++k) {
+            for (int k = 0; k < 8; ++k) {
                 uint32_t word = 0;
-                for (int e = 0; e < 4; ++e) word |= uint32_t((uint64_t(xb[4 * w + e]) >> (8 * k)) & 0xFF) << (8 * e);
-                planes[k * Kw + w] = word;
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t j = 4 * w + e;
+                    const int64_t v = j < K ? (int64_t(__ldcg(x32 + j)) * int32_t(r_inv)) >> 16 : 0;
+                    word |= uint32_t((uint64_t(v) >> (8 * k)) & 0xFF) << (8 * e);
+                }
+                wplanes[k * Kw + w] = word;
             }
         if (threadIdx.x == 0) atomicAdd(&ctl->stats[0], 1ull);
         __syncthreads();
@@ -611,10 +628,10 @@ __device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_un
 #pragma unroll 1
     for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x)
 #pragma unroll 1
-        for (int k = 3; k < 8; ++k) {
+        for (int k = 0; k < 8; ++k) {
             uint32_t word = 0;
             for (int e = 0; e < 4; ++e) word |= uint32_t((uint64_t(xb[4 * w + e]) >> (8 * k)) & 0xFF) << (8 * e);
-            planes[k * Kw + w] = word;
+            wplanes[k * Kw + w] = word;
         }
     if (threadIdx.x == 0) atomicAdd(&ctl->stats[0], 1ull);
     __syncthreads();
@@ -697,6 +714,7 @@ struct GemvRT {
     int64_t* lrow;            // EPI_ARGMAX: this step's logits row
     const int64_t* lut;
     unsigned long long* ssq;  // EPI_RESID: sum-of-squares accumulator
+    int32_t* x32;             // EPI_RESID: int32 copy of the clamped x
     unsigned long long* ytag; // EPI_STORE: tagged word pairs of y
     uint64_t tg;              // their tag << 32
 };
@@ -740,6 +758,7 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
             } else if (g_.epi == EPI_RESID) {
                 const int64_t x = add_clamp(resid, val);
                 g_.y[row] = x;
+                if (g_.x32) g_.x32[row] = int32_t(x);
                 sq = uint64_t(x * x);  // |x| <= 2^24: x^2 < 2^49, 8192 rows < 2^62
             } else {  // EPI_ARGMAX
                 g_.lrow[row] = val;
@@ -1216,9 +1235,11 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
 
 __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const PkArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t depth = a.ring_depth;
     uint8_t* slots = smem;                                                // [warps][depth][SLOT]
-    uint8_t* stage_mem = smem + PK_WARPS * PK_DEPTH * PK_SLOT;            // planes_bytes
+    uint8_t* stage_mem = smem + size_t(PK_WARPS) * depth * PK_SLOT;       // planes_bytes
     uint64_t* bars = reinterpret_cast<uint64_t*>(stage_mem + a.planes_bytes);  // [warps][depth]
+    uint32_t* wide_planes = a.wide_planes + size_t(blockIdx.x) * a.wide_stride;  // 8-limb planes (rare)
     __shared__ u128 red[32];
     __shared__ int64_t s_bv[PK_WARPS];
     __shared__ uint32_t s_bi[PK_WARPS];
@@ -1229,7 +1250,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Sched sc{a.stages, a.n_layer_stages, a.n_steps, a.n_prefill};
     Ctl* const ctl = a.ctl;
-    if (threadIdx.x < PK_WARPS * PK_DEPTH) mbar_init(&bars[threadIdx.x], 1);
+    if (threadIdx.x < PK_WARPS * depth) mbar_init(&bars[threadIdx.x], 1);
     for (int i = threadIdx.x; i < 257; i += PK_THREADS) s_lut[i] = a.exp_lut[i];
     if (threadIdx.x < 64) s_seeds[threadIdx.x] = a.seeds[threadIdx.x];
     constexpr int kStWords = sizeof(PkStage) / 4;
@@ -1241,9 +1262,11 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
 
     // prime this warp's pipeline
     Pipe p;
-    p.slots = slots + size_t(warp) * PK_DEPTH * PK_SLOT;
-    p.bars = bars + warp * PK_DEPTH;
-    p.consumed = 0;
+    p.slots = slots + size_t(warp) * depth * PK_SLOT;
+    p.bars = bars + warp * depth;
+    p.slot = 0;
+    p.phase = 0;
+    p.depth = depth;
     p.f.step = 0;
     p.f.stage = 0;
     p.f.done = sc.n_steps == 0;
@@ -1251,7 +1274,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
         fetch_load(sc, p.f);
         fetch_settle(sc, p.f);
     }
-    for (uint32_t d = 0; d < PK_DEPTH && !p.f.done; ++d) {
+    for (uint32_t d = 0; d < depth && !p.f.done; ++d) {
         if (lane == 0) fetch_issue(p.f, p.slots + d * PK_SLOT, &p.bars[d]);
         fetch_advance(sc, p.f);
     }
@@ -1292,11 +1315,12 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 int L;
                 if (st.mode == MODE_PLAIN) {
                     planes = reinterpret_cast<uint32_t*>(stage_mem);
-                    L = prologue_plain(st.K, st.Kp, st.x, st.in_words, tag7_of(a.tag_base + attn_epoch), planes, ctl);
+                    L = prologue_plain(st.K, st.Kp, st.x, st.in_words, tag7_of(a.tag_base + attn_epoch), planes,
+                                       wide_planes, ctl);
                     if (L < 0) return;
                     if (L == PLAIN_WIDE) {  // grid-uniform: the int64 vector is visible after the barrier
                         if (!grid_sync(a.bar, ctl, nbar++)) return;
-                        L = planes_from_x(st.K, st.Kp, st.x, planes, ctl, true);
+                        L = planes_from_x(st.K, st.Kp, st.x, planes, wide_planes, ctl, true);
                     }
                 } else {
                     // Stages are not always separated by grid barriers: a CTA
@@ -1313,10 +1337,11 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                         L = prologue_norm(st.K, st.Kp, st.gamma_unit != 0, st.x, st.gamma,
                                           embed ? a.embd + size_t(token) * st.K : nullptr,
                                           embed ? a.embd_scales[token] : 0,
-                                          embed && glo == 0 ? a.x_resid : nullptr, xb, planes, red,
-                                          s_seeds, ctl, tr, st.ssq_in);
+                                          embed && glo == 0 ? a.x_resid : nullptr, xb, planes, wide_planes,
+                                          red, s_seeds, ctl, tr, st.ssq_in, st.x32_in);
                     }
                 }
+                if (L == 8) planes = wide_planes;  // out-of-range inputs: 8 planes in the global scratch
                 // the sum the previous stages' prologues consumed: every reader
                 // is done once this stage's inputs are complete
                 if (st.ssq_clear && blockIdx.x == 0 && threadIdx.x == 0) *st.ssq_clear = 0;
@@ -1327,6 +1352,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 g_.out_words = st.out_words; g_.lut = s_lut;
                 g_.lrow = nullptr;
                 g_.ssq = st.ssq_out;
+                g_.x32 = st.x32_out;
                 g_.ytag = st.ytag;
                 g_.tg = uint64_t(a.tag_base + attn_epoch + 1) << 32;  // the coming attention stage's tag
                 if (st.epi == EPI_ARGMAX) {
