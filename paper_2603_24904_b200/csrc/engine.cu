@@ -407,6 +407,8 @@ struct dimg_session {
     unsigned int* bar;
     unsigned long long* xg;  // [H][max_ctx][2] tagged score exchange words
     unsigned long long* qkv_x;  // [3D][2] tagged q/k/v words
+    uint32_t* xwords;           // [2][Kd] tagged residual-stream words (after WO / after down)
+    unsigned long long* parts_w;  // [2][grid][4] tagged lm_head partials
     uint32_t attn_tag = 0;   // attention stages tagged so far (xg tags)
     int32_t *kc32, *vc32;  // int32 mirror of the KV cache
     uint32_t* kvwide;      // [L][H] mirror unusable (sticky per sequence)
@@ -459,55 +461,63 @@ PkStage gemv_stage(const DevMat& d, uint32_t mode, uint32_t epi, const int64_t* 
 // experiments. With the barrier kept, the consumer still polls the words.
 uint32_t barrier_skip_mask() {
     const char* v = std::getenv("DIMG_BARRIER_SKIP");
-    return v ? uint32_t(std::strtoul(v, nullptr, 0)) : 7u;
+    return v ? uint32_t(std::strtoul(v, nullptr, 0)) : 15u;
 }
 
 // The stage program of one forward step (proj/src/engine.cpp:85-101).
 std::vector<PkStage> step_program(const dimg_session& s) {
+    // Hand-offs between stages are tagged words, so a decode step has no grid
+    // barrier at all: q/k/v -> attention, attention -> WO and gate/up -> down
+    // as limb words; the residual stream after WO (buffer A) and after down
+    // (buffer B) as x words that the next rmsnorm polls (it sums x^2 itself)
+    // and the next residual reads; the lm_head partials as tagged entries.
+    // DIMG_BARRIER_SKIP (bit 0 qkv, 1 attention, 2 gate/up, 3 residuals+head)
+    // puts grid barriers back for experiments; the words are used either way.
     const dimg_model& m = *s.m;
+    const uint32_t skip = barrier_skip_mask();
     std::vector<PkStage> p;
+    uint32_t* xa = s.xwords;
+    uint32_t* xb = s.xwords + m.Kd;
     for (uint32_t l = 0; l < m.L; ++l) {
         const auto& lw = m.layers[l];
-        // sums of squares of x: after wo(l) -> gu(l); after down(l) -> qkv(l+1) / head
-        unsigned long long* ssq_wo = s.ssq + 2 * l;
-        unsigned long long* ssq_dn = s.ssq + 2 * l + 1;
-        unsigned long long* ssq_prev = l > 0 ? s.ssq + 2 * l - 1 : nullptr;
         PkStage qkv = gemv_stage(lw.qkv, l == 0 ? MODE_EMBED : MODE_NORM, EPI_STORE, s.x, lw.attn_norm,
                                  s.qkv, lw.attn_unit);
-        qkv.ssq_in = ssq_prev;
-        qkv.x32_in = l > 0 ? s.x32 : nullptr;
-        if (l == 0) qkv.ssq_clear = s.ssq + 2 * m.L - 1;  // consumed by the previous step's head
-        qkv.ytag = s.qkv_x;     // q/k/v reach attention as tagged words:
-        qkv.no_barrier = (barrier_skip_mask() & 1) ? 1 : 0;  // no grid barrier between the two stages
+        if (l > 0) qkv.xw_in = xb;  // down(l-1), same layer tag (attention has not advanced it yet)
+        qkv.ytag = s.qkv_x;
+        qkv.no_barrier = (skip & 1) ? 1 : 0;
         p.push_back(qkv);
         PkStage at{};
         at.kind = SK_ATTN;
         at.layer = l;
         at.out_words = s.words_att;
-        at.no_barrier = (barrier_skip_mask() & 2) ? 1 : 0;  // WO polls the words
+        at.no_barrier = (skip & 2) ? 1 : 0;
         p.push_back(at);
         PkStage wo = gemv_stage(lw.wo, MODE_PLAIN, EPI_RESID, s.att, nullptr, s.x);
         wo.in_words = s.words_att;
-        wo.ssq_out = ssq_wo;
-        wo.x32_out = s.x32;
-        wo.ssq_clear = ssq_prev;  // every CTA's qkv prologue read it before the attention barrier
+        wo.xw_out = xa;
+        if (l > 0) {
+            wo.xw_in = xb;  // residual input: down(l-1)'s words, one layer tag back
+            wo.xw_lag = 1;
+        } else {
+            wo.resid_embed = 1;  // layer 0: the residual input is the token's embedding
+        }
+        wo.no_barrier = (skip & 8) ? 1 : 0;
         p.push_back(wo);
         PkStage gu = gemv_stage(lw.gu, MODE_NORM, EPI_SILU, s.x, lw.ffn_norm, s.h, lw.ffn_unit);
+        gu.xw_in = xa;
         gu.out_words = s.words_h;
-        gu.no_barrier = (barrier_skip_mask() & 4) ? 1 : 0;  // DOWN polls the words
-        gu.ssq_in = ssq_wo;
-        gu.x32_in = s.x32;
+        gu.no_barrier = (skip & 4) ? 1 : 0;
         p.push_back(gu);
         PkStage dn = gemv_stage(lw.down, MODE_PLAIN, EPI_RESID, s.h, nullptr, s.x);
         dn.in_words = s.words_h;
-        dn.ssq_out = ssq_dn;
-        dn.x32_out = s.x32;
-        dn.ssq_clear = ssq_wo;
+        dn.xw_in = xa;
+        dn.xw_out = xb;
+        dn.no_barrier = (skip & 8) ? 1 : 0;
         p.push_back(dn);
     }
     PkStage head = gemv_stage(m.head, MODE_NORM, EPI_ARGMAX, s.x, m.final_norm, s.logits, m.final_unit);
-    head.ssq_in = s.ssq + 2 * m.L - 1;
-    head.x32_in = s.x32;
+    head.xw_in = xb;
+    head.no_barrier = (skip & 8) ? 1 : 0;  // the partials go out as tagged words
     p.push_back(head);
     return p;
 }
@@ -560,6 +570,7 @@ PkArgs pk_args(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
         a.attn_nq_shift = log2_or(dpp / 4);
     }
     a.xg = s.xg;
+    a.parts_w = s.parts_w;
     a.qkv_x = s.qkv_x;
     a.kc32 = s.kc32;
     a.vc32 = s.vc32;
@@ -580,6 +591,7 @@ void launch_pk(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     const uint64_t n_attn = uint64_t(n_steps) * s.m->L;
     if (uint64_t(s.attn_tag) + n_attn + 2 > 0xFFFFFFFFull) {
         CK(cudaMemsetAsync(s.xg, 0, size_t(s.m->H) * s.m->cfg.max_ctx * 16, s.stream));
+        CK(cudaMemsetAsync(s.parts_w, 0, size_t(64) * s.grid, s.stream));
         s.attn_tag = 0;
     }
     a.tag_base = s.attn_tag;
@@ -1136,6 +1148,8 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         s->bar = s->mem.alloc<unsigned int>(64);
         s->xg = s->mem.alloc<unsigned long long>(size_t(m->H) * ctx * 2);
         s->qkv_x = s->mem.alloc<unsigned long long>(size_t(3) * m->D * 2);
+        s->xwords = s->mem.alloc<uint32_t>(size_t(2) * m->Kd);
+        CK(cudaMemsetAsync(s->xwords, 0, size_t(8) * m->Kd, s->stream));
         CK(cudaMemsetAsync(s->qkv_x, 0, size_t(3) * m->D * 16, s->stream));
         CK(cudaMemsetAsync(s->xg, 0, size_t(m->H) * ctx * 16, s->stream));
         s->kc32 = s->mem.alloc<int32_t>(kv);
@@ -1145,6 +1159,8 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         // one CTA per SM; shared memory = weight ring + limb planes + row accumulators
         s->grid = uint32_t(m->ctx->sm_count);
         s->parts = s->mem.alloc<ArgPart>(s->grid);
+        s->parts_w = s->mem.alloc<unsigned long long>(size_t(8) * s->grid);
+        CK(cudaMemsetAsync(s->parts_w, 0, size_t(64) * s->grid, s->stream));
         s->words_att = s->mem.alloc<uint32_t>(m->Kd);
         s->words_h = s->mem.alloc<uint32_t>(m->Kf);
         CK(cudaMemsetAsync(s->words_att, 0, size_t(4) * m->Kd, s->stream));
@@ -1395,6 +1411,9 @@ dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, flo
             st.in_words = nullptr;  // plain inputs: planes straight from the int64 vector
             st.x32_in = nullptr;
             st.x32_out = nullptr;
+            st.xw_in = nullptr;
+            st.xw_out = nullptr;
+            st.resid_embed = 0;
             st.out_words = nullptr;
             prog.push_back(st);
         }

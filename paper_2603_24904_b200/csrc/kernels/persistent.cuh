@@ -62,6 +62,12 @@ struct PkStage {
     uint32_t no_barrier;      // 1: the next stage consumes tagged words, no grid barrier after this one
     int32_t* x32_out;         // EPI_RESID: the clamped x also as int32 (|x| <= 2^24)
     const int32_t* x32_in;    // MODE_NORM after a RESID stage: read that copy (16 KB, not 32)
+    // Residual stream as tagged words (no grid barrier after a RESID stage):
+    // word = (x + 2^24) in bits 0-25 | 6-bit tag in 26-31; two alternating buffers.
+    uint32_t* xw_out;         // EPI_RESID: publish the new x here (tag of the current layer)
+    const uint32_t* xw_in;    // MODE_NORM: poll x from here; EPI_RESID: the residual input
+    uint32_t xw_lag;          // its tag is the current layer's minus xw_lag
+    uint32_t resid_embed;     // EPI_RESID on layer 0: the residual input is the token's embedding
     unsigned long long* ytag; // EPI_STORE: also publish y as tagged word pairs (attention inputs)
     unsigned long long* ssq_out;  // EPI_RESID: sum of the new x^2 (exact: |x| <= 2^24 after the clamp)
     const unsigned long long* ssq_in;  // MODE_NORM after a RESID stage: that sum (nullptr = compute it)
@@ -99,6 +105,7 @@ struct PkArgs {
     int32_t attn_np_shift;    // log2(attn_parts) if a power of two, else -1
     int32_t attn_nq_shift;    // log2(attn_dpp / 4) if a power of two, else -1
     unsigned long long* xg;   // [H][max_ctx][2] tagged score words exchanged by a head's parts
+    unsigned long long* parts_w;  // [2][grid][3] tagged lm_head partials (value lo/hi, index)
     unsigned long long* qkv_x;  // [3D][2] tagged q | k | v words (QKV stage -> attention)
     uint32_t tag_base;        // attention stage k of this launch tags its words tag_base + k (never 0)
     int32_t* kc32;            // int32 mirror of kc / vc (same layout), read while kvwide is clear
@@ -215,11 +222,42 @@ __device__ __forceinline__ uint4 ld_words4(const uint32_t* p) {
 }
 // 1 + (tag mod 127): consecutive uses of a word buffer always differ.
 __device__ __forceinline__ uint32_t tag7_of(uint32_t tag) { return 1u + tag % 127u; }
+// Residual-stream words: |x| <= 2^24 after the clamp, so x + 2^24 fits 26
+// bits; 6-bit tag 1 + (layer mod 63) above it.
+__device__ __forceinline__ uint32_t tag6_of(uint32_t tag) { return 1u + tag % 63u; }
+__device__ __forceinline__ uint32_t x_word(int64_t x, uint32_t tag6) {
+    return uint32_t(x + (int64_t(1) << 24)) | (tag6 << 26);
+}
+__device__ __forceinline__ int32_t x_of_word(uint32_t w) { return int32_t(w & 0x3FFFFFFu) - (1 << 24); }
+__device__ __forceinline__ uint32_t ld_word(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+// Spins until the word's tag (bits >= shift) equals `tag`; a 4 s timeout
+// (or another CTA's timeout) sets ctl->err bit 2 and returns the stale word:
+// the launch then fails instead of hanging the GPU.
+__device__ __noinline__ uint32_t poll_word(const uint32_t* p, uint32_t tag, int shift, Ctl* ctl) {
+    uint64_t g0 = 0;
+    for (uint32_t spins = 1;; ++spins) {
+        const uint32_t w = ld_word(p);
+        if ((w >> shift) == tag) return w;
+        if ((spins & 1023) == 0) {
+            const uint64_t now = globaltimer();
+            if (!g0) g0 = now;
+            if ((*((volatile uint32_t*)&ctl->err) & 4u) || now - g0 > 4000000000ull) {
+                atomicOr(&ctl->err, 4u);
+                return w;
+            }
+        }
+    }
 }
 
 // Block-wide global -> shared copy of `bytes` (multiple of 16), many 16-B
@@ -422,11 +460,32 @@ __device__ __noinline__ int prologue_plain(uint32_t K, uint32_t Kp, const int64_
     int wide = 0, ok = 1;
 #pragma unroll 1
     for (uint32_t w0 = threadIdx.x; w0 < Kw && ok; w0 += B * PK_THREADS) {
+        // the whole batch is reloaded until every word is published: one
+        // round trip per retry, not one per late word
         uint4 q[B];
+        uint64_t g0 = 0;
+        for (uint32_t spins = 1;; ++spins) {
+            bool ready = true;
 #pragma unroll
-        for (int b = 0; b < B; ++b) {
-            const uint32_t w = w0 + b * PK_THREADS;
-            q[b] = w < Kw && 4 * w < K ? ld_words4(words + 4 * w) : make_uint4(0, 0, 0, 0);
+            for (int b = 0; b < B; ++b) {
+                const uint32_t w = w0 + b * PK_THREADS;
+                q[b] = w < Kw && 4 * w < K ? ld_words4(words + 4 * w) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t w = w0 + b * PK_THREADS;
+                ready &= w >= Kw || 4 * w >= K || words_ready(q[b], 4 * w, K, tag7);
+            }
+            if (ready) break;
+            if ((spins & 255) == 0) {
+                const uint64_t now = globaltimer();
+                if (!g0) g0 = now;
+                if ((*((volatile uint32_t*)&ctl->err) & 4u) || now - g0 > 4000000000ull) {
+                    atomicOr(&ctl->err, 4u);
+                    ok = 0;
+                    break;
+                }
+            }
         }
 #pragma unroll
         for (int b = 0; b < B; ++b) {
@@ -434,20 +493,6 @@ __device__ __noinline__ int prologue_plain(uint32_t K, uint32_t Kp, const int64_
             if (w >= Kw) continue;
             uint4 v = q[b];
             if (4 * w < K) {
-                uint32_t spins = 0;
-                uint64_t g0 = 0;
-                while (!words_ready(v, 4 * w, K, tag7)) {  // not published yet: poll this one
-                    v = ld_words4(words + 4 * w);
-                    if ((++spins & 1023) == 0) {
-                        const uint64_t now = globaltimer();
-                        if (!g0) g0 = now;
-                        if ((*((volatile uint32_t*)&ctl->err) & 4u) || now - g0 > 4000000000ull) {
-                            atomicOr(&ctl->err, 4u);
-                            ok = 0;
-                            break;
-                        }
-                    }
-                }
                 if (4 * w + 1 >= K) v.y = 0;  // padding of the last word group
                 if (4 * w + 2 >= K) v.z = 0;
                 if (4 * w + 3 >= K) v.w = 0;
@@ -639,6 +684,120 @@ __device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_un
 }
 
 
+// rmsnorm of the residual stream published as tagged words by the previous
+// residual stage (no grid barrier in between): poll every word (16-byte
+// loads, 8 in flight per thread), keep x (|x| <= 2^24) as int32 in shared
+// memory and sum x^2 exactly (x^2 < 2^48, K < 2^12 -> u64) while doing so;
+// then r = inv_sqrt(ms + 1) and the normalised limb planes. Returns 3, 8
+// (planes in the global scratch) or -1 (a producer never published).
+__device__ __noinline__ int prologue_norm_words(uint32_t K, uint32_t Kp, bool gamma_unit, const int64_t* gamma,
+                                                const uint32_t* words, uint32_t tag6, int32_t* xs32, uint32_t* planes,
+                                                uint32_t* wplanes, const int64_t* seeds, Ctl* ctl,
+                                                unsigned long long* tr) {
+    __shared__ uint64_t s_ss[PK_WARPS];
+    __shared__ int64_t s_r2;
+    const uint32_t Kw = Kp / 4;
+    constexpr int B = 4;
+    uint64_t ss = 0;
+    int ok = 1;
+#pragma unroll 1
+    for (uint32_t w0 = threadIdx.x; w0 < Kw && ok; w0 += B * PK_THREADS) {
+        // the whole batch is reloaded until every word carries this layer's
+        // tag: one round trip per retry, not one per late word
+        uint4 q[B];
+        uint64_t g0 = 0;
+        for (uint32_t spins = 1;; ++spins) {
+            bool ready = true;
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t w = w0 + b * PK_THREADS;
+                q[b] = w < Kw && 4 * w < K ? ld_words4(words + 4 * w) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint32_t j = 4 * (w0 + b * PK_THREADS);
+                ready &= (j >= K || (q[b].x >> 26) == tag6) && (j + 1 >= K || (q[b].y >> 26) == tag6) &&
+                         (j + 2 >= K || (q[b].z >> 26) == tag6) && (j + 3 >= K || (q[b].w >> 26) == tag6);
+            }
+            if (ready) break;
+            if ((spins & 255) == 0) {
+                const uint64_t now = globaltimer();
+                if (!g0) g0 = now;
+                if ((*((volatile uint32_t*)&ctl->err) & 4u) || now - g0 > 4000000000ull) {
+                    atomicOr(&ctl->err, 4u);
+                    ok = 0;
+                    break;
+                }
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const uint32_t w = w0 + b * PK_THREADS;
+            if (w >= Kw) continue;
+            const uint32_t e4[4] = {q[b].x, q[b].y, q[b].z, q[b].w};
+            int32_t xv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                xv[e] = 4 * w + e < K ? x_of_word(e4[e]) : 0;
+                ss += uint64_t(int64_t(xv[e]) * xv[e]);
+            }
+            *reinterpret_cast<int4*>(xs32 + 4 * w) = make_int4(xv[0], xv[1], xv[2], xv[3]);
+        }
+    }
+    if (*((volatile uint32_t*)&ctl->err) & 4u) ok = 0;
+    if (!__syncthreads_and(ok)) return -1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) s_ss[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t t = 0;
+        for (int w = 0; w < PK_WARPS; ++w) t += s_ss[w];
+        const int64_t ms = int64_t((t / K) >> 16);
+        s_r2 = inv_sqrt_q16(ms + 1, seeds);  // ms >= 0: ms + 1 > 0
+    }
+    __syncthreads();
+    if (tr) tr[4] = tr[5] = tr[6] = clock64();
+    const int64_t r_inv = s_r2;  // <= 2^24: 32 x 32-bit products
+    int fits = 1;
+    const int64_t* gk = gamma_unit ? nullptr : gamma;  // mul16(v, ONE) == v: unit gains skipped
+#pragma unroll 4
+    for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
+        const int4 e4 = *reinterpret_cast<const int4*>(xs32 + 4 * w);
+        const int32_t xs[4] = {e4.x, e4.y, e4.z, e4.w};  // padding slots hold 0
+        uint32_t lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            int64_t v = (int64_t(xs[e]) * int32_t(r_inv)) >> 16;
+            if (gk) v = 4 * w + e < K ? mul16(v, ld_cg64(gk + 4 * w + e)) : 0;
+            fits &= uint64_t(v + (int64_t(1) << 23)) < (uint64_t(1) << 24);
+            lo[e] = uint32_t(v);
+        }
+        planes[w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0040), __byte_perm(lo[2], lo[3], 0x0040), 0x5410);
+        planes[Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0051), __byte_perm(lo[2], lo[3], 0x0051), 0x5410);
+        planes[2 * Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0062), __byte_perm(lo[2], lo[3], 0x0062), 0x5410);
+    }
+    fits = __syncthreads_and(fits);
+    if (tr) tr[7] = clock64();
+    if (fits) return 3;
+#pragma unroll 1
+    for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x)
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) {
+            uint32_t word = 0;
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t j = 4 * w + e;
+                int64_t v = j < K ? (int64_t(xs32[j]) * int32_t(r_inv)) >> 16 : 0;
+                if (!gamma_unit && j < K) v = mul16(v, ld_cg64(gamma + j));
+                word |= uint32_t((uint64_t(v) >> (8 * k)) & 0xFF) << (8 * e);
+            }
+            wplanes[k * Kw + w] = word;
+        }
+    if (threadIdx.x == 0) atomicAdd(&ctl->stats[0], 1ull);
+    __syncthreads();
+    return 8;
+}
+
 // ---- one row group: 4 rows x K against the limb planes ------------------------
 
 // Sums of 4 rows spread over the warp -> every lane gets all 4 (wrapping).
@@ -715,6 +874,12 @@ struct GemvRT {
     const int64_t* lut;
     unsigned long long* ssq;  // EPI_RESID: sum-of-squares accumulator
     int32_t* x32;             // EPI_RESID: int32 copy of the clamped x
+    uint32_t* xw_out;         // EPI_RESID: tagged residual-stream words out
+    const uint32_t* xw_in;    // EPI_RESID: tagged residual words in (nullptr: y / embedding)
+    uint32_t tag6_out, tag6_in;
+    const int8_t* erow;       // EPI_RESID on layer 0: the token's embedding row
+    int64_t es;
+    Ctl* ctl;
     unsigned long long* ytag; // EPI_STORE: tagged word pairs of y
     uint64_t tg;              // their tag << 32
 };
@@ -730,7 +895,12 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
     for (uint32_t g = g_lo + (threadIdx.x >> 5); g < g_hi; g += PK_WARPS) {
         const uint32_t r0 = g * PK_ROWS;
         int64_t resid = 0, scale = 0;  // residual issued now, consumed after the dot product
-        if (g_.epi == EPI_RESID && lane < PK_ROWS && r0 + lane < g_.rows) resid = ld_cg64(g_.y + r0 + lane);
+        uint32_t rw = 0;
+        if (g_.epi == EPI_RESID && lane < PK_ROWS && r0 + lane < g_.rows) {
+            if (g_.erow) resid = int64_t(uint64_t(int64_t(g_.erow[r0 + lane])) * uint64_t(g_.es));
+            else if (g_.xw_in) rw = ld_word(g_.xw_in + r0 + lane);
+            else resid = ld_cg64(g_.y + r0 + lane);
+        }
         uint64_t v[PK_ROWS];
         group_dot<L>(sc, p, g_.Kp, g_.n_segs, planes, v, scale);
         uint64_t sq = 0;
@@ -756,9 +926,14 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
                 g_.y[row] = val;
                 if (g_.ytag) st_tagged2(g_.ytag + 2 * row, g_.tg | uint32_t(val), g_.tg | uint32_t(uint64_t(val) >> 32));
             } else if (g_.epi == EPI_RESID) {
+                if (g_.xw_in && !g_.erow) {
+                    if ((rw >> 26) != g_.tag6_in) rw = poll_word(g_.xw_in + row, g_.tag6_in, 26, g_.ctl);
+                    resid = x_of_word(rw);  // published by the previous residual stage
+                }
                 const int64_t x = add_clamp(resid, val);
                 g_.y[row] = x;
                 if (g_.x32) g_.x32[row] = int32_t(x);
+                if (g_.xw_out) st_word(g_.xw_out + row, x_word(x, g_.tag6_out));
                 sq = uint64_t(x * x);  // |x| <= 2^24: x^2 < 2^49, 8192 rows < 2^62
             } else {  // EPI_ARGMAX
                 g_.lrow[row] = val;
@@ -1065,6 +1240,7 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
     const int big = __syncthreads_or(kv_big);
     const bool wide = __syncthreads_or(wide_in != 0) || big || !shape_ok;
     if (owner && threadIdx.x == 0 && (pos == 0 || big)) *reinterpret_cast<volatile uint32_t*>(wflag) = big ? 1u : 0u;
+    if (owner) __threadfence();  // the appended K/V row is read by the other parts in later steps
     if (tr) tr[4] = clock64();
 
     // 3. scores of this part's positions (kernels.cpp:143-151); the newest
@@ -1332,7 +1508,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                     int64_t* xb = reinterpret_cast<int64_t*>(stage_mem);
                     planes = reinterpret_cast<uint32_t*>(xb + st.Kp);
                     L = 3;
-                    if (glo < ghi) {
+                    if (glo < ghi && st.xw_in) {
+                        L = prologue_norm_words(st.K, st.Kp, st.gamma_unit != 0, st.gamma, st.xw_in,
+                                                tag6_of(a.tag_base + attn_epoch - st.xw_lag),
+                                                reinterpret_cast<int32_t*>(xb), planes, wide_planes, s_seeds, ctl,
+                                                tr);
+                        if (L < 0) return;
+                    } else if (glo < ghi) {
                         const bool embed = st.mode == MODE_EMBED;
                         L = prologue_norm(st.K, st.Kp, st.gamma_unit != 0, st.x, st.gamma,
                                           embed ? a.embd + size_t(token) * st.K : nullptr,
@@ -1353,6 +1535,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 g_.lrow = nullptr;
                 g_.ssq = st.ssq_out;
                 g_.x32 = st.x32_out;
+                g_.xw_out = st.xw_out;
+                g_.xw_in = st.xw_in;
+                g_.tag6_out = tag6_of(a.tag_base + attn_epoch);
+                g_.tag6_in = tag6_of(a.tag_base + attn_epoch - st.xw_lag);
+                g_.erow = st.resid_embed ? a.embd + size_t(token) * st.rows : nullptr;
+                g_.es = st.resid_embed ? a.embd_scales[token] : 0;
+                g_.ctl = ctl;
                 g_.ytag = st.ytag;
                 g_.tg = uint64_t(a.tag_base + attn_epoch + 1) << 32;  // the coming attention stage's tag
                 if (st.epi == EPI_ARGMAX) {
@@ -1377,6 +1566,12 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                             if (better(s_bv[w2], s_bi[w2], best_v, best_i)) { best_v = s_bv[w2]; best_i = s_bi[w2]; }
                         a.parts[blockIdx.x].v = best_v;
                         a.parts[blockIdx.x].idx = best_i;
+                        if (a.parts_w) {  // tagged copy: the next token needs no grid barrier
+                            const uint64_t tg = uint64_t(a.tag_base + attn_epoch) << 32;
+                            unsigned long long* pw = a.parts_w + (size_t(step & 1) * gridDim.x + blockIdx.x) * 4;
+                            st_tagged2(pw, tg | uint32_t(uint64_t(best_v)), tg | uint32_t(uint64_t(best_v) >> 32));
+                            st_tagged2(pw + 2, tg | best_i, tg);
+                        }
                     }
                 }
             }
@@ -1391,9 +1586,27 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
             // every CTA reduces the lm_head partials itself (no extra barrier)
             int64_t bv = INT64_MIN;
             uint32_t bi = 0xFFFFFFFFu;
+            const uint32_t ptag = a.tag_base + attn_epoch;
             for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-                int64_t v = ld_cg64(&a.parts[b].v);
-                uint32_t i = ld_cg32(&a.parts[b].idx);
+                int64_t v;
+                uint32_t i;
+                if (a.parts_w) {
+                    const unsigned long long* pw = a.parts_w + (size_t(step & 1) * gridDim.x + b) * 4;
+                    uint64_t w0, w1, w2, w3;
+                    uint32_t spins = 0;
+                    for (;;) {
+                        ld_tagged2(pw, w0, w1);
+                        ld_tagged2(pw + 2, w2, w3);
+                        if (uint32_t(w0 >> 32) == ptag && uint32_t(w1 >> 32) == ptag && uint32_t(w2 >> 32) == ptag) break;
+                        if ((++spins & 1023) == 0 && (*((volatile uint32_t*)&ctl->err) & 4u)) break;
+                        if ((spins & 0xFFFFF) == 0) atomicOr(&ctl->err, 4u);  // ~seconds: give up
+                    }
+                    v = int64_t((w1 << 32) | (w0 & 0xFFFFFFFFull));
+                    i = uint32_t(w2);
+                } else {
+                    v = ld_cg64(&a.parts[b].v);
+                    i = ld_cg32(&a.parts[b].idx);
+                }
                 if (better(v, i, bv, bi)) { bv = v; bi = i; }
             }
 #pragma unroll
