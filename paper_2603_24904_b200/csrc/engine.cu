@@ -1182,14 +1182,16 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         }
         s->planes_bytes = uint32_t((need + 127) & ~size_t(127));
         const size_t bars = size_t(PK_WARPS) * PK_MAX_DEPTH * 8;
-        const size_t avail = size_t(m->ctx->smem_optin) > s->planes_bytes + bars
-                                 ? size_t(m->ctx->smem_optin) - s->planes_bytes - bars
+        // per-stage stream info (FetchInfo) for the step program or a probe program
+        const size_t fi_bytes = std::max<size_t>(s->host_stages.size(), 129) * sizeof(FetchInfo);
+        const size_t avail = size_t(m->ctx->smem_optin) > s->planes_bytes + bars + fi_bytes
+                                 ? size_t(m->ctx->smem_optin) - s->planes_bytes - bars - fi_bytes
                                  : 0;
         s->ring_depth = uint32_t(std::min<size_t>(PK_MAX_DEPTH, avail / (size_t(PK_WARPS) * PK_SLOT)));
         if (s->ring_depth < 2)
             fail(DIMG_EINVAL, "session: shapes need " + std::to_string(s->planes_bytes) +
                                   " B of shared staging per CTA (d_ffn or max_ctx too large for this build)");
-        s->smem = size_t(PK_WARPS) * s->ring_depth * PK_SLOT + s->planes_bytes + size_t(PK_WARPS) * s->ring_depth * 8;
+        s->smem = size_t(PK_WARPS) * s->ring_depth * PK_SLOT + s->planes_bytes + bars + fi_bytes;
         s->wide_stride = 2 * kp_max;  // 8 planes x Kp/4 words
         s->wide_planes = s->mem.alloc<uint32_t>(size_t(s->grid) * s->wide_stride);
         int per_sm = 0;
@@ -1390,6 +1392,7 @@ dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, flo
         const dimg_model& m = *s->m;
         CK(cudaSetDevice(m.device));
         if (which < 0 || which > 4) fail(DIMG_EINVAL, "time_kernel: which in 0..4");
+        if (n == 0 || n > 128) fail(DIMG_EINVAL, "time_kernel: n in 1..128");
         const uint64_t D = m.D, F = m.F, V = m.V;
         const uint64_t bytes[5] = {3 * D * D + 3 * D * 8 + D * 8 + D * 8 + 3 * D * 8,
                                    D * D + D * 8 + D * 8 + 2 * D * 8,

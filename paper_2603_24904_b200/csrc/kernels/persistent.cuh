@@ -116,9 +116,20 @@ struct PkArgs {
 // Scheduling constants, held in registers (never address kernel params or
 // shared structs from hot code: local memory goes through L1, which each
 // grid barrier's fence invalidates, turning every such read into an L2 trip).
+// What a warp's weight stream needs of each stage, copied into shared memory
+// at launch (reading the descriptors in global memory at every stage change
+// cost an L2 round trip -- the grid fences keep L1 cold -- while the warp
+// still had chunks to consume).
+struct FetchInfo {
+    const int8_t* W;
+    uint32_t g_lo, g_hi;  // this CTA's row groups (empty: attention)
+    uint32_t n_segs, Kp;
+};
+
 struct Sched {
     const PkStage* stages;
     uint32_t n_layer_stages, n_steps, n_prefill;
+    const FetchInfo* fi;  // [n_layer_stages + 1], shared memory
 };
 
 // ---- small PTX helpers --------------------------------------------------------
@@ -319,19 +330,13 @@ struct Fetch {
 };
 
 __device__ __forceinline__ void fetch_load(const Sched& sc, Fetch& f) {
-    const PkStage* st = sc.stages + f.stage;
-    if (st->kind != SK_GEMV) {
-        f.g = f.g_end = 0;
-        return;
-    }
-    uint32_t lo, hi;
-    cta_range(st->n_groups, lo, hi);
-    f.g = lo + (threadIdx.x >> 5);
-    f.g_end = hi;
+    const FetchInfo& fi = sc.fi[f.stage];
+    f.g = fi.g_lo + (threadIdx.x >> 5);
+    f.g_end = fi.g_hi;
     f.seg = 0;
-    f.n_segs = st->n_segs;
-    f.Kp = st->Kp;
-    f.W = st->W;
+    f.n_segs = fi.n_segs;
+    f.Kp = fi.Kp;
+    f.W = fi.W;
 }
 
 __device__ __forceinline__ void fetch_settle(const Sched& sc, Fetch& f) {
@@ -1416,6 +1421,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
     uint8_t* stage_mem = smem + size_t(PK_WARPS) * depth * PK_SLOT;       // planes_bytes
     uint64_t* bars = reinterpret_cast<uint64_t*>(stage_mem + a.planes_bytes);  // [warps][depth]
     uint32_t* wide_planes = a.wide_planes + size_t(blockIdx.x) * a.wide_stride;  // 8-limb planes (rare)
+    FetchInfo* s_fi = reinterpret_cast<FetchInfo*>(bars + PK_WARPS * PK_MAX_DEPTH);   // [n_layer_stages + 1]
     __shared__ u128 red[32];
     __shared__ int64_t s_bv[PK_WARPS];
     __shared__ uint32_t s_bi[PK_WARPS];
@@ -1424,7 +1430,19 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
     __shared__ int64_t s_lut[257], s_seeds[64];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const Sched sc{a.stages, a.n_layer_stages, a.n_steps, a.n_prefill};
+    const Sched sc{a.stages, a.n_layer_stages, a.n_steps, a.n_prefill, s_fi};
+    const uint32_t n_stage_all = a.n_layer_stages + (a.n_steps > a.n_prefill ? 1u : 0u);  // + the head
+    for (uint32_t i = threadIdx.x; i < n_stage_all; i += PK_THREADS) {
+        const PkStage* st = a.stages + i;
+        FetchInfo fi{};
+        if (st->kind == SK_GEMV) {
+            cta_range(st->n_groups, fi.g_lo, fi.g_hi);
+            fi.W = st->W;
+            fi.n_segs = st->n_segs;
+            fi.Kp = st->Kp;
+        }
+        s_fi[i] = fi;
+    }
     Ctl* const ctl = a.ctl;
     if (threadIdx.x < PK_WARPS * depth) mbar_init(&bars[threadIdx.x], 1);
     for (int i = threadIdx.x; i < 257; i += PK_THREADS) s_lut[i] = a.exp_lut[i];
