@@ -330,6 +330,22 @@ struct Fetch {
 };
 
 __device__ __forceinline__ void fetch_load(const Sched& sc, Fetch& f) {
+#ifdef DIMG_FETCH_GLOBAL
+    const PkStage* st = sc.stages + f.stage;
+    if (st->kind != SK_GEMV) {
+        f.g = f.g_end = 0;
+        return;
+    }
+    uint32_t lo, hi;
+    cta_range(st->n_groups, lo, hi);
+    f.g = lo + (threadIdx.x >> 5);
+    f.g_end = hi;
+    f.seg = 0;
+    f.n_segs = st->n_segs;
+    f.Kp = st->Kp;
+    f.W = st->W;
+    return;
+#endif
     const FetchInfo& fi = sc.fi[f.stage];
     f.g = fi.g_lo + (threadIdx.x >> 5);
     f.g_end = fi.g_hi;
@@ -773,8 +789,9 @@ __device__ __noinline__ int prologue_norm_words(uint32_t K, uint32_t Kp, bool ga
         uint32_t lo[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
+            const uint32_t j = 4 * w + e;
             int64_t v = (int64_t(xs[e]) * int32_t(r_inv)) >> 16;
-            if (gk) v = 4 * w + e < K ? mul16(v, ld_cg64(gk + 4 * w + e)) : 0;
+            if (gk && j < K) v = mul16(v, ld_cg64(gk + j));
             fits &= uint64_t(v + (int64_t(1) << 23)) < (uint64_t(1) << 24);
             lo[e] = uint32_t(v);
         }
@@ -957,7 +974,7 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
 }
 
 // The 8-limb instantiation only runs on out-of-range activations: out of line.
-__device__ __noinline__ void run_gemv_wide(Sched sc, Pipe& p, GemvRT g_, const uint32_t* planes,
+__device__ __forceinline__ void run_gemv_wide(const Sched& sc, Pipe& p, const GemvRT& g_, const uint32_t* planes,
                                            uint32_t tag, int64_t& best_v, uint32_t& best_i) {
     run_gemv<8>(sc, p, g_, planes, tag, best_v, best_i);
 }
