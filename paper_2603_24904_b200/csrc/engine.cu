@@ -93,8 +93,10 @@ DevCtx& dev_ctx(int device) {
     CK(cudaStreamCreateWithFlags(&c.op_stream, cudaStreamNonBlocking));
     set_gemv_attrs<EPI_STORE, MODE_PLAIN>();
     set_gemv_attrs<EPI_STORE, MODE_NORM>();
-    CK(cudaFuncSetAttribute(limb_gemm_kernel<TG_BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TG_SMEM));
-    CK(cudaFuncSetAttribute(limb_gemm_kernel<TG_BN_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, TG_SMEM));
+    CK(cudaFuncSetAttribute(limb_gemm_kernel<TG_BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            TgShape<TG_BN>::SMEM));
+    CK(cudaFuncSetAttribute(limb_gemm_kernel<TG_BN_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            TgShape<TG_BN_SMALL>::SMEM));
     {
         auto set = [&](auto kern) {
             cudaFuncAttributes fa;
@@ -173,9 +175,9 @@ CUtensorMap tmap_bytes(const void* base, uint64_t inner, uint64_t outer, uint64_
     return m;
 }
 
-// Three byte limbs of int64 rows x[t][0..K) into planes [3][rows_pad][ldp]
-// (l0, l1 unsigned, l2 signed: exact for -2^23 <= x < 2^23); *wide = 1 if
-// some element is outside that range.
+// Three signed byte digits of int64 rows x[t][0..K) into planes
+// [3][rows_pad][ldp] (put_sdigits: exact for -0x808080 <= x <= 0x7F7F7F);
+// *wide = 1 if some element is outside that range.
 __global__ void limbs_kernel(const int64_t* __restrict__ x, uint32_t T, uint32_t K, uint32_t ldx,
                              uint8_t* __restrict__ planes, uint32_t rows_pad, uint32_t ldp, uint32_t* wide) {
     const size_t plane = size_t(rows_pad) * ldp;
@@ -183,11 +185,7 @@ __global__ void limbs_kernel(const int64_t* __restrict__ x, uint32_t T, uint32_t
          i += size_t(gridDim.x) * blockDim.x) {
         const uint32_t t = uint32_t(i / K), j = uint32_t(i % K);
         const int64_t v = x[size_t(t) * ldx + j];
-        uint8_t* p = planes + size_t(t) * ldp + j;
-        p[0] = uint8_t(v);
-        p[plane] = uint8_t(v >> 8);
-        p[2 * plane] = uint8_t(v >> 16);
-        if (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) *wide = 1;
+        if (!put_sdigits(planes + size_t(t) * ldp + j, plane, v)) *wide = 1;
     }
 }
 
@@ -195,19 +193,13 @@ uint32_t gemm_tiles(const TgArgs& a, uint32_t bn) {
     return ((a.n_out + TG_BM - 1) / TG_BM) * ((a.n_tok + bn - 1) / bn);
 }
 
-// Split-K factor for a GEMM with few output tiles: the smallest k that
-// minimises the busiest CTA's share (ceil(tiles * k / SMs) / k), keeping at
-// least 4 K blocks per split.
-uint32_t pick_ksplit(uint32_t tiles, uint32_t n_kblk, uint32_t sms) {
+// Split-K factor for a GEMM with few output tiles (decode batches).
+uint32_t pick_ksplit(uint32_t tiles, uint32_t n_kblk, uint32_t slots) {
+    // the largest k with every split owning its own CTA slot (one item per
+    // CTA: the split epilogue's fence/atomic latency is paid once), >= 4 K
+    // blocks per split
     uint32_t best = 1;
-    double best_t = double((tiles + sms - 1) / sms);
-    for (uint32_t k = 2; k <= 8 && n_kblk / k >= 4; ++k) {
-        const double t = double((tiles * k + sms - 1) / sms) / k;
-        if (t < best_t - 1e-9) {
-            best_t = t;
-            best = k;
-        }
-    }
+    for (uint32_t k = 2; k <= 8 && n_kblk / k >= 4 && tiles * k <= slots; ++k) best = k;
     return best;
 }
 
@@ -218,9 +210,11 @@ void launch_limb_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const uint32_t items = gemm_tiles(a, bn) * std::max(1u, a.ksplit);
-    const uint32_t grid = std::min<uint32_t>(items, uint32_t(sms));
-    if (bn == TG_BN_SMALL) limb_gemm_kernel<TG_BN_SMALL><<<grid, TG_THREADS, TG_SMEM, st>>>(ta, tb, a);
-    else limb_gemm_kernel<TG_BN><<<grid, TG_THREADS, TG_SMEM, st>>>(ta, tb, a);
+    const uint32_t per_sm = bn == TG_BN_SMALL ? 2u : 1u;
+    const uint32_t grid = std::min<uint32_t>(items, per_sm * uint32_t(sms));
+    if (bn == TG_BN_SMALL)
+        limb_gemm_kernel<TG_BN_SMALL><<<grid, TG_THREADS, TgShape<TG_BN_SMALL>::SMEM, st>>>(ta, tb, a);
+    else limb_gemm_kernel<TG_BN><<<grid, TG_THREADS, TgShape<TG_BN>::SMEM, st>>>(ta, tb, a);
     CK(cudaGetLastError());
 }
 
@@ -904,7 +898,7 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
         a.ldp = m.Kf;
         a.lut = m.ctx->exp_lut;
         a.wide = r.wide;
-        a.ksplit = split_k ? pick_ksplit(gemm_tiles(a, bn), a.n_kblk, uint32_t(sms)) : 1;
+        a.ksplit = split_k ? pick_ksplit(gemm_tiles(a, bn), a.n_kblk, 2 * uint32_t(sms)) : 1;
         if (size_t(gemm_tiles(a, bn)) * a.ksplit * TG_L * bn * TG_BM > r.partial_elems) a.ksplit = 1;
         a.partial = r.partial;
         a.tile_cnt = r.tile_cnt;

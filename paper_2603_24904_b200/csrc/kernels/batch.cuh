@@ -147,11 +147,7 @@ __global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __re
             for (uint32_t p = 0; p < T; ++p) sum += uint64_t(mul16_prob(S[p], Vh[size_t(p) * dh + jj]));
         }
         const int64_t v = int64_t(sum);
-        uint8_t* pp = planes + size_t(t) * ldp + h * dh + jj;
-        pp[0] = uint8_t(v);
-        pp[plane] = uint8_t(v >> 8);
-        pp[2 * plane] = uint8_t(v >> 16);
-        if (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) big = 1;
+        if (!put_sdigits(planes + size_t(t) * ldp + h * dh + jj, plane, v)) big = 1;
     }
     if (big) *wide = 1;
 }

@@ -31,10 +31,7 @@ __global__ void pf_embed_kernel(const uint32_t* __restrict__ tok, uint32_t n, co
 }
 
 __device__ __forceinline__ void pf_put_limbs(uint8_t* p, size_t plane, int64_t v, uint32_t* wide) {
-    p[0] = uint8_t(v);
-    p[plane] = uint8_t(v >> 8);
-    p[2 * plane] = uint8_t(v >> 16);
-    if (v < -(int64_t(1) << 23) || v >= (int64_t(1) << 23)) *wide = 1;
+    if (!put_sdigits(p, plane, v)) *wide = 1;
 }
 
 // rmsnorm (proj/src/kernels.cpp:56-68) of every token row, written as the

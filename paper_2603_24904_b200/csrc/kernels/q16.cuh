@@ -21,6 +21,21 @@ __device__ __forceinline__ bool fits_i32(int64_t v) {
     return ((uint64_t(v) + 0x80000000ull) >> 32) == 0;
 }
 
+// The tensor-core operand form of an activation: three balanced signed byte
+// digits, v = d0 + 2^8 d1 + 2^16 d2 with every d in [-128, 127], exact for
+// -0x808080 <= v <= 0x7F7F7F. All three limbs are s8, so one kind::i8 MMA
+// covers them together (tc_gemm.cuh). Writes the digits to p[0], p[plane],
+// p[2 plane]; returns false (digits meaningless) outside that range.
+__device__ __forceinline__ bool put_sdigits(uint8_t* p, size_t plane, int64_t v) {
+    const int64_t d0 = int8_t(v);
+    const int64_t r1 = (v - d0) >> 8;
+    const int64_t d1 = int8_t(r1);
+    p[0] = uint8_t(d0);
+    p[plane] = uint8_t(d1);
+    p[2 * plane] = uint8_t((r1 - d1) >> 8);
+    return uint64_t(v + 0x808080) <= 0xFFFFFFu;
+}
+
 // int64((int128(a) * b) >> k) for 0 < k < 64, exact for every input: the
 // 128-bit product is (hi, lo) = (mul.hi.s64, mul.lo.s64), and the low 64 bits
 // of the arithmetic shift are (lo >>> k) | (hi << (64 - k)). Two multiplies,

@@ -3,18 +3,21 @@
 //
 // dense_forward (proj/src/kernels.cpp:18-30) for T tokens at once:
 //   y[t][n] = ((sum_j W[n][j] * x[t][j])_int64 * s[n]) >> 16
-// with int8 W and int64 activations. Activations with |x| < 2^23 are split
-// into three byte limbs x = l0 + 2^8 l1 + 2^16 l2 (l0, l1 unsigned, l2
-// signed), so each limb product is a plain int8 x int8 GEMM with int32
-// accumulation -- exact: K * 127 * 255 < 2^31 for K <= 66000 -- and
+// with int8 W and int64 activations. Activations in [-0x808080, 0x7F7F7F]
+// are split into three balanced signed byte digits x = l0 + 2^8 l1 + 2^16 l2
+// (put_sdigits, q16.cuh), so each limb product is a plain s8 x s8 GEMM with
+// int32 accumulation -- exact: K * 128 * 128 < 2^31 for K < 131072 -- and
 // acc = D0 + 2^8 D1 + 2^16 D2 is recombined exactly in int64 in the epilogue.
 // (Larger activations are detected by the producers; the engine then takes
 // the exact CUDA-core path instead.)
 //
-// Tiles are 128 features x BN tokens (64, or 16 for decode batches): the weights are the MMA A operand
-// (M = features, K-major), the three limb planes of the tokens are three B
-// operands (N = tokens, K-major) sharing one A tile per stage, and a tile's
-// three accumulators take 3 x 64 TMEM columns. The kernel is persistent (one
+// Tiles are 128 features x BN tokens (64, or 16 for decode batches): the
+// weights are the MMA A operand (M = features, K-major); the three limb
+// planes of the tokens land as three contiguous BN-row B tiles, which one
+// MMA with N = 3 BN consumes together (every limb is s8, so one instruction
+// descriptor fits all three: a third of the MMA instructions of a per-limb
+// issue, whose fixed per-instruction cost dominated small-N tiles), and a
+// tile's accumulators take 3 x BN TMEM columns. The kernel is persistent (one
 // CTA per SM walks tiles round-robin) with two accumulator sets in TMEM, so
 // the epilogue of one tile overlaps the MMAs of the next. TMA loads 128-byte
 // K slices of every operand with the 128B swizzle that the UMMA smem
@@ -41,13 +44,18 @@ constexpr int TG_BK = 128;      // K bytes per stage = one 128-byte swizzle row
 constexpr int TG_L = 3;         // activation limbs
 constexpr int TG_A_BYTES = TG_BM * TG_BK;
 constexpr int TG_THREADS = 192;
-constexpr int TG_SMEM = 200 * 1024 + 1024;  // stage ring (+ alignment slack)
-
 template <int BN>
 struct TgShape {
     static constexpr int B_BYTES = BN * TG_BK;
     static constexpr int STAGE_BYTES = TG_A_BYTES + TG_L * B_BYTES;  // 40 KB (BN 64) / 22 KB (BN 16)
-    static constexpr int STAGES = (200 * 1024) / STAGE_BYTES;
+    // BN 64: one CTA per SM with a ~200 KB ring; BN 16 (decode batches, few
+    // tiles): a ~100 KB ring so two CTAs share an SM and more tiles stream at once
+#ifndef TG_RING_SMALL
+#define TG_RING_SMALL (100 * 1024)
+#endif
+    static constexpr int RING = BN >= 64 ? 200 * 1024 : TG_RING_SMALL;
+    static constexpr int STAGES = RING / STAGE_BYTES;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;  // + alignment slack
     static constexpr int ACC = TG_L * BN;  // TMEM columns of one tile's accumulators
     static constexpr uint32_t TMEM_COLS = 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
 };
@@ -118,11 +126,10 @@ __device__ __forceinline__ uint64_t tg_desc(uint32_t smem_addr) {
            (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
 
-// Instruction descriptor, kind::i8: D s32, A = W (s8), B = limb (u8 or s8),
-// both K-major, M = 128, N = bn.
-__host__ __device__ constexpr uint32_t tg_idesc(bool b_signed, int bn) {
-    return (2u << 4) | (1u << 7) | ((b_signed ? 1u : 0u) << 10) | (uint32_t(bn >> 3) << 17) |
-           (uint32_t(TG_BM >> 4) << 24);
+// Instruction descriptor, kind::i8: D s32, A = W (s8), B = signed digits
+// (s8), both K-major, M = 128, N = n (multiple of 16, <= 256).
+__host__ __device__ constexpr uint32_t tg_idesc(int n) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(TG_BM >> 4) << 24);
 }
 
 __device__ __forceinline__ void tg_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -170,7 +177,7 @@ __device__ __forceinline__ void tg_item(uint32_t item, uint32_t ksplit, uint32_t
 }
 
 template <int BN>
-__global__ void __launch_bounds__(TG_THREADS, 1)
+__global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
     limb_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const TgArgs a) {
     using S = TgShape<BN>;
@@ -241,15 +248,12 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
                     tg_mbar_wait(&full[s], (it / S::STAGES) & 1);
                     tg_fence_after();
                     const uint32_t sa = tg_smem_u32(smem + size_t(s) * S::STAGE_BYTES);
+                    // the three limb tiles are contiguous 128B-swizzled rows: one
+                    // MMA with N = 3 BN reads them all (column l BN + t = limb l of token t)
 #pragma unroll
-                    for (int l = 0; l < TG_L; ++l) {
-                        const uint32_t idesc = tg_idesc(l == TG_L - 1, BN);
-                        const uint32_t sb = sa + TG_A_BYTES + l * S::B_BYTES;
-#pragma unroll
-                        for (int kk = 0; kk < TG_BK / 32; ++kk)  // K = 32 bytes per MMA
-                            tg_mma(dacc + l * BN, tg_desc(sa + 32 * kk), tg_desc(sb + 32 * kk), idesc,
-                                   (kb != kb0) || (kk != 0));
-                    }
+                    for (int kk = 0; kk < TG_BK / 32; ++kk)  // K = 32 bytes per MMA
+                        tg_mma(dacc, tg_desc(sa + 32 * kk), tg_desc(sa + TG_A_BYTES + 32 * kk), tg_idesc(TG_L * BN),
+                               (kb != kb0) || (kk != 0));
                     tg_commit(&empty[s]);  // frees the stage once these MMAs have read it
                 }
                 tg_commit(&acc_full[b]);
@@ -325,28 +329,41 @@ __global__ void __launch_bounds__(TG_THREADS, 1)
                         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tg_smem_u32(&acc_empty[b])) : "memory");
                     }
                 }
+                int64_t val[16];  // the limb accumulators recombined and scaled (d dies here)
 #pragma unroll
-                for (int jj = 0; jj < 16; ++jj) {
-                    const uint32_t t = t0 + c0 + jj;
-                    const int64_t acc = int64_t(d[0][jj]) + (int64_t(d[1][jj]) << 8) + (int64_t(d[2][jj]) << 16);
-                    const int64_t val = scale_row(acc, sc);
-                    if (a.epi == TG_SILU) {
+                for (int jj = 0; jj < 16; ++jj)
+                    val[jj] = scale_row(int64_t(d[0][jj]) + (int64_t(d[1][jj]) << 8) + (int64_t(d[2][jj]) << 16), sc);
+                if (a.epi == TG_SILU) {
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const uint32_t t = t0 + c0 + jj;
                         // rows (2i, 2i+1) = (gate_i, up_i) sit on adjacent lanes
-                        const int64_t up = __shfl_down_sync(0xffffffffu, val, 1);
+                        const int64_t up = __shfl_down_sync(0xffffffffu, val[jj], 1);
                         if (nv && !(n & 1) && t < a.n_tok) {
-                            const int64_t hv = mul16(silu_q16(val, a.lut), up);
+                            const int64_t hv = mul16(silu_q16(val[jj], a.lut), up);
                             const uint32_t i = n >> 1;
                             if (a.y) a.y[size_t(t) * a.ldy + i] = hv;
-                            uint8_t* p = a.planes + size_t(t) * a.ldp + i;
-                            const size_t plane = size_t(a.limb_rows_out) * a.ldp;
-                            p[0] = uint8_t(hv);
-                            p[plane] = uint8_t(hv >> 8);
-                            p[2 * plane] = uint8_t(hv >> 16);
-                            if (hv < -(int64_t(1) << 23) || hv >= (int64_t(1) << 23)) *a.wide = 1;
+                            if (!put_sdigits(a.planes + size_t(t) * a.ldp + i, size_t(a.limb_rows_out) * a.ldp, hv))
+                                *a.wide = 1;
                         }
-                    } else if (nv && t < a.n_tok) {
-                        int64_t* yp = a.y + size_t(t) * a.ldy + n;
-                        *yp = a.epi == TG_RESID ? add_clamp(*yp, val) : val;
+                    }
+                } else {
+                    // RESID: all 16 residual loads in flight before the first store
+                    // (the compiler may not hoist a load above a possibly aliasing store)
+                    if (a.epi == TG_RESID) {
+                        int64_t yold[16];
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) {
+                            const uint32_t t = t0 + c0 + jj;
+                            yold[jj] = nv && t < a.n_tok ? a.y[size_t(t) * a.ldy + n] : 0;
+                        }
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) val[jj] = add_clamp(yold[jj], val[jj]);
+                    }
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        const uint32_t t = t0 + c0 + jj;
+                        if (nv && t < a.n_tok) a.y[size_t(t) * a.ldy + n] = val[jj];
                     }
                 }
             }

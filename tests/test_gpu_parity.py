@@ -245,8 +245,9 @@ def test_dense_tokens_matches_oracle(P, oracle, N, K, T):
     rng = np.random.default_rng(N * 7 + K + T)
     w = rng.integers(-127, 128, (N, K), dtype=np.int8)
     s = rng.integers(1, 1 << 12, N, dtype=np.int64)
-    x = rng.integers(-(1 << 23), 1 << 23, (T, K), dtype=np.int64)
-    x[0, :5] = [-(1 << 23), (1 << 23) - 1, 0, -1, 255]
+    # the whole signed-digit range (put_sdigits: -0x808080 .. 0x7F7F7F) with its ends
+    x = rng.integers(-0x808080, 0x7F7F80, (T, K), dtype=np.int64)
+    x[0, :7] = [-0x808080, 0x7F7F7F, 0, -1, 255, -128, 0x7F7F80 - 0x10000]
     got = P.dense_tokens(w, s, x)
     for t in range(T):
         assert np.array_equal(got[t], oracle.dense(w, s, x[t])), t
@@ -261,6 +262,13 @@ def test_dense_tokens_wide_rows_fall_back_exactly(P, oracle):
     got = P.dense_tokens(w, s, x)
     for t in range(5):
         assert np.array_equal(got[t], oracle.dense(w, s, x[t]))
+    # one past either end of the three-digit range
+    for v in (0x7F7F80, -0x808081):
+        x2 = x.copy()
+        x2[3, 7] = v
+        got = P.dense_tokens(w, s, x2)
+        for t in range(5):
+            assert np.array_equal(got[t], oracle.dense(w, s, x2[t]))
 
 
 # ---- tensor-core prefill (whole prompt per layer) ------------------------------
