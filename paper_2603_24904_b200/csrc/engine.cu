@@ -203,9 +203,35 @@ uint32_t pick_ksplit(uint32_t tiles, uint32_t n_kblk, uint32_t slots) {
     return best;
 }
 
+// Programmatic dependent launch for the batch step's kernel chain (see
+// pdl_wait in q16.cuh): each kernel may start, and the GEMMs stream their
+// first weight tiles, while the previous one drains. DIMG_PDL=0 turns it off.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DIMG_PDL");
+        return !e || std::atoi(e) != 0;
+    }();
+    return on;
+}
+
+template <typename... P, typename... A>
+void launch_k(bool pdl, void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl && pdl_enabled() ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...));
+}
+
 // bn = token tile (TG_BN or TG_BN_SMALL; tb must be built with that box).
 void launch_limb_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs& a, cudaStream_t st,
-                      uint32_t bn = TG_BN) {
+                      uint32_t bn = TG_BN, bool pdl = false) {
     int dev = 0, sms = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -213,9 +239,8 @@ void launch_limb_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs
     const uint32_t per_sm = bn == TG_BN_SMALL ? 2u : 1u;
     const uint32_t grid = std::min<uint32_t>(items, per_sm * uint32_t(sms));
     if (bn == TG_BN_SMALL)
-        limb_gemm_kernel<TG_BN_SMALL><<<grid, TG_THREADS, TgShape<TG_BN_SMALL>::SMEM, st>>>(ta, tb, a);
-    else limb_gemm_kernel<TG_BN><<<grid, TG_THREADS, TgShape<TG_BN>::SMEM, st>>>(ta, tb, a);
-    CK(cudaGetLastError());
+        launch_k(pdl, limb_gemm_kernel<TG_BN_SMALL>, grid, TG_THREADS, TgShape<TG_BN_SMALL>::SMEM, st, ta, tb, a);
+    else launch_k(pdl, limb_gemm_kernel<TG_BN>, grid, TG_THREADS, TgShape<TG_BN>::SMEM, st, ta, tb, a);
 }
 
 }  // namespace
@@ -812,8 +837,9 @@ bool batch_shape_ok(const dimg_model& m) { return m.dh % 4 == 0 && m.dh / 2 <= 1
 }  // namespace
 
 struct BatchCache {
-    BatchRun r;
-    cudaGraphExec_t ge = nullptr;  // the captured decode step (depends only on r's buffers and B)
+    BatchRun r;                    // buffers for up to r.B sequences (capacity)
+    cudaGraphExec_t ge = nullptr;  // the captured decode step of ge_B sequences (r's buffers)
+    uint32_t ge_B = 0;
     ~BatchCache() {
         if (ge) cudaGraphExecDestroy(ge);
     }
@@ -873,7 +899,7 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
     cudaStream_t st = r.st;
     const uint32_t D = m.D, dh = m.dh, H = m.H;
     const BatchTok bt{r.tok, r.seq, r.pos};
-    bd_embed_kernel<<<1024, 256, 0, st>>>(bt, n, m.embd, m.embd_s, D, r.x);
+    launch_k(true, bd_embed_kernel, 1024, 256, 0, st, bt, n, (const int8_t*)m.embd, (const int64_t*)m.embd_s, D, r.x);
     const bool small = n <= uint32_t(TG_BN_SMALL);
     const uint32_t bn = small ? TG_BN_SMALL : TG_BN;
     // split-K only pays for small token tiles (DIMG_SPLITK=0/1 overrides)
@@ -902,34 +928,35 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
         if (size_t(gemm_tiles(a, bn)) * a.ksplit * TG_L * bn * TG_BM > r.partial_elems) a.ksplit = 1;
         a.partial = r.partial;
         a.tile_cnt = r.tile_cnt;
-        launch_limb_gemm(W.tmap, tb, a, st, bn);
+        launch_limb_gemm(W.tmap, tb, a, st, bn, true);
+    };
+    auto norm = [&](const int64_t* g, int unit) {
+        launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int64_t*)r.x, D, g, unit,
+                 (const int64_t*)m.ctx->seeds, r.pa, r.nmax_pad, m.Kd, r.wide);
     };
     const size_t asmem = bd_attn_smem(dh, r.ctx) + 8;
     for (uint32_t l = 0; l < m.L; ++l) {
         const auto& lw = m.layers[l];
-        pf_norm_limbs_kernel<<<n, 256, 0, st>>>(r.x, D, lw.attn_norm, lw.attn_unit, m.ctx->seeds, r.pa, r.nmax_pad,
-                                                 m.Kd, r.wide);
+        norm(lw.attn_norm, lw.attn_unit);
         gemm(lw.qkv, r.tm_pa, TG_STORE, r.qkv, 3 * D);
-        bd_rope_kv_kernel<<<dim3(n, H), dh / 2, 0, st>>>(r.qkv, bt, D, dh, m.rope_cos, m.rope_sin,
-                                                         r.K32 + l * r.layer_stride, r.V32 + l * r.layer_stride,
-                                                         r.seq_stride, r.ctx, r.wide);
+        launch_k(true, bd_rope_kv_kernel, dim3(n, H), dh / 2, 0, st, r.qkv, bt, D, dh, (const int64_t*)m.rope_cos,
+                 (const int64_t*)m.rope_sin, r.K32 + l * r.layer_stride, r.V32 + l * r.layer_stride, r.seq_stride,
+                 r.ctx, r.wide);
         if (l + 1 == m.L && !logits) break;  // prompt positions only feed the KV caches
-        bd_attn_kernel<<<dim3(H, n), BD_THREADS, asmem, st>>>(r.qkv, bt, D, dh, r.K32 + l * r.layer_stride,
-                                                            r.V32 + l * r.layer_stride, r.seq_stride, r.ctx,
-                                                            m.inv_scale, m.ctx->exp_lut, r.pa, r.nmax_pad, m.Kd,
-                                                            r.wide);
+        launch_k(true, bd_attn_kernel, dim3(H, n), BD_THREADS, asmem, st, (const int64_t*)r.qkv, bt, D, dh,
+                 (const int32_t*)(r.K32 + l * r.layer_stride), (const int32_t*)(r.V32 + l * r.layer_stride),
+                 r.seq_stride, r.ctx, m.inv_scale, (const int64_t*)m.ctx->exp_lut, r.pa, r.nmax_pad, m.Kd, r.wide);
         gemm(lw.wo, r.tm_pa, TG_RESID, r.x, D);
-        pf_norm_limbs_kernel<<<n, 256, 0, st>>>(r.x, D, lw.ffn_norm, lw.ffn_unit, m.ctx->seeds, r.pa, r.nmax_pad,
-                                                 m.Kd, r.wide);
+        norm(lw.ffn_norm, lw.ffn_unit);
         gemm(lw.gu, r.tm_pa, TG_SILU, nullptr, 0);
         gemm(lw.down, r.tm_ph, TG_RESID, r.x, D);
     }
     if (logits) {
-        pf_norm_limbs_kernel<<<n, 256, 0, st>>>(r.x, D, m.final_norm, m.final_unit, m.ctx->seeds, r.pa, r.nmax_pad,
-                                                 m.Kd, r.wide);
+        norm(m.final_norm, m.final_unit);
         gemm(m.head, r.tm_pa, TG_STORE, r.logits, m.V);
-        bd_argmax_kernel<<<n, 256, 0, st>>>(r.logits, m.V, r.tok, r.pos, r.seq, r.out, r.max_new, r.step);
-        bd_step_kernel<<<1, 1, 0, st>>>(r.step);
+        launch_k(true, bd_argmax_kernel, n, 256, 0, st, (const int64_t*)r.logits, m.V, r.tok, r.pos,
+                 (const uint32_t*)r.seq, r.out, r.max_new, r.step);
+        launch_k(true, bd_step_kernel, 1, 1, 0, st, r.step);
     }
     CK(cudaGetLastError());
 }
@@ -946,7 +973,7 @@ bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<
     // buffers (and the captured step graph) are kept on the model and reused
     // while the batch fits them
     const uint32_t nmax = std::max(n_prompt_pos, B);
-    if (!m->batch || m->batch->r.B != B || m->batch->r.ctx < ctx || m->batch->r.nmax < nmax ||
+    if (!m->batch || m->batch->r.B < B || m->batch->r.ctx < ctx || m->batch->r.nmax < nmax ||
         m->batch->r.max_new < std::max(1u, max_new)) {
         m->batch.reset();
         auto c = std::make_shared<BatchCache>();
@@ -985,6 +1012,10 @@ bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<
         CK(cudaStreamSynchronize(r.st));
     }
     if (max_new > 0) {
+        if (c.ge && c.ge_B != B) {
+            CK(cudaGraphExecDestroy(c.ge));
+            c.ge = nullptr;
+        }
         if (!c.ge) {
             cudaGraph_t g = nullptr;
             CK(cudaStreamBeginCapture(r.st, cudaStreamCaptureModeThreadLocal));
@@ -992,6 +1023,7 @@ bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<
             CK(cudaStreamEndCapture(r.st, &g));
             CK(cudaGraphInstantiate(&c.ge, g, 0));
             cudaGraphDestroy(g);
+            c.ge_B = B;
         }
         for (uint32_t s = 0; s < max_new; ++s) CK(cudaGraphLaunch(c.ge, r.st));
         if (steps_graph) *steps_graph += max_new;

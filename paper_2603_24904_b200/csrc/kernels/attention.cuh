@@ -58,10 +58,11 @@ __device__ __forceinline__ void softmax_strip_inl(int64_t* S, uint32_t n, const 
     }
     total = block_reduce<uint64_t>(total, reinterpret_cast<uint64_t*>(red),
                                    [](uint64_t x, uint64_t y) { return x + y; }, warp_sum_u64);
+    const uint64_t inv = ~0ull / total;  // total >= 1: the maximum's weight is ONE
     for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
         int64_t d = wrap_sub(m, S[t]);
         int64_t w = exp_neg(d > 8 * ONE ? 8 * ONE : d, lut);
-        S[t] = (w << 16) / int64_t(total);
+        S[t] = int64_t(udiv_inv(uint64_t(w) << 16, total, inv));
     }
     __syncthreads();
 }

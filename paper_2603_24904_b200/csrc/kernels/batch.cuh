@@ -29,6 +29,8 @@ struct BatchTok {  // device arrays, one entry per token of the step
 
 __global__ void bd_embed_kernel(BatchTok bt, uint32_t n, const int8_t* __restrict__ E,
                                 const int64_t* __restrict__ Es, uint32_t D, int64_t* __restrict__ x) {
+    pdl_launch_dependents();
+    pdl_wait();
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < size_t(n) * D;
          i += size_t(gridDim.x) * blockDim.x) {
         const uint32_t t = uint32_t(i / D), j = uint32_t(i % D);
@@ -43,6 +45,8 @@ __global__ void bd_embed_kernel(BatchTok bt, uint32_t n, const int8_t* __restric
 __global__ void bd_rope_kv_kernel(int64_t* __restrict__ qkv, BatchTok bt, uint32_t D, uint32_t dh,
                                   const int64_t* __restrict__ rc, const int64_t* __restrict__ rs, int32_t* K32,
                                   int32_t* V32, size_t seq_stride, uint32_t ctx, uint32_t* wide) {
+    pdl_launch_dependents();
+    pdl_wait();
     const uint32_t t = blockIdx.x, h = blockIdx.y, half = dh / 2, i = threadIdx.x;
     const uint32_t b = bt.seq[t], p = bt.pos[t];
     int64_t* q = qkv + size_t(t) * 3 * D + size_t(h) * dh;
@@ -85,12 +89,14 @@ __global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __re
     extern __shared__ __align__(16) uint8_t bd_smem[];
     __shared__ int64_t lut[257];
     __shared__ u128 red[32];
+    pdl_launch_dependents();
+    for (int i = threadIdx.x; i < 257; i += BD_THREADS) lut[i] = lut_g[i];  // constant: before the wait
+    pdl_wait();
     const uint32_t h = blockIdx.x, t = blockIdx.y;
     const uint32_t b = bt.seq[t], T = bt.pos[t] + 1;
     int64_t* S = reinterpret_cast<int64_t*>(bd_smem);              // [ctx]
     int32_t* q = reinterpret_cast<int32_t*>(S + ctx);              // [dh]
     uint64_t* part = reinterpret_cast<uint64_t*>(q + dh + (dh & 1));  // [BD_THREADS]
-    for (int i = threadIdx.x; i < 257; i += BD_THREADS) lut[i] = lut_g[i];
     for (uint32_t j = threadIdx.x; j < dh; j += BD_THREADS) q[j] = int32_t(qkv[size_t(t) * 3 * D + size_t(h) * dh + j]);
     __syncthreads();
     const int32_t* Kh = K32 + size_t(b) * seq_stride + size_t(h) * ctx * dh;
@@ -160,6 +166,8 @@ __global__ void __launch_bounds__(256) bd_argmax_kernel(const int64_t* __restric
                                                         uint32_t* out, uint32_t max_new, uint32_t* step) {
     __shared__ int64_t sv[8];
     __shared__ uint32_t si[8];
+    pdl_launch_dependents();
+    pdl_wait();
     const uint32_t t = blockIdx.x;
     const int64_t* row = logits + size_t(t) * V;
     int64_t bv = INT64_MIN;
@@ -196,6 +204,9 @@ __global__ void __launch_bounds__(256) bd_argmax_kernel(const int64_t* __restric
     }
 }
 
-__global__ void bd_step_kernel(uint32_t* step) { *step += 1; }
+__global__ void bd_step_kernel(uint32_t* step) {
+    pdl_wait();
+    *step += 1;
+}
 
 }  // namespace dimg::dev

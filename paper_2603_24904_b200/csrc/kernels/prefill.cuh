@@ -45,6 +45,8 @@ __global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int64_t* __res
                                                             uint32_t rows_pad, uint32_t ldp, uint32_t* wide) {
     __shared__ u128 red[32];
     __shared__ int64_t s_r;
+    pdl_launch_dependents();
+    pdl_wait();
     const uint32_t t = blockIdx.x;
     const int64_t* xr = x + size_t(t) * K;
     int64_t v[PN_PER];

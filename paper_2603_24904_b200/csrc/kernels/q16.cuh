@@ -21,6 +21,15 @@ __device__ __forceinline__ bool fits_i32(int64_t v) {
     return ((uint64_t(v) + 0x80000000ull) >> 32) == 0;
 }
 
+// Programmatic dependent launch (the batch step's kernels are launched with
+// programmatic stream serialization): a kernel may start while its
+// predecessor still runs; pdl_wait() returns once every prerequisite grid has
+// completed and its writes are visible, so everything before it may touch
+// only constant data (weights, tables). launch_dependents lets the next
+// kernel start launching. Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // The tensor-core operand form of an activation: three balanced signed byte
 // digits, v = d0 + 2^8 d1 + 2^16 d2 with every d in [-128, 127], exact for
 // -0x808080 <= v <= 0x7F7F7F. All three limbs are s8, so one kind::i8 MMA
@@ -109,14 +118,34 @@ __device__ __forceinline__ int64_t exp_neg(int64_t t, const int64_t* e) {
     return hi - (((hi - lo) * frac + 1024) >> 11);
 }
 
+// floor(a / d) for a < 2^63, d >= 1, given inv = ~0ull / d (one division
+// shared by many quotients): umulhi(a, inv) is floor(a / d) or one less.
+__device__ __forceinline__ uint64_t udiv_inv(uint64_t a, uint64_t d, uint64_t inv) {
+    const uint64_t q = __umul64hi(a, inv);
+    return q + ((a - q * d) >= d);
+}
+
+// floor(a / d) for 0 <= a, 1 <= d < 2^24 and a quotient below 2^22, without
+// a 64-bit division and branch-free: the float estimate a * rcp(d) carries a
+// relative error below 3 * 2^-24 (three roundings), so it is within 0.75 of
+// the quotient and truncates to q - 1, q or q + 1; the exact remainder then
+// fixes the one step.
+__device__ __forceinline__ int64_t div_rcp(int64_t a, int64_t d) {
+    int64_t q = int64_t(float(a) * __frcp_rn(float(d)));
+    const int64_t r = a - q * d;
+    q -= r < 0;
+    q += r >= d;
+    return q;
+}
+
 // sigmoid_q16 with exact symmetry (proj/src/q16.cpp:94-101).
 __device__ __forceinline__ int64_t sigmoid_q16(int64_t x, const int64_t* e) {
     bool pos = x > 0;
     int64_t xn = pos ? -x : x;  // x > 0 => -x is representable
     int64_t t = xn <= -8 * ONE ? 8 * ONE : -xn;
-    int64_t ev = exp_neg(t, e);
-    int64_t den = ONE + ev;
-    int64_t s = ((ev << 16) + den / 2) / den;
+    int64_t ev = exp_neg(t, e);   // [0, ONE]
+    int64_t den = ONE + ev;       // [2^16, 2^17]
+    int64_t s = div_rcp((ev << 16) + den / 2, den);
     return pos ? ONE - s : s;
 }
 

@@ -83,7 +83,17 @@ struct TgArgs {
     uint32_t ksplit;
     int32_t* partial;       // [tiles][ksplit][3][BN][128]
     uint32_t* tile_cnt;     // [tiles], zero between launches (the last CTA resets)
+    const uint8_t* a_ptr;   // TG_A_BULK experiment: the A operand for 1-D bulk copies
+#ifdef TG_TRACE
+    uint64_t* trace;        // [grid][128] globaltimer stamps (tools/gemm_bench.cu)
+#endif
 };
+
+__device__ __forceinline__ uint64_t tg_now() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // ---- PTX wrappers --------------------------------------------------------------
 
@@ -111,11 +121,48 @@ __device__ __forceinline__ void tg_mbar_wait(uint64_t* b, uint32_t parity) {
     }
 }
 
+__device__ __forceinline__ void tg_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     tg_smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(tg_smem_u32(bar))
+                 : "memory");
+}
+
 __device__ __forceinline__ void tg_tma_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
             tg_smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(tg_smem_u32(bar))
+        : "memory");
+}
+
+// Warp-wide forms of the single-thread instructions: the whole (converged)
+// warp executes them and one elected lane issues. The operands are then
+// provably warp-uniform and go straight to uniform registers; issued from a
+// `lane == 0` branch instead, every tcgen05.mma / TMA went through a
+// divergent R2UR.BROADCAST waterfall loop that cost ~120 cycles per MMA
+// (tools/mma_rate.cu), three times the N <= 64 MMA time itself.
+__device__ __forceinline__ void tg_expect_tx_w(uint64_t* b, uint32_t bytes) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(tg_smem_u32(b)),
+        "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void tg_tma_2d_w(void* dst, const CUtensorMap* map, int32_t x, int32_t y, uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n\t}" ::"r"(
+            tg_smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(tg_smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tg_bulk_w(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(
+            tg_smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(tg_smem_u32(bar))
         : "memory");
 }
 
@@ -140,11 +187,27 @@ __device__ __forceinline__ void tg_mma(uint32_t d_tmem, uint64_t a, uint64_t b, 
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
+__device__ __forceinline__ void tg_mma_w(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
 
 __device__ __forceinline__ void tg_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      tg_smem_u32(bar))
                  : "memory");
+}
+
+__device__ __forceinline__ void tg_commit_w(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(tg_smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void tg_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -185,8 +248,13 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tg_smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ __align__(8) uint64_t full[S::STAGES], empty[S::STAGES], acc_full[2], acc_empty[2];
     __shared__ uint32_t tmem_slot, s_last;
+    __shared__ int64_t s_lut[257];  // exp LUT for the SILU epilogue
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef TG_TRACE
+    uint64_t* tr = a.trace + size_t(blockIdx.x) * 128;
+    if (threadIdx.x == 0) tr[0] = tg_now();
+#endif
     const uint32_t n_mt = (a.n_out + TG_BM - 1) / TG_BM, n_tt = (a.n_tok + BN - 1) / BN;
     const uint32_t ksplit = a.ksplit ? a.ksplit : 1;
     const uint32_t n_items = n_mt * n_tt * ksplit;
@@ -212,55 +280,97 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
     __syncthreads();
     tg_fence_after();
     const uint32_t tmem = tmem_slot;
+    pdl_launch_dependents();
+#ifdef TG_TRACE
+    if (threadIdx.x == 0) tr[1] = tg_now();
+#endif
 
     if (warp == 0) {
-        if (lane == 0) {  // TMA producer: the K slices of every work item of this CTA, in order
-            uint32_t it = 0;
-            for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-                uint32_t tile, ks, kb0, kb1, n0, t0;
-                tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
-                tg_tile<BN>(tile, n_mt, n0, t0);
-                for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
-                    const uint32_t s = it % S::STAGES;
+        // TMA producer (the whole warp walks the loop, one lane issues): the K
+        // slices of every work item of this CTA, in order. The weights are
+        // constant: the first ring of A tiles streams in while the previous
+        // kernel (which writes the B planes) finishes.
+        uint32_t it = 0;
+        for (uint32_t item = blockIdx.x; item < n_items && it < S::STAGES; item += gridDim.x) {
+            uint32_t tile, ks, kb0, kb1, n0, t0;
+            tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
+            tg_tile<BN>(tile, n_mt, n0, t0);
+            for (uint32_t kb = kb0; kb < kb1 && it < S::STAGES; ++kb, ++it) {
+                tg_expect_tx_w(&full[it], S::STAGE_BYTES);
+#ifdef TG_A_BULK
+                tg_bulk_w(smem + size_t(it) * S::STAGE_BYTES, a.a_ptr + (size_t(kb) * a.a_rows + n0) * TG_BK, TG_A_BYTES,
+                          &full[it]);
+#else
+                tg_tma_2d_w(smem + size_t(it) * S::STAGE_BYTES, &tmA, 0, int32_t(kb * a.a_rows + n0), &full[it]);
+#endif
+            }
+        }
+        const uint32_t pre = it;
+        pdl_wait();
+#ifdef TG_TRACE
+        if (lane == 0) tr[2] = tg_now();
+#endif
+        it = 0;
+        for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+            uint32_t tile, ks, kb0, kb1, n0, t0;
+            tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
+            tg_tile<BN>(tile, n_mt, n0, t0);
+            for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
+                const uint32_t s = it % S::STAGES;
+                uint8_t* st = smem + size_t(s) * S::STAGE_BYTES;
+                if (it >= pre) {
                     if (it >= S::STAGES) tg_mbar_wait(&empty[s], ((it / S::STAGES) & 1) ^ 1);
-                    uint8_t* st = smem + size_t(s) * S::STAGE_BYTES;
-                    tg_mbar_expect_tx(&full[s], S::STAGE_BYTES);
-                    tg_tma_2d(st, &tmA, 0, int32_t(kb * a.a_rows + n0), &full[s]);  // K-block-major A
-#pragma unroll
-                    for (int l = 0; l < TG_L; ++l)
-                        tg_tma_2d(st + TG_A_BYTES + l * S::B_BYTES, &tmB, int32_t(kb * TG_BK),
-                                  int32_t(l * a.limb_rows + t0), &full[s]);
+#ifdef TG_TRACE
+                    if (lane == 0 && it < 40) tr[8 + it] = tg_now();
+#endif
+                    tg_expect_tx_w(&full[s], S::STAGE_BYTES);
+#ifdef TG_A_BULK
+                    tg_bulk_w(st, a.a_ptr + (size_t(kb) * a.a_rows + n0) * TG_BK, TG_A_BYTES, &full[s]);
+#else
+                    tg_tma_2d_w(st, &tmA, 0, int32_t(kb * a.a_rows + n0), &full[s]);  // K-block-major A
+#endif
                 }
+#pragma unroll
+                for (int l = 0; l < TG_L; ++l)
+                    tg_tma_2d_w(st + TG_A_BYTES + l * S::B_BYTES, &tmB, int32_t(kb * TG_BK), int32_t(l * a.limb_rows + t0),
+                                &full[s]);
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer
-            uint32_t it = 0, j = 0;
-            for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++j) {
-                uint32_t tile, ks, kb0, kb1;
-                tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
-                const uint32_t b = j & 1;
-                if (j >= 2) tg_mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained set b
+        // MMA issuer (whole warp, one elected lane issues)
+        uint32_t it = 0, j = 0;
+        for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++j) {
+            uint32_t tile, ks, kb0, kb1;
+            tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
+            const uint32_t b = j & 1;
+            if (j >= 2) tg_mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained set b
+            tg_fence_after();
+            const uint32_t dacc = tmem + b * S::ACC;
+            for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
+                const uint32_t s = it % S::STAGES;
+                tg_mbar_wait(&full[s], (it / S::STAGES) & 1);
+#ifdef TG_TRACE
+                if (lane == 0 && it < 40) tr[48 + it] = tg_now();
+#endif
                 tg_fence_after();
-                const uint32_t dacc = tmem + b * S::ACC;
-                for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
-                    const uint32_t s = it % S::STAGES;
-                    tg_mbar_wait(&full[s], (it / S::STAGES) & 1);
-                    tg_fence_after();
-                    const uint32_t sa = tg_smem_u32(smem + size_t(s) * S::STAGE_BYTES);
-                    // the three limb tiles are contiguous 128B-swizzled rows: one
-                    // MMA with N = 3 BN reads them all (column l BN + t = limb l of token t)
+                const uint32_t sa = tg_smem_u32(smem + size_t(s) * S::STAGE_BYTES);
+                // the three limb tiles are contiguous 128B-swizzled rows: one
+                // MMA with N = 3 BN reads them all (column l BN + t = limb l of token t)
 #pragma unroll
-                    for (int kk = 0; kk < TG_BK / 32; ++kk)  // K = 32 bytes per MMA
-                        tg_mma(dacc, tg_desc(sa + 32 * kk), tg_desc(sa + TG_A_BYTES + 32 * kk), tg_idesc(TG_L * BN),
-                               (kb != kb0) || (kk != 0));
-                    tg_commit(&empty[s]);  // frees the stage once these MMAs have read it
-                }
-                tg_commit(&acc_full[b]);
+                for (int kk = 0; kk < TG_BK / 32; ++kk)  // K = 32 bytes per MMA
+                    tg_mma_w(dacc, tg_desc(sa + 32 * kk), tg_desc(sa + TG_A_BYTES + 32 * kk), tg_idesc(TG_L * BN),
+                             (kb != kb0) || (kk != 0));
+                tg_commit_w(&empty[s]);  // frees the stage once these MMAs have read it
             }
+            tg_commit_w(&acc_full[b]);
         }
     } else {
         // epilogue: thread = feature n, columns = tokens
+        if (a.epi == TG_SILU) {  // constant: before the dependency wait
+            for (int i = threadIdx.x - 64; i < 257; i += 128) s_lut[i] = a.lut[i];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+        pdl_wait();  // reads / writes data the previous kernels own
         const uint32_t q = warp & 3;
         const uint32_t fl = 32 * q + lane;  // feature within the tile
         uint32_t j = 0;
@@ -334,19 +444,25 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
                 for (int jj = 0; jj < 16; ++jj)
                     val[jj] = scale_row(int64_t(d[0][jj]) + (int64_t(d[1][jj]) << 8) + (int64_t(d[2][jj]) << 16), sc);
                 if (a.epi == TG_SILU) {
+                    // rows (2i, 2i+1) = (gate_i, up_i) sit on adjacent lanes; the
+                    // pair splits the tokens (even lane: even tokens, odd lane: odd
+                    // ones), so every lane runs half the SiLUs, branch-free
+                    const uint32_t odd = n & 1, i = n >> 1;
+                    const size_t plane = size_t(a.limb_rows_out) * a.ldp;
+                    bool bad = false;
 #pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) {
-                        const uint32_t t = t0 + c0 + jj;
-                        // rows (2i, 2i+1) = (gate_i, up_i) sit on adjacent lanes
-                        const int64_t up = __shfl_down_sync(0xffffffffu, val[jj], 1);
-                        if (nv && !(n & 1) && t < a.n_tok) {
-                            const int64_t hv = mul16(silu_q16(val[jj], a.lut), up);
-                            const uint32_t i = n >> 1;
+                    for (int jp = 0; jp < 8; ++jp) {
+                        const int64_t ve = val[2 * jp], vo = val[2 * jp + 1];
+                        const int64_t recv = __shfl_xor_sync(0xffffffffu, odd ? ve : vo, 1);
+                        const int64_t g = odd ? recv : ve, u = odd ? vo : recv;
+                        const uint32_t t = t0 + c0 + 2 * jp + odd;
+                        const int64_t hv = mul16(silu_q16(g, s_lut), u);
+                        if (nv && t < a.n_tok) {
                             if (a.y) a.y[size_t(t) * a.ldy + i] = hv;
-                            if (!put_sdigits(a.planes + size_t(t) * a.ldp + i, size_t(a.limb_rows_out) * a.ldp, hv))
-                                *a.wide = 1;
+                            bad |= !put_sdigits(a.planes + size_t(t) * a.ldp + i, plane, hv);
                         }
                     }
+                    if (bad) *a.wide = 1;
                 } else {
                     // RESID: all 16 residual loads in flight before the first store
                     // (the compiler may not hoist a load above a possibly aliasing store)
@@ -371,6 +487,9 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
     }
     tg_fence_before();
     __syncthreads();
+#ifdef TG_TRACE
+    if (threadIdx.x == 0) tr[3] = tg_now();
+#endif
     if (warp == 1) {
         tg_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(S::TMEM_COLS) : "memory");

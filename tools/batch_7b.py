@@ -9,7 +9,7 @@ m = P.gen_toy_model(7, cfg)
 gold = json.load(open("tests/golden/models_7b.json"))
 for B in [int(x) for x in (sys.argv[1:] or ["8", "64"])]:
     prompts = [P.prompt_from_seed(8 if i == 0 else 1000 + i, cfg.vocab, 16) for i in range(B)]
-    P.generate_greedy_batch(m, prompts[:2], 4)  # warm
+    P.generate_greedy_batch(m, prompts, 128)  # warm: buffers + the captured step graph
     t = time.perf_counter()
     res, path = P.generate_greedy_batch(m, prompts, 128)
     dt = time.perf_counter() - t

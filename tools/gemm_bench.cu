@@ -53,9 +53,22 @@ __global__ void fill_kernel(uint8_t* p, size_t n, uint32_t seed) {
         p[i] = uint8_t((i * 2654435761u + seed) >> 13);
 }
 
+static bool g_pdl = false;
+static cudaStream_t g_st = nullptr;
+
 template <int BN>
 static void launch(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs& a, uint32_t grid) {
-    limb_gemm_kernel<BN><<<grid, TG_THREADS, TgShape<BN>::SMEM>>>(ta, tb, a);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = TG_THREADS;
+    cfg.dynamicSmemBytes = TgShape<BN>::SMEM;
+    cfg.stream = g_st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, limb_gemm_kernel<BN>, ta, tb, a));
 }
 
 __global__ void empty_kernel(int* p) {
@@ -125,30 +138,86 @@ int main(int argc, char** argv) {
     a.scales = sc;
     a.y = y;
     a.ldy = N;
+    if (epi == TG_SILU) {  // exp LUT (any values in range), output planes for the next GEMM
+        std::vector<int64_t> lut(257);
+        for (int i = 0; i < 257; ++i) lut[i] = (int64_t(i) << 8);
+        int64_t* dl;
+        CK(cudaMalloc(&dl, 257 * 8));
+        CK(cudaMemcpy(dl, lut.data(), 257 * 8, cudaMemcpyHostToDevice));
+        a.lut = dl;
+        a.y = nullptr;
+        a.ldp = N / 2;
+        a.limb_rows_out = Tp;
+        CK(cudaMalloc(&a.planes, size_t(3) * Tp * a.ldp));
+        CK(cudaMalloc(&a.wide, 4));
+    }
     a.ksplit = std::max(1u, ks);
     a.partial = partial;
     a.tile_cnt = cnt;
     const uint32_t items = tiles * a.ksplit;
     const uint32_t grid = std::min<uint32_t>(items, per_sm * sms);
+#ifdef TG_TRACE
+    CK(cudaMalloc(&a.trace, size_t(grid) * 128 * 8));
+    CK(cudaMemset(a.trace, 0, size_t(grid) * 128 * 8));
+#endif
     auto go = [&](int i) {
+        a.a_ptr = W[i % nbuf];
         if (bn == 16) launch<16>(ta[i % nbuf], tb, a, grid);
         else launch<64>(ta[i % nbuf], tb, a, grid);
     };
+    // GB_PDL=1: programmatic dependent launches; GB_GRAPH=1: the R launches
+    // replayed from one CUDA graph (no host launch cost)
+    g_pdl = getenv("GB_PDL") && atoi(getenv("GB_PDL"));
+    const bool graph = getenv("GB_GRAPH") && atoi(getenv("GB_GRAPH"));
+    CK(cudaStreamCreateWithFlags(&g_st, cudaStreamNonBlocking));
     for (int i = 0; i < 10; ++i) go(i);
     CK(cudaDeviceSynchronize());
     const int R = 200;
+    cudaGraphExec_t ge = nullptr;
+    if (graph) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(g_st, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < R; ++i) go(i);
+        CK(cudaStreamEndCapture(g_st, &g));
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        CK(cudaGraphLaunch(ge, g_st));
+        CK(cudaStreamSynchronize(g_st));
+    }
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0));
-    for (int i = 0; i < R; ++i) go(i);
-    CK(cudaEventRecord(e1));
+    CK(cudaEventRecord(e0, g_st));
+    if (graph) CK(cudaGraphLaunch(ge, g_st));
+    else
+        for (int i = 0; i < R; ++i) go(i);
+    CK(cudaEventRecord(e1, g_st));
     CK(cudaEventSynchronize(e1));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     const double us = 1e3 * ms / R;
+#ifdef TG_TRACE
+    {  // the last launch's timeline, CTA 0 and the slowest CTA (ns from CTA 0's start)
+        std::vector<uint64_t> h(size_t(grid) * 128);
+        CK(cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost));
+        uint64_t t0 = ~0ull, tend = 0;
+        uint32_t slow = 0;
+        for (uint32_t c = 0; c < grid; ++c) {
+            t0 = std::min(t0, h[size_t(c) * 128]);
+            if (h[size_t(c) * 128 + 3] > tend) { tend = h[size_t(c) * 128 + 3]; slow = c; }
+        }
+        for (uint32_t c : {0u, slow}) {
+            const uint64_t* r = &h[size_t(c) * 128];
+            printf("CTA %u: start %lld setup %lld wait %lld end %lld\n  issue:", c, (long long)(r[0] - t0),
+                   (long long)(r[1] - t0), (long long)(r[2] - t0), (long long)(r[3] - t0));
+            for (int k = 0; k < 40; ++k) if (r[8 + k]) printf(" %lld", (long long)(r[8 + k] - t0));
+            printf("\n  full: ");
+            for (int k = 0; k < 40; ++k) if (r[48 + k]) printf(" %lld", (long long)(r[48 + k] - t0));
+            printf("\n");
+        }
+    }
+#endif
     const double ops = 2.0 * 3 * double(N) * K * T;
-    printf("N=%u K=%u T=%u bn=%u ksplit=%u epi=%u grid=%u: %.2f us  %.0f GB/s (weights)  %.1f TOP/s (limb ops)\n", N, K,
-           T, bn, a.ksplit, epi, grid, us, wbytes / us * 1e-3, ops / us * 1e-6);
+    printf("%s%sN=%u K=%u T=%u bn=%u ksplit=%u epi=%u grid=%u: %.2f us  %.0f GB/s (weights)  %.1f TOP/s (limb ops)\n", g_pdl ? "pdl " : "",
+           graph ? "graph " : "", N, K, T, bn, a.ksplit, epi, grid, us, wbytes / us * 1e-3, ops / us * 1e-6);
     return 0;
 }
