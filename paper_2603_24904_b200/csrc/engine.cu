@@ -108,7 +108,6 @@ DevCtx& dev_ctx(int device) {
         set(pf_attn_kernel<2>);
         set(pf_attn_kernel<4>);
         set(pf_attn_kernel<8>);
-        set(pf_attn_kernel<16>);
         set(bd_attn_kernel);
     }
     set_gemv_attrs<EPI_STORE, MODE_EMBED>();
@@ -409,6 +408,7 @@ struct PrefillWs {
     uint8_t* pa = nullptr;           // [3][cap_pad][Kd] limb planes of D-wide inputs
     uint8_t* ph = nullptr;           // [3][cap_pad][Kf] limb planes of the FFN hidden vector
     uint32_t* wide = nullptr;        // some value needed the exact path
+    int32_t* strips = nullptr;       // attention score / probability strips (pf_attn_strip_elems)
     CUtensorMap tm_pa, tm_ph;
 };
 
@@ -686,8 +686,8 @@ bool tc_prefill_ok(const dimg_session& s, uint32_t n) {
     const dimg_model& m = *s.m;
     const uint32_t mode = prefill_mode();
     if (mode == 2 || n == 0) return false;
-    if (m.dh % 4 || m.dh > 512 || m.dh / 2 > 1024 || n > kTcPrefillMaxTokens) return false;
-    if (pf_attn_smem(m.dh, n) > size_t(m.ctx->smem_optin)) return false;
+    if (m.dh % 4 || m.dh > 256 || n > kTcPrefillMaxTokens) return false;
+    if (pf_attn_smem(m.dh) > size_t(m.ctx->smem_optin)) return false;
     return mode == 1 || n >= 32;
 }
 
@@ -704,6 +704,7 @@ void ensure_prefill_ws(dimg_session& s, uint32_t n) {
     CK(cudaMemset(w.pa, 0, size_t(3) * w.cap_pad * m.Kd));
     CK(cudaMemset(w.ph, 0, size_t(3) * w.cap_pad * m.Kf));
     if (!w.wide) w.wide = s.mem.alloc<uint32_t>(1);
+    w.strips = s.mem.alloc<int32_t>(pf_attn_strip_elems(m.H, w.cap));
     w.tm_pa = tmap_bytes(w.pa, m.D, size_t(3) * w.cap_pad, m.Kd, TG_BN);
     w.tm_ph = tmap_bytes(w.ph, m.F, size_t(3) * w.cap_pad, m.Kf, TG_BN);
 }
@@ -714,8 +715,7 @@ void launch_pf_attn(uint32_t dh, dim3 grid, size_t smem, cudaStream_t st, A... a
     if (dpl <= 1) pf_attn_kernel<1><<<grid, PA_THREADS, smem, st>>>(args...);
     else if (dpl <= 2) pf_attn_kernel<2><<<grid, PA_THREADS, smem, st>>>(args...);
     else if (dpl <= 4) pf_attn_kernel<4><<<grid, PA_THREADS, smem, st>>>(args...);
-    else if (dpl <= 8) pf_attn_kernel<8><<<grid, PA_THREADS, smem, st>>>(args...);
-    else pf_attn_kernel<16><<<grid, PA_THREADS, smem, st>>>(args...);
+    else pf_attn_kernel<8><<<grid, PA_THREADS, smem, st>>>(args...);  // dh <= 256 (tc_prefill_ok)
 }
 
 // Positions 0..n-1 of the prompt through every layer on the tensor cores;
@@ -748,7 +748,7 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
         a.wide = w.wide;
         launch_limb_gemm(W.tmap, tb, a, st);
     };
-    const size_t asmem = pf_attn_smem(dh, n);
+    const size_t asmem = pf_attn_smem(dh);
     for (uint32_t l = 0; l < m.L; ++l) {
         const auto& lw = m.layers[l];
         pf_norm_limbs_kernel<<<n, 256, 0, st>>>(w.x, D, lw.attn_norm, lw.attn_unit, m.ctx->seeds, w.pa, w.cap_pad,
@@ -758,8 +758,9 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
                                                          s.vc + l * kv_layer, s.kc32 + l * kv_layer,
                                                          s.vc32 + l * kv_layer, size_t(m.cfg.max_ctx) * dh, w.wide);
         if (l + 1 == m.L) break;  // the last layer's output feeds only the lm_head
-        launch_pf_attn(dh, dim3(H, (n + PA_Q - 1) / PA_Q), asmem, st, w.qkv, n, D, dh, s.kc32 + l * kv_layer,
-                       s.vc32 + l * kv_layer, size_t(m.cfg.max_ctx) * dh, m.inv_scale, m.ctx->exp_lut, w.pa,
+        launch_pf_attn(dh, dim3(H, (n + PA_Q - 1) / PA_Q), asmem, st, (const int64_t*)w.qkv, n, D, dh,
+                       (const int32_t*)(s.kc32 + l * kv_layer), (const int32_t*)(s.vc32 + l * kv_layer),
+                       size_t(m.cfg.max_ctx) * dh, m.inv_scale, (const int64_t*)m.ctx->exp_lut, w.strips, w.pa,
                        w.cap_pad, m.Kd, w.wide);
         gemm(lw.wo, w.tm_pa, TG_RESID, w.x, D);
         pf_norm_limbs_kernel<<<n, 256, 0, st>>>(w.x, D, lw.ffn_norm, lw.ffn_unit, m.ctx->seeds, w.pa, w.cap_pad,

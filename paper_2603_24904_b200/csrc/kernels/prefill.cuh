@@ -118,13 +118,31 @@ __global__ void pf_rope_kv_kernel(int64_t* __restrict__ qkv, uint32_t D, uint32_
     if (!fits_i32(k0) || !fits_i32(k1) || !fits_i32(v0) || !fits_i32(v1) || !b23(q0) || !b23(q1)) *wide = 1;
 }
 
-constexpr int PA_Q = 16;        // queries per CTA (two per warp)
+constexpr int PA_Q = 32;        // queries per CTA
+constexpr int PA_QW = 4;        // queries per warp
 constexpr int PA_CH = 64;       // cached positions per K / V chunk
 constexpr int PA_THREADS = 256;
+static_assert(PA_Q == PA_QW * PA_THREADS / 32, "every warp owns PA_QW queries");
 
-__host__ __device__ constexpr size_t pf_attn_smem(uint32_t dh, uint32_t n) {
-    return size_t(PA_Q) * ((n + 3) & ~3u) * 4 + size_t(PA_CH) * dh * 4 + size_t(PA_Q) * dh * 4;
+// shared memory: K/V chunk double buffer + the CTA's queries + one chunk of
+// probabilities ([query][position])
+__host__ __device__ constexpr size_t pf_attn_smem(uint32_t dh) {
+    return 2 * size_t(PA_CH) * dh * 4 + size_t(PA_Q) * dh * 4 + size_t(PA_CH) * PA_Q * 4;
 }
+// global score / probability strips, [H][n rounded to PA_Q][ld] int32
+__host__ __device__ constexpr size_t pf_attn_strip_elems(uint32_t H, uint32_t n) {
+    return size_t(H) * ((n + PA_Q - 1) / PA_Q * PA_Q) * ((n + 3) & ~3u);
+}
+
+__device__ __forceinline__ void pa_cp16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<uint32_t>(
+                     __cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void pa_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void pa_cp_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void pa_cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Causal attention (proj/src/kernels.cpp:117-177) of n queries against the
 // cache of positions <= each query, exact:
@@ -134,27 +152,32 @@ __host__ __device__ constexpr size_t pf_attn_smem(uint32_t dh, uint32_t n) {
 //   PV: sum_p floor(p_p v_pj / 2^16) computed as
 //       (sum_p p v - sum_p (p v mod 2^16)) / 2^16 -- both sums exact (int64,
 //       and 16-bit remainders in 32 bits), the difference divisible by 2^16.
-// grid = (H, ceil(n / PA_Q)); each warp owns two queries. Scores, then
-// probabilities, live in shared memory as int32 (flagged if one does not
-// fit). K chunks are stored as 4-dim quads [dh/4][PA_CH] so a lane reads
-// 16 bytes per position; V chunks row-major. DPL = dims per lane in PV
-// (dh <= 32 DPL). Output: limb planes of the attention vector (WO's B operand).
+// grid = (H, ceil(n / PA_Q)); each warp owns PA_QW consecutive queries, so
+// every K / V value read from shared memory feeds PA_QW queries. The score
+// (then probability) strips live in a global scratch that stays in L2: a
+// lane writes and re-reads the same positions (p mod 32 = lane), and the PV
+// pass stages one chunk of them in shared memory after a CTA barrier. K / V
+// chunks are double-buffered with cp.async (K as 4-dim quads [dh/4][PA_CH]
+// so a lane reads 16 bytes per position; V row-major). DPL = dims per lane in
+// PV (dh <= 32 DPL). Output: digit planes of the attention vector (WO's B
+// operand); values outside the fast representation set *wide.
 template <int DPL>
-__global__ void __launch_bounds__(PA_THREADS) pf_attn_kernel(const int64_t* __restrict__ qkv, uint32_t n,
-                                                             uint32_t D, uint32_t dh,
-                                                             const int32_t* __restrict__ K32,
-                                                             const int32_t* __restrict__ V32,
-                                                             size_t head_stride, int64_t inv_scale,
-                                                             const int64_t* __restrict__ lut_g, uint8_t* planes,
-                                                             uint32_t rows_pad, uint32_t ldp, uint32_t* wide) {
+__global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* __restrict__ qkv, uint32_t n,
+                                                                uint32_t D, uint32_t dh,
+                                                                const int32_t* __restrict__ K32,
+                                                                const int32_t* __restrict__ V32,
+                                                                size_t head_stride, int64_t inv_scale,
+                                                                const int64_t* __restrict__ lut_g, int32_t* strips,
+                                                                uint8_t* planes, uint32_t rows_pad, uint32_t ldp,
+                                                                uint32_t* wide) {
     extern __shared__ __align__(16) uint8_t pa_smem[];
     __shared__ int64_t lut[257];
     const uint32_t h = blockIdx.x, q0 = blockIdx.y * PA_Q;
     const uint32_t npos = min(n, q0 + PA_Q);  // positions any query of this CTA sees
-    const uint32_t ld = (n + 3) & ~3u, nq = dh / 4;
-    int32_t* S = reinterpret_cast<int32_t*>(pa_smem);   // [PA_Q][ld]
-    int4* KV = reinterpret_cast<int4*>(S + size_t(PA_Q) * ld);  // K: [nq][PA_CH] quads; V: [PA_CH][nq]
-    int4* Q = KV + size_t(PA_CH) * nq;                   // [PA_Q][nq]
+    const uint32_t ld = (n + 3) & ~3u, nq = dh / 4, chunk_q = PA_CH * nq;
+    int4* KV = reinterpret_cast<int4*>(pa_smem);          // 2 x chunk: K [nq][PA_CH] quads / V [PA_CH][nq]
+    int4* Q = KV + 2 * size_t(chunk_q);                     // [PA_Q][nq]
+    int32_t* Ps = reinterpret_cast<int32_t*>(Q + size_t(PA_Q) * nq);  // [PA_Q][PA_CH]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 257; i += PA_THREADS) lut[i] = lut_g[i];
     for (uint32_t i = threadIdx.x; i < PA_Q * nq; i += PA_THREADS) {
@@ -168,119 +191,171 @@ __global__ void __launch_bounds__(PA_THREADS) pf_attn_kernel(const int64_t* __re
     }
     const int4* Kh = reinterpret_cast<const int4*>(K32 + size_t(h) * head_stride);
     const int4* Vh = reinterpret_cast<const int4*>(V32 + size_t(h) * head_stride);
-    const uint32_t ta = q0 + 2 * warp, tb = ta + 1;  // this warp's two queries
-    const int4* qa = Q + (2 * warp) * nq;
-    const int4* qb = qa + nq;
-    int32_t* Sa = S + size_t(2 * warp) * ld;
-    int32_t* Sb = Sa + ld;
+    const uint32_t tw = q0 + PA_QW * warp;  // this warp's first query
+    int32_t* Sw = strips + ((size_t(h) * gridDim.y + blockIdx.y) * PA_Q + PA_QW * warp) * ld;  // its rows
+    const uint32_t nch = (npos + PA_CH - 1) / PA_CH;
     int big = 0;
 
-    // scores (kernels.cpp:143-151): lane = positions c0 + lane, c0 + lane + 32
-    for (uint32_t c0 = 0; c0 < npos; c0 += PA_CH) {
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < PA_CH * nq; i += PA_THREADS) {
+    // ---- scores (kernels.cpp:143-151): lane = positions c0 + lane, c0 + lane + 32
+    auto load_k = [&](uint32_t c, int4* dst) {
+        const uint32_t c0 = c * PA_CH;
+        for (uint32_t i = threadIdx.x; i < chunk_q; i += PA_THREADS) {
             const uint32_t p = i / nq, jq = i % nq;
-            KV[jq * PA_CH + p] = c0 + p < npos ? Kh[size_t(c0 + p) * nq + jq] : make_int4(0, 0, 0, 0);
+            const bool ok = c0 + p < npos;
+            pa_cp16(dst + jq * PA_CH + p, Kh + size_t(ok ? c0 + p : 0) * nq + jq, ok);
         }
-        __syncthreads();
-        if (ta >= n || c0 > tb) continue;  // warp-uniform: nothing of this chunk is visible
-        int64_t a0 = 0, a1 = 0, b0 = 0, b1 = 0;
-#pragma unroll 4
-        for (uint32_t jq = 0; jq < nq; ++jq) {
-            const int4 x = qa[jq], y = qb[jq];
-            const int4 k0 = KV[jq * PA_CH + lane], k1 = KV[jq * PA_CH + lane + 32];
-            a0 += int64_t(x.x) * k0.x + int64_t(x.y) * k0.y + int64_t(x.z) * k0.z + int64_t(x.w) * k0.w;
-            a1 += int64_t(x.x) * k1.x + int64_t(x.y) * k1.y + int64_t(x.z) * k1.z + int64_t(x.w) * k1.w;
-            b0 += int64_t(y.x) * k0.x + int64_t(y.y) * k0.y + int64_t(y.z) * k0.z + int64_t(y.w) * k0.w;
-            b1 += int64_t(y.x) * k1.x + int64_t(y.y) * k1.y + int64_t(y.z) * k1.z + int64_t(y.w) * k1.w;
+        pa_cp_commit();
+    };
+    int32_t mx[PA_QW];
+#pragma unroll
+    for (int u = 0; u < PA_QW; ++u) mx[u] = INT32_MIN;
+    load_k(0, KV);
+    for (uint32_t c = 0; c < nch; ++c) {
+        int4* cur = KV + (c & 1) * chunk_q;
+        if (c + 1 < nch) {
+            load_k(c + 1, KV + ((c + 1) & 1) * chunk_q);
+            pa_cp_wait_prev();
+        } else {
+            pa_cp_wait_all();
         }
-        const uint32_t p0 = c0 + lane, p1 = p0 + 32;
-        if (p0 <= ta) {
-            const int64_t v = mul16(a0 >> 16, inv_scale);
-            big |= !fits_i32(v);
-            Sa[p0] = int32_t(v);
+        __syncthreads();  // chunk c visible to every warp
+        const uint32_t c0 = c * PA_CH;
+        if (tw < n && c0 <= tw + PA_QW - 1) {  // warp-uniform: part of this chunk is visible
+            int64_t acc[PA_QW][2];
+#pragma unroll
+            for (int u = 0; u < PA_QW; ++u) acc[u][0] = acc[u][1] = 0;
+            const int4* qw = Q + size_t(PA_QW * warp) * nq;
+#pragma unroll 2
+            for (uint32_t jq = 0; jq < nq; ++jq) {
+                const int4 k0 = cur[jq * PA_CH + lane], k1 = cur[jq * PA_CH + lane + 32];
+#pragma unroll
+                for (int u = 0; u < PA_QW; ++u) {
+                    const int4 x = qw[u * nq + jq];
+                    acc[u][0] += int64_t(x.x) * k0.x + int64_t(x.y) * k0.y + int64_t(x.z) * k0.z + int64_t(x.w) * k0.w;
+                    acc[u][1] += int64_t(x.x) * k1.x + int64_t(x.y) * k1.y + int64_t(x.z) * k1.z + int64_t(x.w) * k1.w;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < PA_QW; ++u) {
+                const uint32_t t = tw + u;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const uint32_t p = c0 + lane + 32 * e;
+                    if (t < n && p <= t) {
+                        const int64_t v = mul16(acc[u][e] >> 16, inv_scale);
+                        big |= !fits_i32(v);
+                        const int32_t v32 = int32_t(v);
+                        Sw[size_t(u) * ld + p] = v32;
+                        mx[u] = v32 > mx[u] ? v32 : mx[u];
+                    }
+                }
+            }
         }
-        if (p1 <= ta) {
-            const int64_t v = mul16(a1 >> 16, inv_scale);
-            big |= !fits_i32(v);
-            Sa[p1] = int32_t(v);
-        }
-        if (tb < n && p0 <= tb) {
-            const int64_t v = mul16(b0 >> 16, inv_scale);
-            big |= !fits_i32(v);
-            Sb[p0] = int32_t(v);
-        }
-        if (tb < n && p1 <= tb) {
-            const int64_t v = mul16(b1 >> 16, inv_scale);
-            big |= !fits_i32(v);
-            Sb[p1] = int32_t(v);
-        }
+        __syncthreads();  // everyone done with chunk c before it is overwritten
     }
-    // softmax_q16 (kernels.cpp:90-107), one warp per query row
+
+    // ---- softmax_q16 (kernels.cpp:90-107) over each of the warp's rows; a lane
+    // re-reads only positions it wrote (p = lane mod 32)
 #pragma unroll 1
-    for (int u = 0; u < 2; ++u) {
-        const uint32_t t = u ? tb : ta;
-        int32_t* R = u ? Sb : Sa;
-        if (t >= n) continue;
-        int32_t m = INT32_MIN;
-        for (uint32_t p = lane; p <= t; p += 32) m = R[p] > m ? R[p] : m;
-        m = __reduce_max_sync(0xffffffffu, m);
+    for (int u = 0; u < PA_QW; ++u) {
+        const uint32_t t = tw + u;
+        if (t >= n) break;
+        int32_t* R = Sw + size_t(u) * ld;
+        const int32_t m = __reduce_max_sync(0xffffffffu, mx[u]);
         uint32_t tot = 0;  // <= 2^16 per weight, n <= 2560 positions
         for (uint32_t p = lane; p <= t; p += 32) {
             const int64_t d = int64_t(m) - R[p];
-            const int64_t w = exp_neg(d > 8 * ONE ? 8 * ONE : d, lut);
-            R[p] = int32_t(w);
-            tot += uint32_t(w);
+            tot += uint32_t(exp_neg(d > 8 * ONE ? 8 * ONE : d, lut));
         }
         const uint64_t total = __reduce_add_sync(0xffffffffu, tot);
         const uint64_t inv = ~0ull / total;
         for (uint32_t p = lane; p <= t; p += 32) {
-            const uint64_t a = uint64_t(R[p]) << 16;
-            uint64_t qv = __umul64hi(a, inv);
-            qv += (a - qv * total) >= total;
-            R[p] = int32_t(qv);  // <= 2^16
+            const int64_t d = int64_t(m) - R[p];
+            const uint64_t w = uint64_t(exp_neg(d > 8 * ONE ? 8 * ONE : d, lut));
+            R[p] = int32_t(udiv_inv(w << 16, total, inv));  // <= 2^16
         }
     }
-    // PV (kernels.cpp:153-159): lane owns dims lane * DPL ... + DPL - 1
-    int64_t fa[DPL], fb[DPL];
-    uint32_t ra[DPL], rb[DPL];
+
+    // ---- PV (kernels.cpp:153-159): lane owns dims lane * DPL ... + DPL - 1
+    int64_t f[PA_QW][DPL];
+    uint32_t r[PA_QW][DPL];
 #pragma unroll
-    for (int z = 0; z < DPL; ++z) fa[z] = fb[z] = 0, ra[z] = rb[z] = 0;
+    for (int u = 0; u < PA_QW; ++u)
+#pragma unroll
+        for (int z = 0; z < DPL; ++z) f[u][z] = 0, r[u][z] = 0;
     const uint32_t jl = lane * DPL;  // first dim of this lane
     const bool lane_on = jl < dh;
-    for (uint32_t c0 = 0; c0 < npos; c0 += PA_CH) {
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < PA_CH * nq; i += PA_THREADS) {
+    const int32_t* Sc = strips + (size_t(h) * gridDim.y + blockIdx.y) * PA_Q * ld;  // the CTA's rows
+    auto load_v = [&](uint32_t c, int4* dst) {
+        const uint32_t c0 = c * PA_CH;
+        for (uint32_t i = threadIdx.x; i < chunk_q; i += PA_THREADS) {
             const uint32_t p = i / nq, jq = i % nq;
-            KV[p * nq + jq] = c0 + p < npos ? Vh[size_t(c0 + p) * nq + jq] : make_int4(0, 0, 0, 0);
+            const bool ok = c0 + p < npos;
+            pa_cp16(dst + p * nq + jq, Vh + size_t(ok ? c0 + p : 0) * nq + jq, ok);
+        }
+        pa_cp_commit();
+    };
+    __syncthreads();  // every row's probabilities written (global, same CTA)
+    load_v(0, KV);
+    for (uint32_t c = 0; c < nch; ++c) {
+        const int4* cur = KV + (c & 1) * chunk_q;
+        const uint32_t c0 = c * PA_CH;
+        // this chunk's probabilities, [query][position] (0 past each query)
+        for (uint32_t i = threadIdx.x; i < PA_CH * PA_Q; i += PA_THREADS) {
+            const uint32_t qi = i / PA_CH, pp = i % PA_CH, t = q0 + qi, p = c0 + pp;
+            Ps[i] = (t < n && p <= t) ? Sc[size_t(qi) * ld + p] : 0;
+        }
+        if (c + 1 < nch) {
+            load_v(c + 1, KV + ((c + 1) & 1) * chunk_q);
+            pa_cp_wait_prev();
+        } else {
+            pa_cp_wait_all();
         }
         __syncthreads();
-        if (ta >= n || c0 > tb || !lane_on) continue;
-        const uint32_t pend = min(uint32_t(PA_CH), min(npos, tb + 1) - c0);
-        const int32_t* Vs = reinterpret_cast<const int32_t*>(KV);
+        if (tw < n && c0 <= tw + PA_QW - 1 && lane_on) {
+            const uint32_t pend = min(uint32_t(PA_CH), min(npos, tw + PA_QW) - c0);
+            const int32_t* Vs = reinterpret_cast<const int32_t*>(cur);
 #pragma unroll 2
-        for (uint32_t pp = 0; pp < pend; ++pp) {
-            const uint32_t p = c0 + pp;
-            const int32_t pa = p <= ta ? Sa[p] : 0, pb = p <= tb && tb < n ? Sb[p] : 0;
-            const int32_t* vr = Vs + pp * dh + jl;
+            for (uint32_t pp = 0; pp < pend; ++pp) {
+                int32_t pq[PA_QW];
 #pragma unroll
-            for (int z = 0; z < DPL; ++z) {
-                const int32_t v = vr[z];
-                fa[z] += int64_t(pa) * v;
-                fb[z] += int64_t(pb) * v;
-                ra[z] += (uint32_t(pa) * uint32_t(v)) & 0xFFFFu;  // low bits of the exact product
-                rb[z] += (uint32_t(pb) * uint32_t(v)) & 0xFFFFu;
+                for (int u = 0; u < PA_QW; ++u) pq[u] = Ps[(PA_QW * warp + u) * PA_CH + pp];  // broadcast
+                int32_t vv[DPL];
+                if constexpr (DPL >= 4) {
+#pragma unroll
+                    for (int z = 0; z < DPL; z += 4) {
+                        const int4 q4 = *reinterpret_cast<const int4*>(Vs + pp * dh + jl + z);
+                        vv[z] = q4.x, vv[z + 1] = q4.y, vv[z + 2] = q4.z, vv[z + 3] = q4.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int z = 0; z < DPL; ++z) vv[z] = Vs[pp * dh + jl + z];
+                }
+#pragma unroll
+                for (int u = 0; u < PA_QW; ++u)
+#pragma unroll
+                    for (int z = 0; z < DPL; ++z) {
+                        // one wide product (the multiply pipe is the bound), its low
+                        // 16 bits summed separately on the ALU pipe
+                        const int64_t prod = int64_t(pq[u]) * vv[z];
+                        f[u][z] += prod;
+                        r[u][z] += uint32_t(prod) & 0xFFFFu;
+                    }
             }
         }
+        __syncthreads();  // chunk c and Ps consumed
     }
     if (lane_on) {
         const size_t plane = size_t(rows_pad) * ldp;
 #pragma unroll
-        for (int z = 0; z < DPL; ++z) {
-            const uint32_t j = jl + z;
-            if (j >= dh) break;
-            if (ta < n) pf_put_limbs(planes + size_t(ta) * ldp + h * dh + j, plane, (fa[z] - int64_t(ra[z])) >> 16, wide);
-            if (tb < n) pf_put_limbs(planes + size_t(tb) * ldp + h * dh + j, plane, (fb[z] - int64_t(rb[z])) >> 16, wide);
+        for (int u = 0; u < PA_QW; ++u) {
+            const uint32_t t = tw + u;
+            if (t >= n) break;
+#pragma unroll
+            for (int z = 0; z < DPL; ++z) {
+                const uint32_t j = jl + z;
+                if (j < dh) pf_put_limbs(planes + size_t(t) * ldp + h * dh + j, plane, (f[u][z] - int64_t(r[u][z])) >> 16, wide);
+            }
         }
     }
     if (big) *wide = 1;
