@@ -886,9 +886,10 @@ void batch_alloc(BatchRun& r, dimg_model* m, uint32_t B, uint32_t ctx, uint32_t 
     for (uint32_t rw : rows) {
         const uint32_t tiles = (rw + TG_BM - 1) / TG_BM * tok_tiles;
         r.tiles_max = std::max(r.tiles_max, tiles);
-        r.partial_elems = std::max(r.partial_elems, size_t(tiles) * 8 * TG_L * bn * TG_BM);
+        r.partial_elems = std::max(r.partial_elems, size_t(tiles) * TG_L * bn * TG_BM);
     }
     r.partial = r.mem.alloc<int32_t>(r.partial_elems);
+    CK(cudaMemsetAsync(r.partial, 0, r.partial_elems * 4, r.st));
     r.tile_cnt = r.mem.alloc<uint32_t>(r.tiles_max);
     CK(cudaMemsetAsync(r.tile_cnt, 0, size_t(r.tiles_max) * 4, r.st));
 }
@@ -903,9 +904,12 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
     launch_k(true, bd_embed_kernel, 1024, 256, 0, st, bt, n, (const int8_t*)m.embd, (const int64_t*)m.embd_s, D, r.x);
     const bool small = n <= uint32_t(TG_BN_SMALL);
     const uint32_t bn = small ? TG_BN_SMALL : TG_BN;
-    // split-K only pays for small token tiles (DIMG_SPLITK=0/1 overrides)
+    // split-K (DIMG_SPLITK=0 turns it off): 16-token tiles split whenever the
+    // tiles leave CTA slots free (two CTAs per SM); 64-token tiles only for
+    // long K (w_down), where the saved K blocks outweigh the accumulation
+    // traffic (tools/gemm_bench.cu: 30 -> 22 us at 64 tokens)
     const char* sk = std::getenv("DIMG_SPLITK");
-    const bool split_k = sk ? std::atoi(sk) != 0 : small;
+    const bool split_k = sk ? std::atoi(sk) != 0 : true;
     int sms = m.ctx->sm_count;
     auto gemm = [&](const DevMat& W, const CUtensorMap& tb_big, uint32_t epi, int64_t* y, uint32_t ldy) {
         const bool in_h = &tb_big == &r.tm_ph;
@@ -925,8 +929,11 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
         a.ldp = m.Kf;
         a.lut = m.ctx->exp_lut;
         a.wide = r.wide;
-        a.ksplit = split_k ? pick_ksplit(gemm_tiles(a, bn), a.n_kblk, 2 * uint32_t(sms)) : 1;
-        if (size_t(gemm_tiles(a, bn)) * a.ksplit * TG_L * bn * TG_BM > r.partial_elems) a.ksplit = 1;
+        a.ksplit = !split_k ? 1
+                   : small  ? pick_ksplit(gemm_tiles(a, bn), a.n_kblk, 2 * uint32_t(sms))
+                   : a.n_kblk >= 64 ? std::min(4u, pick_ksplit(gemm_tiles(a, bn), a.n_kblk, uint32_t(sms)))
+                                    : 1;
+        if (size_t(gemm_tiles(a, bn)) * TG_L * bn * TG_BM > r.partial_elems) a.ksplit = 1;
         a.partial = r.partial;
         a.tile_cnt = r.tile_cnt;
         launch_limb_gemm(W.tmap, tb, a, st, bn, true);

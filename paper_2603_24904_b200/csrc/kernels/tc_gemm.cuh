@@ -57,7 +57,8 @@ struct TgShape {
     static constexpr int STAGES = RING / STAGE_BYTES;
     static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;  // + alignment slack
     static constexpr int ACC = TG_L * BN;  // TMEM columns of one tile's accumulators
-    static constexpr uint32_t TMEM_COLS = 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
+    static constexpr int NB = 2;  // accumulator sets (double-buffered: epilogue || next MMAs)
+    static constexpr uint32_t TMEM_COLS = NB * ACC <= 128 ? 128 : NB * ACC <= 256 ? 256 : 512;
 };
 
 enum { TG_STORE = 0, TG_RESID = 1, TG_SILU = 2 };
@@ -78,10 +79,12 @@ struct TgArgs {
     const int64_t* lut;     // exp LUT (SILU)
     uint32_t* wide;         // set to 1 if an output needs more than 3 limbs (SILU planes)
     // split-K (few output tiles, e.g. decode batches): ksplit CTAs share a
-    // tile; each stores its int32 limb partials, the last one to finish sums
-    // them (integer sums: exact in any order) and runs the epilogue.
+    // tile; each adds its int32 limb partials into the tile's accumulator
+    // with red.global.add (integer sums: exact in any order, and the total
+    // is the unsplit int32 accumulator, so no overflow), the last one to
+    // finish reads it once, zeroes it and runs the epilogue.
     uint32_t ksplit;
-    int32_t* partial;       // [tiles][ksplit][3][BN][128]
+    int32_t* partial;       // [tiles][3][BN][128], zero between launches (the last CTA resets)
     uint32_t* tile_cnt;     // [tiles], zero between launches (the last CTA resets)
     const uint8_t* a_ptr;   // TG_A_BULK experiment: the A operand for 1-D bulk copies
 #ifdef TG_TRACE
@@ -342,8 +345,8 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
         for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++j) {
             uint32_t tile, ks, kb0, kb1;
             tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
-            const uint32_t b = j & 1;
-            if (j >= 2) tg_mbar_wait(&acc_empty[b], ((j >> 1) & 1) ^ 1);  // epilogue drained set b
+            const uint32_t b = j % S::NB;
+            if (j >= S::NB) tg_mbar_wait(&acc_empty[b], ((j / S::NB) & 1) ^ 1);  // epilogue drained set b
             tg_fence_after();
             const uint32_t dacc = tmem + b * S::ACC;
             for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
@@ -378,16 +381,16 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
             uint32_t tile, ks, kb0, kb1, n0, t0;
             tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
             tg_tile<BN>(tile, n_mt, n0, t0);
-            const uint32_t b = j & 1;
+            const uint32_t b = j % S::NB;
             const uint32_t n = n0 + fl;
             const bool nv = n < a.n_out;
-            tg_mbar_wait(&acc_full[b], (j >> 1) & 1);
+            tg_mbar_wait(&acc_full[b], (j / S::NB) & 1);
             tg_fence_after();
             const uint32_t tbase = tmem + ((32 * q) << 16) + b * S::ACC;
-            int32_t* part = ksplit > 1 ? a.partial + (size_t(tile) * ksplit) * (TG_L * BN * TG_BM) : nullptr;
+            int32_t* part = ksplit > 1 ? a.partial + size_t(tile) * (TG_L * BN * TG_BM) : nullptr;
             bool last = true;
             if (ksplit > 1) {
-                // this split's partials -> global, then the last split of the tile sums them
+                // this split's partials added into the tile accumulator (fire and forget)
                 for (uint32_t c0 = 0; c0 < BN; c0 += 16) {
                     int32_t d[TG_L][16];
 #pragma unroll
@@ -397,7 +400,9 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
                     for (int l = 0; l < TG_L; ++l)
 #pragma unroll
                         for (int jj = 0; jj < 16; ++jj)
-                            part[((size_t(ks) * TG_L + l) * BN + c0 + jj) * TG_BM + fl] = d[l][jj];
+                            asm volatile("red.global.add.s32 [%0], %1;" ::"l"(part + (size_t(l) * BN + c0 + jj) * TG_BM + fl),
+                                         "r"(d[l][jj])
+                                         : "memory");
                 }
                 tg_fence_before();
                 __syncwarp();
@@ -417,18 +422,15 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
             for (uint32_t c0 = 0; c0 < BN; c0 += 16) {
                 int32_t d[TG_L][16];
                 if (ksplit > 1) {
-                    // sum the splits: 48 independent loads in flight per split
+                    // the summed accumulator: 48 independent loads, then zero it for the next launch
 #pragma unroll
                     for (int l = 0; l < TG_L; ++l)
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) d[l][jj] = 0;
-                    for (uint32_t k2 = 0; k2 < ksplit; ++k2) {
-                        const int32_t* pk = part + (size_t(k2) * TG_L * BN + c0) * TG_BM + fl;
+                        for (int jj = 0; jj < 16; ++jj) d[l][jj] = __ldcg(part + (size_t(l) * BN + c0 + jj) * TG_BM + fl);
 #pragma unroll
-                        for (int l = 0; l < TG_L; ++l)
+                    for (int l = 0; l < TG_L; ++l)
 #pragma unroll
-                            for (int jj = 0; jj < 16; ++jj) d[l][jj] += __ldcg(pk + (size_t(l) * BN + jj) * TG_BM);
-                    }
+                        for (int jj = 0; jj < 16; ++jj) __stcg(part + (size_t(l) * BN + c0 + jj) * TG_BM + fl, 0);
                 } else {
 #pragma unroll
                     for (int l = 0; l < TG_L; ++l) tg_ld16(tbase + l * BN + c0, d[l]);

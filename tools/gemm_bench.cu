@@ -122,7 +122,8 @@ int main(int argc, char** argv) {
     const uint32_t tiles = (rows128 / 128) * ((T + bn - 1) / bn);
     int32_t* partial;
     uint32_t* cnt;
-    CK(cudaMalloc(&partial, size_t(tiles) * std::max(1u, ks) * 3 * bn * 128 * 4));
+    CK(cudaMalloc(&partial, size_t(tiles) * 3 * bn * 128 * 4));
+    CK(cudaMemset(partial, 0, size_t(tiles) * 3 * bn * 128 * 4));
     CK(cudaMalloc(&cnt, size_t(tiles) * 4));
     CK(cudaMemset(cnt, 0, size_t(tiles) * 4));
     std::vector<CUtensorMap> ta(nbuf);
