@@ -410,6 +410,10 @@ struct PrefillWs {
     uint32_t* wide = nullptr;        // some value needed the exact path
     int32_t* strips = nullptr;       // attention score / probability strips (pf_attn_strip_elems)
     CUtensorMap tm_pa, tm_ph;
+    CUtensorMap tm_pa_s, tm_ph_s;    // box rows TG_BN_SMALL (prompts of <= 16 tokens)
+    int32_t* partial = nullptr;      // split-K accumulators of the 16-token tiles (zero between launches)
+    uint32_t* tile_cnt = nullptr;
+    size_t partial_elems = 0;
 };
 
 struct dimg_session {
@@ -672,10 +676,11 @@ void begin(dimg_session& s, const uint32_t* prompt, uint32_t p, uint32_t n, bool
 
 uint32_t n_layer_stages(const dimg_session& s) { return 5 * s.m->L; }
 
-// Largest prompt the tensor-core prefill takes (the attention kernel keeps a
-// query tile's score rows in shared memory); longer prompts and shapes it
-// does not cover go through the decode kernel, one token per step.
-constexpr uint32_t kTcPrefillMaxTokens = 2560;
+// Largest prompt the tensor-core prefill takes (its attention keeps every
+// head's score strips in a global scratch of H * n^2 int32, 2 GB at 4096
+// tokens and 32 heads); longer prompts and shapes it does not cover go
+// through the decode kernel, one token per step.
+constexpr uint32_t kTcPrefillMaxTokens = 4096;
 
 uint32_t prefill_mode() {  // DIMG_PREFILL: 0 auto, 1 always tensor cores, 2 always decode steps
     const char* v = std::getenv("DIMG_PREFILL");
@@ -688,7 +693,7 @@ bool tc_prefill_ok(const dimg_session& s, uint32_t n) {
     if (mode == 2 || n == 0) return false;
     if (m.dh % 4 || m.dh > 256 || n > kTcPrefillMaxTokens) return false;
     if (pf_attn_smem(m.dh) > size_t(m.ctx->smem_optin)) return false;
-    return mode == 1 || n >= 32;
+    return mode == 1 || n >= 3;  // tools/prefill_small.py: 3.3 ms flat vs 1.7 ms per decode step
 }
 
 void ensure_prefill_ws(dimg_session& s, uint32_t n) {
@@ -707,6 +712,16 @@ void ensure_prefill_ws(dimg_session& s, uint32_t n) {
     w.strips = s.mem.alloc<int32_t>(pf_attn_strip_elems(m.H, w.cap));
     w.tm_pa = tmap_bytes(w.pa, m.D, size_t(3) * w.cap_pad, m.Kd, TG_BN);
     w.tm_ph = tmap_bytes(w.ph, m.F, size_t(3) * w.cap_pad, m.Kf, TG_BN);
+    w.tm_pa_s = tmap_bytes(w.pa, m.D, size_t(3) * w.cap_pad, m.Kd, TG_BN_SMALL);
+    w.tm_ph_s = tmap_bytes(w.ph, m.F, size_t(3) * w.cap_pad, m.Kf, TG_BN_SMALL);
+    if (!w.partial) {  // one 16-token tile column: the largest matrix's row tiles
+        const uint32_t tiles = (std::max({3 * m.D, 2 * m.F, m.V}) + TG_BM - 1) / TG_BM;
+        w.partial_elems = size_t(tiles) * TG_L * TG_BN_SMALL * TG_BM;
+        w.partial = s.mem.alloc<int32_t>(w.partial_elems);
+        w.tile_cnt = s.mem.alloc<uint32_t>(tiles);
+        CK(cudaMemset(w.partial, 0, w.partial_elems * 4));
+        CK(cudaMemset(w.tile_cnt, 0, size_t(tiles) * 4));
+    }
 }
 
 template <class... A>
@@ -730,7 +745,12 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
     CK(cudaMemsetAsync(w.wide, 0, 4, st));
     CK(cudaMemsetAsync(s.kvwide, 0, size_t(m.L) * H * 4, st));
     pf_embed_kernel<<<1024, 256, 0, st>>>(s.tokens, n, m.embd, m.embd_s, D, w.x);
-    auto gemm = [&](const DevMat& W, const CUtensorMap& tb, uint32_t epi, int64_t* y, uint32_t ldy) {
+    // short prompts: 16-token tiles split over K (one split per CTA slot), as the decode batches
+    const bool small = n <= uint32_t(TG_BN_SMALL);
+    const uint32_t bn = small ? TG_BN_SMALL : TG_BN;
+    const uint32_t sms = uint32_t(m.ctx->sm_count);
+    auto gemm = [&](const DevMat& W, const CUtensorMap& tb_big, uint32_t epi, int64_t* y, uint32_t ldy) {
+        const CUtensorMap& tb = !small ? tb_big : (&tb_big == &w.tm_ph ? w.tm_ph_s : w.tm_pa_s);
         TgArgs a{};
         a.n_out = W.rows;
         a.a_rows = W.rows128;
@@ -746,7 +766,12 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
         a.ldp = m.Kf;
         a.lut = m.ctx->exp_lut;
         a.wide = w.wide;
-        launch_limb_gemm(W.tmap, tb, a, st);
+        if (small) {
+            a.ksplit = pick_ksplit(gemm_tiles(a, bn), a.n_kblk, 2 * sms);
+            a.partial = w.partial;
+            a.tile_cnt = w.tile_cnt;
+        }
+        launch_limb_gemm(W.tmap, tb, a, st, bn);
     };
     const size_t asmem = pf_attn_smem(dh);
     for (uint32_t l = 0; l < m.L; ++l) {
