@@ -212,6 +212,13 @@ dimg_status dimg_op_dense(int device, const dimg_qtensor* w, const int64_t* x, i
 /* dense_forward (proj/src/kernels.cpp:18-30) applied to T tokens x[T][cols]
  * -> out[T][rows]: the prefill GEMM (tcgen05 kind::i8 over byte limbs). */
 dimg_status dimg_op_dense_tokens(int device, const dimg_qtensor* w, const int64_t* x, uint32_t T, int64_t* out);
+/* BLAKE3 (hash mode, 32 bytes) on the GPU: weight_hash / deserialize of the
+ * model bytes (proj/src/model.cpp:310-316, attest.cpp:93) as a tree hash at
+ * HBM speed. _device: `data` is a device pointer on `device` (ms, if not
+ * NULL, receives the kernels' CUDA-event time); _gpu: host bytes, uploaded
+ * first. Bit-identical to dimg_blake3. */
+dimg_status dimg_blake3_device(int device, const void* data, size_t len, uint8_t out[32], float* ms);
+dimg_status dimg_blake3_gpu(int device, const void* data, size_t len, uint8_t out[32]);
 dimg_status dimg_op_rmsnorm(int device, const int64_t* x, const int64_t* g, uint32_t n,
                             int64_t* out);
 dimg_status dimg_op_softmax(int device, const int64_t* s, uint32_t n, int64_t* out);

@@ -91,6 +91,8 @@ def _load():
         "dimg_session_trace": ([vp, C.c_uint32, u64p, C.c_uint32], C.c_int),
         "dimg_op_dense": ([C.c_int, C.POINTER(QTensor), i64p, i64p], C.c_int),
         "dimg_op_dense_tokens": ([C.c_int, C.POINTER(QTensor), i64p, C.c_uint32, i64p], C.c_int),
+        "dimg_blake3_device": ([C.c_int, vp, C.c_size_t, u8p, C.POINTER(C.c_float)], C.c_int),
+        "dimg_blake3_gpu": ([C.c_int, vp, C.c_size_t, u8p], C.c_int),
         "dimg_op_rmsnorm": ([C.c_int, i64p, i64p, C.c_uint32, i64p], C.c_int),
         "dimg_op_softmax": ([C.c_int, i64p, C.c_uint32, i64p], C.c_int),
         "dimg_op_attention": ([C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_uint32,

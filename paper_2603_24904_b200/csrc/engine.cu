@@ -33,6 +33,8 @@
 #include "kernels/tc_gemm.cuh"
 #include "kernels/prefill.cuh"
 #include "kernels/batch.cuh"
+#include "kernels/blake3.cuh"
+#include "host/blake3.hpp"
 
 using namespace dimg;
 using namespace dimg::dev;
@@ -1617,6 +1619,64 @@ dimg_status dimg_op_dense(int device, const dimg_qtensor* w, const int64_t* x, i
         launch_gemv<EPI_STORE, MODE_PLAIN>(a, o.c, o.c.op_stream);
         CK(cudaGetLastError());
         o.get(out, a.y, w->rows);
+    })
+}
+
+// BLAKE3 of len device bytes on stream st: the chunk kernel folds 256
+// chunks per CTA, each further launch 256 nodes, until the root
+// (kernels/blake3.cuh). ms (optional): CUDA-event time of the kernels.
+static void blake3_device_run(const uint8_t* d, size_t len, uint8_t out[32], cudaStream_t st, DevBuf& mem,
+                              float* ms) {
+    if (len == 0) {  // one empty chunk: nothing to stream
+        const auto h = b3::hash(nullptr, 0, 1);
+        std::memcpy(out, h.data(), 32);
+        if (ms) *ms = 0.f;
+        return;
+    }
+    const uint64_t n_chunks = (len + 1023) / 1024;
+    uint64_t g = (n_chunks + B3_FOLD - 1) / B3_FOLD;
+    uint32_t* a = mem.alloc<uint32_t>(g * 8);
+    uint32_t* b = mem.alloc<uint32_t>(((g + B3_FOLD - 1) / B3_FOLD) * 8 + 8);
+    uint32_t* root = mem.alloc<uint32_t>(8);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ms) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, st));
+    }
+    b3_chunks_kernel<<<uint32_t(g), B3_FOLD, 0, st>>>(d, len, a, root);
+    for (uint64_t cnt = g; cnt > 1; cnt = (cnt + B3_FOLD - 1) / B3_FOLD) {
+        b3_fold_kernel<<<uint32_t((cnt + B3_FOLD - 1) / B3_FOLD), B3_FOLD, 0, st>>>(a, cnt, b, root);
+        std::swap(a, b);
+    }
+    CK(cudaGetLastError());
+    if (ms) {
+        CK(cudaEventRecord(e1, st));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    CK(cudaMemcpyAsync(out, root, 32, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+}
+
+dimg_status dimg_blake3_device(int device, const void* data, size_t len, uint8_t out[32], float* ms) {
+    // weight_hash / deserialize (proj/src/model.cpp:310-316) on device-resident bytes
+    DIMG_API_GUARD({
+        if (!data && len) fail(DIMG_EINVAL, "blake3_device: null data");
+        OpScope o(device);
+        blake3_device_run(static_cast<const uint8_t*>(data), len, out, o.c.op_stream, o.mem, ms);
+    })
+}
+
+dimg_status dimg_blake3_gpu(int device, const void* data, size_t len, uint8_t out[32]) {
+    // the same for host bytes: one upload, then the device tree hash
+    DIMG_API_GUARD({
+        if (!data && len) fail(DIMG_EINVAL, "blake3_gpu: null data");
+        OpScope o(device);
+        const uint8_t* d = o.put(static_cast<const uint8_t*>(data), len);
+        blake3_device_run(d, len, out, o.c.op_stream, o.mem, nullptr);
     })
 }
 

@@ -271,6 +271,25 @@ def dense_forward(w, scales, x, device: int = 0) -> np.ndarray:
     return out
 
 
+def blake3_gpu(data, device: int = 0) -> bytes:
+    """BLAKE3 of host bytes on the GPU (upload + device tree hash): the
+    model-bytes hash of weight_hash (proj/src/model.cpp:310-316)."""
+    buf = np.frombuffer(memoryview(data).cast("B"), np.uint8) if not isinstance(data, np.ndarray) \
+        else np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+    out = (C.c_uint8 * 32)()
+    check(lib.dimg_blake3_gpu(device, buf.ctypes.data_as(C.c_void_p), buf.size, out))
+    return bytes(out)
+
+
+def blake3_device(ptr: int, length: int, device: int = 0, timed: bool = False):
+    """BLAKE3 of `length` bytes at device pointer `ptr` (e.g. a CUDA tensor's
+    data_ptr()); with timed=True returns (digest, kernel ms)."""
+    out = (C.c_uint8 * 32)()
+    ms = C.c_float()
+    check(lib.dimg_blake3_device(device, C.c_void_p(ptr), length, out, C.byref(ms) if timed else None))
+    return (bytes(out), ms.value) if timed else bytes(out)
+
+
 def dense_tokens(w, scales, x, device: int = 0) -> np.ndarray:
     """dense_forward for every row of x [T, cols] -> [T, rows]: the prefill
     GEMM on the tensor cores (exact byte-limb int8 products)."""
