@@ -219,6 +219,44 @@ dimg_status dimg_op_dense_tokens(int device, const dimg_qtensor* w, const int64_
  * first. Bit-identical to dimg_blake3. */
 dimg_status dimg_blake3_device(int device, const void* data, size_t len, uint8_t out[32], float* ms);
 dimg_status dimg_blake3_gpu(int device, const void* data, size_t len, uint8_t out[32]);
+
+/* Attestation (proj/include/dim/attest.hpp:16-68, proj/src/attest.cpp). The
+ * 112-byte wire format: model_id | input_hash | output_hash | bond (u64 LE) |
+ * challenge_period (u64 LE). decode of any other size: DIMG_EPARSE with
+ * parse kind DIMG_PARSE_TRUNCATED. */
+typedef struct {
+    uint8_t model_id[32];     /* BLAKE3 of the model bytes */
+    uint8_t input_hash[32];   /* hash_token_ids(prompt) */
+    uint8_t output_hash[32];  /* GenerationResult::output_hash */
+    uint64_t bond, challenge_period;
+} dimg_attestation;
+/* VerifyOutcome: confirmed, or refuted at stage 0 model / 1 input / 2 output
+ * with the claimed (expected) and recomputed (found) digests. */
+typedef struct {
+    uint32_t confirmed;
+    uint32_t refuted_stage;
+    uint8_t expected[32], found[32];
+} dimg_verify_outcome;
+dimg_status dimg_attestation_encode(const dimg_attestation* a, uint8_t out[112]);
+dimg_status dimg_attestation_decode(const uint8_t* bytes, size_t n, dimg_attestation* out);
+/* to_text (attest.cpp:54-62); writes at most cap-1 chars + NUL, *len = full length */
+dimg_status dimg_attestation_text(const dimg_attestation* a, char* buf, size_t cap, size_t* len);
+/* make_attestation (attest.cpp:68-78): the model id by the GPU BLAKE3 on `device`. */
+dimg_status dimg_make_attestation(int device, const uint8_t* model_bytes, size_t n_bytes, const uint32_t* prompt,
+                                  size_t n_prompt, const uint8_t output_hash[32], uint64_t bond,
+                                  uint64_t challenge_period, dimg_attestation* out);
+/* verify_by_reexecution (attest.cpp:89-117): model id (GPU BLAKE3), input hash,
+ * then deserialize + one greedy re-execution on `device`; the first stage
+ * that differs refutes. Unparseable model bytes: DIMG_EPARSE (no verdict). */
+dimg_status dimg_verify_by_reexecution(int device, const dimg_attestation* att, const uint8_t* model_bytes,
+                                       size_t n_bytes, const uint32_t* prompt, size_t n_prompt, uint32_t max_new,
+                                       dimg_verify_outcome* out);
+/* dispute_game (attest.cpp:119-125): *winner 0 = attester, 1 = challenger. */
+dimg_status dimg_dispute_game(int device, const dimg_attestation* att, const uint8_t* model_bytes, size_t n_bytes,
+                              const uint32_t* prompt, size_t n_prompt, uint32_t max_new, uint32_t* winner,
+                              dimg_verify_outcome* out);
+/* generation_counter (engine.cpp:165-168): generation runs in this process. */
+dimg_status dimg_generation_counter(uint64_t* out);
 dimg_status dimg_op_rmsnorm(int device, const int64_t* x, const int64_t* g, uint32_t n,
                             int64_t* out);
 dimg_status dimg_op_softmax(int device, const int64_t* s, uint32_t n, int64_t* out);

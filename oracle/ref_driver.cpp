@@ -8,11 +8,14 @@
 // proj/include/dim/kernels.hpp) without its CLI. Nothing here reimplements
 // reference behaviour; it only marshals plain buffers into dim:: types.
 #include <cstdint>
+#include <cstdio>
+#include <string>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
 #include <vector>
 
+#include "dim/attest.hpp"
 #include "dim/blake3.hpp"
 #include "dim/chacha20.hpp"
 #include "dim/engine.hpp"
@@ -276,5 +279,30 @@ int ref_session_forward(void* s, uint32_t token, uint32_t pos, int64_t* logits, 
     })
 }
 uint64_t ref_generation_counter() { return generation_counter().load(); }
+
+// ---- attestation (proj/src/attest.cpp) ----------------------------------------
+// make_attestation of a fresh greedy generation: wire bytes + to_text
+int ref_attestation(void* m, const uint32_t* prompt, uint32_t p, uint32_t n, uint64_t bond, uint64_t period,
+                    uint8_t wire[112], char* text, size_t cap) {
+    GUARD({
+        auto& mf = *static_cast<ModelFile*>(m);
+        const std::span<const uint32_t> pr(prompt, p);
+        const auto a = make_attestation(mf.bytes, pr, generate_greedy(mf, pr, n), bond, period);
+        const auto w = a.encode();
+        std::memcpy(wire, w.data(), 112);
+        const std::string t = a.to_text();
+        std::snprintf(text, cap, "%s", t.c_str());
+    })
+}
+// verify_by_reexecution of wire bytes: the outcome's to_text
+int ref_verify(const uint8_t* wire, void* m, const uint32_t* prompt, uint32_t p, uint32_t n, char* text,
+               size_t cap) {
+    GUARD({
+        auto& mf = *static_cast<ModelFile*>(m);
+        const auto a = Attestation::decode(std::span<const uint8_t>(wire, 112));
+        const auto o = verify_by_reexecution(a, mf.bytes, std::span<const uint32_t>(prompt, p), n);
+        std::snprintf(text, cap, "%s", o.to_text().c_str());
+    })
+}
 
 } // extern "C"

@@ -4,7 +4,9 @@ ARC engine, as re-created by the reference `dim`).
 Public API mirrors proj/include/dim/{engine,model}.hpp; everything executes in
 libdimg.so (sm_100a kernels + C++ host library) through include/dimg.h.
 """
-from . import errors
+from . import attest, errors
+from .attest import (Attestation, DisputeResult, VerifyOutcome, dispute_game, make_attestation, prompt_hash,
+                     verify_by_reexecution)
 from ._lib import LIB_PATH, lib
 from .engine import (EngineOptions, GenerationResult, InferenceSession, attention_steps, blake3_device,
                      blake3_gpu, build_rope_tables, dense_forward, dense_tokens, device_count, ffn_silu, generate_greedy,
@@ -22,5 +24,6 @@ __all__ = [
     "device_count", "release_sessions", "ModelConfig", "ModelFile", "DeviceModel",
     "gen_toy_model", "deserialize", "load_model", "weight_hash", "ONE", "errors",
     "ContextOverflow", "DomainError", "InvalidArgument", "LengthError", "LogicError",
-    "OutOfRange", "ParseError", "LIB_PATH", "lib",
+    "OutOfRange", "ParseError", "LIB_PATH", "lib", "attest", "Attestation", "VerifyOutcome", "DisputeResult",
+    "make_attestation", "verify_by_reexecution", "dispute_game", "prompt_hash",
 ]

@@ -36,6 +36,16 @@ class ModelDesc(C.Structure):
                 ("rope_sin", i64p), ("rope_max_ctx", C.c_uint32)]
 
 
+class Attestation(C.Structure):
+    _fields_ = [("model_id", C.c_uint8 * 32), ("input_hash", C.c_uint8 * 32), ("output_hash", C.c_uint8 * 32),
+                ("bond", C.c_uint64), ("challenge_period", C.c_uint64)]
+
+
+class VerifyOutcome(C.Structure):
+    _fields_ = [("confirmed", C.c_uint32), ("refuted_stage", C.c_uint32), ("expected", C.c_uint8 * 32),
+                ("found", C.c_uint8 * 32)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -93,6 +103,16 @@ def _load():
         "dimg_op_dense_tokens": ([C.c_int, C.POINTER(QTensor), i64p, C.c_uint32, i64p], C.c_int),
         "dimg_blake3_device": ([C.c_int, vp, C.c_size_t, u8p, C.POINTER(C.c_float)], C.c_int),
         "dimg_blake3_gpu": ([C.c_int, vp, C.c_size_t, u8p], C.c_int),
+        "dimg_attestation_encode": ([C.POINTER(Attestation), u8p], C.c_int),
+        "dimg_attestation_decode": ([u8p, C.c_size_t, C.POINTER(Attestation)], C.c_int),
+        "dimg_attestation_text": ([C.POINTER(Attestation), C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
+        "dimg_make_attestation": ([C.c_int, vp, C.c_size_t, u32p, C.c_size_t, u8p, C.c_uint64, C.c_uint64,
+                                   C.POINTER(Attestation)], C.c_int),
+        "dimg_verify_by_reexecution": ([C.c_int, C.POINTER(Attestation), vp, C.c_size_t, u32p, C.c_size_t,
+                                        C.c_uint32, C.POINTER(VerifyOutcome)], C.c_int),
+        "dimg_dispute_game": ([C.c_int, C.POINTER(Attestation), vp, C.c_size_t, u32p, C.c_size_t, C.c_uint32,
+                               u32p, C.POINTER(VerifyOutcome)], C.c_int),
+        "dimg_generation_counter": ([u64p], C.c_int),
         "dimg_op_rmsnorm": ([C.c_int, i64p, i64p, C.c_uint32, i64p], C.c_int),
         "dimg_op_softmax": ([C.c_int, i64p, C.c_uint32, i64p], C.c_int),
         "dimg_op_attention": ([C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_uint32,

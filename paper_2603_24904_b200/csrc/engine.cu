@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -1074,6 +1075,9 @@ bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<
 
 }  // namespace
 
+// generation_counter (proj/src/engine.cpp:165-168): one per run_generation
+static std::atomic<uint64_t> g_generations{0};
+
 extern "C" {
 
 dimg_status dimg_device_count(int* n) { DIMG_API_GUARD(CK(cudaGetDeviceCount(n))) }
@@ -1318,6 +1322,7 @@ dimg_status dimg_generate_greedy(dimg_session* s, const uint32_t* prompt, uint32
     // lm_head only where a selection follows -- one persistent launch.
     DIMG_API_GUARD({
         begin(*s, prompt, n_prompt, max_new, logits_out != nullptr);
+        g_generations.fetch_add(1, std::memory_order_relaxed);
         if (max_new > 0) {
             const uint32_t np = n_prompt - 1;
             if (try_prefill_tc(*s)) launch_pk(*s, s->stages, n_layer_stages(*s), max_new, 0);
@@ -1356,6 +1361,7 @@ dimg_status dimg_generate_greedy_batch(dimg_model* m, uint32_t n_seqs, const uin
         static uint64_t graph_steps = 0;
         if (n_seqs && batch_shape_ok(*m) && generate_batch_tc(m, n_seqs, ps, max_new, tokens_out, &graph_steps)) {
             used = 1;
+            g_generations.fetch_add(n_seqs, std::memory_order_relaxed);
         } else if (n_seqs) {
             dimg_session* s = nullptr;
             const dimg_status st = dimg_session_create(m, 0, &s);
@@ -1667,6 +1673,84 @@ dimg_status dimg_blake3_device(int device, const void* data, size_t len, uint8_t
         if (!data && len) fail(DIMG_EINVAL, "blake3_device: null data");
         OpScope o(device);
         blake3_device_run(static_cast<const uint8_t*>(data), len, out, o.c.op_stream, o.mem, ms);
+    })
+}
+
+dimg_status dimg_generation_counter(uint64_t* out) { DIMG_API_GUARD(*out = g_generations.load()) }
+
+dimg_status dimg_make_attestation(int device, const uint8_t* model_bytes, size_t n_bytes, const uint32_t* prompt,
+                                  size_t n_prompt, const uint8_t output_hash[32], uint64_t bond,
+                                  uint64_t challenge_period, dimg_attestation* out) {
+    // make_attestation (proj/src/attest.cpp:68-78)
+    DIMG_API_GUARD({
+        const dimg_status st = dimg_blake3_gpu(device, model_bytes, n_bytes, out->model_id);
+        if (st != DIMG_OK) return st;
+        const auto ih = b3::hash(prompt, n_prompt * 4, 1);  // hash_token_ids (u32 LE)
+        std::memcpy(out->input_hash, ih.data(), 32);
+        std::memcpy(out->output_hash, output_hash, 32);
+        out->bond = bond;
+        out->challenge_period = challenge_period;
+    })
+}
+
+dimg_status dimg_verify_by_reexecution(int device, const dimg_attestation* att, const uint8_t* model_bytes,
+                                       size_t n_bytes, const uint32_t* prompt, size_t n_prompt, uint32_t max_new,
+                                       dimg_verify_outcome* out) {
+    // verify_by_reexecution (proj/src/attest.cpp:89-117): the first stage whose
+    // recomputed digest differs refutes; only an intact model and prompt are
+    // re-executed (once).
+    DIMG_API_GUARD({
+        *out = dimg_verify_outcome{};
+        auto refute = [&](uint32_t stage, const uint8_t* expected, const uint8_t* found) {
+            out->refuted_stage = stage;
+            std::memcpy(out->expected, expected, 32);
+            std::memcpy(out->found, found, 32);
+        };
+        uint8_t found[32];
+        dimg_status st = dimg_blake3_gpu(device, model_bytes, n_bytes, found);
+        if (st != DIMG_OK) return st;
+        if (std::memcmp(found, att->model_id, 32)) {
+            refute(0, att->model_id, found);
+            return DIMG_OK;
+        }
+        const auto ih = b3::hash(prompt, n_prompt * 4, 1);
+        if (std::memcmp(ih.data(), att->input_hash, 32)) {
+            refute(1, att->input_hash, ih.data());
+            return DIMG_OK;
+        }
+        dimg_host_model* hm = nullptr;
+        if ((st = dimg_host_model_from_bytes(model_bytes, n_bytes, &hm)) != DIMG_OK) return st;  // ParseError
+        std::unique_ptr<dimg_host_model, dimg_status (*)(dimg_host_model*)> keep_hm(hm, dimg_host_model_free);
+        dimg_model_desc desc;
+        if ((st = dimg_host_model_desc(hm, &desc)) != DIMG_OK) return st;
+        dimg_model* dm = nullptr;
+        if ((st = dimg_model_upload(device, &desc, 0, 1, &dm)) != DIMG_OK) return st;
+        std::unique_ptr<dimg_model, dimg_status (*)(dimg_model*)> keep_dm(dm, dimg_model_free);
+        dimg_session* s = nullptr;
+        if ((st = dimg_session_create(dm, 0, &s)) != DIMG_OK) return st;
+        std::unique_ptr<dimg_session, dimg_status (*)(dimg_session*)> keep_s(s, dimg_session_free);
+        std::vector<uint32_t> toks(max_new);
+        uint8_t oh[32];
+        if ((st = dimg_generate_greedy(s, prompt, uint32_t(n_prompt), max_new, toks.data(), oh, nullptr)) != DIMG_OK)
+            return st;
+        if (std::memcmp(oh, att->output_hash, 32)) {
+            refute(2, att->output_hash, oh);
+            return DIMG_OK;
+        }
+        out->confirmed = 1;
+    })
+}
+
+dimg_status dimg_dispute_game(int device, const dimg_attestation* att, const uint8_t* model_bytes, size_t n_bytes,
+                              const uint32_t* prompt, size_t n_prompt, uint32_t max_new, uint32_t* winner,
+                              dimg_verify_outcome* out) {
+    // dispute_game (proj/src/attest.cpp:119-125): the challenger wins iff
+    // re-execution refutes the attestation
+    DIMG_API_GUARD({
+        const dimg_status st =
+            dimg_verify_by_reexecution(device, att, model_bytes, n_bytes, prompt, n_prompt, max_new, out);
+        if (st != DIMG_OK) return st;
+        *winner = out->confirmed ? 0 : 1;
     })
 }
 

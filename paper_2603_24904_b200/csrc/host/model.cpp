@@ -1,6 +1,9 @@
 // DIM1 container build / parse and the FP64-built tables.
 #include "model.hpp"
 
+#include <algorithm>
+#include <thread>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 
@@ -218,6 +221,46 @@ HostModel gen_toy_model(uint64_t seed, const dimg_config& cfg, int threads) {
     return m;
 }
 
+namespace {
+
+// Splits [0, n) over the host threads (one piece each for small n).
+template <class F>
+void parallel_ranges(size_t n, F&& f) {
+    const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t parts = n < (size_t(16) << 20) ? 1 : std::min<size_t>(hw, n >> 20);
+    if (parts <= 1) {
+        f(size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> ts;
+    for (size_t t = 0; t < parts; ++t) ts.emplace_back([&, t] { f(n * t / parts, n * (t + 1) / parts); });
+    for (auto& th : ts) th.join();
+}
+
+// Does any byte equal 0x80 (int8 -128)? Eight bytes at a time: a byte of
+// v ^ 0x80..80 is zero exactly where v held 0x80.
+bool has_minus128(const uint8_t* p, size_t n) {
+    std::atomic<bool> hit{false};
+    parallel_ranges(n, [&](size_t a, size_t b) {
+        size_t i = a;
+        for (; i < b && (reinterpret_cast<uintptr_t>(p + i) & 7); ++i)
+            if (p[i] == 0x80) { hit = true; return; }
+        constexpr uint64_t k80 = 0x8080808080808080ull, k01 = 0x0101010101010101ull;
+        for (; i + 8 <= b; i += 8) {
+            if ((i & ((1u << 20) - 1)) == 0 && hit.load(std::memory_order_relaxed)) return;
+            uint64_t v;
+            std::memcpy(&v, p + i, 8);
+            const uint64_t x = v ^ k80;
+            if ((x - k01) & ~x & k80) { hit = true; return; }
+        }
+        for (; i < b; ++i)
+            if (p[i] == 0x80) { hit = true; return; }
+    });
+    return hit.load();
+}
+
+}  // namespace
+
 HostModel deserialize(const uint8_t* bytes, size_t n) {
     // strict parse (proj/src/model.cpp:251-312)
     Reader r{bytes, n};
@@ -256,9 +299,8 @@ HostModel deserialize(const uint8_t* bytes, size_t n) {
             bool bad_scale = false;
             for (uint32_t i = 0; i < e.rows; ++i) bad_scale |= r.le<int64_t>() <= 0;
             r.need(size_t(e.rows) * e.cols);
-            const int8_t* w = reinterpret_cast<const int8_t*>(bytes + r.off);
-            for (size_t i = 0, k = size_t(e.rows) * e.cols; i < k; ++i)
-                if (w[i] == -128) fail_parse(DIMG_PARSE_INVARIANT, e.name + ": weight value -128");
+            if (has_minus128(bytes + r.off, size_t(e.rows) * e.cols))
+                fail_parse(DIMG_PARSE_INVARIANT, e.name + ": weight value -128");
             if (bad_scale) fail_parse(DIMG_PARSE_INVARIANT, e.name + ": non-positive scale");
             r.off += size_t(e.rows) * e.cols;
         } else {
@@ -268,7 +310,7 @@ HostModel deserialize(const uint8_t* bytes, size_t n) {
     }
     if (r.off != n) fail_parse(DIMG_PARSE_INVARIANT, "model: trailing bytes");
     layout(m);  // offsets are a pure function of the config
-    std::memcpy(m.bytes.data(), bytes, n);
+    parallel_ranges(n, [&](size_t a, size_t b) { std::memcpy(m.bytes.data() + a, bytes + a, b - a); });
     gather_aligned(m);
     return m;
 }

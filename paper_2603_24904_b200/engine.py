@@ -8,7 +8,6 @@ Every forward pass runs on the GPU through libdimg.so; there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
-import itertools
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -18,13 +17,12 @@ from . import errors
 from ._lib import QTensor, check, i8p, i64p, lib, ptr, u8p, u32p, u64p
 from .model import ModelFile
 
-_generation_counter = itertools.count()
-_generations = 0
-
-
 def generation_counter() -> int:
-    """Count of generation runs in this process (engine.cpp:165-168)."""
-    return _generations
+    """Count of generation runs in this process (engine.cpp:165-168): kept by
+    the library (dimg_generate_greedy, the batch call, re-execution)."""
+    n = C.c_uint64()
+    check(lib.dimg_generation_counter(C.byref(n)))
+    return n.value
 
 
 @dataclass
@@ -222,9 +220,7 @@ def generate_greedy(model: ModelFile, prompt: Sequence[int], max_new: int,
                     opts: Optional[EngineOptions] = None, imported_tables=None) -> GenerationResult:
     """generate_greedy (engine.cpp:142-147) on the GPU: prompt + greedy
     continuation + BLAKE3 output hash; logits when opts.keep_logits."""
-    global _generations
     opts = opts or EngineOptions()
-    _generations += 1
     sess = _cached_session(model, opts, max_new if opts.keep_logits else 0, imported_tables)
     return sess.generate_greedy(prompt, max_new, keep_logits=opts.keep_logits)
 
