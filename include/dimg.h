@@ -255,6 +255,19 @@ dimg_status dimg_verify_by_reexecution(int device, const dimg_attestation* att, 
 dimg_status dimg_dispute_game(int device, const dimg_attestation* att, const uint8_t* model_bytes, size_t n_bytes,
                               const uint32_t* prompt, size_t n_prompt, uint32_t max_new, uint32_t* winner,
                               dimg_verify_outcome* out);
+/* Seeded sampling (proj/src/engine.cpp:122-163). dimg_sample_key: the RNG key
+ * BLAKE3(model bytes || prompt ids as u32 LE), hashed on the GPU.
+ * dimg_generate_sampled: generate_sampled with that key and a Q16
+ * temperature (> 0, else DIMG_EINVAL); each step's token is drawn on the
+ * device (sample_from_logits with the step's ChaCha20 u32). dimg_op_sample:
+ * sample_from_logits of one row with a given draw (parity tests). */
+dimg_status dimg_sample_key(int device, const uint8_t* model_bytes, size_t n_bytes, const uint32_t* prompt,
+                            size_t n_prompt, uint8_t key[32]);
+dimg_status dimg_generate_sampled(dimg_session* s, const uint32_t* prompt, uint32_t n_prompt, uint32_t max_new,
+                                  int64_t temperature, const uint8_t key[32], uint32_t* tokens_out,
+                                  uint8_t hash_out[32]);
+dimg_status dimg_op_sample(int device, const int64_t* logits, uint32_t V, int64_t temperature, uint32_t draw,
+                           uint32_t* out);
 /* generation_counter (engine.cpp:165-168): generation runs in this process. */
 dimg_status dimg_generation_counter(uint64_t* out);
 dimg_status dimg_op_rmsnorm(int device, const int64_t* x, const int64_t* g, uint32_t n,

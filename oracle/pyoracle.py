@@ -30,6 +30,35 @@ i64p = C.POINTER(C.c_int64)
 u32p = C.POINTER(C.c_uint32)
 
 
+def chacha20_u32s(key32: bytes, n: int):
+    """The first n next_u32() of ChaCha20Rng(key) (proj/src/chacha20.cpp:48-78):
+    RFC 8439 blocks, key words little-endian, nonce 0, counter from 0, bytes
+    consumed in order, u32 = 4 bytes LE. Pure Python (small n)."""
+    M = 0xFFFFFFFF
+    key = [int.from_bytes(key32[4 * i:4 * i + 4], "little") for i in range(8)]
+
+    def rotl(x, r):
+        return ((x << r) | (x >> (32 - r))) & M
+
+    def qr(s, a, b, c, d):
+        s[a] = (s[a] + s[b]) & M; s[d] = rotl(s[d] ^ s[a], 16)
+        s[c] = (s[c] + s[d]) & M; s[b] = rotl(s[b] ^ s[c], 12)
+        s[a] = (s[a] + s[b]) & M; s[d] = rotl(s[d] ^ s[a], 8)
+        s[c] = (s[c] + s[d]) & M; s[b] = rotl(s[b] ^ s[c], 7)
+
+    out, ctr = bytearray(), 0
+    while len(out) < 4 * n:
+        init = [0x61707865, 0x3320646E, 0x79622D32, 0x6B206574] + key + [ctr, 0, 0, 0]
+        s = list(init)
+        for _ in range(10):
+            qr(s, 0, 4, 8, 12); qr(s, 1, 5, 9, 13); qr(s, 2, 6, 10, 14); qr(s, 3, 7, 11, 15)
+            qr(s, 0, 5, 10, 15); qr(s, 1, 6, 11, 12); qr(s, 2, 7, 8, 13); qr(s, 3, 4, 9, 14)
+        for i in range(16):
+            out += ((s[i] + init[i]) & M).to_bytes(4, "little")
+        ctr += 1
+    return [int.from_bytes(out[4 * i:4 * i + 4], "little") for i in range(n)]
+
+
 def _ptr(a, t):
     return a.ctypes.data_as(t)
 
@@ -233,6 +262,30 @@ class Oracle:
         out = np.empty_like(s)
         self.lib.orc_softmax(_ptr(s, i64p), C.c_uint32(len(s)), _ptr(out, i64p))
         return out
+
+    def sample_from_logits(self, logits, temperature: int, draw: int) -> int:
+        """sample_from_logits (proj/src/engine.cpp:122-139) given the step's
+        ChaCha20 u32: truncating int128 temperature division (low 64 bits),
+        softmax_q16 (the C oracle's), threshold (draw * sum p) >> 32, first
+        index whose cumulative mass exceeds it."""
+        if temperature <= 0 or len(logits) == 0:
+            raise ValueError("sample: temperature must be positive / empty logits")
+        scaled = []
+        for v in logits:
+            num = int(v) << 16
+            q = abs(num) // temperature
+            q = q if num >= 0 else -q
+            q &= (1 << 64) - 1
+            scaled.append(q - (1 << 64) if q >= 1 << 63 else q)
+        p = self.softmax(np.array(scaled, np.int64))
+        total = int(sum(int(x) for x in p))
+        threshold = (int(draw) * total) >> 32
+        cum = 0
+        for i, x in enumerate(p):
+            cum += int(x)
+            if cum > threshold:
+                return i
+        return len(p) - 1
 
     def attention(self, H, dh, max_ctx, theta, q, k, v):
         """Consecutive attention steps at pos 0..T-1; q/k/v [T, H*dh]."""

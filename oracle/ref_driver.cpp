@@ -279,6 +279,23 @@ int ref_session_forward(void* s, uint32_t token, uint32_t pos, int64_t* logits, 
     })
 }
 uint64_t ref_generation_counter() { return generation_counter().load(); }
+// generate_sampled (proj/src/engine.cpp:148-163) with the per-step logits
+int ref_generate_sampled(void* m, const uint32_t* prompt, uint32_t p, uint32_t n, int64_t temperature,
+                         uint32_t* tokens_out, uint8_t hash_out[32], int64_t* logits_out) {
+    GUARD({
+        EngineOptions o;
+        o.keep_logits = logits_out != nullptr;
+        auto r = generate_sampled(*static_cast<ModelFile*>(m), std::span<const uint32_t>(prompt, p), n,
+                                  q16{temperature}, o);
+        for (size_t i = 0; i < r.token_ids.size(); ++i) tokens_out[i] = r.token_ids[i];
+        std::memcpy(hash_out, r.output_hash.bytes.data(), 32);
+        if (logits_out) {
+            size_t V = static_cast<ModelFile*>(m)->config.vocab;
+            for (size_t i = 0; i < r.logits.size(); ++i)
+                for (size_t j = 0; j < V; ++j) logits_out[i * V + j] = r.logits[i][j].raw;
+        }
+    })
+}
 
 // ---- attestation (proj/src/attest.cpp) ----------------------------------------
 // make_attestation of a fresh greedy generation: wire bytes + to_text

@@ -9,7 +9,7 @@ from .attest import (Attestation, DisputeResult, VerifyOutcome, dispute_game, ma
                      verify_by_reexecution)
 from ._lib import LIB_PATH, lib
 from .engine import (EngineOptions, GenerationResult, InferenceSession, attention_steps, blake3_device,
-                     blake3_gpu, build_rope_tables, dense_forward, dense_tokens, device_count, ffn_silu, generate_greedy,
+                     blake3_gpu, build_rope_tables, generate_sampled, sample_from_logits, sample_key, dense_forward, dense_tokens, device_count, ffn_silu, generate_greedy,
                      generate_greedy_batch, generation_counter, hash_token_ids, parse_prompt, prompt_from_seed,
                      release_sessions, rmsnorm, select_greedy, softmax_q16)
 from .errors import (ContextOverflow, DomainError, InvalidArgument, LengthError, LogicError,
@@ -20,7 +20,7 @@ from .model import (ONE, DeviceModel, ModelConfig, ModelFile, deserialize, gen_t
 __all__ = [
     "EngineOptions", "GenerationResult", "InferenceSession", "generate_greedy", "generate_greedy_batch",
     "generation_counter", "hash_token_ids", "select_greedy", "parse_prompt", "prompt_from_seed",
-    "build_rope_tables", "blake3_device", "blake3_gpu", "dense_forward", "dense_tokens", "rmsnorm", "softmax_q16", "attention_steps", "ffn_silu",
+    "build_rope_tables", "blake3_device", "blake3_gpu", "generate_sampled", "sample_from_logits", "sample_key", "dense_forward", "dense_tokens", "rmsnorm", "softmax_q16", "attention_steps", "ffn_silu",
     "device_count", "release_sessions", "ModelConfig", "ModelFile", "DeviceModel",
     "gen_toy_model", "deserialize", "load_model", "weight_hash", "ONE", "errors",
     "ContextOverflow", "DomainError", "InvalidArgument", "LengthError", "LogicError",

@@ -113,6 +113,9 @@ def _load():
         "dimg_dispute_game": ([C.c_int, C.POINTER(Attestation), vp, C.c_size_t, u32p, C.c_size_t, C.c_uint32,
                                u32p, C.POINTER(VerifyOutcome)], C.c_int),
         "dimg_generation_counter": ([u64p], C.c_int),
+        "dimg_sample_key": ([C.c_int, u8p, C.c_size_t, u32p, C.c_size_t, u8p], C.c_int),
+        "dimg_generate_sampled": ([vp, u32p, C.c_uint32, C.c_uint32, C.c_int64, u8p, u32p, u8p], C.c_int),
+        "dimg_op_sample": ([C.c_int, i64p, C.c_uint32, C.c_int64, C.c_uint32, u32p], C.c_int),
         "dimg_op_rmsnorm": ([C.c_int, i64p, i64p, C.c_uint32, i64p], C.c_int),
         "dimg_op_softmax": ([C.c_int, i64p, C.c_uint32, i64p], C.c_int),
         "dimg_op_attention": ([C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_uint32,

@@ -35,7 +35,9 @@
 #include "kernels/prefill.cuh"
 #include "kernels/batch.cuh"
 #include "kernels/blake3.cuh"
+#include "kernels/sample.cuh"
 #include "host/blake3.hpp"
+#include "host/chacha20.hpp"
 
 using namespace dimg;
 using namespace dimg::dev;
@@ -445,6 +447,9 @@ struct dimg_session {
     std::vector<PkStage> host_stages;
     PkStage* probe_stages = nullptr;  // [L] scratch program for time_kernel
     uint32_t keep_cap = 0;
+    uint32_t* draws = nullptr;        // generate_sampled: the steps' ChaCha20 draws
+    uint32_t draws_cap = 0;
+    int64_t* sample_scratch = nullptr;  // [vocab] scaled logits / probabilities
     uint32_t len = 0;  // host mirror of the cache length
     uint32_t n_prompt = 0, max_new = 0;
     uint32_t grid = 0, planes_bytes = 0, ring_depth = 2, wide_stride = 0;
@@ -1751,6 +1756,86 @@ dimg_status dimg_dispute_game(int device, const dimg_attestation* att, const uin
             dimg_verify_by_reexecution(device, att, model_bytes, n_bytes, prompt, n_prompt, max_new, out);
         if (st != DIMG_OK) return st;
         *winner = out->confirmed ? 0 : 1;
+    })
+}
+
+dimg_status dimg_sample_key(int device, const uint8_t* model_bytes, size_t n_bytes, const uint32_t* prompt,
+                            size_t n_prompt, uint8_t key[32]) {
+    // generate_sampled's RNG key (proj/src/engine.cpp:151-157): BLAKE3 of the
+    // model bytes followed by the prompt ids (u32 LE), one device buffer
+    DIMG_API_GUARD({
+        OpScope o(device);
+        uint8_t* d = o.mem.alloc<uint8_t>(n_bytes + 4 * n_prompt);
+        if (n_bytes) CK(cudaMemcpyAsync(d, model_bytes, n_bytes, cudaMemcpyHostToDevice, o.c.op_stream));
+        if (n_prompt)
+            CK(cudaMemcpyAsync(d + n_bytes, prompt, 4 * n_prompt, cudaMemcpyHostToDevice, o.c.op_stream));
+        blake3_device_run(d, n_bytes + 4 * n_prompt, key, o.c.op_stream, o.mem, nullptr);
+    })
+}
+
+dimg_status dimg_op_sample(int device, const int64_t* logits, uint32_t V, int64_t temperature, uint32_t draw,
+                           uint32_t* out) {
+    // sample_from_logits (proj/src/engine.cpp:122-139) of one row with a given draw
+    DIMG_API_GUARD({
+        if (temperature <= 0) fail(DIMG_EINVAL, "sample: temperature must be positive");
+        if (V == 0) fail(DIMG_EINVAL, "sample: empty logits");
+        OpScope o(device);
+        const int64_t* dl = o.put(logits, V);
+        const uint32_t* dd = o.put(&draw, 1);
+        int64_t* scratch = o.mem.alloc<int64_t>(V);
+        uint32_t* tok = o.mem.alloc<uint32_t>(2);
+        sample_kernel<<<1, SM_THREADS, 0, o.c.op_stream>>>(dl, V, temperature, dd, 0, o.c.exp_lut, scratch, tok, 0);
+        CK(cudaGetLastError());
+        o.get(out, tok + 1, 1);
+    })
+}
+
+dimg_status dimg_generate_sampled(dimg_session* s, const uint32_t* prompt, uint32_t n_prompt, uint32_t max_new,
+                                  int64_t temperature, const uint8_t key[32], uint32_t* tokens_out,
+                                  uint8_t hash_out[32]) {
+    // generate_sampled (proj/src/engine.cpp:148-163): run_generation with
+    // sample_from_logits as the selection. The prompt prefill as for greedy;
+    // then per step one decode step (logits to the session's scratch row)
+    // and the sampling kernel, which writes the token the next step reads --
+    // all enqueued back to back, no host round trip per token.
+    DIMG_API_GUARD({
+        if (temperature <= 0) fail(DIMG_EINVAL, "sample: temperature must be positive");
+        const dimg_model& m = *s->m;
+        begin(*s, prompt, n_prompt, max_new, false);
+        g_generations.fetch_add(1, std::memory_order_relaxed);
+        if (max_new > 0) {
+            if (s->draws_cap < max_new) {
+                CK(cudaStreamSynchronize(s->stream));
+                s->draws = s->mem.alloc<uint32_t>(max_new);
+                s->draws_cap = max_new;
+            }
+            if (!s->sample_scratch) s->sample_scratch = s->mem.alloc<int64_t>(m.V);
+            chacha::Key k;
+            for (int i = 0; i < 8; ++i)
+                k[i] = uint32_t(key[4 * i]) | uint32_t(key[4 * i + 1]) << 8 | uint32_t(key[4 * i + 2]) << 16 |
+                       uint32_t(key[4 * i + 3]) << 24;
+            chacha::Stream rng(k);
+            std::vector<uint32_t> dr(max_new);
+            for (auto& d : dr) d = rng.u32();
+            CK(cudaMemcpyAsync(s->draws, dr.data(), size_t(max_new) * 4, cudaMemcpyHostToDevice, s->stream));
+            run_prefill(*s);  // positions 0 .. P-2
+            for (uint32_t step = 0; step < max_new; ++step) {
+                const uint32_t pos = n_prompt - 1 + step;
+                write_ctl(*s, pos, pos, 0);  // logits to the scratch row 0
+                launch_pk(*s, s->stages, n_layer_stages(*s), 1, 0);
+                sample_kernel<<<1, SM_THREADS, 0, s->stream>>>(s->logits, m.V, temperature, s->draws, step,
+                                                                m.ctx->exp_lut, s->sample_scratch, s->tokens, pos);
+            }
+            CK(cudaGetLastError());
+            s->len = n_prompt - 1 + max_new;
+            CK(cudaMemcpyAsync(tokens_out, s->tokens + n_prompt, size_t(max_new) * 4, cudaMemcpyDeviceToHost,
+                               s->stream));
+        }
+        check_ctl_err(*s);
+        if (hash_out) {
+            auto d = b3::hash(tokens_out, size_t(max_new) * 4, 1);
+            std::memcpy(hash_out, d.data(), 32);
+        }
     })
 }
 

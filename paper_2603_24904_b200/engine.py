@@ -134,6 +134,17 @@ class InferenceSession:
             res.logits = [logits[i] for i in range(max_new)]
         return res
 
+    def generate_sampled(self, prompt: Sequence[int], max_new: int, temperature: int, key: bytes):
+        """generate_sampled (engine.cpp:148-163) with the RNG key given
+        (sample_key); tokens drawn on the device step by step."""
+        p = np.ascontiguousarray(prompt, dtype=np.uint32)
+        toks = np.zeros(max(1, max_new), np.uint32)
+        h = (C.c_uint8 * 32)()
+        k = (C.c_uint8 * 32)(*key)
+        check(lib.dimg_generate_sampled(self._h, ptr(p, u32p), p.size, max_new, int(temperature), k,
+                                        ptr(toks, u32p), h))
+        return GenerationResult([int(t) for t in toks[:max_new]], bytes(h))
+
     # ---- device-resident stepping (bench)
     def begin(self, prompt: Sequence[int], max_new: int):
         p = np.ascontiguousarray(prompt, dtype=np.uint32)
@@ -265,6 +276,38 @@ def dense_forward(w, scales, x, device: int = 0) -> np.ndarray:
     out = np.empty(qt.rows, np.int64)
     check(lib.dimg_op_dense(device, C.byref(qt), ptr(x, i64p), ptr(out, i64p)))
     return out
+
+
+def sample_key(model_bytes, prompt: Sequence[int], device: int = 0) -> bytes:
+    """generate_sampled's RNG key (engine.cpp:151-157): BLAKE3(model bytes ||
+    prompt ids u32 LE), hashed on the GPU."""
+    mb = np.frombuffer(memoryview(model_bytes).cast("B"), np.uint8) if not isinstance(model_bytes, np.ndarray) \
+        else np.ascontiguousarray(model_bytes).view(np.uint8).reshape(-1)
+    p = np.ascontiguousarray(prompt, np.uint32)
+    out = (C.c_uint8 * 32)()
+    check(lib.dimg_sample_key(device, mb.ctypes.data_as(u8p), mb.size, ptr(p, u32p), p.size, out))
+    return bytes(out)
+
+
+def sample_from_logits(logits, temperature: int, draw: int, device: int = 0) -> int:
+    """sample_from_logits (engine.cpp:122-139) of one row with the given
+    ChaCha20 draw, on the GPU."""
+    a = np.ascontiguousarray(logits, np.int64)
+    out = C.c_uint32()
+    check(lib.dimg_op_sample(device, ptr(a, i64p), a.size, int(temperature), int(draw), C.byref(out)))
+    return out.value
+
+
+def generate_sampled(model: ModelFile, prompt: Sequence[int], max_new: int, temperature: int,
+                     opts: Optional[EngineOptions] = None) -> GenerationResult:
+    """generate_sampled (engine.cpp:148-163): Q16 temperature > 0, the RNG
+    keyed by BLAKE3(model bytes || prompt)."""
+    opts = opts or EngineOptions()
+    if temperature <= 0:
+        raise errors.InvalidArgument("sample: temperature must be positive")
+    key = sample_key(model.bytes, prompt, opts.device)
+    sess = _cached_session(model, opts, 0, None)
+    return sess.generate_sampled(prompt, max_new, temperature, key)
 
 
 def blake3_gpu(data, device: int = 0) -> bytes:

@@ -160,3 +160,24 @@ def test_generation_errors(oracle):
         oracle.generate_greedy(m, np.array([1, 2], np.uint32), 1000)
     with pytest.raises(RuntimeError):
         oracle.generate_greedy(m, np.array([1, 64], np.uint32), 4)
+
+
+def test_sample_restatement_matches_reference_fixtures(oracle):
+    """sample_from_logits (proj/src/engine.cpp:122-139) restated on the oracle's
+    softmax: every per-step selection of the reference's generate_sampled
+    (tests/golden/make_sample_golden.py) and the extreme rows."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "sample_ops.npz"))
+    for row, n, t, d, tok in zip(z["logits"], z["lens"], z["temperature"], z["draw"], z["token"]):
+        assert oracle.sample_from_logits(row[:n], int(t), int(d)) == int(tok)
+
+
+def test_chacha20_restatement_matches_reference_prompts(oracle, kat):
+    """The restated ChaCha20Rng (draws of generate_sampled) against the
+    reference's seeded prompts: prompt[i] = ChaCha20Rng(seed).next_u32() % V,
+    the key BLAKE3(seed as u64 LE) (proj/src/chacha20.cpp:57-78)."""
+    from oracle.pyoracle import chacha20_u32s
+    for name, ids in kat["prompts"].items():
+        seed, vocab, n = (int(x) for x in name.split("_"))
+        key = bytes.fromhex(oracle.blake3(seed.to_bytes(8, "little")))
+        assert [w % vocab for w in chacha20_u32s(key, n)] == ids, name
