@@ -114,6 +114,9 @@ typedef struct dimg_host_model dimg_host_model;
 /* gen_toy_model (proj/src/model.cpp:189-215); threads <= 0 = all cores. */
 dimg_status dimg_host_model_gen_toy(uint64_t seed, const dimg_config* cfg, int threads,
                                     dimg_host_model** out);
+/* gen_toy_model with its weight stream (ChaCha20 keystream, 0xFF rejected)
+ * synthesised on GPU `device` and copied into the container: the same bytes. */
+dimg_status dimg_host_model_gen_toy_gpu(int device, uint64_t seed, const dimg_config* cfg, dimg_host_model** out);
 /* deserialize (proj/src/model.cpp:251-312) / load_model (:332-334). */
 dimg_status dimg_host_model_from_bytes(const uint8_t* bytes, size_t n, dimg_host_model** out);
 dimg_status dimg_host_model_load(const char* path, dimg_host_model** out);

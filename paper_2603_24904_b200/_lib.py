@@ -68,6 +68,7 @@ def _load():
         "dimg_exp_lut": ([i64p], C.c_int),
         "dimg_invsqrt_seeds": ([i64p], C.c_int),
         "dimg_host_model_gen_toy": ([C.c_uint64, C.POINTER(Config), C.c_int, pp], C.c_int),
+        "dimg_host_model_gen_toy_gpu": ([C.c_int, C.c_uint64, C.POINTER(Config), pp], C.c_int),
         "dimg_host_model_from_bytes": ([u8p, C.c_size_t, pp], C.c_int),
         "dimg_host_model_load": ([C.c_char_p, pp], C.c_int),
         "dimg_host_model_save": ([vp, C.c_char_p], C.c_int),

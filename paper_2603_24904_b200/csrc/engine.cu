@@ -36,6 +36,7 @@
 #include "kernels/batch.cuh"
 #include "kernels/blake3.cuh"
 #include "kernels/sample.cuh"
+#include "kernels/chacha.cuh"
 #include "host/blake3.hpp"
 #include "host/chacha20.hpp"
 
@@ -1079,6 +1080,48 @@ bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<
 }
 
 }  // namespace
+
+namespace dimg::chacha {
+
+// The toy-model weight stream on the GPU (kernels/chacha.cuh), copied into
+// the host spans in order: the same bytes as weight_stream.
+void gpu_weight_stream(int device, uint64_t seed, const Span* spans, size_t n_spans) {
+    uint64_t n = 0;
+    for (size_t i = 0; i < n_spans; ++i) n += spans[i].len;
+    if (n == 0) return;
+    CK(cudaSetDevice(device));
+    const Key hk = key_from_seed(seed);
+    dev::CcKey key;
+    for (int i = 0; i < 8; ++i) key.k[i] = hk[i];
+    DevBuf mem;
+    int8_t* out = mem.alloc<int8_t>(n);
+    uint64_t* grand = mem.alloc<uint64_t>(1);
+    // 64 bytes per block accept 63.75 on average: n / 63 blocks (+ slack)
+    // almost always suffice; otherwise grow and count again
+    for (uint64_t nb = n / 63 + 4096;; nb += nb / 16) {
+        if (nb >= (uint64_t(1) << 32)) fail(DIMG_EINVAL, "gen_toy_model: weight stream exceeds the block counter");
+        const uint64_t g = (nb + dev::CC_THREADS - 1) / dev::CC_THREADS;
+        DevBuf scratch;
+        uint8_t* cnt = scratch.alloc<uint8_t>(nb);
+        uint64_t* tot = scratch.alloc<uint64_t>(g);
+        dev::cc_count_kernel<<<uint32_t(g), dev::CC_THREADS>>>(key, nb, cnt, tot);
+        dev::cc_scan_kernel<<<1, dev::CC_THREADS>>>(tot, g, grand);
+        uint64_t have = 0;
+        CK(cudaMemcpy(&have, grand, 8, cudaMemcpyDeviceToHost));
+        if (have < n) continue;
+        dev::cc_compact_kernel<<<uint32_t(g), dev::CC_THREADS>>>(key, nb, cnt, tot, n, out);
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+        break;
+    }
+    uint64_t o = 0;
+    for (size_t i = 0; i < n_spans; ++i) {
+        CK(cudaMemcpy(spans[i].dst, out + o, spans[i].len, cudaMemcpyDeviceToHost));
+        o += spans[i].len;
+    }
+}
+
+}  // namespace dimg::chacha
 
 // generation_counter (proj/src/engine.cpp:165-168): one per run_generation
 static std::atomic<uint64_t> g_generations{0};

@@ -127,6 +127,11 @@ dimg_status dimg_host_model_gen_toy(uint64_t seed, const dimg_config* cfg, int t
     DIMG_API_GUARD(*out = new dimg_host_model{gen_toy_model(seed, *cfg, threads)})
 }
 
+dimg_status dimg_host_model_gen_toy_gpu(int device, uint64_t seed, const dimg_config* cfg, dimg_host_model** out) {
+    // gen_toy_model with the ChaCha20 weight stream synthesised on the GPU
+    DIMG_API_GUARD(*out = new dimg_host_model{gen_toy_model(seed, *cfg, 1, device)})
+}
+
 dimg_status dimg_host_model_from_bytes(const uint8_t* bytes, size_t n, dimg_host_model** out) {
     DIMG_API_GUARD(*out = new dimg_host_model{deserialize(bytes, n)})
 }

@@ -44,5 +44,8 @@ struct Span {
 // stream, in order, into the concatenation of `spans` (the container's
 // tensor payloads); threads <= 0 = all hardware threads.
 void weight_stream(uint64_t seed, const Span* spans, size_t n_spans, int threads);
+// The same stream generated on GPU `device` (engine.cu, kernels/chacha.cuh)
+// and copied into the host spans.
+void gpu_weight_stream(int device, uint64_t seed, const Span* spans, size_t n_spans);
 
 }  // namespace dimg::chacha

@@ -200,7 +200,7 @@ int64_t q16_from_ratio(int64_t num, int64_t den) {
     return int64_t(q);
 }
 
-HostModel gen_toy_model(uint64_t seed, const dimg_config& cfg, int threads) {
+HostModel gen_toy_model(uint64_t seed, const dimg_config& cfg, int threads, int device) {
     validate_config(cfg);
     HostModel m;
     m.cfg = cfg;
@@ -216,7 +216,8 @@ HostModel gen_toy_model(uint64_t seed, const dimg_config& cfg, int threads) {
     }
     for (size_t off : m.norm_off)  // gains = ONE
         for (uint32_t j = 0; j < cfg.d_model; ++j) Writer{m.bytes.data() + off + 8 * j}.le<uint64_t>(kOne);
-    chacha::weight_stream(seed, spans.data(), spans.size(), threads);
+    if (device >= 0) chacha::gpu_weight_stream(device, seed, spans.data(), spans.size());
+    else chacha::weight_stream(seed, spans.data(), spans.size(), threads);
     gather_aligned(m);
     return m;
 }

@@ -30,7 +30,8 @@ struct HostModel {
     dimg_model_desc desc() const;
 };
 
-HostModel gen_toy_model(uint64_t seed, const dimg_config& cfg, int threads);
+// device >= 0: the weight stream synthesised on that GPU (same bytes)
+HostModel gen_toy_model(uint64_t seed, const dimg_config& cfg, int threads, int device = -1);
 HostModel deserialize(const uint8_t* bytes, size_t n);
 HostModel serialize_desc(const dimg_model_desc& d);
 

@@ -78,10 +78,14 @@ class ModelFile:
 
     # ---- construction (model.cpp:189-215, 217-334)
     @classmethod
-    def gen_toy(cls, seed: int, config: ModelConfig, threads: int = 0) -> "ModelFile":
+    def gen_toy(cls, seed: int, config: ModelConfig, threads: int = 0, device: Optional[int] = None) -> "ModelFile":
+        """gen_toy_model; device=N synthesises the weight stream on GPU N."""
         h = C.c_void_p()
         c = config.to_c()
-        check(lib.dimg_host_model_gen_toy(C.c_uint64(seed), C.byref(c), threads, C.byref(h)))
+        if device is None:
+            check(lib.dimg_host_model_gen_toy(C.c_uint64(seed), C.byref(c), threads, C.byref(h)))
+        else:
+            check(lib.dimg_host_model_gen_toy_gpu(device, C.c_uint64(seed), C.byref(c), C.byref(h)))
         return cls(h)
 
     @classmethod
@@ -201,9 +205,10 @@ class DeviceModel:
             pass
 
 
-def gen_toy_model(seed: int, config: ModelConfig, threads: int = 0) -> ModelFile:
-    """gen_toy_model (proj/src/model.cpp:189-215), all host cores."""
-    return ModelFile.gen_toy(seed, config, threads)
+def gen_toy_model(seed: int, config: ModelConfig, threads: int = 0, device: Optional[int] = None) -> ModelFile:
+    """gen_toy_model (proj/src/model.cpp:189-215): all host cores, or the
+    weight stream synthesised on GPU `device`."""
+    return ModelFile.gen_toy(seed, config, threads, device)
 
 
 def deserialize(data) -> ModelFile:
