@@ -316,7 +316,7 @@ def run_ours(args, rank, world, local):
     dev = local
     cfg = P.ModelConfig(*CFG7B)
     t0 = time.time()
-    mf = P.gen_toy_model(MODEL_SEED, cfg)
+    mf = P.gen_toy_model(MODEL_SEED, cfg, device=dev)  # weight stream on the GPU (same bytes)
     gen_s = time.time() - t0
     wh_ok = None
     if rank == 0:

@@ -330,22 +330,6 @@ struct Fetch {
 };
 
 __device__ __forceinline__ void fetch_load(const Sched& sc, Fetch& f) {
-#ifdef DIMG_FETCH_GLOBAL
-    const PkStage* st = sc.stages + f.stage;
-    if (st->kind != SK_GEMV) {
-        f.g = f.g_end = 0;
-        return;
-    }
-    uint32_t lo, hi;
-    cta_range(st->n_groups, lo, hi);
-    f.g = lo + (threadIdx.x >> 5);
-    f.g_end = hi;
-    f.seg = 0;
-    f.n_segs = st->n_segs;
-    f.Kp = st->Kp;
-    f.W = st->W;
-    return;
-#endif
     const FetchInfo& fi = sc.fi[f.stage];
     f.g = fi.g_lo + (threadIdx.x >> 5);
     f.g_end = fi.g_hi;

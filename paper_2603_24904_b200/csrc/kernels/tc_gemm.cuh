@@ -86,7 +86,6 @@ struct TgArgs {
     uint32_t ksplit;
     int32_t* partial;       // [tiles][3][BN][128], zero between launches (the last CTA resets)
     uint32_t* tile_cnt;     // [tiles], zero between launches (the last CTA resets)
-    const uint8_t* a_ptr;   // TG_A_BULK experiment: the A operand for 1-D bulk copies
 #ifdef TG_TRACE
     uint64_t* trace;        // [grid][128] globaltimer stamps (tools/gemm_bench.cu)
 #endif
@@ -124,12 +123,6 @@ __device__ __forceinline__ void tg_mbar_wait(uint64_t* b, uint32_t parity) {
     }
 }
 
-__device__ __forceinline__ void tg_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     tg_smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(tg_smem_u32(bar))
-                 : "memory");
-}
 
 __device__ __forceinline__ void tg_tma_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y, uint64_t* bar) {
     asm volatile(
@@ -158,14 +151,6 @@ __device__ __forceinline__ void tg_tma_2d_w(void* dst, const CUtensorMap* map, i
         "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n\t}" ::"r"(
             tg_smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(tg_smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tg_bulk_w(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(
-            tg_smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(tg_smem_u32(bar))
         : "memory");
 }
 
@@ -300,12 +285,7 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
             tg_tile<BN>(tile, n_mt, n0, t0);
             for (uint32_t kb = kb0; kb < kb1 && it < S::STAGES; ++kb, ++it) {
                 tg_expect_tx_w(&full[it], S::STAGE_BYTES);
-#ifdef TG_A_BULK
-                tg_bulk_w(smem + size_t(it) * S::STAGE_BYTES, a.a_ptr + (size_t(kb) * a.a_rows + n0) * TG_BK, TG_A_BYTES,
-                          &full[it]);
-#else
                 tg_tma_2d_w(smem + size_t(it) * S::STAGE_BYTES, &tmA, 0, int32_t(kb * a.a_rows + n0), &full[it]);
-#endif
             }
         }
         const uint32_t pre = it;
@@ -327,11 +307,7 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
                     if (lane == 0 && it < 40) tr[8 + it] = tg_now();
 #endif
                     tg_expect_tx_w(&full[s], S::STAGE_BYTES);
-#ifdef TG_A_BULK
-                    tg_bulk_w(st, a.a_ptr + (size_t(kb) * a.a_rows + n0) * TG_BK, TG_A_BYTES, &full[s]);
-#else
                     tg_tma_2d_w(st, &tmA, 0, int32_t(kb * a.a_rows + n0), &full[s]);  // K-block-major A
-#endif
                 }
 #pragma unroll
                 for (int l = 0; l < TG_L; ++l)

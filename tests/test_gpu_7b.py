@@ -22,7 +22,7 @@ def P():
 @pytest.fixture(scope="module")
 def model7b(P, golden_7b):
     g = golden_7b["c2"]
-    m = P.gen_toy_model(g["seed"], P.ModelConfig(*g["config"]))
+    m = P.gen_toy_model(g["seed"], P.ModelConfig(*g["config"]), device=0)
     assert m.weight_hash == g["weight_hash"]
     return m
 

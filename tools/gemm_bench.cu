@@ -162,7 +162,6 @@ int main(int argc, char** argv) {
     CK(cudaMemset(a.trace, 0, size_t(grid) * 128 * 8));
 #endif
     auto go = [&](int i) {
-        a.a_ptr = W[i % nbuf];
         if (bn == 16) launch<16>(ta[i % nbuf], tb, a, grid);
         else launch<64>(ta[i % nbuf], tb, a, grid);
     };
