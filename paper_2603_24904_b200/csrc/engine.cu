@@ -33,6 +33,7 @@
 #include "kernels/persistent.cuh"
 #include "kernels/tc_gemm.cuh"
 #include "kernels/prefill.cuh"
+#include "kernels/pf_scores.cuh"
 #include "kernels/batch.cuh"
 #include "kernels/blake3.cuh"
 #include "kernels/sample.cuh"
@@ -114,6 +115,7 @@ DevCtx& dev_ctx(int device) {
         set(pf_attn_kernel<2>);
         set(pf_attn_kernel<4>);
         set(pf_attn_kernel<8>);
+        CK(cudaFuncSetAttribute(pf_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pf_scores_smem())));
         set(bd_attn_kernel);
     }
     set_gemv_attrs<EPI_STORE, MODE_EMBED>();
@@ -420,6 +422,9 @@ struct PrefillWs {
     int32_t* partial = nullptr;      // split-K accumulators of the 16-token tiles (zero between launches)
     uint32_t* tile_cnt = nullptr;
     size_t partial_elems = 0;
+    int8_t* kdig = nullptr;          // key digit planes [H][4][kdig_pad][128] (tensor-core scores, dh 128)
+    uint32_t kdig_pad = 0;
+    CUtensorMap tm_kdig;
 };
 
 struct dimg_session {
@@ -722,6 +727,11 @@ void ensure_prefill_ws(dimg_session& s, uint32_t n) {
     w.tm_pa = tmap_bytes(w.pa, m.D, size_t(3) * w.cap_pad, m.Kd, TG_BN);
     w.tm_ph = tmap_bytes(w.ph, m.F, size_t(3) * w.cap_pad, m.Kf, TG_BN);
     w.tm_pa_s = tmap_bytes(w.pa, m.D, size_t(3) * w.cap_pad, m.Kd, TG_BN_SMALL);
+    if (m.dh == PS_DH) {
+        w.kdig_pad = (w.cap + PS_M - 1) / PS_M * PS_M;
+        w.kdig = s.mem.alloc<int8_t>(size_t(m.H) * PS_KD * w.kdig_pad * PS_DH);
+        w.tm_kdig = tmap_bytes(w.kdig, PS_DH, size_t(m.H) * PS_KD * w.kdig_pad, PS_DH, PS_M);
+    }
     w.tm_ph_s = tmap_bytes(w.ph, m.F, size_t(3) * w.cap_pad, m.Kf, TG_BN_SMALL);
     if (!w.partial) {  // one 16-token tile column: the largest matrix's row tiles
         const uint32_t tiles = (std::max({3 * m.D, 2 * m.F, m.V}) + TG_BM - 1) / TG_BM;
@@ -783,19 +793,28 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
         launch_limb_gemm(W.tmap, tb, a, st, bn);
     };
     const size_t asmem = pf_attn_smem(dh);
+    // attention scores on the tensor cores when dh = 128 (pf_scores.cuh);
+    // DIMG_PF_SCORES=0 keeps them on the CUDA cores
+    const char* ps_env = std::getenv("DIMG_PF_SCORES");
+    const bool tc_scores = w.kdig && (!ps_env || std::atoi(ps_env) != 0);
     for (uint32_t l = 0; l < m.L; ++l) {
         const auto& lw = m.layers[l];
         pf_norm_limbs_kernel<<<n, 256, 0, st>>>(w.x, D, lw.attn_norm, lw.attn_unit, m.ctx->seeds, w.pa, w.cap_pad,
                                                  m.Kd, w.wide);
         gemm(lw.qkv, w.tm_pa, TG_STORE, w.qkv, 3 * D);
+        const bool last = l + 1 == m.L;  // the last layer's output feeds only the lm_head
         pf_rope_kv_kernel<<<dim3(n, H), dh / 2, 0, st>>>(w.qkv, D, dh, m.rope_cos, m.rope_sin, s.kc + l * kv_layer,
                                                          s.vc + l * kv_layer, s.kc32 + l * kv_layer,
-                                                         s.vc32 + l * kv_layer, size_t(m.cfg.max_ctx) * dh, w.wide);
-        if (l + 1 == m.L) break;  // the last layer's output feeds only the lm_head
+                                                         s.vc32 + l * kv_layer, size_t(m.cfg.max_ctx) * dh, w.wide,
+                                                         tc_scores && !last ? w.kdig : nullptr, w.kdig_pad);
+        if (last) break;
+        if (tc_scores)
+            pf_scores_kernel<<<dim3(H, (n + PS_Q - 1) / PS_Q), PS_THREADS, pf_scores_smem(), st>>>(
+                w.tm_kdig, w.qkv, n, w.kdig_pad, D, m.inv_scale, w.strips, w.wide);
         launch_pf_attn(dh, dim3(H, (n + PA_Q - 1) / PA_Q), asmem, st, (const int64_t*)w.qkv, n, D, dh,
                        (const int32_t*)(s.kc32 + l * kv_layer), (const int32_t*)(s.vc32 + l * kv_layer),
                        size_t(m.cfg.max_ctx) * dh, m.inv_scale, (const int64_t*)m.ctx->exp_lut, w.strips, w.pa,
-                       w.cap_pad, m.Kd, w.wide);
+                       w.cap_pad, m.Kd, w.wide, tc_scores);
         gemm(lw.wo, w.tm_pa, TG_RESID, w.x, D);
         pf_norm_limbs_kernel<<<n, 256, 0, st>>>(w.x, D, lw.ffn_norm, lw.ffn_unit, m.ctx->seeds, w.pa, w.cap_pad,
                                                  m.Kd, w.wide);

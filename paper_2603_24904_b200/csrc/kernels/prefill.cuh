@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int64_t* __res
 __global__ void pf_rope_kv_kernel(int64_t* __restrict__ qkv, uint32_t D, uint32_t dh,
                                   const int64_t* __restrict__ rc, const int64_t* __restrict__ rs,
                                   int64_t* K64, int64_t* V64, int32_t* K32, int32_t* V32, size_t head_stride,
-                                  uint32_t* wide) {
+                                  uint32_t* wide, int8_t* kdig, uint32_t n_pad) {
     const uint32_t t = blockIdx.x, h = blockIdx.y, half = dh / 2, i = threadIdx.x;
     int64_t* q = qkv + size_t(t) * 3 * D + size_t(h) * dh;
     const int64_t* k = q + D;
@@ -115,7 +115,24 @@ __global__ void pf_rope_kv_kernel(int64_t* __restrict__ qkv, uint32_t D, uint32_
     V32[kv + i] = int32_t(v0);
     V32[kv + i + half] = int32_t(v1);
     const auto b23 = [](int64_t a) { return a >= -(int64_t(1) << 23) && a < (int64_t(1) << 23); };
-    if (!fits_i32(k0) || !fits_i32(k1) || !fits_i32(v0) || !fits_i32(v1) || !b23(q0) || !b23(q1)) *wide = 1;
+    bool bad = !fits_i32(k0) || !fits_i32(k1) || !fits_i32(v0) || !fits_i32(v1) || !b23(q0) || !b23(q1);
+    if (kdig) {  // the key's 4 signed digit planes for the tensor-core scores (pf_scores.cuh)
+        const int64_t kk[2] = {k0, k1};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            int64_t r = kk[e];
+            int8_t* dst = kdig + (size_t(h) * 4 * n_pad + t) * dh + i + e * half;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const int64_t dg = int8_t(r);
+                dst[size_t(d) * n_pad * dh] = int8_t(dg);
+                r = (r - dg) >> 8;
+            }
+            dst[size_t(3) * n_pad * dh] = int8_t(r);
+            bad |= r < -128 || r > 127;
+        }
+    }
+    if (bad) *wide = 1;
 }
 
 constexpr int PA_Q = 32;        // queries per CTA
@@ -169,7 +186,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
                                                                 size_t head_stride, int64_t inv_scale,
                                                                 const int64_t* __restrict__ lut_g, int32_t* strips,
                                                                 uint8_t* planes, uint32_t rows_pad, uint32_t ldp,
-                                                                uint32_t* wide) {
+                                                                uint32_t* wide, bool scores_ready) {
     extern __shared__ __align__(16) uint8_t pa_smem[];
     __shared__ int64_t lut[257];
     const uint32_t h = blockIdx.x, q0 = blockIdx.y * PA_Q;
@@ -209,8 +226,17 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
     int32_t mx[PA_QW];
 #pragma unroll
     for (int u = 0; u < PA_QW; ++u) mx[u] = INT32_MIN;
-    load_k(0, KV);
-    for (uint32_t c = 0; c < nch; ++c) {
+    if (scores_ready) {  // pf_scores_kernel wrote the strips: only the row maxima
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < PA_QW; ++u) {
+            const uint32_t t = tw + u;
+            if (t < n)
+                for (uint32_t p = lane; p <= t; p += 32) mx[u] = Sw[size_t(u) * ld + p] > mx[u] ? Sw[size_t(u) * ld + p] : mx[u];
+        }
+    }
+    if (!scores_ready) load_k(0, KV);
+    for (uint32_t c = 0; c < nch && !scores_ready; ++c) {
         int4* cur = KV + (c & 1) * chunk_q;
         if (c + 1 < nch) {
             load_k(c + 1, KV + ((c + 1) & 1) * chunk_q);
