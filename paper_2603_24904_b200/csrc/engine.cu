@@ -991,9 +991,13 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
         a.tile_cnt = r.tile_cnt;
         launch_limb_gemm(W.tmap, tb, a, st, bn, true);
     };
-    auto norm = [&](const int64_t* g, int unit) {
-        launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int64_t*)r.x, D, g, unit,
-                 (const int64_t*)m.ctx->seeds, r.pa, r.nmax_pad, m.Kd, r.wide);
+    auto norm = [&](const int64_t* g, int unit) {  // decode steps: a CTA cluster per token
+        if (n <= uint32_t(TG_BN_SMALL))
+            launch_k(true, bd_norm_cluster_kernel, n * BD_NCL, 256, 0, st, (const int64_t*)r.x, D, g, unit,
+                     (const int64_t*)m.ctx->seeds, r.pa, r.nmax_pad, m.Kd, r.wide);
+        else
+            launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int64_t*)r.x, D, g, unit,
+                     (const int64_t*)m.ctx->seeds, r.pa, r.nmax_pad, m.Kd, r.wide);
     };
     const size_t asmem = bd_attn_smem(dh, r.ctx) + 8;
     for (uint32_t l = 0; l < m.L; ++l) {

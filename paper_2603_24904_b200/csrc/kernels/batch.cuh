@@ -14,9 +14,12 @@
 // sequence path instead.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include <cstdint>
 
 #include "attention.cuh"
+#include "prefill.cuh"
 #include "q16.cuh"
 
 namespace dimg::dev {
@@ -67,6 +70,70 @@ __global__ void bd_rope_kv_kernel(int64_t* __restrict__ qkv, BatchTok bt, uint32
     V32[kv + i + half] = int32_t(v1);
     const auto b23 = [](int64_t a) { return a >= -(int64_t(1) << 23) && a < (int64_t(1) << 23); };
     if (!fits_i32(k0) || !fits_i32(k1) || !fits_i32(v0) || !fits_i32(v1) || !b23(q0) || !b23(q1)) *wide = 1;
+}
+
+// rmsnorm (proj/src/kernels.cpp:56-68) of each token row into the next
+// GEMM's digit planes, for the few tokens of a decode batch: a cluster of
+// BD_NCL CTAs per token, each summing x^2 over a quarter of the row; the
+// partial sums meet through distributed shared memory behind one cluster
+// barrier, and every CTA derives the same r (inv_sqrt_q16 of the u128 total,
+// order-free) and writes its quarter. A single CTA per token left 8 SMs
+// working through a long load -> reduce -> Newton -> store chain.
+constexpr int BD_NCL = 4;
+
+__global__ void __cluster_dims__(BD_NCL, 1, 1) __launch_bounds__(256)
+    bd_norm_cluster_kernel(const int64_t* __restrict__ x, uint32_t K, const int64_t* __restrict__ gamma,
+                           int gamma_unit, const int64_t* __restrict__ seeds, uint8_t* planes, uint32_t rows_pad,
+                           uint32_t ldp, uint32_t* wide) {
+    namespace cg = cooperative_groups;
+    __shared__ u128 red[32];
+    __shared__ u128 part;
+    __shared__ int64_t s_r;
+    cg::cluster_group cl = cg::this_cluster();
+    pdl_launch_dependents();
+    pdl_wait();
+    const uint32_t rank = cl.block_rank(), t = blockIdx.x / BD_NCL;
+    const uint32_t per = (K + BD_NCL - 1) / BD_NCL, j0 = min(K, rank * per), j1 = min(K, j0 + per);
+    const int64_t* xr = x + size_t(t) * K;
+    constexpr int PER = 4;  // elements per thread in registers (K <= 4096)
+    int64_t v[PER];
+    u128 ss = 0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const uint32_t j = j0 + threadIdx.x + u * 256;
+        v[u] = j < j1 ? xr[j] : 0;
+        ss += mul_full(v[u], v[u]);
+    }
+    for (uint32_t j = j0 + threadIdx.x + PER * 256; j < j1; j += 256) ss += mul_full(xr[j], xr[j]);
+    ss = block_sum_u128(ss, red);
+    if (threadIdx.x == 0) part = ss;
+    cl.sync();
+    if (threadIdx.x == 0) {
+        u128 tot = 0;
+        for (uint32_t r = 0; r < BD_NCL; ++r) tot += *cl.map_shared_rank(&part, r);
+        const int64_t ms = (tot >> 63) == 0 ? int64_t((uint64_t(tot) / K) >> 16) : int64_t((i128(tot) / i128(K)) >> 16);
+        s_r = ms + 1 > 0 ? inv_sqrt_q16(ms + 1, seeds) : 0;
+        if (ms + 1 <= 0) *wide = 1;  // the reference throws (domain_error): the exact path reports it
+    }
+    __syncthreads();
+    const int64_t r = s_r;
+    const size_t plane = size_t(rows_pad) * ldp;
+    uint8_t* pr = planes + size_t(t) * ldp;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const uint32_t j = j0 + threadIdx.x + u * 256;
+        if (j < j1) {
+            int64_t o = mul16(v[u], r);
+            if (!gamma_unit) o = mul16(o, gamma[j]);
+            pf_put_limbs(pr + j, plane, o, wide);
+        }
+    }
+    for (uint32_t j = j0 + threadIdx.x + PER * 256; j < j1; j += 256) {
+        int64_t o = mul16(xr[j], r);
+        if (!gamma_unit) o = mul16(o, gamma[j]);
+        pf_put_limbs(pr + j, plane, o, wide);
+    }
+    cl.sync();  // peers may still be reading this CTA's partial
 }
 
 constexpr int BD_THREADS = 256;
