@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
     int32_t* Ps = reinterpret_cast<int32_t*>(Q + size_t(PA_Q) * nq);  // [PA_Q][PA_CH]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 257; i += PA_THREADS) lut[i] = lut_g[i];
-    for (uint32_t i = threadIdx.x; i < PA_Q * nq; i += PA_THREADS) {
+    for (uint32_t i = threadIdx.x; i < PA_Q * nq && !scores_ready; i += PA_THREADS) {
         const uint32_t qi = i / nq, j = 4 * (i % nq);
         int4 v = make_int4(0, 0, 0, 0);
         if (q0 + qi < n) {
