@@ -790,6 +790,9 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
             a.partial = w.partial;
             a.tile_cnt = w.tile_cnt;
         }
+        // token tiles fastest when the activation planes stay L2-resident
+        // (K = d_model: 25 MB at 2048 tokens); w_down's 68 MB do not
+        a.token_fast = size_t(3) * n * W.K <= (size_t(32) << 20) ? 1 : 0;
         launch_limb_gemm(W.tmap, tb, a, st, bn);
     };
     const size_t asmem = pf_attn_smem(dh);

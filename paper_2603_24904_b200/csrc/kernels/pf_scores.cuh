@@ -33,7 +33,7 @@ constexpr int PS_Q = 32;        // queries per CTA (= PA_Q)
 constexpr int PS_KD = 4;        // key digits
 constexpr int PS_QD = 3;        // query digits
 constexpr int PS_DH = 128;      // head dim (one 128-byte K block)
-constexpr int PS_THREADS = 128;
+constexpr int PS_THREADS = 256;  // 8 warps: warps w and w + 4 share TMEM lane quarter w, 16 queries each
 constexpr int PS_A_BYTES = PS_KD * PS_M * PS_DH;   // one tile: 4 planes x 128 rows x 128 B
 constexpr int PS_B_BYTES = PS_QD * PS_Q * PS_DH;   // 96 rows x 128 B
 constexpr int PS_N = PS_QD * PS_Q;                 // MMA N
@@ -138,11 +138,12 @@ __global__ void __launch_bounds__(PS_THREADS, 1) pf_scores_kernel(const __grid_c
         tg_mbar_wait(&mma_done, t & 1);
         tg_fence_after();
         if (warp == 0 && t + 2 < n_tiles) load_tile(t + 2);  // its buffer is free: the MMAs read it
-        // epilogue: thread = position p (TMEM lane), 16 queries at a time
-        const uint32_t p = t * PS_M + 32 * warp + lane;
-        const uint32_t tb = tmem + ((32 * warp) << 16);
-#pragma unroll 1
-        for (int half = 0; half < 2; ++half) {
+        // epilogue: thread = position p (TMEM lane of quarter warp % 4), the
+        // warp's half of the 32 queries
+        const uint32_t p = t * PS_M + 32 * (warp & 3) + lane;
+        const uint32_t tb = tmem + ((32 * (warp & 3)) << 16);
+        {
+            const int half = warp >> 2;
             int64_t s[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) s[e] = 0;

@@ -86,6 +86,11 @@ struct TgArgs {
     uint32_t ksplit;
     int32_t* partial;       // [tiles][3][BN][128], zero between launches (the last CTA resets)
     uint32_t* tile_cnt;     // [tiles], zero between launches (the last CTA resets)
+    // tile order: 0 = feature tiles fastest (concurrent CTAs share the token
+    // tile; weights re-read per token tile), 1 = token tiles fastest
+    // (concurrent CTAs share the weight tile, which streams from HBM once;
+    // the activation planes are re-read and must fit L2)
+    uint32_t token_fast;
 #ifdef TG_TRACE
     uint64_t* trace;        // [grid][128] globaltimer stamps (tools/gemm_bench.cu)
 #endif
@@ -213,9 +218,15 @@ __device__ __forceinline__ void tg_ld_wait() { asm volatile("tcgen05.wait::ld.sy
 // ---- the kernel ---------------------------------------------------------------------
 
 template <int BN>
-__device__ __forceinline__ void tg_tile(uint32_t tile, uint32_t n_mt, uint32_t& n0, uint32_t& t0) {
-    n0 = (tile % n_mt) * TG_BM;  // feature tiles fastest: consecutive CTAs share the token tile
-    t0 = (tile / n_mt) * BN;
+__device__ __forceinline__ void tg_tile(uint32_t tile, uint32_t n_mt, uint32_t n_tt, uint32_t token_fast,
+                                        uint32_t& n0, uint32_t& t0) {
+    if (token_fast) {
+        n0 = (tile / n_tt) * TG_BM;
+        t0 = (tile % n_tt) * BN;
+    } else {
+        n0 = (tile % n_mt) * TG_BM;
+        t0 = (tile / n_mt) * BN;
+    }
 }
 
 // work item -> (tile, K-block range)
@@ -282,7 +293,7 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
         for (uint32_t item = blockIdx.x; item < n_items && it < S::STAGES; item += gridDim.x) {
             uint32_t tile, ks, kb0, kb1, n0, t0;
             tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
-            tg_tile<BN>(tile, n_mt, n0, t0);
+            tg_tile<BN>(tile, n_mt, n_tt, a.token_fast, n0, t0);
             for (uint32_t kb = kb0; kb < kb1 && it < S::STAGES; ++kb, ++it) {
                 tg_expect_tx_w(&full[it], S::STAGE_BYTES);
                 tg_tma_2d_w(smem + size_t(it) * S::STAGE_BYTES, &tmA, 0, int32_t(kb * a.a_rows + n0), &full[it]);
@@ -297,7 +308,7 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
         for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
             uint32_t tile, ks, kb0, kb1, n0, t0;
             tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
-            tg_tile<BN>(tile, n_mt, n0, t0);
+            tg_tile<BN>(tile, n_mt, n_tt, a.token_fast, n0, t0);
             for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
                 const uint32_t s = it % S::STAGES;
                 uint8_t* st = smem + size_t(s) * S::STAGE_BYTES;
@@ -356,7 +367,7 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
         for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++j) {
             uint32_t tile, ks, kb0, kb1, n0, t0;
             tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
-            tg_tile<BN>(tile, n_mt, n0, t0);
+            tg_tile<BN>(tile, n_mt, n_tt, a.token_fast, n0, t0);
             const uint32_t b = j % S::NB;
             const uint32_t n = n0 + fl;
             const bool nv = n < a.n_out;
