@@ -423,6 +423,7 @@ struct PrefillWs {
     uint32_t* tile_cnt = nullptr;
     size_t partial_elems = 0;
     int8_t* kdig = nullptr;          // key digit planes [H][4][kdig_pad][128] (tensor-core scores, dh 128)
+    uint32_t* kd4 = nullptr;         // [layers]: some key of the layer needs the 4th digit
     uint32_t kdig_pad = 0;
     CUtensorMap tm_kdig;
 };
@@ -731,6 +732,7 @@ void ensure_prefill_ws(dimg_session& s, uint32_t n) {
         w.kdig_pad = (w.cap + PS_M - 1) / PS_M * PS_M;
         w.kdig = s.mem.alloc<int8_t>(size_t(m.H) * PS_KD * w.kdig_pad * PS_DH);
         w.tm_kdig = tmap_bytes(w.kdig, PS_DH, size_t(m.H) * PS_KD * w.kdig_pad, PS_DH, PS_M);
+        if (!w.kd4) w.kd4 = s.mem.alloc<uint32_t>(m.L);
     }
     w.tm_ph_s = tmap_bytes(w.ph, m.F, size_t(3) * w.cap_pad, m.Kf, TG_BN_SMALL);
     if (!w.partial) {  // one 16-token tile column: the largest matrix's row tiles
@@ -800,6 +802,9 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
     // DIMG_PF_SCORES=0 keeps them on the CUDA cores
     const char* ps_env = std::getenv("DIMG_PF_SCORES");
     const bool tc_scores = w.kdig && (!ps_env || std::atoi(ps_env) != 0);
+    // DIMG_PF_KD4=1 forces the 4th key digit plane (tests of that path)
+    const char* kd4_env = std::getenv("DIMG_PF_KD4");
+    if (tc_scores) CK(cudaMemsetAsync(w.kd4, kd4_env && std::atoi(kd4_env) ? 1 : 0, size_t(m.L) * 4, st));
     for (uint32_t l = 0; l < m.L; ++l) {
         const auto& lw = m.layers[l];
         pf_norm_limbs_kernel<<<n, 256, 0, st>>>(w.x, D, lw.attn_norm, lw.attn_unit, m.ctx->seeds, w.pa, w.cap_pad,
@@ -809,11 +814,12 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
         pf_rope_kv_kernel<<<dim3(n, H), dh / 2, 0, st>>>(w.qkv, D, dh, m.rope_cos, m.rope_sin, s.kc + l * kv_layer,
                                                          s.vc + l * kv_layer, s.kc32 + l * kv_layer,
                                                          s.vc32 + l * kv_layer, size_t(m.cfg.max_ctx) * dh, w.wide,
-                                                         tc_scores && !last ? w.kdig : nullptr, w.kdig_pad);
+                                                         tc_scores && !last ? w.kdig : nullptr, w.kdig_pad,
+                                                         tc_scores ? w.kd4 + l : nullptr);
         if (last) break;
         if (tc_scores)
             pf_scores_kernel<<<dim3(H, (n + PS_Q - 1) / PS_Q), PS_THREADS, pf_scores_smem(), st>>>(
-                w.tm_kdig, w.qkv, n, w.kdig_pad, D, m.inv_scale, w.strips, w.wide);
+                w.tm_kdig, w.qkv, n, w.kdig_pad, D, m.inv_scale, w.strips, w.wide, w.kd4 + l);
         launch_pf_attn(dh, dim3(H, (n + PA_Q - 1) / PA_Q), asmem, st, (const int64_t*)w.qkv, n, D, dh,
                        (const int32_t*)(s.kc32 + l * kv_layer), (const int32_t*)(s.vc32 + l * kv_layer),
                        size_t(m.cfg.max_ctx) * dh, m.inv_scale, (const int64_t*)m.ctx->exp_lut, w.strips, w.pa,

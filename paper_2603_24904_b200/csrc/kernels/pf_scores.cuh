@@ -65,7 +65,7 @@ __device__ __forceinline__ bool ps_digits(int64_t v, int e, uint32_t (&packed)[N
 __global__ void __launch_bounds__(PS_THREADS, 1) pf_scores_kernel(const __grid_constant__ CUtensorMap kmap,
                                                                   const int64_t* __restrict__ qkv, uint32_t n,
                                                                   uint32_t n_pad, uint32_t D, int64_t inv_scale,
-                                                                  int32_t* strips, uint32_t* wide) {
+                                                                  int32_t* strips, uint32_t* wide, const uint32_t* kd4) {
     extern __shared__ uint8_t ps_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ps_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* A = smem;                    // 2 x tile
@@ -77,6 +77,9 @@ __global__ void __launch_bounds__(PS_THREADS, 1) pf_scores_kernel(const __grid_c
     const uint32_t n_tiles = last_q / PS_M + 1;   // tiles of positions 0 .. last_q
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t ld = (n + 3) & ~3u;
+    // keys within 3 digits (|k| <= 0x7F7F7F, the usual case) leave the 4th
+    // plane zero: 9 digit pairs instead of 12
+    const int n_kd = *kd4 ? PS_KD : PS_KD - 1;
     int big = 0;
 
     if (threadIdx.x == 0) {
@@ -112,10 +115,12 @@ __global__ void __launch_bounds__(PS_THREADS, 1) pf_scores_kernel(const __grid_c
     // warp 0 issues the TMA loads and MMAs (converged, one elected lane)
     auto load_tile = [&](uint32_t t) {  // the 4 key digit planes of positions [128 t, 128 t + 128)
         uint8_t* dst = A + (t & 1) * PS_A_BYTES;
-        tg_expect_tx_w(&full[t & 1], PS_A_BYTES);
+        tg_expect_tx_w(&full[t & 1], n_kd * PS_M * PS_DH);
 #pragma unroll
         for (int i = 0; i < PS_KD; ++i)
-            tg_tma_2d_w(dst + i * PS_M * PS_DH, &kmap, 0, int32_t((h * PS_KD + i) * n_pad + t * PS_M), &full[t & 1]);
+            if (i < n_kd)
+                tg_tma_2d_w(dst + i * PS_M * PS_DH, &kmap, 0, int32_t((h * PS_KD + i) * n_pad + t * PS_M),
+                            &full[t & 1]);
     };
     if (warp == 0) {
         load_tile(0);
@@ -129,10 +134,11 @@ __global__ void __launch_bounds__(PS_THREADS, 1) pf_scores_kernel(const __grid_c
             const uint32_t sa = tg_smem_u32(A + (t & 1) * PS_A_BYTES), sb = tg_smem_u32(B);
 #pragma unroll
             for (int i = 0; i < PS_KD; ++i)
+                if (i < n_kd)
 #pragma unroll
-                for (int kk = 0; kk < PS_DH / 32; ++kk)
-                    tg_mma_w(tmem + i * PS_N, tg_desc(sa + i * PS_M * PS_DH + 32 * kk), tg_desc(sb + 32 * kk),
-                             tg_idesc(PS_N), kk != 0);
+                    for (int kk = 0; kk < PS_DH / 32; ++kk)
+                        tg_mma_w(tmem + i * PS_N, tg_desc(sa + i * PS_M * PS_DH + 32 * kk), tg_desc(sb + 32 * kk),
+                                 tg_idesc(PS_N), kk != 0);
             tg_commit_w(&mma_done);
         }
         tg_mbar_wait(&mma_done, t & 1);
@@ -149,6 +155,7 @@ __global__ void __launch_bounds__(PS_THREADS, 1) pf_scores_kernel(const __grid_c
             for (int e = 0; e < 16; ++e) s[e] = 0;
 #pragma unroll
             for (int i = 0; i < PS_KD; ++i) {  // the three query digits of key digit i: one wait
+                if (i >= n_kd) break;
                 int32_t v[PS_QD][16];
 #pragma unroll
                 for (int d = 0; d < PS_QD; ++d) tg_ld16(tb + i * PS_N + d * PS_Q + 16 * half, v[d]);

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int64_t* __res
 __global__ void pf_rope_kv_kernel(int64_t* __restrict__ qkv, uint32_t D, uint32_t dh,
                                   const int64_t* __restrict__ rc, const int64_t* __restrict__ rs,
                                   int64_t* K64, int64_t* V64, int32_t* K32, int32_t* V32, size_t head_stride,
-                                  uint32_t* wide, int8_t* kdig, uint32_t n_pad) {
+                                  uint32_t* wide, int8_t* kdig, uint32_t n_pad, uint32_t* kd4) {
     const uint32_t t = blockIdx.x, h = blockIdx.y, half = dh / 2, i = threadIdx.x;
     int64_t* q = qkv + size_t(t) * 3 * D + size_t(h) * dh;
     const int64_t* k = q + D;
@@ -130,6 +130,7 @@ __global__ void pf_rope_kv_kernel(int64_t* __restrict__ qkv, uint32_t D, uint32_
             }
             dst[size_t(3) * n_pad * dh] = int8_t(r);
             bad |= r < -128 || r > 127;
+            if (r != 0) atomicOr(kd4, 1u);  // this layer's keys need the 4th digit plane
         }
     }
     if (bad) *wide = 1;

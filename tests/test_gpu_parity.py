@@ -273,11 +273,15 @@ def test_dense_tokens_wide_rows_fall_back_exactly(P, oracle):
 
 # ---- tensor-core prefill (whole prompt per layer) ------------------------------
 
-@pytest.mark.parametrize("cfg6,plen,seed", [((2, 64, 2, 64, 64, 256), 200, 3), ((2, 256, 2, 512, 300, 400), 300, 4),
-                                            ((3, 96, 3, 160, 77, 200), 40, 5)])
-def test_tensor_core_prefill_matches_oracle(P, oracle, monkeypatch, cfg6, plen, seed):
+@pytest.mark.parametrize("cfg6,plen,seed,kd4", [((2, 64, 2, 64, 64, 256), 200, 3, 0),
+                                                 ((2, 256, 2, 512, 300, 400), 300, 4, 0),
+                                                 ((2, 256, 2, 512, 300, 400), 300, 4, 1),
+                                                 ((3, 96, 3, 160, 77, 200), 40, 5, 0)])
+def test_tensor_core_prefill_matches_oracle(P, oracle, monkeypatch, cfg6, plen, seed, kd4):
+    """kd4=1 forces the tensor-core scores' 4th key digit plane (dh = 128)."""
     from oracle.pyoracle import Config
     monkeypatch.setenv("DIMG_PREFILL", "1")
+    monkeypatch.setenv("DIMG_PF_KD4", str(kd4))
     m = P.gen_toy_model(seed, P.ModelConfig(*cfg6))
     om = oracle.gen_toy(seed, Config(*cfg6))
     prompt = P.prompt_from_seed(seed + 100, cfg6[4], plen)
