@@ -274,6 +274,7 @@ struct BatchCache;  // batched-generation buffers + captured step graph (see bel
 
 struct dimg_model {
     std::shared_ptr<BatchCache> batch;  // declared first: released after the weights' users
+    std::mutex batch_mu;                // one batched generation at a time uses `batch`
     int device;
     DevCtx* ctx;
     dimg_config cfg;
@@ -1037,7 +1038,7 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
 
 // The batch path: true if every sequence's tokens were produced exactly.
 bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<uint32_t>>& prompts,
-                       uint32_t max_new, uint32_t* tokens_out, uint64_t* steps_graph) {
+                       uint32_t max_new, uint32_t* tokens_out) {
     uint32_t ctx = 0, n_prompt_pos = 0;
     for (const auto& p : prompts) {
         ctx = std::max<uint32_t>(ctx, uint32_t(p.size()) + max_new);
@@ -1100,7 +1101,6 @@ bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<
             c.ge_B = B;
         }
         for (uint32_t s = 0; s < max_new; ++s) CK(cudaGraphLaunch(c.ge, r.st));
-        if (steps_graph) *steps_graph += max_new;
     }
     uint32_t wide = 0;
     CK(cudaMemcpyAsync(&wide, r.wide, 4, cudaMemcpyDeviceToHost, r.st));
@@ -1438,8 +1438,8 @@ dimg_status dimg_generate_greedy_batch(dimg_model* m, uint32_t n_seqs, const uin
             check_prompt(*m, ps[b].data(), p_lens[b], max_new);
         }
         uint32_t used = 0;
-        static uint64_t graph_steps = 0;
-        if (n_seqs && batch_shape_ok(*m) && generate_batch_tc(m, n_seqs, ps, max_new, tokens_out, &graph_steps)) {
+        std::unique_lock<std::mutex> lk(m->batch_mu);
+        if (n_seqs && batch_shape_ok(*m) && generate_batch_tc(m, n_seqs, ps, max_new, tokens_out)) {
             used = 1;
             g_generations.fetch_add(n_seqs, std::memory_order_relaxed);
         } else if (n_seqs) {
