@@ -749,10 +749,10 @@ void ensure_prefill_ws(dimg_session& s, uint32_t n) {
 template <class... A>
 void launch_pf_attn(uint32_t dh, dim3 grid, size_t smem, cudaStream_t st, A... args) {
     const uint32_t dpl = (dh + 31) / 32;
-    if (dpl <= 1) pf_attn_kernel<1><<<grid, PA_THREADS, smem, st>>>(args...);
-    else if (dpl <= 2) pf_attn_kernel<2><<<grid, PA_THREADS, smem, st>>>(args...);
-    else if (dpl <= 4) pf_attn_kernel<4><<<grid, PA_THREADS, smem, st>>>(args...);
-    else pf_attn_kernel<8><<<grid, PA_THREADS, smem, st>>>(args...);  // dh <= 256 (tc_prefill_ok)
+    if (dpl <= 1) launch_k(true, pf_attn_kernel<1>, grid, PA_THREADS, smem, st, args...);
+    else if (dpl <= 2) launch_k(true, pf_attn_kernel<2>, grid, PA_THREADS, smem, st, args...);
+    else if (dpl <= 4) launch_k(true, pf_attn_kernel<4>, grid, PA_THREADS, smem, st, args...);
+    else launch_k(true, pf_attn_kernel<8>, grid, PA_THREADS, smem, st, args...);  // dh <= 256 (tc_prefill_ok)
 }
 
 // Positions 0..n-1 of the prompt through every layer on the tensor cores;
@@ -766,7 +766,9 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
     const size_t kv_layer = size_t(H) * m.cfg.max_ctx * dh;
     CK(cudaMemsetAsync(w.wide, 0, 4, st));
     CK(cudaMemsetAsync(s.kvwide, 0, size_t(m.L) * H * 4, st));
-    pf_embed_kernel<<<1024, 256, 0, st>>>(s.tokens, n, m.embd, m.embd_s, D, w.x);
+    // every kernel of the chain by programmatic dependent launch (pdl_wait in each)
+    launch_k(true, pf_embed_kernel, 1024, 256, 0, st, (const uint32_t*)s.tokens, n, (const int8_t*)m.embd,
+             (const int64_t*)m.embd_s, D, w.x);
     // short prompts: 16-token tiles split over K (one split per CTA slot), as the decode batches
     const bool small = n <= uint32_t(TG_BN_SMALL);
     const uint32_t bn = small ? TG_BN_SMALL : TG_BN;
@@ -796,7 +798,7 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
         // token tiles fastest when the activation planes stay L2-resident
         // (K = d_model: 25 MB at 2048 tokens); w_down's 68 MB do not
         a.token_fast = size_t(3) * n * W.K <= (size_t(32) << 20) ? 1 : 0;
-        launch_limb_gemm(W.tmap, tb, a, st, bn);
+        launch_limb_gemm(W.tmap, tb, a, st, bn, true);
     };
     const size_t asmem = pf_attn_smem(dh);
     // attention scores on the tensor cores when dh = 128 (pf_scores.cuh);
@@ -808,26 +810,26 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
     if (tc_scores) CK(cudaMemsetAsync(w.kd4, kd4_env && std::atoi(kd4_env) ? 1 : 0, size_t(m.L) * 4, st));
     for (uint32_t l = 0; l < m.L; ++l) {
         const auto& lw = m.layers[l];
-        pf_norm_limbs_kernel<<<n, 256, 0, st>>>(w.x, D, lw.attn_norm, lw.attn_unit, m.ctx->seeds, w.pa, w.cap_pad,
-                                                 m.Kd, w.wide);
+        launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int64_t*)w.x, D, (const int64_t*)lw.attn_norm,
+                 int(lw.attn_unit), (const int64_t*)m.ctx->seeds, w.pa, w.cap_pad, m.Kd, w.wide);
         gemm(lw.qkv, w.tm_pa, TG_STORE, w.qkv, 3 * D);
         const bool last = l + 1 == m.L;  // the last layer's output feeds only the lm_head
-        pf_rope_kv_kernel<<<dim3(n, H), dh / 2, 0, st>>>(w.qkv, D, dh, m.rope_cos, m.rope_sin, s.kc + l * kv_layer,
-                                                         s.vc + l * kv_layer, s.kc32 + l * kv_layer,
-                                                         s.vc32 + l * kv_layer, size_t(m.cfg.max_ctx) * dh, w.wide,
-                                                         tc_scores && !last ? w.kdig : nullptr, w.kdig_pad,
-                                                         tc_scores ? w.kd4 + l : nullptr);
+        launch_k(true, pf_rope_kv_kernel, dim3(n, H), dh / 2, 0, st, w.qkv, D, dh, (const int64_t*)m.rope_cos,
+                 (const int64_t*)m.rope_sin, s.kc + l * kv_layer, s.vc + l * kv_layer, s.kc32 + l * kv_layer,
+                 s.vc32 + l * kv_layer, size_t(m.cfg.max_ctx) * dh, w.wide, tc_scores && !last ? w.kdig : nullptr,
+                 w.kdig_pad, tc_scores ? w.kd4 + l : (uint32_t*)nullptr);
         if (last) break;
         if (tc_scores)
-            pf_scores_kernel<<<dim3(H, (n + PS_Q - 1) / PS_Q), PS_THREADS, pf_scores_smem(), st>>>(
-                w.tm_kdig, w.qkv, n, w.kdig_pad, D, m.inv_scale, w.strips, w.wide, w.kd4 + l);
+            launch_k(true, pf_scores_kernel, dim3(H, (n + PS_Q - 1) / PS_Q), PS_THREADS, pf_scores_smem(), st,
+                     w.tm_kdig, (const int64_t*)w.qkv, n, w.kdig_pad, D, m.inv_scale, w.strips, w.wide,
+                     (const uint32_t*)(w.kd4 + l));
         launch_pf_attn(dh, dim3(H, (n + PA_Q - 1) / PA_Q), asmem, st, (const int64_t*)w.qkv, n, D, dh,
                        (const int32_t*)(s.kc32 + l * kv_layer), (const int32_t*)(s.vc32 + l * kv_layer),
                        size_t(m.cfg.max_ctx) * dh, m.inv_scale, (const int64_t*)m.ctx->exp_lut, w.strips, w.pa,
                        w.cap_pad, m.Kd, w.wide, tc_scores);
         gemm(lw.wo, w.tm_pa, TG_RESID, w.x, D);
-        pf_norm_limbs_kernel<<<n, 256, 0, st>>>(w.x, D, lw.ffn_norm, lw.ffn_unit, m.ctx->seeds, w.pa, w.cap_pad,
-                                                 m.Kd, w.wide);
+        launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int64_t*)w.x, D, (const int64_t*)lw.ffn_norm,
+                 int(lw.ffn_unit), (const int64_t*)m.ctx->seeds, w.pa, w.cap_pad, m.Kd, w.wide);
         gemm(lw.gu, w.tm_pa, TG_SILU, nullptr, 0);
         gemm(lw.down, w.tm_ph, TG_RESID, w.x, D);
     }

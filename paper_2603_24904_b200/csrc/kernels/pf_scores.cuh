@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(PS_THREADS, 1) pf_scores_kernel(const __grid_c
     const uint32_t ld = (n + 3) & ~3u;
     // keys within 3 digits (|k| <= 0x7F7F7F, the usual case) leave the 4th
     // plane zero: 9 digit pairs instead of 12
-    const int n_kd = *kd4 ? PS_KD : PS_KD - 1;
+    int n_kd = PS_KD;
     int big = 0;
 
     if (threadIdx.x == 0) {
@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(PS_THREADS, 1) pf_scores_kernel(const __grid_c
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
+    pdl_launch_dependents();
+    pdl_wait();  // q (QKV GEMM) and the key digits (RoPE/KV kernel) come from the previous kernels
     // query digits: thread = (query, 4-dim group) pairs, one u32 per digit plane
     for (uint32_t i = threadIdx.x; i < PS_Q * (PS_DH / 4); i += PS_THREADS) {
         const uint32_t qi = i / (PS_DH / 4), j = 4 * (i % (PS_DH / 4));
@@ -107,6 +109,7 @@ __global__ void __launch_bounds__(PS_THREADS, 1) pf_scores_kernel(const __grid_c
         for (int d = 0; d < PS_QD; ++d)
             *reinterpret_cast<uint32_t*>(B + ps_sw128(d * PS_Q + qi, j)) = pk[d];
     }
+    n_kd = *kd4 ? PS_KD : PS_KD - 1;  // set by the RoPE/KV kernel: after the wait
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> MMA operand reads
     tg_fence_before();
     __syncthreads();

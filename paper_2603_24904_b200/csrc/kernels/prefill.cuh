@@ -22,6 +22,8 @@ namespace dimg::dev {
 // x[t] = embed_token(tok[t]) (proj/src/engine.cpp:10-19)
 __global__ void pf_embed_kernel(const uint32_t* __restrict__ tok, uint32_t n, const int8_t* __restrict__ E,
                                 const int64_t* __restrict__ Es, uint32_t D, int64_t* __restrict__ x) {
+    pdl_launch_dependents();
+    pdl_wait();
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < size_t(n) * D;
          i += size_t(gridDim.x) * blockDim.x) {
         const uint32_t t = uint32_t(i / D), j = uint32_t(i % D);
@@ -93,6 +95,8 @@ __global__ void pf_rope_kv_kernel(int64_t* __restrict__ qkv, uint32_t D, uint32_
                                   const int64_t* __restrict__ rc, const int64_t* __restrict__ rs,
                                   int64_t* K64, int64_t* V64, int32_t* K32, int32_t* V32, size_t head_stride,
                                   uint32_t* wide, int8_t* kdig, uint32_t n_pad, uint32_t* kd4) {
+    pdl_launch_dependents();
+    pdl_wait();
     const uint32_t t = blockIdx.x, h = blockIdx.y, half = dh / 2, i = threadIdx.x;
     int64_t* q = qkv + size_t(t) * 3 * D + size_t(h) * dh;
     const int64_t* k = q + D;
@@ -197,7 +201,9 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
     int4* Q = KV + 2 * size_t(chunk_q);                     // [PA_Q][nq]
     int32_t* Ps = reinterpret_cast<int32_t*>(Q + size_t(PA_Q) * nq);  // [PA_Q][PA_CH]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < 257; i += PA_THREADS) lut[i] = lut_g[i];
+    pdl_launch_dependents();
+    for (int i = threadIdx.x; i < 257; i += PA_THREADS) lut[i] = lut_g[i];  // constant: before the wait
+    pdl_wait();
     for (uint32_t i = threadIdx.x; i < PA_Q * nq && !scores_ready; i += PA_THREADS) {
         const uint32_t qi = i / nq, j = 4 * (i % nq);
         int4 v = make_int4(0, 0, 0, 0);
