@@ -246,8 +246,9 @@ void launch_limb_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs
     const uint32_t per_sm = bn == TG_BN_SMALL ? 2u : 1u;
     const uint32_t grid = std::min<uint32_t>(items, per_sm * uint32_t(sms));
     if (bn == TG_BN_SMALL)
-        launch_k(pdl, limb_gemm_kernel<TG_BN_SMALL>, grid, TG_THREADS, TgShape<TG_BN_SMALL>::SMEM, st, ta, tb, a);
-    else launch_k(pdl, limb_gemm_kernel<TG_BN>, grid, TG_THREADS, TgShape<TG_BN>::SMEM, st, ta, tb, a);
+        launch_k(pdl, limb_gemm_kernel<TG_BN_SMALL>, grid, TgShape<TG_BN_SMALL>::THREADS, TgShape<TG_BN_SMALL>::SMEM,
+                 st, ta, tb, a);
+    else launch_k(pdl, limb_gemm_kernel<TG_BN>, grid, TgShape<TG_BN>::THREADS, TgShape<TG_BN>::SMEM, st, ta, tb, a);
 }
 
 }  // namespace

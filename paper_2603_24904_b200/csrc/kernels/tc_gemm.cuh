@@ -43,7 +43,7 @@ constexpr int TG_BN_SMALL = 16; // tokens per tile for decode batches of <= 16 s
 constexpr int TG_BK = 128;      // K bytes per stage = one 128-byte swizzle row
 constexpr int TG_L = 3;         // activation limbs
 constexpr int TG_A_BYTES = TG_BM * TG_BK;
-constexpr int TG_THREADS = 192;
+constexpr int TG_THREADS = 192;  // BN 16: producer + MMA warp + 4 epilogue warps
 template <int BN>
 struct TgShape {
     static constexpr int B_BYTES = BN * TG_BK;
@@ -58,6 +58,12 @@ struct TgShape {
     static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;  // + alignment slack
     static constexpr int ACC = TG_L * BN;  // TMEM columns of one tile's accumulators
     static constexpr int NB = 2;  // accumulator sets (double-buffered: epilogue || next MMAs)
+    // epilogue warps: 8 for 64-token tiles (two per TMEM lane quarter, each
+    // taking half of the tile's 16-column chunks: the SiLU epilogue of a tile
+    // is then not exposed behind a short tile list), 4 for 16-token tiles
+    static constexpr int EPI_WARPS = BN >= 64 ? 8 : 4;
+    static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+    static constexpr int MIN_BLOCKS = BN >= 64 ? 1 : 2;
     static constexpr uint32_t TMEM_COLS = NB * ACC <= 128 ? 128 : NB * ACC <= 256 ? 256 : 512;
 };
 
@@ -239,7 +245,7 @@ __device__ __forceinline__ void tg_item(uint32_t item, uint32_t ksplit, uint32_t
 }
 
 template <int BN>
-__global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
+__global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
     limb_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const TgArgs a) {
     using S = TgShape<BN>;
@@ -265,7 +271,7 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
         }
         for (int b = 0; b < 2; ++b) {
             tg_mbar_init(&acc_full[b], 1);
-            tg_mbar_init(&acc_empty[b], 4);  // the four epilogue warps
+            tg_mbar_init(&acc_empty[b], S::EPI_WARPS);  // every epilogue warp releases the set
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -357,11 +363,13 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
     } else {
         // epilogue: thread = feature n, columns = tokens
         if (a.epi == TG_SILU) {  // constant: before the dependency wait
-            for (int i = threadIdx.x - 64; i < 257; i += 128) s_lut[i] = a.lut[i];
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            for (int i = threadIdx.x - 64; i < 257; i += 32 * S::EPI_WARPS) s_lut[i] = a.lut[i];
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * S::EPI_WARPS) : "memory");
         }
         pdl_wait();  // reads / writes data the previous kernels own
-        const uint32_t q = warp & 3;
+        const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+        constexpr uint32_t NH = S::EPI_WARPS / 4;      // warps per lane quarter
+        const uint32_t c_first = 16 * ((warp - 2) / 4);  // this warp's first 16-column chunk
         const uint32_t fl = 32 * q + lane;  // feature within the tile
         uint32_t j = 0;
         for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++j) {
@@ -378,7 +386,7 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
             bool last = true;
             if (ksplit > 1) {
                 // this split's partials added into the tile accumulator (fire and forget)
-                for (uint32_t c0 = 0; c0 < BN; c0 += 16) {
+                for (uint32_t c0 = c_first; c0 < BN; c0 += 16 * NH) {
                     int32_t d[TG_L][16];
 #pragma unroll
                     for (int l = 0; l < TG_L; ++l) tg_ld16(tbase + l * BN + c0, d[l]);
@@ -395,9 +403,9 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
                 __syncwarp();
                 if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tg_smem_u32(&acc_empty[b])) : "memory");
                 __threadfence();
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * S::EPI_WARPS) : "memory");
                 if (threadIdx.x == 64) s_last = atomicAdd(a.tile_cnt + tile, 1u) == ksplit - 1;
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * S::EPI_WARPS) : "memory");
                 last = s_last != 0;
                 if (last) {
                     __threadfence();
@@ -406,7 +414,7 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
             }
             if (!last) continue;
             const int64_t sc = nv ? a.scales[n] : 0;
-            for (uint32_t c0 = 0; c0 < BN; c0 += 16) {
+            for (uint32_t c0 = c_first; c0 < BN; c0 += 16 * NH) {
                 int32_t d[TG_L][16];
                 if (ksplit > 1) {
                     // the summed accumulator: 48 independent loads, then zero it for the next launch
@@ -422,7 +430,7 @@ __global__ void __launch_bounds__(TG_THREADS, 2)  // BN 16: two CTAs per SM
 #pragma unroll
                     for (int l = 0; l < TG_L; ++l) tg_ld16(tbase + l * BN + c0, d[l]);
                     tg_ld_wait();
-                    if (c0 + 16 >= BN) {  // every column of set b is in registers: hand it back
+                    if (c0 + 16 * NH >= BN) {  // this warp's columns of set b are in registers: hand it back
                         tg_fence_before();
                         __syncwarp();
                         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tg_smem_u32(&acc_empty[b])) : "memory");

@@ -60,7 +60,7 @@ template <int BN>
 static void launch(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs& a, uint32_t grid) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
-    cfg.blockDim = TG_THREADS;
+    cfg.blockDim = TgShape<BN>::THREADS;
     cfg.dynamicSmemBytes = TgShape<BN>::SMEM;
     cfg.stream = g_st;
     cudaLaunchAttribute at[1];
