@@ -1005,7 +1005,7 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
         launch_limb_gemm(W.tmap, tb, a, st, bn, true);
     };
     auto norm = [&](const int64_t* g, int unit) {  // decode steps: a CTA cluster per token
-        if (n <= uint32_t(TG_BN_SMALL))
+        if (n <= 64u)
             launch_k(true, bd_norm_cluster_kernel, n * BD_NCL, 256, 0, st, (const int64_t*)r.x, D, g, unit,
                      (const int64_t*)m.ctx->seeds, r.pa, r.nmax_pad, m.Kd, r.wide);
         else
