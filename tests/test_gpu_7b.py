@@ -64,10 +64,12 @@ def test_7b_c5_sequences(P, golden_7b, model7b):
         assert res.output_hash.hex() == g["output_hash"], k
 
 
-def test_7b_c5_batch_on_tensor_cores(P, golden_7b, model7b):
-    """C5: the sequences generated together (tensor-core batch path), each
-    stream and hash identical to the oracle's single-sequence goldens."""
-    names = sorted((k for k in golden_7b if k.startswith("c5_")), key=lambda k: int(k[3:]))[:8]
+@pytest.mark.parametrize("n_seqs", [8, 16])
+def test_7b_c5_batch_on_tensor_cores(P, golden_7b, model7b, n_seqs):
+    """C5: the sequences generated together (tensor-core batch path; 8 = the
+    per-GPU share of C5's 64 on 8 GPUs), each stream and hash identical to the
+    oracle's single-sequence goldens."""
+    names = sorted((k for k in golden_7b if k.startswith("c5_")), key=lambda k: int(k[3:]))[:n_seqs]
     if not names:
         pytest.skip("c5 goldens not generated")
     gs = [golden_7b[k] for k in names]

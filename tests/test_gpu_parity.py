@@ -313,7 +313,10 @@ def test_tensor_core_prefill_falls_back_exactly(P, oracle, golden_models, monkey
 
 @pytest.mark.parametrize("cfg6,n_seqs,plen,new", [((2, 64, 2, 64, 64, 256), 5, 12, 9),
                                                   ((2, 256, 2, 512, 300, 200), 8, 30, 6),
-                                                  ((3, 96, 3, 160, 77, 100), 3, 1, 7)])
+                                                  ((3, 96, 3, 160, 77, 100), 3, 1, 7),
+                                                  ((2, 64, 2, 64, 64, 256), 1, 8, 5),      # one sequence
+                                                  ((2, 128, 2, 256, 100, 128), 20, 5, 6),  # 64-token tiles, cluster norm
+                                                  ((2, 64, 2, 64, 64, 128), 70, 3, 4)])    # two token tiles
 def test_batch_generation_matches_single(P, oracle, cfg6, n_seqs, plen, new):
     from oracle.pyoracle import Config
     m = P.gen_toy_model(11, P.ModelConfig(*cfg6))
