@@ -28,7 +28,10 @@ CASES = [((2, 16, 2, 32, 32, 64), 1001, [4, 8, 15], ONE, 12),
          ((2, 16, 2, 32, 32, 64), 1001, [4, 8, 15], ONE // 4, 12),
          ((2, 16, 2, 32, 32, 64), 1001, [4, 8, 15], 3 * ONE, 12),
          ((2, 64, 2, 160, 100, 64), 3, None, ONE // 2, 20),
-         ((2, 64, 4, 128, 300, 96), 5, None, 2 * ONE, 16)]
+         ((2, 64, 4, 128, 300, 96), 5, None, 2 * ONE, 16),
+         ((2, 16, 2, 32, 32, 64), 1001, [4, 8, 15], 1, 10),         # T = 1 raw: logit << 16 wraps
+         ((2, 16, 2, 32, 32, 64), 1001, [4, 8, 15], 1 << 40, 10),   # T = 2^24 ONE: near-flat
+         ((2, 64, 2, 160, 1000, 64), 7, None, ONE, 12)]             # larger vocabulary
 
 
 def main():
