@@ -104,6 +104,23 @@ dimg_status dimg_parse_prompt(const char* csv, const char* bytes, uint32_t* out,
 /* RoPE tables [max_ctx][d_head/2] in Q16 (proj/src/rope.cpp:17-39). */
 dimg_status dimg_rope_tables(double theta, uint32_t d_head, uint32_t max_ctx, int64_t* cos_out,
                              int64_t* sin_out);
+/* RTAB, the reference's byte-exact RoPE table artifact (serialize_rope_tables /
+ * deserialize_rope_tables / save_rope_tables / load_rope_tables,
+ * proj/src/rope.cpp:41-93, proj/include/dim/rope.hpp:28-39): "RTAB", u32
+ * version 1, u32 max_ctx, u32 half_dim, f64 theta_base, cos then sin as i64,
+ * little-endian. serialize with out == NULL: *n = the size. deserialize with
+ * cos_out == sin_out == NULL: header only (dims and theta, fully validated);
+ * errors are DIMG_EPARSE with the reference's ParseError kind (bad magic, bad
+ * version, truncated, invariant = empty dims or trailing bytes). The tables
+ * feed dimg_model_desc.rope_cos/rope_sin. save/load: DIMG_EIO when the file
+ * cannot be opened/written; load returns the file's bytes (out == NULL: size). */
+dimg_status dimg_rtab_serialize(double theta, uint32_t max_ctx, uint32_t half_dim, const int64_t* cos_raw,
+                                const int64_t* sin_raw, uint8_t* out, size_t cap, size_t* n);
+dimg_status dimg_rtab_deserialize(const uint8_t* bytes, size_t n, uint32_t* max_ctx, uint32_t* half_dim,
+                                  double* theta, int64_t* cos_out, int64_t* sin_out, size_t cap_cells);
+dimg_status dimg_rtab_save(const char* path, double theta, uint32_t max_ctx, uint32_t half_dim,
+                           const int64_t* cos_raw, const int64_t* sin_raw);
+dimg_status dimg_rtab_load(const char* path, uint8_t* out, size_t cap, size_t* n);
 /* The 257-entry exp LUT (q16.cpp:70-79) and 64 Q48 inv-sqrt seeds (:28-43). */
 dimg_status dimg_exp_lut(int64_t out[257]);
 dimg_status dimg_invsqrt_seeds(int64_t out[64]);

@@ -297,9 +297,23 @@ static const int64_t* exp_table(void) {
     return g_exp;
 }
 
+/* exp_neg_lut's std::domain_error for t outside [0, 8] (q16.cpp:82): the
+ * restatement raises a sticky thread-local flag instead of throwing
+ * (orc_domain_error reads and clears it); the weight is then 0. */
+static _Thread_local int g_domain_error;
+int orc_domain_error(void) {
+    int e = g_domain_error;
+    g_domain_error = 0;
+    return e;
+}
+
 int64_t orc_exp_neg(int64_t t) {
     /* 2048 raw units per cell, round-half-up interpolation (q16.cpp:81-92) */
     const int64_t* e = exp_table();
+    if (t < 0 || t > 8 * ONE) {
+        g_domain_error = 1;
+        return 0;
+    }
     int64_t cell = t >> 11, frac = t & 2047;
     if (cell == 256) return e[0];
     int64_t hi = e[256 - cell], lo = e[255 - cell];

@@ -69,6 +69,7 @@ int64_t orc_inv_sqrt(int64_t x);                       /* q16.cpp:56-68 (x>0) */
 int64_t orc_invsqrt_seed(int b);                       /* q16.cpp:28-43 */
 int64_t orc_exp_entry(int i);                          /* q16.cpp:70-79 */
 int64_t orc_exp_neg(int64_t t);                        /* q16.cpp:81-92 (0<=t<=8*ONE) */
+int orc_domain_error(void);                             /* exp_neg_lut domain_error since last call */
 int64_t orc_sigmoid(int64_t x);                        /* q16.cpp:94-101 */
 int64_t orc_silu(int64_t x);                           /* q16.cpp:103-105 */
 /* RoPE tables [max_ctx][d_head/2] (proj/src/rope.cpp:17-39). */

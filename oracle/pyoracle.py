@@ -277,7 +277,10 @@ class Oracle:
             q = q if num >= 0 else -q
             q &= (1 << 64) - 1
             scaled.append(q - (1 << 64) if q >= 1 << 63 else q)
+        self.lib.orc_domain_error()  # clear
         p = self.softmax(np.array(scaled, np.int64))
+        if self.lib.orc_domain_error():  # exp_neg_lut's std::domain_error (q16.cpp:82)
+            raise ArithmeticError("exp_neg_lut: argument outside [0, 8]")
         total = int(sum(int(x) for x in p))
         threshold = (int(draw) * total) >> 32
         cum = 0
@@ -381,7 +384,17 @@ class Reference:
                                       i64p, i64p, i64p, C.c_int, i64p]
         lib.ref_ffn.argtypes = [C.c_uint32, C.c_uint32, i8p, i64p, i8p, i64p, i8p, i64p, i64p, i64p]
         lib.ref_generation_counter.restype = C.c_uint64
+        lib.ref_sample_from_logits.argtypes = [i64p, C.c_uint32, C.c_int64, u8p, u32p]
         self.lib = lib
+
+    def sample_from_logits(self, logits, temperature: int, key32: bytes):
+        """The reference's sample_from_logits with ChaCha20Rng(key32): (status,
+        token); status 0 ok, 1 invalid_argument, 6 domain_error."""
+        a = np.ascontiguousarray(logits, np.int64)
+        out = C.c_uint32(0xFFFFFFFF)
+        k = (C.c_uint8 * 32)(*key32)
+        rc = self.lib.ref_sample_from_logits(_ptr(a, i64p), len(a), int(temperature), k, C.byref(out))
+        return rc, out.value
 
     def blake3(self, data: bytes) -> str:
         out = (C.c_uint8 * 32)()

@@ -7,6 +7,7 @@
 // own public API (dim::generate_greedy, dim::InferenceSession, the kernels in
 // proj/include/dim/kernels.hpp) without its CLI. Nothing here reimplements
 // reference behaviour; it only marshals plain buffers into dim:: types.
+#include <array>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -23,6 +24,7 @@
 #include "dim/model.hpp"
 #include "dim/q16.hpp"
 #include "dim/rope.hpp"
+#include "dim/serial.hpp"
 
 using namespace dim;
 
@@ -35,7 +37,7 @@ int code_of(const std::exception& e) {
     if (dynamic_cast<const std::out_of_range*>(&e)) return 2;
     if (dynamic_cast<const std::length_error*>(&e)) return 5;
     if (dynamic_cast<const std::invalid_argument*>(&e)) return 1;
-    if (dynamic_cast<const std::domain_error*>(&e)) return 1;
+    if (dynamic_cast<const std::domain_error*>(&e)) return 6;  // DIMG_EDOMAIN
     if (dynamic_cast<const std::logic_error*>(&e)) return 3;
     return 99;
 }
@@ -295,6 +297,42 @@ int ref_generate_sampled(void* m, const uint32_t* prompt, uint32_t p, uint32_t n
                 for (size_t j = 0; j < V; ++j) logits_out[i * V + j] = r.logits[i][j].raw;
         }
     })
+}
+
+// sample_from_logits (proj/src/engine.cpp:122-139) of one row, the draw being
+// the first u32 of ChaCha20Rng(key) (the caller recomputes it)
+int ref_sample_from_logits(const int64_t* logits, uint32_t V, int64_t temperature, const uint8_t key[32],
+                           uint32_t* out) {
+    GUARD({
+        std::vector<q16> row(V);
+        for (uint32_t i = 0; i < V; ++i) row[i].raw = logits[i];
+        std::array<uint8_t, 32> k;
+        std::memcpy(k.data(), key, 32);
+        ChaCha20Rng rng(k);
+        *out = sample_from_logits(std::span<const q16>(row.data(), row.size()), q16{temperature}, rng);
+    })
+}
+
+// RTAB codec (proj/src/rope.cpp:41-93): the reference's bytes for built
+// tables, and the ParseError kind (or 0) of deserializing arbitrary bytes
+int ref_rtab_serialize(double theta, uint32_t dh, uint32_t ctx, uint8_t* out, size_t cap, size_t* n) {
+    GUARD({
+        const auto b = serialize_rope_tables(build_rope_tables(theta, dh, ctx));
+        *n = b.size();
+        if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+    })
+}
+int ref_rtab_parse(const uint8_t* bytes, size_t n, int* kind) {
+    *kind = -1;
+    try {
+        (void)deserialize_rope_tables(std::span<const uint8_t>(bytes, n));
+        return 0;
+    } catch (const ParseError& e) {
+        *kind = int(e.kind);
+        return 7;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
 }
 
 // ---- attestation (proj/src/attest.cpp) ----------------------------------------

@@ -11,7 +11,8 @@ from ._lib import LIB_PATH, lib
 from .engine import (EngineOptions, GenerationResult, InferenceSession, attention_steps, blake3_device,
                      blake3_gpu, build_rope_tables, generate_sampled, sample_from_logits, sample_key, dense_forward, dense_tokens, device_count, ffn_silu, generate_greedy,
                      generate_greedy_batch, generation_counter, hash_token_ids, parse_prompt, prompt_from_seed,
-                     release_sessions, rmsnorm, select_greedy, softmax_q16)
+                     release_sessions, rmsnorm, select_greedy, softmax_q16, RopeTables, serialize_rope_tables,
+                     deserialize_rope_tables, save_rope_tables, load_rope_tables)
 from .errors import (ContextOverflow, DomainError, InvalidArgument, LengthError, LogicError,
                      OutOfRange, ParseError)
 from .model import (ONE, DeviceModel, ModelConfig, ModelFile, deserialize, gen_toy_model,
@@ -26,4 +27,5 @@ __all__ = [
     "ContextOverflow", "DomainError", "InvalidArgument", "LengthError", "LogicError",
     "OutOfRange", "ParseError", "LIB_PATH", "lib", "attest", "Attestation", "VerifyOutcome", "DisputeResult",
     "make_attestation", "verify_by_reexecution", "dispute_game", "prompt_hash",
+    "RopeTables", "serialize_rope_tables", "deserialize_rope_tables", "save_rope_tables", "load_rope_tables",
 ]

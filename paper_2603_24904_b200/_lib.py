@@ -65,6 +65,12 @@ def _load():
         "dimg_prompt_from_seed": ([C.c_uint64, C.c_uint32, C.c_uint32, u32p], C.c_int),
         "dimg_parse_prompt": ([C.c_char_p, C.c_char_p, u32p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
         "dimg_rope_tables": ([C.c_double, C.c_uint32, C.c_uint32, i64p, i64p], C.c_int),
+        "dimg_rtab_serialize": ([C.c_double, C.c_uint32, C.c_uint32, i64p, i64p, u8p, C.c_size_t,
+                                 C.POINTER(C.c_size_t)], C.c_int),
+        "dimg_rtab_deserialize": ([u8p, C.c_size_t, u32p, u32p, C.POINTER(C.c_double), i64p, i64p, C.c_size_t],
+                                  C.c_int),
+        "dimg_rtab_save": ([C.c_char_p, C.c_double, C.c_uint32, C.c_uint32, i64p, i64p], C.c_int),
+        "dimg_rtab_load": ([C.c_char_p, u8p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
         "dimg_exp_lut": ([i64p], C.c_int),
         "dimg_invsqrt_seeds": ([i64p], C.c_int),
         "dimg_host_model_gen_toy": ([C.c_uint64, C.POINTER(Config), C.c_int, pp], C.c_int),

@@ -67,6 +67,9 @@ struct DevCtx {
     int smem_optin = 0;
     Ctl* op_ctl = nullptr;  // control block for the operator-level exports
     cudaStream_t op_stream = nullptr;
+    // the operator exports share op_ctl / op_stream: one op at a time per
+    // device (recursive: dense_tokens falls back to dense inside its scope)
+    std::recursive_mutex op_mu;
 };
 
 std::mutex g_ctx_mu;
@@ -131,6 +134,7 @@ DevCtx& dev_ctx(int device) {
     c.smem_optin = int(prop.sharedMemPerBlockOptin) - int(fa.sharedSizeBytes);
     CK(cudaFuncSetAttribute(decode_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             c.smem_optin));
+    CK(cudaDeviceSynchronize());  // the tables above landed before any non-blocking stream reads them
     c.device = device;
     return c;
 }
@@ -303,11 +307,15 @@ namespace {
 
 // Copies rows x cols int8 (row-major, pitch cols) into a device buffer with
 // row pitch dpitch, starting at row offset `row0` with row stride `rstride`.
+// The copy is ordered on `st` (the stream whose kernels read dst): a plain
+// cudaMemcpy2D from pageable memory may return before its DMA lands and is not
+// ordered against a non-blocking stream. src_pitch = row stride of the source
+// (cols for a whole matrix; the full width for a column slice).
 void put_rows(int8_t* dst, size_t dpitch, size_t row0, size_t rstride, const int8_t* src,
-              uint32_t rows, uint32_t cols) {
+              uint32_t rows, uint32_t cols, cudaStream_t st, size_t src_pitch = 0) {
     if (rows == 0) return;
-    CK(cudaMemcpy2D(dst + row0 * dpitch, dpitch * rstride, src, cols, cols, rows,
-                    cudaMemcpyHostToDevice));
+    CK(cudaMemcpy2DAsync(dst + row0 * dpitch, dpitch * rstride, src, src_pitch ? src_pitch : cols, cols, rows,
+                         cudaMemcpyHostToDevice, st));
 }
 
 template <class T>
@@ -375,6 +383,7 @@ __global__ void kmajor_kernel(const int8_t* __restrict__ src, uint32_t Kp, uint3
 struct RowPart {
     const int8_t* src;
     uint32_t rows, row0, rstride;
+    size_t src_pitch = 0;  // source row stride (0: K, a whole matrix)
 };
 
 DevMat upload_mat(dimg_model& m, uint32_t rows, uint32_t K, const std::vector<RowPart>& parts,
@@ -387,7 +396,7 @@ DevMat upload_mat(dimg_model& m, uint32_t rows, uint32_t K, const std::vector<Ro
     d.n_segs = (d.Kp + PK_SEG - 1) / PK_SEG;
     const size_t bytes = size_t(d.n_groups) * PK_ROWS * d.Kp;
     CK(cudaMemset(staging, 0, bytes));
-    for (const auto& p : parts) put_rows(staging, d.Kp, p.row0, p.rstride, p.src, p.rows, K);
+    for (const auto& p : parts) put_rows(staging, d.Kp, p.row0, p.rstride, p.src, p.rows, K, nullptr, p.src_pitch);
     d.s = upload(m.mem, scales.data(), scales.size());
     // tensor-core copy, K-block-major: [K/128][rows padded to 128][128 bytes],
     // so every 128-row x 128-byte TMA box is one contiguous 16 KB block
@@ -424,6 +433,10 @@ struct PrefillWs {
     int32_t* partial = nullptr;      // split-K accumulators of the 16-token tiles (zero between launches)
     uint32_t* tile_cnt = nullptr;
     size_t partial_elems = 0;
+    uint32_t tiles = 0;
+    // set while a prefill is in flight: a call that fails part-way leaves the
+    // split-K scratch possibly nonzero, so the next prefill re-zeroes it
+    bool dirty = false;
     int8_t* kdig = nullptr;          // key digit planes [H][4][kdig_pad][128] (tensor-core scores, dh 128)
     uint32_t* kd4 = nullptr;         // [layers]: some key of the layer needs the 4th digit
     uint32_t kdig_pad = 0;
@@ -657,6 +670,14 @@ void check_ctl_err(dimg_session& s) {
     if (err & 1u) fail(DIMG_EDOMAIN, "inv_sqrt_q16: input must be positive");
 }
 
+// The sampler's sticky error word (write_ctl does not clear it).
+void check_sample_err(dimg_session& s) {
+    uint32_t err = 0;
+    CK(cudaMemcpyAsync(&err, &s.ctl->serr, 4, cudaMemcpyDeviceToHost, s.stream));
+    CK(cudaStreamSynchronize(s.stream));
+    if (err & 2u) fail(DIMG_EDOMAIN, "exp_neg_lut: argument outside [0, 8]");
+}
+
 void ensure_keep(dimg_session& s, uint32_t need) {
     if (need <= s.keep_cap) return;
     CK(cudaStreamSynchronize(s.stream));
@@ -667,8 +688,8 @@ void ensure_keep(dimg_session& s, uint32_t need) {
     s.keep_cap = need;
     // the head stage's output pointer lives in the stage table
     s.host_stages.back().y = s.logits;
-    CK(cudaMemcpy(s.stages + s.host_stages.size() - 1, &s.host_stages.back(), sizeof(PkStage),
-                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(s.stages + s.host_stages.size() - 1, &s.host_stages.back(), sizeof(PkStage),
+                       cudaMemcpyHostToDevice, s.stream));
 }
 
 void check_prompt(const dimg_model& m, const uint32_t* prompt, uint32_t p, uint32_t n) {
@@ -723,8 +744,10 @@ void ensure_prefill_ws(dimg_session& s, uint32_t n) {
     w.qkv = s.mem.alloc<int64_t>(size_t(w.cap) * 3 * m.D);
     w.pa = s.mem.alloc<uint8_t>(size_t(3) * w.cap_pad * m.Kd);
     w.ph = s.mem.alloc<uint8_t>(size_t(3) * w.cap_pad * m.Kf);
-    CK(cudaMemset(w.pa, 0, size_t(3) * w.cap_pad * m.Kd));
-    CK(cudaMemset(w.ph, 0, size_t(3) * w.cap_pad * m.Kf));
+    // zeroed on the session stream (a legacy-stream cudaMemset of device
+    // memory is not ordered before the non-blocking session stream's kernels)
+    CK(cudaMemsetAsync(w.pa, 0, size_t(3) * w.cap_pad * m.Kd, s.stream));
+    CK(cudaMemsetAsync(w.ph, 0, size_t(3) * w.cap_pad * m.Kf, s.stream));
     if (!w.wide) w.wide = s.mem.alloc<uint32_t>(1);
     w.strips = s.mem.alloc<int32_t>(pf_attn_strip_elems(m.H, w.cap));
     w.tm_pa = tmap_bytes(w.pa, m.D, size_t(3) * w.cap_pad, m.Kd, TG_BN);
@@ -742,8 +765,9 @@ void ensure_prefill_ws(dimg_session& s, uint32_t n) {
         w.partial_elems = size_t(tiles) * TG_L * TG_BN_SMALL * TG_BM;
         w.partial = s.mem.alloc<int32_t>(w.partial_elems);
         w.tile_cnt = s.mem.alloc<uint32_t>(tiles);
-        CK(cudaMemset(w.partial, 0, w.partial_elems * 4));
-        CK(cudaMemset(w.tile_cnt, 0, size_t(tiles) * 4));
+        w.tiles = tiles;
+        CK(cudaMemsetAsync(w.partial, 0, w.partial_elems * 4, s.stream));
+        CK(cudaMemsetAsync(w.tile_cnt, 0, size_t(tiles) * 4, s.stream));
     }
 }
 
@@ -765,6 +789,11 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
     cudaStream_t st = s.stream;
     const uint32_t D = m.D, dh = m.dh, H = m.H;
     const size_t kv_layer = size_t(H) * m.cfg.max_ctx * dh;
+    if (w.dirty) {  // the previous prefill failed part-way: its split-K scratch may be dirty
+        CK(cudaMemsetAsync(w.partial, 0, w.partial_elems * 4, st));
+        CK(cudaMemsetAsync(w.tile_cnt, 0, size_t(w.tiles) * 4, st));
+    }
+    w.dirty = true;
     CK(cudaMemsetAsync(w.wide, 0, 4, st));
     CK(cudaMemsetAsync(s.kvwide, 0, size_t(m.L) * H * 4, st));
     // every kernel of the chain by programmatic dependent launch (pdl_wait in each)
@@ -838,6 +867,7 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
     uint32_t wide = 0;
     CK(cudaMemcpyAsync(&wide, w.wide, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    w.dirty = false;  // every split-K launch completed: the scratch is zero again
     return wide == 0;
 }
 
@@ -894,6 +924,7 @@ struct BatchRun {
     uint32_t* tile_cnt = nullptr;
     size_t partial_elems = 0;
     uint32_t tiles_max = 0;
+    bool dirty = false;  // a batch call failed part-way: re-zero the split-K scratch first
     ~BatchRun() {
         if (st) cudaStreamDestroy(st);
     }
@@ -1060,6 +1091,11 @@ bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<
     }
     BatchCache& c = *m->batch;
     BatchRun& r = c.r;
+    if (r.dirty) {
+        CK(cudaMemsetAsync(r.partial, 0, r.partial_elems * 4, r.st));
+        CK(cudaMemsetAsync(r.tile_cnt, 0, size_t(r.tiles_max) * 4, r.st));
+    }
+    r.dirty = true;
     CK(cudaMemsetAsync(r.step, 0, 4, r.st));
     CK(cudaMemsetAsync(r.wide, 0, 4, r.st));
     // prompt phase: all positions but each prompt's last, one forward pass
@@ -1111,6 +1147,7 @@ bool generate_batch_tc(dimg_model* m, uint32_t B, const std::vector<std::vector<
         CK(cudaMemcpy2DAsync(tokens_out, size_t(max_new) * 4, r.out, size_t(r.max_new) * 4, size_t(max_new) * 4, B,
                              cudaMemcpyDeviceToHost, r.st));
     CK(cudaStreamSynchronize(r.st));
+    r.dirty = false;
     return wide == 0;
 }
 
@@ -1347,8 +1384,8 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
                                                          s->smem));
         if (per_sm < 1) fail(DIMG_ECUDA, "session: persistent kernel does not fit one SM");
         s->stages = s->mem.alloc<PkStage>(s->host_stages.size());
-        CK(cudaMemcpy(s->stages, s->host_stages.data(), s->host_stages.size() * sizeof(PkStage),
-                      cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(s->stages, s->host_stages.data(), s->host_stages.size() * sizeof(PkStage),
+                           cudaMemcpyHostToDevice, s->stream));
         CK(cudaMemsetAsync(s->ctl, 0, sizeof(Ctl), s->stream));
         CK(cudaMemsetAsync(s->tokens, 0, (ctx + 1) * 4, s->stream));
         CK(cudaStreamSynchronize(s->stream));
@@ -1572,8 +1609,8 @@ dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, flo
         }
         if (!s->probe_stages || n > 0) {
             s->probe_stages = s->mem.alloc<PkStage>(prog.size());
-            CK(cudaMemcpy(s->probe_stages, prog.data(), prog.size() * sizeof(PkStage),
-                          cudaMemcpyHostToDevice));
+            CK(cudaMemcpyAsync(s->probe_stages, prog.data(), prog.size() * sizeof(PkStage),
+                               cudaMemcpyHostToDevice, s->stream));
         }
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
@@ -1638,8 +1675,9 @@ namespace {
 
 struct OpScope {
     DevCtx& c;
+    std::unique_lock<std::recursive_mutex> lk;
     DevBuf mem;
-    explicit OpScope(int device) : c(dev_ctx(device)) {
+    explicit OpScope(int device) : c(dev_ctx(device)), lk(c.op_mu) {
         CK(cudaSetDevice(device));
         CK(cudaMemsetAsync(c.op_ctl, 0, sizeof(Ctl), c.op_stream));
     }
@@ -1656,17 +1694,17 @@ struct OpScope {
             dst = mem.alloc<int8_t>(size_t(rows_total) * Kp);
             CK(cudaMemsetAsync(dst, 0, size_t(rows_total) * Kp, c.op_stream));
         }
-        CK(cudaStreamSynchronize(c.op_stream));
-        put_rows(dst, Kp, row0, row_stride, w.data, w.rows, w.cols);
+        put_rows(dst, Kp, row0, row_stride, w.data, w.rows, w.cols, c.op_stream);
         return dst;
     }
     template <class T>
     void get(T* dst, const T* src, size_t n) {
         CK(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, c.op_stream));
         CK(cudaStreamSynchronize(c.op_stream));
-        uint32_t err = 0;
-        CK(cudaMemcpy(&err, &c.op_ctl->err, 4, cudaMemcpyDeviceToHost));
-        if (err & 1u) fail(DIMG_EDOMAIN, "inv_sqrt_q16: input must be positive");
+        uint32_t err[2] = {0, 0};
+        CK(cudaMemcpy(err, &c.op_ctl->err, 8, cudaMemcpyDeviceToHost));
+        if (err[0] & 1u) fail(DIMG_EDOMAIN, "inv_sqrt_q16: input must be positive");
+        if (err[1] & 2u) fail(DIMG_EDOMAIN, "exp_neg_lut: argument outside [0, 8]");
     }
     GemvArgs args() {
         GemvArgs a{};
@@ -1862,7 +1900,8 @@ dimg_status dimg_op_sample(int device, const int64_t* logits, uint32_t V, int64_
         const uint32_t* dd = o.put(&draw, 1);
         int64_t* scratch = o.mem.alloc<int64_t>(V);
         uint32_t* tok = o.mem.alloc<uint32_t>(2);
-        sample_kernel<<<1, SM_THREADS, 0, o.c.op_stream>>>(dl, V, temperature, dd, 0, o.c.exp_lut, scratch, tok, 0);
+        sample_kernel<<<1, SM_THREADS, 0, o.c.op_stream>>>(dl, V, temperature, dd, 0, o.c.exp_lut, scratch, tok, 0,
+                                                           &o.c.op_ctl->serr);
         CK(cudaGetLastError());
         o.get(out, tok + 1, 1);
     })
@@ -1896,13 +1935,15 @@ dimg_status dimg_generate_sampled(dimg_session* s, const uint32_t* prompt, uint3
             std::vector<uint32_t> dr(max_new);
             for (auto& d : dr) d = rng.u32();
             CK(cudaMemcpyAsync(s->draws, dr.data(), size_t(max_new) * 4, cudaMemcpyHostToDevice, s->stream));
+            CK(cudaMemsetAsync(&s->ctl->serr, 0, 4, s->stream));
             run_prefill(*s);  // positions 0 .. P-2
             for (uint32_t step = 0; step < max_new; ++step) {
                 const uint32_t pos = n_prompt - 1 + step;
                 write_ctl(*s, pos, pos, 0);  // logits to the scratch row 0
                 launch_pk(*s, s->stages, n_layer_stages(*s), 1, 0);
                 sample_kernel<<<1, SM_THREADS, 0, s->stream>>>(s->logits, m.V, temperature, s->draws, step,
-                                                                m.ctx->exp_lut, s->sample_scratch, s->tokens, pos);
+                                                                m.ctx->exp_lut, s->sample_scratch, s->tokens, pos,
+                                                                &s->ctl->serr);
             }
             CK(cudaGetLastError());
             s->len = n_prompt - 1 + max_new;
@@ -1910,6 +1951,7 @@ dimg_status dimg_generate_sampled(dimg_session* s, const uint32_t* prompt, uint3
                                s->stream));
         }
         check_ctl_err(*s);
+        if (max_new > 0) check_sample_err(*s);
         if (hash_out) {
             auto d = b3::hash(tokens_out, size_t(max_new) * 4, 1);
             std::memcpy(hash_out, d.data(), 32);

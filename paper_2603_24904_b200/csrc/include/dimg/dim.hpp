@@ -156,6 +156,68 @@ inline Digest hash_token_ids(std::span<const uint32_t> ids) {  // engine.cpp:104
     return d;
 }
 
+// ---- RoPE tables and the RTAB artifact (proj/include/dim/rope.hpp:15-39) -----
+struct RopeTables {
+    uint32_t max_ctx = 0;
+    uint32_t half_dim = 0;
+    double theta_base = 10000.0;
+    std::vector<int64_t> cos_raw;  // max_ctx * half_dim, row-major
+    std::vector<int64_t> sin_raw;
+    int64_t cos_at(uint32_t pos, uint32_t k) const { return cos_raw[size_t(pos) * half_dim + k]; }
+    int64_t sin_at(uint32_t pos, uint32_t k) const { return sin_raw[size_t(pos) * half_dim + k]; }
+    friend bool operator==(const RopeTables&, const RopeTables&) = default;
+};
+
+inline RopeTables build_rope_tables(double theta_base, uint32_t d_head, uint32_t max_ctx) {  // rope.cpp:17-39
+    if (d_head == 0 || d_head % 2 != 0) throw std::invalid_argument("rope: d_head must be even");
+    RopeTables t;
+    t.max_ctx = max_ctx;
+    t.half_dim = d_head / 2;
+    t.theta_base = theta_base;
+    t.cos_raw.resize(size_t(max_ctx) * t.half_dim);
+    t.sin_raw.resize(t.cos_raw.size());
+    check(dimg_rope_tables(theta_base, d_head, max_ctx, t.cos_raw.data(), t.sin_raw.data()));
+    return t;
+}
+
+inline std::vector<uint8_t> serialize_rope_tables(const RopeTables& t) {  // rope.cpp:41-51
+    size_t n = 0;
+    check(dimg_rtab_serialize(t.theta_base, t.max_ctx, t.half_dim, t.cos_raw.data(), t.sin_raw.data(), nullptr, 0, &n));
+    std::vector<uint8_t> out(n);
+    check(dimg_rtab_serialize(t.theta_base, t.max_ctx, t.half_dim, t.cos_raw.data(), t.sin_raw.data(), out.data(),
+                              out.size(), &n));
+    return out;
+}
+
+inline RopeTables deserialize_rope_tables(std::span<const uint8_t> bytes) {  // rope.cpp:53-78
+    RopeTables t;
+    check(dimg_rtab_deserialize(bytes.data(), bytes.size(), &t.max_ctx, &t.half_dim, &t.theta_base, nullptr, nullptr,
+                                0));
+    const size_t cells = size_t(t.max_ctx) * t.half_dim;
+    t.cos_raw.resize(cells);
+    t.sin_raw.resize(cells);
+    check(dimg_rtab_deserialize(bytes.data(), bytes.size(), &t.max_ctx, &t.half_dim, &t.theta_base, t.cos_raw.data(),
+                                t.sin_raw.data(), cells));
+    return t;
+}
+
+inline void save_rope_tables(const RopeTables& t, const std::string& path) {  // rope.cpp:80-86
+    const dimg_status s = dimg_rtab_save(path.c_str(), t.theta_base, t.max_ctx, t.half_dim, t.cos_raw.data(),
+                                         t.sin_raw.data());
+    if (s == DIMG_EIO) throw std::runtime_error(dimg_last_error());
+    check(s);
+}
+
+inline RopeTables load_rope_tables(const std::string& path) {  // rope.cpp:88-93
+    size_t n = 0;
+    dimg_status s = dimg_rtab_load(path.c_str(), nullptr, 0, &n);
+    if (s == DIMG_EIO) throw std::runtime_error(dimg_last_error());
+    check(s);
+    std::vector<uint8_t> b(n);
+    check(dimg_rtab_load(path.c_str(), b.data(), b.size(), &n));
+    return deserialize_rope_tables(b);
+}
+
 inline uint32_t select_greedy(std::span<const int64_t> logits) {  // engine.cpp:113-120
     uint32_t i = 0;
     check(dimg_select_greedy(logits.data(), logits.size(), &i));

@@ -53,7 +53,8 @@ struct Ctl {
     uint32_t keep_cap;      // capacity of the kept-logits buffer (vectors)
     uint32_t argmax_count;  // CTAs of the lm_head that finished this step
     uint32_t err;           // bit 0: inv_sqrt domain error (ms + 1 <= 0)
-    uint32_t pad[3];
+    uint32_t serr;          // bit 1: sampling's exp_neg_lut domain error (kept across steps)
+    uint32_t pad[2];
     unsigned long long stats[4];  // [0] CTAs on the 8-limb path, [1] attention parts on the int64 KV path
 };
 

@@ -8,6 +8,13 @@
 // The draw is the step's ChaCha20 u32 (precomputed on the host from the
 // BLAKE3(model bytes || prompt) key). The token goes to tokens[pos + 1],
 // where the next decode step reads it.
+// Reference edge cases kept:
+//   * scaled logits spanning more than 2^63: m - s wraps negative and
+//     exp_neg_lut throws std::domain_error (q16.cpp:82) -> bit 1 of *err
+//     (DIMG_EDOMAIN at the API), no LUT read out of range;
+//   * every probability truncated to 0 (vocab > 65536, near-flat): the
+//     cumulative walk never passes the threshold and the reference returns
+//     V - 1 (engine.cpp:138).
 #pragma once
 
 #include <cstdint>
@@ -40,7 +47,7 @@ __global__ void __launch_bounds__(SM_THREADS) sample_kernel(const int64_t* __res
                                                             int64_t temperature, const uint32_t* __restrict__ draws,
                                                             uint32_t step, const int64_t* __restrict__ lut_g,
                                                             int64_t* __restrict__ scratch, uint32_t* tokens,
-                                                            uint32_t pos) {
+                                                            uint32_t pos, uint32_t* err) {
     __shared__ int64_t lut[257];
     __shared__ int64_t red[32];
     __shared__ uint64_t scan[SM_THREADS];
@@ -57,9 +64,15 @@ __global__ void __launch_bounds__(SM_THREADS) sample_kernel(const int64_t* __res
     const int64_t m = sm_block_reduce<int64_t>(mx, red, [](int64_t a, int64_t b) { return a > b ? a : b; });
     // 2. softmax_q16 weights (kernels.cpp:90-107) and their total
     int64_t tot = 0;
+    int bad = 0;
     for (uint32_t i = i0; i < i1; ++i) {
         int64_t d = wrap_sub(m, scratch[i]);
-        tot += exp_neg(d > 8 * ONE ? 8 * ONE : d, lut);
+        bad |= d < 0;
+        tot += d < 0 ? 0 : exp_neg(d > 8 * ONE ? 8 * ONE : d, lut);
+    }
+    if (__syncthreads_or(bad)) {  // exp_neg_lut's domain_error: no token
+        if (threadIdx.x == 0) atomicOr(err, 2u);
+        return;
     }
     const int64_t total = sm_block_reduce<int64_t>(tot, red, [](int64_t a, int64_t b) { return a + b; });
     // 3. probabilities (truncating division by the total) and this segment's mass
@@ -85,6 +98,10 @@ __global__ void __launch_bounds__(SM_THREADS) sample_kernel(const int64_t* __res
     const uint64_t mass = scan[SM_THREADS - 1];
     const uint64_t start = scan[threadIdx.x] - seg;
     const int64_t threshold = int64_t((uint64_t(draws[step]) * mass) >> 32);
+    if (mass == 0) {  // no cumulative mass ever exceeds the threshold (0): the reference's V - 1
+        if (threadIdx.x == 0) tokens[pos + 1] = V - 1;
+        return;
+    }
     if (int64_t(start) <= threshold && threshold < int64_t(start + seg)) {
         int64_t cum = int64_t(start);
         for (uint32_t i = i0; i < i1; ++i) {

@@ -88,6 +88,74 @@ def build_rope_tables(theta: float, d_head: int, max_ctx: int):
     return c, s
 
 
+class RopeTables:
+    """RopeTables (proj/include/dim/rope.hpp:15-26): Q16 cos/sin
+    [max_ctx][half_dim]. Unpacks as (cos_raw, sin_raw), the form
+    InferenceSession's imported_tables takes."""
+
+    def __init__(self, max_ctx: int, half_dim: int, theta_base: float, cos_raw, sin_raw):
+        self.max_ctx, self.half_dim, self.theta_base = int(max_ctx), int(half_dim), float(theta_base)
+        self.cos_raw = np.ascontiguousarray(cos_raw, np.int64).reshape(-1)
+        self.sin_raw = np.ascontiguousarray(sin_raw, np.int64).reshape(-1)
+
+    @classmethod
+    def build(cls, theta: float, d_head: int, max_ctx: int) -> "RopeTables":
+        c, s = build_rope_tables(theta, d_head, max_ctx)
+        return cls(max_ctx, d_head // 2, theta, c, s)
+
+    def __iter__(self):
+        return iter((self.cos_raw, self.sin_raw))
+
+    def __eq__(self, o):
+        return (isinstance(o, RopeTables) and (self.max_ctx, self.half_dim) == (o.max_ctx, o.half_dim)
+                and np.float64(self.theta_base).tobytes() == np.float64(o.theta_base).tobytes()
+                and np.array_equal(self.cos_raw, o.cos_raw) and np.array_equal(self.sin_raw, o.sin_raw))
+
+
+def serialize_rope_tables(t: RopeTables) -> bytes:
+    """The RTAB artifact (proj/src/rope.cpp:41-51), byte-exact."""
+    n = C.c_size_t()
+    check(lib.dimg_rtab_serialize(t.theta_base, t.max_ctx, t.half_dim, ptr(t.cos_raw, i64p),
+                                  ptr(t.sin_raw, i64p), None, 0, C.byref(n)))
+    out = np.empty(n.value, np.uint8)
+    check(lib.dimg_rtab_serialize(t.theta_base, t.max_ctx, t.half_dim, ptr(t.cos_raw, i64p),
+                                  ptr(t.sin_raw, i64p), ptr(out, u8p), out.size, C.byref(n)))
+    return out.tobytes()
+
+
+def deserialize_rope_tables(data: bytes) -> RopeTables:
+    """deserialize_rope_tables (proj/src/rope.cpp:53-78): ParseError with the
+    reference's kind on bad magic / version, truncation, empty dims or
+    trailing bytes."""
+    b = np.frombuffer(bytes(data), np.uint8).copy()
+    if b.size == 0:
+        b = np.zeros(1, np.uint8)[:0]
+    mc, hd, th = C.c_uint32(), C.c_uint32(), C.c_double()
+    bp = ptr(b, u8p) if b.size else None
+    check(lib.dimg_rtab_deserialize(bp, b.size, C.byref(mc), C.byref(hd), C.byref(th), None, None, 0))
+    cells = mc.value * hd.value
+    c = np.empty(cells, np.int64)
+    s = np.empty(cells, np.int64)
+    check(lib.dimg_rtab_deserialize(bp, b.size, C.byref(mc), C.byref(hd), C.byref(th), ptr(c, i64p),
+                                    ptr(s, i64p), cells))
+    return RopeTables(mc.value, hd.value, th.value, c, s)
+
+
+def save_rope_tables(t: RopeTables, path: str) -> None:
+    """save_rope_tables (proj/src/rope.cpp:80-86); IOFailure if unwritable."""
+    check(lib.dimg_rtab_save(path.encode(), t.theta_base, t.max_ctx, t.half_dim, ptr(t.cos_raw, i64p),
+                             ptr(t.sin_raw, i64p)))
+
+
+def load_rope_tables(path: str) -> RopeTables:
+    """load_rope_tables (proj/src/rope.cpp:88-93)."""
+    n = C.c_size_t()
+    check(lib.dimg_rtab_load(path.encode(), None, 0, C.byref(n)))
+    out = np.empty(max(1, n.value), np.uint8)
+    check(lib.dimg_rtab_load(path.encode(), ptr(out, u8p), out.size, C.byref(n)))
+    return deserialize_rope_tables(out[:n.value].tobytes())
+
+
 class InferenceSession:
     """Owns one sequence's KV cache on a GPU; single writer (engine.hpp:41-57)."""
 

@@ -41,6 +41,30 @@ int host() {
         REQUIRE(false);
     } catch (const std::invalid_argument&) {
     }
+    // RTAB round trip and the reference's error kinds (proj/src/rope.cpp:41-93)
+    auto t = dimg::build_rope_tables(10000.0, 8, 16);
+    auto rb = dimg::serialize_rope_tables(t);
+    REQUIRE(rb.size() == 24 + 2 * 16 * 4 * 8);
+    REQUIRE(dimg::deserialize_rope_tables(rb) == t);
+    rb.push_back(0);
+    try {
+        dimg::deserialize_rope_tables(rb);
+        REQUIRE(false);
+    } catch (const dimg::ParseError& e) {
+        REQUIRE(e.kind == dimg::ParseError::Kind::invariant);
+    }
+    rb.resize(20);
+    try {
+        dimg::deserialize_rope_tables(rb);
+        REQUIRE(false);
+    } catch (const dimg::ParseError& e) {
+        REQUIRE(e.kind == dimg::ParseError::Kind::truncated);
+    }
+    try {
+        dimg::load_rope_tables("/nonexistent/dir/t.rtab");
+        REQUIRE(false);
+    } catch (const std::runtime_error&) {
+    }
     std::printf("host ok %s\n", m.weight_hash().hex().c_str());
     return 0;
 }

@@ -10,6 +10,14 @@ oracle/_ref/libdimref.so, shim ref_generate_sampled):
                    first checks against every reference step
 
     python tests/golden/make_sample_golden.py      (needs /root/reference)
+    python tests/golden/make_sample_golden.py edge (sample_edge.npz only)
+
+  sample_edge.npz  rows at the reference's edges, answered by the reference's
+                   own sample_from_logits (shim ref_sample_from_logits):
+                   scaled logits spanning more than 2^63 (exp_neg_lut throws
+                   std::domain_error: status 6) and vocabularies above 65536
+                   whose probabilities all truncate to 0 (the walk falls
+                   through to V - 1)
 """
 import ctypes as C
 import json
@@ -84,5 +92,48 @@ def main():
     print(len(cases), "cases,", len(rows), "selection fixtures")
 
 
+def edge():
+    ref, orc = Reference(), Oracle()
+    rng = np.random.default_rng(23)
+    rows, temps = [], []
+    # spans beyond 2^63 after the temperature division: domain_error
+    rows.append(np.array([1 << 62, -(1 << 62)], np.int64)); temps.append(ONE)
+    rows.append(np.array([5, 1 << 46, 7, -(1 << 46)], np.int64)); temps.append(1)
+    rows.append(np.concatenate([rng.integers(-ONE, ONE, 300), [(1 << 62) + 5, -(1 << 62)]]).astype(np.int64))
+    temps.append(ONE)
+    # span exactly 2^63 - 1: allowed
+    rows.append(np.array([(1 << 62) - 1, -(1 << 62)], np.int64)); temps.append(ONE)
+    # vocab > 65536, near-flat: every p truncates to 0 -> V - 1
+    rows.append(rng.integers(-ONE, ONE, 70000).astype(np.int64)); temps.append(1 << 40)
+    rows.append(np.full(131072, 3 * ONE, np.int64)); temps.append(ONE)
+    # vocab > 65536 with a peak: ordinary walk
+    r = rng.integers(-4 * ONE, 4 * ONE, 70000).astype(np.int64)
+    r[12345] = 40 * ONE
+    rows.append(r); temps.append(ONE)
+    # exactly 65536 flat: p = 1 each
+    rows.append(np.zeros(65536, np.int64)); temps.append(ONE)
+    keys, status, toks = [], [], []
+    for i, (row, T) in enumerate(zip(rows, temps)):
+        key = bytes((7 * i + j) & 0xFF for j in range(32))
+        rc, tok = ref.sample_from_logits(row, T, key)
+        assert rc in (0, 6), rc
+        d = chacha20_u32s(key, 1)[0]
+        try:  # the restatement agrees, error included
+            got = orc.sample_from_logits(row, T, d)
+        except ArithmeticError:
+            got = None
+        assert (rc == 6 and got is None) or (rc == 0 and got == tok), (i, rc, tok, got)
+        keys.append(np.frombuffer(key, np.uint8)); status.append(rc); toks.append(tok if rc == 0 else 0xFFFFFFFF)
+        print(i, len(row), T, rc, tok)
+    width = max(len(r) for r in rows)
+    L = np.zeros((len(rows), width), np.int64)
+    for i, r in enumerate(rows):
+        L[i, :len(r)] = r
+    np.savez_compressed(os.path.join(HERE, "sample_edge.npz"), logits=L,
+                        lens=np.array([len(r) for r in rows], np.uint32), temperature=np.array(temps, np.int64),
+                        key=np.array(keys), draw=np.array([chacha20_u32s(bytes(k), 1)[0] for k in keys], np.uint32),
+                        status=np.array(status, np.int32), token=np.array(toks, np.uint32))
+
+
 if __name__ == "__main__":
-    main()
+    edge() if sys.argv[1:] == ["edge"] else main()

@@ -338,3 +338,48 @@ def test_batch_generation_wild_falls_back(P, golden_models):
     single = [P.generate_greedy(m, p, 4) for p in prompts]
     assert [r.token_ids for r in res] == [s.token_ids for s in single]
     assert [r.output_hash for r in res] == [s.output_hash for s in single]
+
+
+# ---- repeat determinism of the tensor-core paths (proj/tests/test_engine.cpp:87-111) ----
+
+def test_dense_tokens_ragged_repeat_stress(P, oracle):
+    """Ragged shapes through the tensor-core GEMM export, 200 calls per shape
+    group with fresh device buffers each call, against the oracle: the upload
+    of the weights is stream-ordered before the K-block-major relayout and the
+    GEMM (a pageable legacy-stream copy was not)."""
+    import itertools
+    shapes = list(itertools.product((33, 100, 130), (17, 300, 4095), (1, 7, 65)))
+    rng = np.random.default_rng(2024)
+    cases = []
+    for N, K, T in shapes:
+        w = rng.integers(-127, 128, (N, K), dtype=np.int8)
+        s = rng.integers(1, 1 << 12, N, dtype=np.int64)
+        x = rng.integers(-0x808080, 0x7F7F80, (T, K), dtype=np.int64)
+        want = np.stack([oracle.dense(w, s, x[t]) for t in range(T)])
+        cases.append((w, s, x, want))
+    for rep in range(200 // 8):
+        for i, (w, s, x, want) in enumerate(cases):
+            if (rep + i) % 3 and rep > 0:
+                continue  # every shape at least ~8x, 200+ calls in all
+            got = P.dense_tokens(w, s, x)
+            assert np.array_equal(got, want), (rep, w.shape, x.shape)
+
+
+def test_tensor_core_prefill_and_batch_repeat(P, oracle, monkeypatch):
+    """The same small tensor-core prefill and batch generations 20 times:
+    identical tokens every time (split-K scratch and PDL chains included)."""
+    from oracle.pyoracle import Config
+    cfg6 = (2, 128, 2, 256, 100, 160)
+    m = P.gen_toy_model(21, P.ModelConfig(*cfg6))
+    om = oracle.gen_toy(21, Config(*cfg6))
+    prompts = [P.prompt_from_seed(900 + i, cfg6[4], 5 + (i % 4)) for i in range(9)]
+    want = [oracle.generate_greedy(om, p, 6)[0] for p in prompts]
+    want = [[int(t) for t in w] for w in want]
+    monkeypatch.setenv("DIMG_PREFILL", "1")
+    s = P.InferenceSession(m)
+    for rep in range(20):
+        for p, wt in zip(prompts[:3], want[:3]):
+            assert s.generate_greedy(p, 6).token_ids == wt, rep
+        res, path = P.generate_greedy_batch(m, prompts, 6)
+        assert path == "tensor_cores"
+        assert [r.token_ids for r in res] == want, rep

@@ -40,3 +40,18 @@ def test_temperature_must_be_positive(P):
         P.generate_sampled(m, [1, 2], 4, 0)
     with pytest.raises(P.InvalidArgument):
         P.sample_from_logits(np.arange(8), -1, 5)
+
+
+def test_selection_edges_match_reference(P):
+    """sample_edge.npz: the reference's own answers at its edges -- scaled
+    logits spanning more than 2^63 (exp_neg_lut's std::domain_error,
+    q16.cpp:82) and vocabularies above 65536 whose probabilities all
+    truncate to 0 (engine.cpp:138 falls through to V - 1)."""
+    z = np.load(os.path.join(G, "sample_edge.npz"))
+    for i, (row, n, t, d, st, tok) in enumerate(zip(z["logits"], z["lens"], z["temperature"], z["draw"],
+                                                     z["status"], z["token"])):
+        if st == 6:
+            with pytest.raises(P.DomainError):
+                P.sample_from_logits(row[:n], int(t), int(d))
+        else:
+            assert P.sample_from_logits(row[:n], int(t), int(d)) == int(tok), i

@@ -174,3 +174,48 @@ def test_device_entry_points_fail_loudly_without_gpu(P):
         P.generate_greedy(m, [1, 2], 3)
     with pytest.raises(P.errors.CudaError):
         P.dense_forward(np.ones((2, 4), np.int8), np.ones(2, np.int64), np.ones(4, np.int64))
+
+
+# ---- RTAB codec (proj/src/rope.cpp:41-93) against the reference's own bytes ----
+
+def _rtab_golden():
+    import json
+    import os
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden", "rtab.json")))
+
+
+def test_rtab_serialize_is_byte_exact_with_reference():
+    import paper_2603_24904_b200 as P
+    g = _rtab_golden()
+    for t in g["tables"]:
+        tab = P.RopeTables.build(t["theta"], t["d_head"], t["max_ctx"])
+        assert P.serialize_rope_tables(tab).hex() == t["hex"]
+        back = P.deserialize_rope_tables(bytes.fromhex(t["hex"]))  # import the reference's artifact
+        assert back == tab
+    b = g["big"]
+    big = P.serialize_rope_tables(P.RopeTables.build(b["theta"], b["d_head"], b["max_ctx"]))
+    assert len(big) == b["size"] and P.weight_hash(big) == b["blake3"]
+
+
+def test_rtab_parse_errors_match_reference():
+    import paper_2603_24904_b200 as P
+    for c in _rtab_golden()["parse"]:
+        data = bytes.fromhex(c["hex"])
+        if c["outcome"] == 0:
+            P.deserialize_rope_tables(data)
+            continue
+        with pytest.raises(P.ParseError) as e:
+            P.deserialize_rope_tables(data)
+        assert e.value.kind == P.ParseError.KINDS[c["outcome"] - 100], c
+
+
+def test_rtab_save_load_roundtrip(tmp_path):
+    import paper_2603_24904_b200 as P
+    t = P.RopeTables.build(10000.0, 16, 33)
+    p = str(tmp_path / "t.rtab")
+    P.save_rope_tables(t, p)
+    assert P.load_rope_tables(p) == t
+    with pytest.raises(P.errors.IOFailure):
+        P.load_rope_tables(str(tmp_path / "missing.rtab"))
+    with pytest.raises(P.errors.IOFailure):
+        P.save_rope_tables(t, str(tmp_path / "no" / "dir.rtab"))

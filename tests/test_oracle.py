@@ -181,3 +181,21 @@ def test_chacha20_restatement_matches_reference_prompts(oracle, kat):
         seed, vocab, n = (int(x) for x in name.split("_"))
         key = bytes.fromhex(oracle.blake3(seed.to_bytes(8, "little")))
         assert [w % vocab for w in chacha20_u32s(key, n)] == ids, name
+
+
+def test_sample_restatement_matches_reference_edges(oracle):
+    """The reference's answers at its edges (tests/golden/sample_edge.npz):
+    scaled logits spanning more than 2^63 raise exp_neg_lut's domain_error
+    (proj/src/q16.cpp:82) and an all-zero probability mass falls through to
+    V - 1 (proj/src/engine.cpp:138); the draws are ChaCha20Rng(key)'s first u32."""
+    import os
+    from oracle.pyoracle import chacha20_u32s
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "sample_edge.npz"))
+    for i, (row, n, t, key, d, st, tok) in enumerate(zip(z["logits"], z["lens"], z["temperature"], z["key"],
+                                                          z["draw"], z["status"], z["token"])):
+        assert chacha20_u32s(bytes(key), 1)[0] == int(d)
+        if st == 6:
+            with pytest.raises(ArithmeticError):
+                oracle.sample_from_logits(row[:n], int(t), int(d))
+        else:
+            assert oracle.sample_from_logits(row[:n], int(t), int(d)) == int(tok), i
