@@ -226,6 +226,44 @@ dimg_status dimg_session_launches(const dimg_session* s, uint32_t* per_decode,
  * tensor-core prefills redone on the exact decode path (high 32 bits). */
 dimg_status dimg_session_stats(dimg_session* s, uint64_t out[4]);
 
+/* ---- tensor parallelism (BASELINE config C4) ----
+ * One model sharded Megatron-style over tp_size ranks: q/k/v and the FFN
+ * gate/up rows and lm_head vocab rows column-parallel, wo and w_down
+ * row-parallel (input columns); the PRE-SCALE int64 accumulators of wo and
+ * w_down (dense_forward's acc before (acc*s)>>16, proj/src/kernels.cpp:18-30)
+ * are summed over the ranks (uint64: wrapping, order-free -- the reference's
+ * chunk invariance, kernels.cpp:32-50) and the rescale, residual and clamp
+ * run on every rank; the greedy pick gathers every rank's (max, lowest index)
+ * pair (select_greedy, engine.cpp:113-120). Tokens and hashes are identical
+ * to the single-GPU engine and the reference at every tp_size.
+ * Backends:
+ *   DIMG_TP_NCCL   this process is rank tp_rank (one process per GPU,
+ *                  `device` its GPU); nccl_id from rank 0's
+ *                  dimg_nccl_unique_id, distributed by the caller.
+ *   DIMG_TP_LOCAL  all tp_size shards on `device` in this process, the sums
+ *                  done by kernels (testing the sharded kernels on one GPU).
+ * tp_size must divide n_heads. keep_logits_cap: logits vectors a generate
+ * call may return. */
+typedef struct dimg_tp dimg_tp;
+typedef enum { DIMG_TP_LOCAL = 0, DIMG_TP_NCCL = 1 } dimg_tp_backend;
+dimg_status dimg_nccl_unique_id(uint8_t id[128]);
+dimg_status dimg_tp_create(int device, const dimg_model_desc* desc, int backend, int tp_rank, int tp_size,
+                           const uint8_t nccl_id[128], uint32_t keep_logits_cap, dimg_tp** out);
+dimg_status dimg_tp_free(dimg_tp* t);
+/* generate_greedy (engine.cpp:31-54,142-147) on the sharded model; host
+ * buffers as dimg_generate_greedy; every rank returns the same tokens. */
+dimg_status dimg_tp_generate_greedy(dimg_tp* t, const uint32_t* prompt, uint32_t n_prompt, uint32_t max_new,
+                                    uint32_t* tokens_out, uint8_t hash_out[32], int64_t* logits_out);
+/* The prompt steps, then n_steps decode steps between CUDA events on the
+ * group's stream; the tokens through dimg_tp_tokens. */
+dimg_status dimg_tp_time_decode(dimg_tp* t, const uint32_t* prompt, uint32_t n_prompt, uint32_t n_steps,
+                                float* ms);
+dimg_status dimg_tp_tokens(dimg_tp* t, uint32_t* out, uint32_t n_generated);
+dimg_status dimg_tp_stream(dimg_tp* t, void** stream);
+/* Device bytes of this process's shards; kernel launches + collectives per
+ * decode step (after the first generation). */
+dimg_status dimg_tp_info(dimg_tp* t, uint64_t* weight_bytes, uint64_t* launches_per_step);
+
 /* ---- operator-level exports (host buffers in/out) for unit parity with
  *      proj/src/kernels.cpp; they run the engine's own device kernels. ---- */
 dimg_status dimg_op_dense(int device, const dimg_qtensor* w, const int64_t* x, int64_t* out);

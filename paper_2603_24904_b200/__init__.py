@@ -15,6 +15,7 @@ from .engine import (EngineOptions, GenerationResult, InferenceSession, attentio
                      deserialize_rope_tables, save_rope_tables, load_rope_tables)
 from .errors import (ContextOverflow, DomainError, InvalidArgument, LengthError, LogicError,
                      OutOfRange, ParseError)
+from .parallel import TensorParallel, nccl_unique_id
 from .model import (ONE, DeviceModel, ModelConfig, ModelFile, deserialize, gen_toy_model,
                     load_model, weight_hash)
 
@@ -27,5 +28,5 @@ __all__ = [
     "ContextOverflow", "DomainError", "InvalidArgument", "LengthError", "LogicError",
     "OutOfRange", "ParseError", "LIB_PATH", "lib", "attest", "Attestation", "VerifyOutcome", "DisputeResult",
     "make_attestation", "verify_by_reexecution", "dispute_game", "prompt_hash",
-    "RopeTables", "serialize_rope_tables", "deserialize_rope_tables", "save_rope_tables", "load_rope_tables",
+    "TensorParallel", "nccl_unique_id", "RopeTables", "serialize_rope_tables", "deserialize_rope_tables", "save_rope_tables", "load_rope_tables",
 ]

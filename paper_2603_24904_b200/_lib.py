@@ -106,6 +106,15 @@ def _load():
         "dimg_session_time_kernel": ([vp, C.c_int, C.c_uint32, C.POINTER(C.c_float), u64p], C.c_int),
         "dimg_session_stats": ([vp, u64p], C.c_int),
         "dimg_session_trace": ([vp, C.c_uint32, u64p, C.c_uint32], C.c_int),
+        "dimg_nccl_unique_id": ([u8p], C.c_int),
+        "dimg_tp_create": ([C.c_int, C.POINTER(ModelDesc), C.c_int, C.c_int, C.c_int, u8p, C.c_uint32, pp],
+                           C.c_int),
+        "dimg_tp_free": ([vp], C.c_int),
+        "dimg_tp_generate_greedy": ([vp, u32p, C.c_uint32, C.c_uint32, u32p, u8p, i64p], C.c_int),
+        "dimg_tp_time_decode": ([vp, u32p, C.c_uint32, C.c_uint32, C.POINTER(C.c_float)], C.c_int),
+        "dimg_tp_tokens": ([vp, u32p, C.c_uint32], C.c_int),
+        "dimg_tp_stream": ([vp, pp], C.c_int),
+        "dimg_tp_info": ([vp, u64p, u64p], C.c_int),
         "dimg_op_dense": ([C.c_int, C.POINTER(QTensor), i64p, i64p], C.c_int),
         "dimg_op_dense_tokens": ([C.c_int, C.POINTER(QTensor), i64p, C.c_uint32, i64p], C.c_int),
         "dimg_blake3_device": ([C.c_int, vp, C.c_size_t, u8p, C.POINTER(C.c_float)], C.c_int),

@@ -271,6 +271,7 @@ struct DevMat {
     int64_t* s = nullptr;      // scales [rows]
     uint32_t rows = 0, K = 0, Kp = 0, n_groups = 0, n_segs = 0;
     int8_t* plain = nullptr;   // K-block-major [kblk][rows128][128] (tensor-core A operand)
+    int8_t* rm = nullptr;      // row-major [rows][Kp] (tensor-parallel shards' GEMVs)
     uint32_t kblk = 0, rows128 = 0;
     CUtensorMap tmap;          // its TMA map (128 x 128-byte boxes, 128B swizzle)
 };
@@ -285,6 +286,10 @@ struct dimg_model {
     dimg_config cfg;
     uint32_t D, F, V, H, dh, L, Kd, Kf;
     int tp_rank, tp_size;
+    // this rank's shard: heads [h0, h0 + Hl) (q/k/v rows and wo
+    // columns [h0 dh, (h0 + Hl) dh)), FFN rows/columns [f0, f0 + Fl), vocab
+    // rows [v0, v0 + Vl); the whole model when tp_size == 1
+    uint32_t Hl, Dl, Fl, Vl, h0, f0, v0;
     struct Layer {
         DevMat qkv, wo, gu, down;
         int64_t* attn_norm;
@@ -395,6 +400,16 @@ DevMat upload_mat(dimg_model& m, uint32_t rows, uint32_t K, const std::vector<Ro
     d.n_groups = (rows + PK_ROWS - 1) / PK_ROWS;
     d.n_segs = (d.Kp + PK_SEG - 1) / PK_SEG;
     const size_t bytes = size_t(d.n_groups) * PK_ROWS * d.Kp;
+    if (m.tp_size > 1) {
+        // a tensor-parallel shard: the row-major [rows][Kp] layout the
+        // per-stage GEMVs stream (no persistent-kernel or tensor-core copy)
+        d.rm = m.mem.alloc<int8_t>(bytes);
+        CK(cudaMemset(d.rm, 0, bytes));
+        for (const auto& p : parts) put_rows(d.rm, d.Kp, p.row0, p.rstride, p.src, p.rows, K, nullptr, p.src_pitch);
+        d.s = upload(m.mem, scales.data(), scales.size());
+        CK(cudaDeviceSynchronize());
+        return d;
+    }
     CK(cudaMemset(staging, 0, bytes));
     for (const auto& p : parts) put_rows(staging, d.Kp, p.row0, p.rstride, p.src, p.rows, K, nullptr, p.src_pitch);
     d.s = upload(m.mem, scales.data(), scales.size());
@@ -1208,8 +1223,10 @@ dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank,
         validate_config(d->cfg);
         if (pad16(d->cfg.d_model) > 8192)
             fail(DIMG_EINVAL, "model_upload: d_model above 8192");  // persistent.cuh MAXW
-        if (tp_size != 1 || tp_rank != 0)
-            fail(DIMG_EINVAL, "model_upload: tensor-parallel sharding is not built yet");
+        if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size)
+            fail(DIMG_EINVAL, "model_upload: bad tensor-parallel rank/size");
+        if (d->cfg.n_heads % uint32_t(tp_size))
+            fail(DIMG_EINVAL, "model_upload: n_heads must be a multiple of the tensor-parallel size");
         DevCtx& c = dev_ctx(device);
         CK(cudaSetDevice(device));
         auto m = std::make_unique<dimg_model>();
@@ -1220,8 +1237,13 @@ dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank,
         m->dh = m->D / m->H; m->L = d->cfg.n_layers; m->Kd = pad16(m->D); m->Kf = pad16(m->F);
         m->tp_rank = tp_rank; m->tp_size = tp_size;
         const uint32_t D = m->D, F = m->F, V = m->V;
-        auto check_qt = [&](const dimg_qtensor& t, uint32_t r, uint32_t k, const char* what) {
-            if (t.rows != r || t.cols != k) fail(DIMG_EINVAL, std::string("model_upload: bad shape of ") + what);
+        const uint32_t g = uint32_t(tp_size), r = uint32_t(tp_rank);
+        m->Hl = m->H / g; m->h0 = r * m->Hl; m->Dl = m->Hl * m->dh;
+        m->f0 = uint32_t(uint64_t(F) * r / g); m->Fl = uint32_t(uint64_t(F) * (r + 1) / g) - m->f0;
+        m->v0 = uint32_t(uint64_t(V) * r / g); m->Vl = uint32_t(uint64_t(V) * (r + 1) / g) - m->v0;
+        const uint32_t Dl = m->Dl, Fl = m->Fl, q0 = m->h0 * m->dh, f0 = m->f0;
+        auto check_qt = [&](const dimg_qtensor& t, uint32_t rr, uint32_t k, const char* what) {
+            if (t.rows != rr || t.cols != k) fail(DIMG_EINVAL, std::string("model_upload: bad shape of ") + what);
         };
         // staging for the largest matrix (row-major, rows padded to 4)
         size_t stage_bytes = 0;
@@ -1230,8 +1252,8 @@ dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank,
         };
         grow(3 * D, D); grow(2 * F, D); grow(D, F); grow(V, D);
         int8_t* staging = nullptr;
-        CK(cudaMalloc(&staging, stage_bytes));
-        struct Free { int8_t* p; ~Free() { cudaFree(p); } } free_staging{staging};
+        if (tp_size == 1) CK(cudaMalloc(&staging, stage_bytes));
+        struct Free { int8_t* p; ~Free() { if (p) cudaFree(p); } } free_staging{staging};
         m->layers.resize(m->L);
         for (uint32_t l = 0; l < m->L; ++l) {
             const dimg_qtensor* t = d->layers + 7 * size_t(l);
@@ -1239,19 +1261,27 @@ dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank,
             for (int i = 0; i < 7; ++i)
                 check_qt(t[i], i < 4 ? D : (i < 6 ? F : D), i < 6 ? D : F, names[i]);
             auto& lw = m->layers[l];
-            std::vector<int64_t> s(3 * size_t(D));
-            for (int i = 0; i < 3; ++i) std::copy(t[i].scales, t[i].scales + D, s.begin() + size_t(i) * D);
-            lw.qkv = upload_mat(*m, 3 * D, D, {{t[0].data, D, 0, 1}, {t[1].data, D, D, 1}, {t[2].data, D, 2 * D, 1}},
+            // column-parallel q/k/v: this rank's heads (rows q0 .. q0 + Dl of each)
+            std::vector<int64_t> s(3 * size_t(Dl));
+            for (int i = 0; i < 3; ++i)
+                std::copy(t[i].scales + q0, t[i].scales + q0 + Dl, s.begin() + size_t(i) * Dl);
+            const size_t qo = size_t(q0) * D;
+            lw.qkv = upload_mat(*m, 3 * Dl, D,
+                                {{t[0].data + qo, Dl, 0, 1}, {t[1].data + qo, Dl, Dl, 1}, {t[2].data + qo, Dl, 2 * Dl, 1}},
                                 s, staging);
-            lw.wo = upload_mat(*m, D, D, {{t[3].data, D, 0, 1}},
+            // row-parallel wo: the same heads' input columns, every output row
+            lw.wo = upload_mat(*m, D, Dl, {{t[3].data + q0, D, 0, 1, D}},
                                std::vector<int64_t>(t[3].scales, t[3].scales + D), staging);
-            std::vector<int64_t> gs(2 * size_t(F));
-            for (uint32_t i = 0; i < F; ++i) {
-                gs[2 * i] = t[4].scales[i];
-                gs[2 * i + 1] = t[5].scales[i];
+            // column-parallel gate/up rows f0 .. f0 + Fl, interleaved
+            std::vector<int64_t> gs(2 * size_t(Fl));
+            for (uint32_t i = 0; i < Fl; ++i) {
+                gs[2 * i] = t[4].scales[f0 + i];
+                gs[2 * i + 1] = t[5].scales[f0 + i];
             }
-            lw.gu = upload_mat(*m, 2 * F, D, {{t[4].data, F, 0, 2}, {t[5].data, F, 1, 2}}, gs, staging);
-            lw.down = upload_mat(*m, D, F, {{t[6].data, D, 0, 1}},
+            lw.gu = upload_mat(*m, 2 * Fl, D, {{t[4].data + size_t(f0) * D, Fl, 0, 2}, {t[5].data + size_t(f0) * D, Fl, 1, 2}},
+                               gs, staging);
+            // row-parallel w_down: input columns f0 .. f0 + Fl
+            lw.down = upload_mat(*m, D, Fl, {{t[6].data + f0, D, 0, 1, F}},
                                  std::vector<int64_t>(t[6].scales, t[6].scales + D), staging);
             lw.attn_norm = upload(m->mem, d->norms + size_t(2 * l) * D, D);
             lw.ffn_norm = upload(m->mem, d->norms + size_t(2 * l + 1) * D, D);
@@ -1262,8 +1292,10 @@ dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank,
         check_qt(d->output, V, D, "output");
         m->embd = upload(m->mem, d->tok_embd.data, size_t(V) * D);
         m->embd_s = upload(m->mem, d->tok_embd.scales, V);
-        m->head = upload_mat(*m, V, D, {{d->output.data, V, 0, 1}},
-                             std::vector<int64_t>(d->output.scales, d->output.scales + V), staging);
+        // column-parallel lm_head: vocab rows v0 .. v0 + Vl
+        m->head = upload_mat(*m, m->Vl, D, {{d->output.data + size_t(m->v0) * D, m->Vl, 0, 1}},
+                             std::vector<int64_t>(d->output.scales + m->v0, d->output.scales + m->v0 + m->Vl),
+                             staging);
         m->final_norm = upload(m->mem, d->norms + size_t(2 * m->L) * D, D);
         m->final_unit = all_one(d->norms + size_t(2 * m->L) * D, D);
         // RoPE tables: imported (RTAB) or built on the host (rope.cpp:17-39)
@@ -1311,6 +1343,7 @@ dimg_status dimg_model_bytes_on_device(const dimg_model* m, uint64_t* bytes) {
 
 dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_session** out) {
     DIMG_API_GUARD({
+        if (m->tp_size != 1) fail(DIMG_EINVAL, "session: a tensor-parallel shard generates through dimg_tp");
         CK(cudaSetDevice(m->device));
         auto s = std::make_unique<dimg_session>();
         s->m = m;
@@ -1469,6 +1502,7 @@ dimg_status dimg_generate_greedy_batch(dimg_model* m, uint32_t n_seqs, const uin
     // together on the tensor cores; an exact per-sequence rerun when some
     // value falls outside the batch path's fast representations.
     DIMG_API_GUARD({
+        if (m->tp_size != 1) fail(DIMG_EINVAL, "batch: a tensor-parallel shard generates through dimg_tp");
         CK(cudaSetDevice(m->device));
         std::vector<std::vector<uint32_t>> ps(n_seqs);
         size_t off = 0;
@@ -2123,3 +2157,5 @@ dimg_status dimg_op_ffn(int device, const dimg_qtensor* gate, const dimg_qtensor
 }
 
 }  // extern "C"
+
+#include "tp_engine.cuh"

@@ -12,16 +12,25 @@
     bit-identical at every g (the reference's chunk-invariance argument,
     proj/tests/test_kernels.cpp:79-97);
   - argmax: rank-local (max, lowest index) then a deterministic global pick.
-`TPPlan` is the single source of these slices for the host-side sharding
-(`shard_tensors`) and its tests (tests/test_parallel.py).
+`TPPlan` states these slices for the host-side sharding (`shard_tensors`)
+and its gloo tests (tests/test_parallel.py); the device shards are cut by
+dimg_model_upload with the same balanced blocks.
+
+`TensorParallel` runs the sharded model on the GPU (dimg_tp_*): backend
+"nccl" = this process is one rank (one process per GPU, NCCL all-reduce of
+the pre-scale accumulators); backend "local" = all shards on one device in
+this process (the sums done by kernels), for testing on one GPU.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
 from typing import List, Tuple
 
+import ctypes as C
+
 import numpy as np
 
+from ._lib import ModelDesc, check, i64p, lib, ptr, u32p, u64p
 from .model import LAYER_TENSORS, ModelConfig, ModelFile
 
 
@@ -106,3 +115,75 @@ def pick_argmax(candidates) -> int:
         if best is None or v > best[0] or (v == best[0] and i < best[1]):
             best = (v, i)
     return int(best[1])
+
+
+BACKENDS = {"local": 0, "nccl": 1}
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 creates it; the caller broadcasts it)."""
+    b = (C.c_uint8 * 128)()
+    check(lib.dimg_nccl_unique_id(b))
+    return bytes(b)
+
+
+class TensorParallel:
+    """generate_greedy (proj/src/engine.cpp:31-54) on a model sharded over
+    tp_size ranks. Tokens and hashes equal the
+    single-GPU engine's at every tp_size."""
+
+    def __init__(self, model: ModelFile, tp_size: int, backend: str = "local", rank: int = 0,
+                 nccl_id: bytes = None, device: int = 0, keep_logits_cap: int = 0):
+        from .engine import GenerationResult  # noqa: F401  (import cycle)
+        model.config.validate()
+        d = ModelDesc()
+        check(lib.dimg_host_model_desc(model._h, C.byref(d)))
+        idb = (C.c_uint8 * 128)(*nccl_id) if nccl_id is not None else None
+        h = C.c_void_p()
+        check(lib.dimg_tp_create(device, C.byref(d), BACKENDS[backend], rank, tp_size, idb, keep_logits_cap,
+                                 C.byref(h)))
+        self._h = h
+        self._model = model  # the desc's host buffers are borrowed during upload only
+        self.tp_size, self.backend, self.rank = tp_size, backend, rank
+        self.vocab = model.config.vocab
+
+    def generate_greedy(self, prompt, max_new: int, keep_logits: bool = False):
+        from .engine import GenerationResult
+        p = np.ascontiguousarray(prompt, dtype=np.uint32)
+        toks = np.zeros(max(1, max_new), np.uint32)
+        h = (C.c_uint8 * 32)()
+        logits = np.empty((max_new, self.vocab), np.int64) if keep_logits else None
+        check(lib.dimg_tp_generate_greedy(self._h, ptr(p, u32p), p.size, max_new, ptr(toks, u32p), h,
+                                          ptr(logits, i64p) if keep_logits else None))
+        res = GenerationResult([int(t) for t in toks[:max_new]], bytes(h))
+        if keep_logits:
+            res.logits = [logits[i] for i in range(max_new)]
+        return res
+
+    def time_decode(self, prompt, n_steps: int) -> float:
+        """ms of n_steps decode steps (CUDA events on the group's stream)."""
+        p = np.ascontiguousarray(prompt, dtype=np.uint32)
+        ms = C.c_float()
+        check(lib.dimg_tp_time_decode(self._h, ptr(p, u32p), p.size, n_steps, C.byref(ms)))
+        return ms.value
+
+    def tokens(self, n: int):
+        out = np.zeros(max(1, n), np.uint32)
+        check(lib.dimg_tp_tokens(self._h, ptr(out, u32p), n))
+        return [int(t) for t in out[:n]]
+
+    def info(self):
+        b, n = C.c_uint64(), C.c_uint64()
+        check(lib.dimg_tp_info(self._h, C.byref(b), C.byref(n)))
+        return {"weight_bytes": b.value, "launches_per_step": n.value}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.dimg_tp_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
