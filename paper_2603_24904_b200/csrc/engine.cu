@@ -286,6 +286,7 @@ struct dimg_model {
     dimg_config cfg;
     uint32_t D, F, V, H, dh, L, Kd, Kf;
     int tp_rank, tp_size;
+    bool rowmajor = false;  // weights in the row-major GEMV layout only (tensor-parallel groups)
     // this rank's shard: heads [h0, h0 + Hl) (q/k/v rows and wo
     // columns [h0 dh, (h0 + Hl) dh)), FFN rows/columns [f0, f0 + Fl), vocab
     // rows [v0, v0 + Vl); the whole model when tp_size == 1
@@ -400,7 +401,7 @@ DevMat upload_mat(dimg_model& m, uint32_t rows, uint32_t K, const std::vector<Ro
     d.n_groups = (rows + PK_ROWS - 1) / PK_ROWS;
     d.n_segs = (d.Kp + PK_SEG - 1) / PK_SEG;
     const size_t bytes = size_t(d.n_groups) * PK_ROWS * d.Kp;
-    if (m.tp_size > 1) {
+    if (m.rowmajor) {
         // a tensor-parallel shard: the row-major [rows][Kp] layout the
         // per-stage GEMVs stream (no persistent-kernel or tensor-core copy)
         d.rm = m.mem.alloc<int8_t>(bytes);
@@ -1217,9 +1218,22 @@ extern "C" {
 
 dimg_status dimg_device_count(int* n) { DIMG_API_GUARD(CK(cudaGetDeviceCount(n))) }
 
-dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank, int tp_size,
+}  // extern "C"
+
+namespace {
+dimg_model* model_upload(int device, const dimg_model_desc* d, int tp_rank, int tp_size, bool rowmajor);
+}
+
+extern "C" dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank, int tp_size,
                               dimg_model** out) {
-    DIMG_API_GUARD({
+    DIMG_API_GUARD(*out = model_upload(device, d, tp_rank, tp_size, tp_size > 1))
+}
+
+namespace {
+// rowmajor: the per-stage GEMV layout of tensor-parallel groups (dimg_tp),
+// instead of the persistent kernel's and tensor cores' copies
+dimg_model* model_upload(int device, const dimg_model_desc* d, int tp_rank, int tp_size, bool rowmajor) {
+    {
         validate_config(d->cfg);
         if (pad16(d->cfg.d_model) > 8192)
             fail(DIMG_EINVAL, "model_upload: d_model above 8192");  // persistent.cuh MAXW
@@ -1235,7 +1249,7 @@ dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank,
         m->cfg = d->cfg;
         m->D = d->cfg.d_model; m->F = d->cfg.d_ffn; m->V = d->cfg.vocab; m->H = d->cfg.n_heads;
         m->dh = m->D / m->H; m->L = d->cfg.n_layers; m->Kd = pad16(m->D); m->Kf = pad16(m->F);
-        m->tp_rank = tp_rank; m->tp_size = tp_size;
+        m->tp_rank = tp_rank; m->tp_size = tp_size; m->rowmajor = rowmajor;
         const uint32_t D = m->D, F = m->F, V = m->V;
         const uint32_t g = uint32_t(tp_size), r = uint32_t(tp_rank);
         m->Hl = m->H / g; m->h0 = r * m->Hl; m->Dl = m->Hl * m->dh;
@@ -1252,7 +1266,7 @@ dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank,
         };
         grow(3 * D, D); grow(2 * F, D); grow(D, F); grow(V, D);
         int8_t* staging = nullptr;
-        if (tp_size == 1) CK(cudaMalloc(&staging, stage_bytes));
+        if (!rowmajor) CK(cudaMalloc(&staging, stage_bytes));
         struct Free { int8_t* p; ~Free() { if (p) cudaFree(p); } } free_staging{staging};
         m->layers.resize(m->L);
         for (uint32_t l = 0; l < m->L; ++l) {
@@ -1324,9 +1338,12 @@ dimg_status dimg_model_upload(int device, const dimg_model_desc* d, int tp_rank,
             m->inv_scale = int64_t((y + (__int128(1) << 31)) >> 32);
         }
         CK(cudaDeviceSynchronize());
-        *out = m.release();
-    })
+        return m.release();
+    }
 }
+}  // namespace
+
+extern "C" {
 
 dimg_status dimg_model_free(dimg_model* m) {
     DIMG_API_GUARD({
@@ -1343,7 +1360,7 @@ dimg_status dimg_model_bytes_on_device(const dimg_model* m, uint64_t* bytes) {
 
 dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_session** out) {
     DIMG_API_GUARD({
-        if (m->tp_size != 1) fail(DIMG_EINVAL, "session: a tensor-parallel shard generates through dimg_tp");
+        if (m->rowmajor) fail(DIMG_EINVAL, "session: a tensor-parallel shard generates through dimg_tp");
         CK(cudaSetDevice(m->device));
         auto s = std::make_unique<dimg_session>();
         s->m = m;
@@ -1502,7 +1519,7 @@ dimg_status dimg_generate_greedy_batch(dimg_model* m, uint32_t n_seqs, const uin
     // together on the tensor cores; an exact per-sequence rerun when some
     // value falls outside the batch path's fast representations.
     DIMG_API_GUARD({
-        if (m->tp_size != 1) fail(DIMG_EINVAL, "batch: a tensor-parallel shard generates through dimg_tp");
+        if (m->rowmajor) fail(DIMG_EINVAL, "batch: a tensor-parallel shard generates through dimg_tp");
         CK(cudaSetDevice(m->device));
         std::vector<std::vector<uint32_t>> ps(n_seqs);
         size_t off = 0;

@@ -399,10 +399,7 @@ dimg_status dimg_tp_create(int device, const dimg_model_desc* desc, int backend,
         const int lo = backend == DIMG_TP_LOCAL ? 0 : tp_rank, hi = backend == DIMG_TP_LOCAL ? tp_size : tp_rank + 1;
         for (int r = lo; r < hi; ++r) {
             auto rk = std::make_unique<TpRank>();
-            dimg_model* m = nullptr;
-            const dimg_status s = dimg_model_upload(device, desc, r, tp_size, &m);
-            if (s != DIMG_OK) fail(s, dimg_last_error());
-            rk->m.reset(m);
+            rk->m.reset(model_upload(device, desc, r, tp_size, true));
             tp_build_rank(*t, *rk);
             t->ranks.push_back(std::move(rk));
         }
