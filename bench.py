@@ -6,21 +6,33 @@ configs[1]: 7B-shaped random-init int8 weights, seed 7; ChaCha20 prompt seed 8,
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 A step is one greedy decode token: one full forward of the 32-layer model
-(6.62 GB of int8 weights + scales streamed from HBM) plus the on-device
-argmax that appends the next token. With N > 1 (torchrun, one process per
-GPU) every rank decodes its own independent sequence (weak scaling, no
-data-path collective; C5's sequence sharding): value = all ranks' tokens /
-max-over-ranks time.
+(6.62 GB of int8 weights + scales) plus the argmax that appends the next token.
+
+  N = 1   the persistent decode kernel (one launch for all K steps).
+  N > 1   (torchrun, one process per GPU) TENSOR PARALLEL decode of the same
+          single sequence (BASELINE configs[3]): each rank holds
+          1/N of every matrix, the pre-scale WO / w_down accumulators are
+          NCCL all-reduced (uint64 sum), the lm_head argmax pairs all-gathered;
+          value = K / max-over-ranks time (strong scaling: the work per token
+          is fixed, each GPU streams 1/N of it). The tokens are checked
+          against the C2 golden. Extra keys at N > 1:
+            c5  every rank generates its 8 C5 sequences through the batch
+                call (seqs 8r .. 8r+7), per-sequence hashes vs the goldens
+            dp  every rank decodes its own sequence with the single-GPU
+                kernel (weak-scaling replicas, the N = 1 kernel's aggregate)
 
 Keys beyond the base contract:
   e2e           the same metric through the reference-shaped C-ABI call
-                dimg_generate_greedy with HOST buffers (prompt H2D, tokens D2H
-                and the BLAKE3 hash inside the timed region)
-  roofline      dominant kernel (gate/up GEMV): algorithmic bytes per launch /
-                CUDA-event launch time, vs MEASURED_PEAKS.json hbm_gbs
+                (dimg_generate_greedy / dimg_tp_generate_greedy) with HOST
+                buffers: prompt H2D, tokens D2H and the BLAKE3 hash inside
+                the timed region
+  roofline      the dominant kernel per decode step: algorithmic bytes per
+                step (per GPU at N > 1) / CUDA-event step time, vs
+                MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the reference engine (oracle/_ref, compiled from its own
                 sources) timed on this host, rank 0, N=1
---impl reference times that reference engine alone on the same workload.
+--impl reference times that reference engine alone on the same workload
+(same prompt, same decode positions, same config dict).
 """
 from __future__ import annotations
 
@@ -114,6 +126,32 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------
+def host_cpu():
+    """nproc and the CPU model of this host (SURVEY §8d asks for both)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def config_dict(world, extra=None):
+    """The workload description both arms print (same_config)."""
+    d = {"workload": "C2: Llama-2-7B-shaped int8/Q16 model, batch-1 greedy decode",
+         "model": "llama2-7b-shaped-int", "layers": CFG7B[0], "d_model": CFG7B[1], "d_ffn": CFG7B[3],
+         "vocab": CFG7B[4], "seed": MODEL_SEED, "prompt_seed": PROMPT_SEED, "prompt_len": PROMPT_LEN,
+         "decode_positions": "15+W .. 14+W+K (after the 15 prompt positions and W warm-up steps)",
+         "global_batch": 1, "parallelism": f"tp{world}" if world > 1 else "single GPU",
+         "l2": "weights 6.6 GB/step > 126 MB L2 (no flush needed)"}
+    d.update(extra or {})
+    return d
+
+
 def reference_model(ref, cfg):
     """The reference's own gen_toy_model (proj/src/model.cpp:189-215)."""
     return ref.gen_toy(MODEL_SEED, cfg)
@@ -121,28 +159,40 @@ def reference_model(ref, cfg):
 
 def time_reference(ref, m, n_warm, n_timed, prompt, threads):
     """Greedy decode through dim::InferenceSession::forward (+select_greedy),
-    the reference's stock path. Returns seconds per decode forward."""
+    the reference's stock path: prompt[:-1] untimed, then the decode steps
+    (the first one feeds prompt[-1]) -- the GPU arm's positions. Returns
+    (seconds per decode forward, tokens of the warm + timed steps)."""
     import ctypes as C
-
-    import numpy as np
     h = C.c_void_p()
     assert ref.lib.ref_session_new(m.h, threads, C.byref(h)) == 0
     nxt = C.c_uint32()
     pos = 0
-    for t in prompt:  # prefill sample (untimed)
+    for t in prompt[:-1]:  # prefill (untimed)
         assert ref.lib.ref_session_forward(h, int(t), pos, None, C.byref(nxt)) == 0
         pos += 1
+    tok, toks = int(prompt[-1]), []
     for _ in range(n_warm):
-        assert ref.lib.ref_session_forward(h, nxt.value, pos, None, C.byref(nxt)) == 0
+        assert ref.lib.ref_session_forward(h, tok, pos, None, C.byref(nxt)) == 0
+        tok = nxt.value
+        toks.append(tok)
         pos += 1
     t0 = time.perf_counter()
     for _ in range(n_timed):
-        assert ref.lib.ref_session_forward(h, nxt.value, pos, None, C.byref(nxt)) == 0
+        assert ref.lib.ref_session_forward(h, tok, pos, None, C.byref(nxt)) == 0
+        tok = nxt.value
+        toks.append(tok)
         pos += 1
     dt = time.perf_counter() - t0
     ref.lib.ref_session_free(h)
-    del np
-    return dt / max(1, n_timed)
+    return dt / max(1, n_timed), toks
+
+
+def golden_c2():
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "models_7b.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
 
 
 def run_reference(args, rank, world):
@@ -158,21 +208,24 @@ def run_reference(args, rank, world):
     t0 = time.time()
     m = reference_model(ref, cfg)
     gen_s = time.time() - t0
-    prompt = ref.prompt(PROMPT_SEED, cfg.vocab, PROMPT_LEN)[:4]
-    spf = time_reference(ref, m, args.warmup, args.steps, prompt, threads)
+    prompt = ref.prompt(PROMPT_SEED, cfg.vocab, PROMPT_LEN)
+    spf, toks = time_reference(ref, m, args.warmup, args.steps, prompt, threads)
+    gold = golden_c2().get("c2", {}).get("tokens", [])
+    n = min(len(toks), len(gold))
     value = 1.0 / spf
-    sample = (f"dim::InferenceSession::forward + select_greedy, {args.steps} timed decode "
-              f"forwards after a 4-token prompt and {args.warmup} warm-up forwards "
-              f"(threads={threads}: the reference's dense matvec is single-threaded)")
+    sample = (f"dim::InferenceSession::forward + select_greedy: the 16-token prompt's first 15 positions "
+              f"untimed, {args.warmup} warm-up and {args.steps} timed decode forwards (threads={threads}; "
+              f"the reference's dense matvec is single-threaded, so 1 core does the work)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": spf * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": spf * 1e3, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference gen_toy_model seed 7)",
-        "config": {"workload": "C2: Llama-2-7B-shaped int8/Q16 model, batch-1 greedy decode",
-                   "model": "llama2-7b-shaped-int", "seed": MODEL_SEED, "prompt_seed": PROMPT_SEED},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "reference",
-                         "sample": sample, "threads_setting": threads, "model_gen_s": round(gen_s, 1)},
+        "config": config_dict(world),
+        "tokens_match_c2_golden": toks[:n] == gold[:n] if n else None,
+        "cpu_baseline": dict({"value": value, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                              "sample": sample, "threads_setting": threads, "model_gen_s": round(gen_s, 1)},
+                             **host_cpu()),
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -181,7 +234,8 @@ def run_reference(args, rank, world):
 
 # --------------------------------------------------------------------------
 def cpu_baseline(model_file, cfg_t):
-    """Reference engine on this host over the SAME weights (bounded sample)."""
+    """Reference engine on this host over the SAME weights (bounded sample:
+    a 2-token prompt, then 10 timed decode forwards, threads=1)."""
     try:
         from oracle.pyoracle import Config, Reference
         if not Reference.available():
@@ -196,21 +250,47 @@ def cpu_baseline(model_file, cfg_t):
         m = ref.model_from_arrays(cfg, w, s, model_file.norms())
         del w, s
         prompt = ref.prompt(PROMPT_SEED, cfg.vocab, PROMPT_LEN)[:2]
-        spf = time_reference(ref, m, 0, 3, prompt, 1)
-        return {"value": 1.0 / spf, "unit": "tokens/s", "cores": 1, "kind": "reference",
-                "sample": "3 decode forwards (dim::InferenceSession::forward + select_greedy) after a "
-                          "2-token prompt, same weights, threads=1"}
+        spf, _ = time_reference(ref, m, 0, 10, prompt, 1)
+        return dict({"value": 1.0 / spf, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                     "sample": "10 timed decode forwards (dim::InferenceSession::forward + select_greedy) after "
+                               "a 2-token prompt, same weights, threads=1 (the dense matvec is single-threaded)"},
+                    **host_cpu())
     except Exception as e:  # reported, never fatal for the GPU number
         return {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference",
                 "sample": f"unavailable: {e}"}
 
 
+def mma_i8_peak():
+    """Measured dense kind::i8 tcgen05 rate (profiles/r02_mma_rate.json,
+    tools/mma_rate.cu on this pool's B200), else 2 x the bf16 burst."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_mma_rate.json")) as f:
+            d = json.load(f)
+        return float(d["i8_tops"]), "measured kind::i8 tcgen05.mma rate (profiles/r02_mma_rate.json)"
+    except Exception:
+        pass
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return 2 * json.load(f)["bf16_tflops"], "2 x measured bf16 burst (kind::i8 at twice kind::f16)"
+    except Exception:
+        return 2 * 1590.0, "2 x fallback bf16"
+
+
+def c3_algorithmic_ops(cfg, T):
+    """2 x the int8 MACs of every layer GEMM at T tokens + the
+    last position's lm_head + the causal attention's QK^T and PV."""
+    L, D, F, V, H = cfg.n_layers, cfg.d_model, cfg.d_ffn, cfg.vocab, cfg.n_heads
+    dh = D // H
+    return 2 * L * (4 * D * D + 3 * D * F) * T + 2 * V * D + 2 * 2 * L * H * dh * T * (T + 1) // 2
+
+
 def prefill_c3(P, mf, cfg, dev):
-    """C3: prefill of a 2048-token synthetic prompt (prompt seed 9) on the
-    tensor cores, timed with CUDA events (2 warm + 3 timed); the positions
-    0..2046 go through every layer, the last prompt token is the first decode
-    step. Roofline: int8 tensor ops of the limb GEMMs (3 limbs per dense MAC)
-    against 2 x the measured bf16 peak (kind::i8 issues at twice kind::f16)."""
+    """C3: prefill of a 2048-token synthetic prompt (prompt seed 9): positions
+    0..2046 through every layer on the tensor cores (dimg_session_time_prefill)
+    plus the last prompt position's decode step that yields the first token
+    (dimg_session_time_decode), both CUDA-event timed; 2 warm + 3 timed,
+    median. Roofline: the ALGORITHMIC int8 ops of the whole 2048-token prefill
+    (SURVEY §8d: 2.763e13) per second against the measured kind::i8 rate."""
     try:
         n_prompt = 2048
         prompt = P.prompt_from_seed(9, cfg.vocab, n_prompt)
@@ -219,41 +299,38 @@ def prefill_c3(P, mf, cfg, dev):
         for i in range(5):
             s.begin(prompt, 1)
             ms, used = s.time_prefill()
+            ms += s.time_decode(1)
             tc &= used
             if i >= 2:
                 times.append(ms)
         ms = sorted(times)[len(times) // 2]
-        n = n_prompt - 1
-        D, F, L = cfg.d_model, cfg.d_ffn, cfg.n_layers
-        macs = n * ((L - 1) * (4 * D * D + 3 * F * D) + 3 * D * D)
-        limb_ops = 2 * 3 * macs
-        try:
-            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-                peak = 2 * json.load(f)["bf16_tflops"]
-            kind = "2 x measured bf16 burst (kind::i8 at twice the kind::f16 rate)"
-        except Exception:
-            peak, kind = 2 * 1590.0, "2 x fallback bf16"
-        return {"workload": "C3: Llama-2-7B-shaped prefill of a 2048-token synthetic prompt",
-                "path": "tensor cores (tcgen05 kind::i8 limb GEMMs + exact causal attention)" if tc
+        ops = c3_algorithmic_ops(cfg, n_prompt)
+        peak, kind = mma_i8_peak()
+        tops = ops / (ms / 1e3) / 1e12
+        first = s.tokens(1)[0]
+        gold = golden_c2().get("c3", {}).get("tokens", [None])[0]
+        return {"workload": "C3: Llama-2-7B-shaped prefill of a 2048-token synthetic prompt (+ first token)",
+                "path": "tensor cores (tcgen05 kind::i8 signed-digit GEMMs + exact causal attention)" if tc
                         else "decode kernel (exact fallback)",
-                "prompt_tokens": n_prompt, "positions_prefilled": n, "ms": ms,
-                "tokens_per_s": n / (ms / 1e3),
-                "roofline_whole_prefill": {"bound": "tensor", "achieved": limb_ops / (ms / 1e3) / 1e12,
-                                           "peak": peak, "unit": "TOP/s (int8)",
-                                           "frac": limb_ops / (ms / 1e3) / 1e12 / peak, "peak_kind": kind,
-                                           "note": "whole prefill time incl. the CUDA-core attention "
-                                                   "(profiles/r01_prefill_launches.txt has the split)"}}
+                "prompt_tokens": n_prompt, "ms": ms, "tokens_per_s": n_prompt / (ms / 1e3),
+                "first_token_matches_golden": (first == gold) if gold is not None else None,
+                "roofline": {"bound": "tensor", "achieved": tops, "peak": peak, "unit": "TOP/s (int8)",
+                             "frac": tops / peak, "peak_kind": kind, "algorithmic_ops": ops,
+                             "note": "algorithmic ops (SURVEY 8d) over the whole prefill time, CUDA-core "
+                                     "attention included; the signed-digit GEMMs issue 3 MMAs per MAC"}}
     except Exception as e:
         return {"workload": "C3", "unavailable": str(e)}
 
 
-def batch_c5(P, mf, cfg, dev, n_seqs=8):
-    """C5 on this GPU: n_seqs independent sequences (prompt seeds 8, 1001,
-    ...; P=16, N=128) generated together through the public batch call
-    (host prompts in, host tokens + BLAKE3 hashes out), wall-clock; hashes
-    checked against the committed goldens (tests/golden/models_7b.json)."""
+def batch_c5(P, mf, cfg, dev, rank=0, n_seqs=8):
+    """C5 shard of rank r: sequences 8r .. 8r+7 (prompt seed 8 for sequence
+    0, 1000+i otherwise; P=16, N=128) generated together through the public
+    batch call (host prompts in, host tokens + BLAKE3 hashes out), wall
+    clock; every hash checked against the committed goldens
+    (tests/golden/models_7b.json c5_i, C oracle pinned to the reference)."""
     try:
-        prompts = [P.prompt_from_seed(8 if i == 0 else 1000 + i, cfg.vocab, 16) for i in range(n_seqs)]
+        ids = list(range(n_seqs * rank, n_seqs * (rank + 1)))
+        prompts = [P.prompt_from_seed(8 if i == 0 else 1000 + i, cfg.vocab, 16) for i in ids]
         P.generate_greedy_batch(mf, prompts, 128, device=dev)  # warm: buffers + the captured step graph
         times = []
         for _ in range(3):
@@ -261,16 +338,13 @@ def batch_c5(P, mf, cfg, dev, n_seqs=8):
             res, path = P.generate_greedy_batch(mf, prompts, 128, device=dev)
             times.append(time.perf_counter() - t)
         dt = sorted(times)[1]
-        ok = None
-        try:
-            with open(os.path.join(ROOT, "tests", "golden", "models_7b.json")) as f:
-                gold = json.load(f)
-            ok = sum(res[i].output_hash.hex() == gold[f"c5_{i}"]["output_hash"] for i in range(n_seqs)
-                     if f"c5_{i}" in gold)
-        except Exception:
-            pass
-        return {"workload": f"C5 shard: {n_seqs} independent sequences, P=16, N=128, generated together",
-                "path": path, "seconds": dt, "tokens_per_s": n_seqs * 128 / dt, "golden_hash_matches": ok,
+        gold = golden_c2()
+        checked = [i for i in ids if f"c5_{i}" in gold]
+        ok = sum(res[ids.index(i)].output_hash.hex() == gold[f"c5_{i}"]["output_hash"] for i in checked)
+        return {"workload": f"C5 shard: {n_seqs} independent sequences (ids {ids[0]}..{ids[-1]}), P=16, N=128, "
+                            "generated together",
+                "path": path, "seconds": dt, "tokens_per_s": n_seqs * 128 / dt, "golden_checked": len(checked),
+                "golden_hash_matches": ok, "mismatches": len(checked) - ok,
                 "timing": "wall clock of dimg_generate_greedy_batch (prompt phase + 128 graph-replayed steps), "
                           "median of 3 after one warm call"}
     except Exception as e:
@@ -304,8 +378,6 @@ def blake3_leg(P, mf, dev, peak_gbs):
 
 
 def run_ours(args, rank, world, local):
-    import numpy as np
-
     import paper_2603_24904_b200 as P
     dist = None
     if world > 1:
@@ -318,109 +390,149 @@ def run_ours(args, rank, world, local):
     t0 = time.time()
     mf = P.gen_toy_model(MODEL_SEED, cfg, device=dev)  # weight stream on the GPU (same bytes)
     gen_s = time.time() - t0
-    wh_ok = None
-    if rank == 0:
-        wh_ok = mf.weight_hash == WEIGHT_HASH_7B
-    # rank r decodes its own sequence: C5's prompt seeds (8, then 1000+r)
-    pseed = PROMPT_SEED if rank == 0 else 1000 + rank
-    prompt = P.prompt_from_seed(pseed, cfg.vocab, PROMPT_LEN)
-    sess = P.InferenceSession(mf, P.EngineOptions(device=dev))
-    n_total = args.warmup + args.steps
-    sess.begin(prompt, n_total)
-    sess.prefill()
-    sess.decode(args.warmup)
-    sess.sync()
+    wh_ok = mf.weight_hash == WEIGHT_HASH_7B if rank == 0 else None
+    prompt = P.prompt_from_seed(PROMPT_SEED, cfg.vocab, PROMPT_LEN)
+    gold = golden_c2().get("c2", {})
+    peak, peak_kind = peaks()
+    step_bytes = bytes_per_token(cfg.n_layers, cfg.d_model, cfg.d_ffn, cfg.vocab)
 
     def barrier():
         if dist is not None:
             dist.barrier()
 
-    barrier()
-    with ClockSampler(dev) as clk:
-        ms = sess.time_decode(args.steps)  # CUDA events on the session stream, synced both sides
-    barrier()
-    ms_max = ms
-    if dist is not None:
+    def allreduce(v, op):
+        if dist is None:
+            return v
         import torch
-        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
-    toks = sess.tokens(n_total)
-    per_step_ms = ms_max / args.steps
-    value = world * args.steps / (ms_max / 1e3)
-    launches_per_step, _ = sess.launches()
+        t = torch.tensor([v], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
 
-    # per-stage probes (each stage kind replayed over the layers in one launch)
-    kern = {}
-    for which, name in enumerate(sess.KERNELS):
-        kms, kb = sess.time_kernel(which, 64 if which != 4 else 16)
-        kern[name] = {"ms": kms, "bytes": kb, "gbs": kb / (kms * 1e-3) / 1e9}
-    peak, peak_kind = peaks()
-    step_bytes = bytes_per_token(cfg.n_layers, cfg.d_model, cfg.d_ffn, cfg.vocab)
-    step_gbs = step_bytes / (per_step_ms * 1e-3) / 1e9
-    traffic = None
+    with ClockSampler(dev) as clk_all:
+        if world == 1 and not args.tp:
+            sess = P.InferenceSession(mf, P.EngineOptions(device=dev))
+            n_total = args.warmup + args.steps
+            sess.begin(prompt, n_total)
+            sess.prefill()
+            sess.decode(args.warmup)
+            sess.sync()
+            with ClockSampler(dev) as clk:
+                ms = sess.time_decode(args.steps)  # CUDA events on the session stream, synced both sides
+            toks = sess.tokens(n_total)
+            launches, _ = sess.launches()
+            gpu_launches = launches  # one persistent launch runs all K steps
+            kernel = "decode_persistent_kernel (per decode step)"
+            # e2e: the reference-shaped call with host buffers (C2: P=16, N=128)
+            sess.generate_greedy(prompt, 128)  # warm
+            t1 = time.perf_counter()
+            for _ in range(3):
+                res = sess.generate_greedy(prompt, 128)
+            e2e_s = (time.perf_counter() - t1) / 3
+            e2e_call = "dimg_generate_greedy(prompt 16 -> 128 tokens, BLAKE3 on host)"
+            extra = {}
+        else:
+            # tensor parallel: rank 0 makes the NCCL id, torch.distributed carries it
+            obj = [P.nccl_unique_id() if rank == 0 else None]
+            if dist is not None:
+                dist.broadcast_object_list(obj, src=0)
+            tp = P.TensorParallel(mf, world, backend="nccl", rank=rank, nccl_id=obj[0], device=dev)
+            tp.time_decode(prompt, args.warmup)  # warm: graphs captured, NCCL channels up
+            barrier()
+            with ClockSampler(dev) as clk:
+                ms = tp.time_decode(prompt, args.warmup + args.steps)
+                ms_w = tp.time_decode(prompt, args.warmup)
+            barrier()
+            # the K steps after W warm ones: difference of two CUDA-event timed runs
+            ms = max(ms - ms_w, 1e-6)
+            toks = tp.tokens(args.warmup + args.steps)
+            info = tp.info()
+            gpu_launches = info["launches_per_step"] * args.steps
+            kernel = "per-stage GEMVs + NCCL all-reduce (per decode step, per GPU)"
+            tp.generate_greedy(prompt, 128)  # warm
+            barrier()
+            t1 = time.perf_counter()
+            for _ in range(3):
+                res = tp.generate_greedy(prompt, 128)
+            e2e_s = (time.perf_counter() - t1) / 3
+            e2e_call = "dimg_tp_generate_greedy(prompt 16 -> 128 tokens, BLAKE3 on host), NCCL tp"
+            tp.close()
+            extra = {"nccl": {"backend": "nccl", "ranks": world, "rank0_comm_init": "ncclCommInitRank",
+                              "weight_bytes_per_rank": info["weight_bytes"]}}
+    ms_max = allreduce(ms, dist.ReduceOp.MAX if dist else None)
+    e2e_s = allreduce(e2e_s, dist.ReduceOp.MAX if dist else None)
+    per_step_ms = ms_max / args.steps
+    value = args.steps / (ms_max / 1e3)
+    n_chk = min(len(toks), len(gold.get("tokens", [])))
+    tokens_ok = toks[:n_chk] == gold["tokens"][:n_chk] if n_chk else None
+    gpu_bytes = step_bytes / world
+    step_gbs = gpu_bytes / (per_step_ms * 1e-3) / 1e9
+    traffic, traffic_src = None, None
     try:  # dram__bytes_read+write per decode step from the committed ncu capture
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            traffic = json.load(f)["traffic_bytes_per_step"]
+        for fn in ("r02_traffic.json", "r01_traffic.json"):
+            pth = os.path.join(ROOT, "profiles", fn)
+            if os.path.exists(pth):
+                with open(pth) as f:
+                    traffic = json.load(f)["traffic_bytes_per_step"]
+                traffic_src = f"profiles/{fn} (ncu --set full capture of one decode step, not this run)"
+                break
     except Exception:
         pass
+    e2e = {"value": 128 / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": 4 * PROMPT_LEN,
+           "d2h_bytes_per_step": 4 * 128, "call": e2e_call, "output_hash": res.output_hash.hex(),
+           "hash_matches_c2_golden": res.output_hash.hex() == gold.get("output_hash")}
 
-    # e2e: the reference-shaped call with host buffers (C2: P=16, N=128)
-    e2e = None
-    if rank == 0 or world > 1:
-        n_new = 128
-        sess.generate_greedy(prompt, n_new)  # warm
-        reps = 3
-        t1 = time.perf_counter()
-        for _ in range(reps):
-            res = sess.generate_greedy(prompt, n_new)
-        e2e_s = (time.perf_counter() - t1) / reps
-        e2e = {"value": n_new / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": 4 * PROMPT_LEN,
-               "d2h_bytes_per_step": 4 * n_new,
-               "call": "dimg_generate_greedy(prompt 16 -> 128 tokens, BLAKE3 on host)",
-               "output_hash": res.output_hash.hex()}
-    if dist is not None:
-        import torch
-        t = torch.tensor([e2e["value"] if e2e else 0.0], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        if e2e:
-            e2e["value"] = float(t.item()) * world
     base = cpu_baseline(mf, CFG7B) if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
-    prefill = prefill_c3(P, mf, cfg, dev) if rank == 0 and not args.no_prefill else None
-    batch = batch_c5(P, mf, cfg, dev) if rank == 0 and not args.no_prefill else None
-    blake3 = blake3_leg(P, mf, dev, peak) if rank == 0 and not args.no_prefill else None
+    legs = not args.no_prefill
+    prefill = prefill_c3(P, mf, cfg, dev) if rank == 0 and legs else None
+    batch = batch_c5(P, mf, cfg, dev, rank=rank) if legs else None
+    blake3 = blake3_leg(P, mf, dev, peak) if rank == 0 and legs and world == 1 else None
+    c5 = dp = None
+    if world > 1 and legs:
+        # C5 across the ranks: 8 sequences each, hashes vs the goldens
+        n_ok = allreduce(float(batch.get("golden_hash_matches", 0) or 0), dist.ReduceOp.SUM)
+        n_chk = allreduce(float(batch.get("golden_checked", 0) or 0), dist.ReduceOp.SUM)
+        t_max = allreduce(float(batch.get("seconds", 0) or 0), dist.ReduceOp.MAX)
+        c5 = {"workload": f"C5: {8 * world} independent sequences, 8 per GPU, P=16, N=128",
+              "tokens_per_s": 8 * world * 128 / t_max if t_max else None, "seconds_max_over_ranks": t_max,
+              "golden_checked": int(n_chk), "golden_hash_matches": int(n_ok), "mismatches": int(n_chk - n_ok),
+              "rank0": batch}
+        # weak-scaling replicas: every rank its own sequence on the single-GPU kernel
+        sess = P.InferenceSession(mf, P.EngineOptions(device=dev))
+        pseed = PROMPT_SEED if rank == 0 else 1000 + rank
+        sess.begin(P.prompt_from_seed(pseed, cfg.vocab, PROMPT_LEN), args.warmup + args.steps)
+        sess.prefill()
+        sess.decode(args.warmup)
+        sess.sync()
+        barrier()
+        dms = allreduce(sess.time_decode(args.steps), dist.ReduceOp.MAX)
+        dp = {"workload": f"{world} independent batch-1 sequences, one per GPU (persistent kernel)",
+              "tokens_per_s": world * args.steps / (dms / 1e3), "ms_per_step": dms / args.steps}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "int64",
             "data": "synthetic (gen_toy_model seed 7: uniform int8 weights, Q16 scales; ChaCha20 prompt)",
-            "config": {"workload": "C2: Llama-2-7B-shaped int8/Q16 model, batch-1 greedy decode",
-                       "model": "llama2-7b-shaped-int", "layers": cfg.n_layers,
-                       "d_model": cfg.d_model, "d_ffn": cfg.d_ffn, "vocab": cfg.vocab,
-                       "seed": MODEL_SEED, "prompt_seed": PROMPT_SEED, "prompt_len": PROMPT_LEN,
-                       "global_batch": world, "parallelism": f"dp{world} (independent sequences)",
-                       "l2": "weights 6.6 GB/step > 126 MB L2 (no flush needed)",
-                       "weight_hash_ok": wh_ok, "model_gen_s": round(gen_s, 1)},
+            "config": config_dict(world, {"weight_hash_ok": wh_ok, "model_gen_s": round(gen_s, 1)}),
+            "tokens_match_c2_golden": tokens_ok,
             "e2e": e2e,
-            "gpu_launches": launches_per_step,  # one persistent launch runs all K steps
-            # dominant kernel: the persistent decode kernel (99.8% of GPU time,
-            # profiles/r01_bench_launches.csv); one decode step = 6.62 GB of
-            # algorithmic weight bytes, timed with CUDA events on its stream
+            "gpu_launches": gpu_launches,
             "roofline": {"bound": "hbm", "achieved": step_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": step_gbs / peak, "traffic": traffic,
-                         "kernel": "decode_persistent_kernel (per decode step)",
-                         "bytes_per_step": step_bytes, "ms_per_step": per_step_ms,
+                         "frac": step_gbs / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": kernel, "bytes_per_step_per_gpu": gpu_bytes, "ms_per_step": per_step_ms,
                          "peak_kind": peak_kind},
-            "stages": kern,
-            "clocks": clk.summary(),
+            "clocks": dict(clk.summary(), whole_run=clk_all.summary()),
             "cpu_baseline": base,
             "prefill": prefill,
-            "batch": batch,
+            "batch": batch if world == 1 else None,
+            "c5": c5,
+            "dp": dp,
             "blake3": blake3,
             "tokens_head": toks[:8],
         }
+        line.update(extra)
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
@@ -435,6 +547,7 @@ def main():
     ap.add_argument("--no-prefill", action="store_true", help="skip the C3 prefill and C5 batch measurements")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tp", action="store_true", help="the tensor-parallel (NCCL) path even at N = 1 (tests)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank, world, local = env_rank()

@@ -99,7 +99,39 @@ void run(int grid, int variant = 0) {
     cudaFree(d);
 }
 
-int main() {
+// Whole-GPU dense kind::i8 rate: one CTA per SM issuing N = 192 MMAs back to
+// back (operands resident), CUDA-event timed: the roofline denominator of the
+// tensor-core prefill (bench.py reads profiles/r02_mma_rate.json).
+void peak() {
+    int dev = 0, sms = 0, clk = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+    const int smem = 4 * STG + 1024;
+    cudaFuncSetAttribute(rate_kernel<192, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    unsigned long long* d;
+    cudaMalloc(&d, 8);
+    const int R = 1 << 16;
+    rate_kernel<192, false><<<sms, 128, smem>>>(R, d, 0);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    rate_kernel<192, false><<<sms, 128, smem>>>(R, d, 0);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = 2.0 * sms * double(R) * 128 * 192 * 32;
+    printf("{\"i8_tops\": %.1f, \"sms\": %d, \"ms\": %.3f, \"N\": 192, \"mmas_per_sm\": %d, "
+           "\"max_clock_mhz\": %d, \"err\": \"%s\"}\n",
+           ops / (ms * 1e-3) / 1e12, sms, ms, R, clk / 1000, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main(int argc, char** argv) {
+    if (argc > 1 && argv[1][0] == 'p') {
+        peak();
+        return 0;
+    }
     for (int v : {0, 1, 3, 5, 7, 13, 15}) {
         run<16, false>(1, v);
         run<48, false>(1, v);
