@@ -215,6 +215,10 @@ dimg_status dimg_session_time_kernel(dimg_session* s, int which, uint32_t n, flo
  * attention stage. cap stages recorded. */
 #define DIMG_TRACE_WORDS 32
 dimg_status dimg_session_trace(dimg_session* s, uint32_t n_steps, uint64_t* out, uint32_t cap);
+/* Hand-off skew: n decode steps with every CTA stamping %globaltimer at the end
+ * of each GEMV stage's prologue and of its chunk loop:
+ * out[(i * grid + cta) * 2 + {0, 1}] for the first cap stages (grid = SMs). */
+dimg_status dimg_session_trace_all(dimg_session* s, uint32_t n_steps, uint64_t* out, uint32_t cap);
 /* Kernel launches per decode step / per prefill step (for the bench claim). */
 dimg_status dimg_session_launches(const dimg_session* s, uint32_t* per_decode,
                                   uint32_t* per_prefill);

@@ -106,6 +106,7 @@ def _load():
         "dimg_session_time_kernel": ([vp, C.c_int, C.c_uint32, C.POINTER(C.c_float), u64p], C.c_int),
         "dimg_session_stats": ([vp, u64p], C.c_int),
         "dimg_session_trace": ([vp, C.c_uint32, u64p, C.c_uint32], C.c_int),
+        "dimg_session_trace_all": ([vp, C.c_uint32, u64p, C.c_uint32], C.c_int),
         "dimg_nccl_unique_id": ([u8p], C.c_int),
         "dimg_tp_create": ([C.c_int, C.POINTER(ModelDesc), C.c_int, C.c_int, C.c_int, u8p, C.c_uint32, pp],
                            C.c_int),

@@ -650,11 +650,13 @@ PkArgs pk_args(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
 }
 
 void launch_pk(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, uint32_t n_steps,
-               uint32_t n_prefill, unsigned long long* trace = nullptr, uint32_t trace_cap = 0) {
+               uint32_t n_prefill, unsigned long long* trace = nullptr, uint32_t trace_cap = 0,
+               unsigned long long* trace_all = nullptr) {
     if (n_steps == 0) return;
     PkArgs a = pk_args(s, stages, n_layer_stages, n_steps, n_prefill);
     a.trace = trace;
     a.trace_cap = trace_cap;
+    a.trace_all = trace_all;
 
     // tags of the attention score exchange: unique per attention stage, never 0
     const uint64_t n_attn = uint64_t(n_steps) * s.m->L;
@@ -1692,6 +1694,25 @@ dimg_status dimg_session_trace(dimg_session* s, uint32_t n_steps, uint64_t* out,
         launch_pk(*s, s->stages, n_layer_stages(*s), n_steps, 0, d, cap);
         s->len += n_steps;
         CK(cudaMemcpyAsync(out, d, size_t(cap) * DIMG_TRACE_WORDS * 8, cudaMemcpyDeviceToHost, s->stream));
+        check_ctl_err(*s);
+    })
+}
+
+dimg_status dimg_session_trace_all(dimg_session* s, uint32_t n_steps, uint64_t* out, uint32_t cap) {
+    // n decode steps with EVERY CTA stamping %globaltimer at the end of each
+    // GEMV stage's prologue and chunk loop: out[(i * grid + cta) * 2 + 0/1]
+    // for the first cap stages (the hand-off skew between CTAs)
+    DIMG_API_GUARD({
+        if (uint64_t(s->len) + n_steps > s->m->cfg.max_ctx)
+            fail(DIMG_ECTX, "decode: context overflow");
+        const size_t n = size_t(cap) * s->grid * 2;
+        unsigned long long* d = s->mem.alloc<unsigned long long>(n);
+        unsigned long long* d0 = s->mem.alloc<unsigned long long>(size_t(cap) * DIMG_TRACE_WORDS);
+        CK(cudaMemsetAsync(d, 0, n * 8, s->stream));
+        CK(cudaMemsetAsync(d0, 0, size_t(cap) * DIMG_TRACE_WORDS * 8, s->stream));
+        launch_pk(*s, s->stages, n_layer_stages(*s), n_steps, 0, d0, cap, d);
+        s->len += n_steps;
+        CK(cudaMemcpyAsync(out, d, n * 8, cudaMemcpyDeviceToHost, s->stream));
         check_ctl_err(*s);
     })
 }

@@ -111,6 +111,7 @@ struct PkArgs {
     int32_t* kc32;            // int32 mirror of kc / vc (same layout), read while kvwide is clear
     int32_t* vc32;
     uint32_t* kvwide;         // [L][H] some cached K/V value of the head needs more than 32 bits
+    unsigned long long* trace_all;  // optional: [stage_seq][grid][2] every CTA's prologue end / chunk-loop end
 };
 
 // Scheduling constants, held in registers (never address kernel params or
@@ -539,7 +540,7 @@ __device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_un
         const int64_t r_inv = s_r;
         if (tr) tr[6] = clock64();
         int fits = 1;
-#pragma unroll 4
+#pragma unroll 1
         for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
             const int4 e4 = *reinterpret_cast<const int4*>(xs32 + 4 * w);
             const int32_t xs[4] = {e4.x, e4.y, e4.z, e4.w};
@@ -766,7 +767,7 @@ __device__ __noinline__ int prologue_norm_words(uint32_t K, uint32_t Kp, bool ga
     const int64_t r_inv = s_r2;  // <= 2^24: 32 x 32-bit products
     int fits = 1;
     const int64_t* gk = gamma_unit ? nullptr : gamma;  // mul16(v, ONE) == v: unit gains skipped
-#pragma unroll 4
+#pragma unroll 1
     for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
         const int4 e4 = *reinterpret_cast<const int4*>(xs32 + 4 * w);
         const int32_t xs[4] = {e4.x, e4.y, e4.z, e4.w};  // padding slots hold 0
@@ -1547,6 +1548,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 // is done once this stage's inputs are complete
                 if (st.ssq_clear && blockIdx.x == 0 && threadIdx.x == 0) *st.ssq_clear = 0;
                 if (tr) tr[1] = globaltimer();
+                if (a.trace_all && threadIdx.x == 0 && nseq - 1 < a.trace_cap)
+                    a.trace_all[(size_t(nseq - 1) * gridDim.x + blockIdx.x) * 2] = globaltimer();
                 GemvRT g_;
                 g_.epi = st.epi; g_.rows = st.rows; g_.Kp = st.Kp; g_.n_groups = st.n_groups;
                 g_.n_segs = st.n_segs; g_.tag7 = tag7_of(a.tag_base + attn_epoch); g_.y = st.y;
@@ -1571,6 +1574,8 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 if (L == 3) run_gemv<3>(sc, p, g_, planes, tag, best_v, best_i);
                 else run_gemv_wide(sc, p, g_, planes, tag, best_v, best_i);
                 if (tr) tr[2] = globaltimer();
+                if (a.trace_all && threadIdx.x == 0 && nseq - 1 < a.trace_cap)
+                    a.trace_all[(size_t(nseq - 1) * gridDim.x + blockIdx.x) * 2 + 1] = globaltimer();
                 if (st.epi == EPI_ARGMAX) {
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {

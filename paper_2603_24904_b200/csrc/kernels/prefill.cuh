@@ -310,12 +310,16 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
     }
 
     // ---- PV (kernels.cpp:153-159): lane owns dims lane * DPL ... + DPL - 1
-    int64_t f[PA_QW][DPL];
-    uint32_t r[PA_QW][DPL];
+    // floor(p v / 2^16) = p vh + floor(p vl / 2^16) with v = vh 2^16 + vl,
+    // vl in [0, 2^16): p <= 2^16 makes p vl < 2^32 (one 32-bit product), and
+    // sum_t p_t vh_t is within int32 (sum p <= 2^16, |vh| <= 2^15). Two 32-bit
+    // multiplies per product, no 64-bit arithmetic.
+    int32_t fh[PA_QW][DPL];
+    uint32_t fl[PA_QW][DPL];
 #pragma unroll
     for (int u = 0; u < PA_QW; ++u)
 #pragma unroll
-        for (int z = 0; z < DPL; ++z) f[u][z] = 0, r[u][z] = 0;
+        for (int z = 0; z < DPL; ++z) fh[u][z] = 0, fl[u][z] = 0;
     const uint32_t jl = lane * DPL;  // first dim of this lane
     const bool lane_on = jl < dh;
     const int32_t* Sc = strips + (size_t(h) * gridDim.y + blockIdx.y) * PA_Q * ld;  // the CTA's rows
@@ -365,15 +369,15 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
                     for (int z = 0; z < DPL; ++z) vv[z] = Vs[pp * dh + jl + z];
                 }
 #pragma unroll
-                for (int u = 0; u < PA_QW; ++u)
+                for (int z = 0; z < DPL; ++z) {
+                    const int32_t vh = vv[z] >> 16;
+                    const uint32_t vl = uint32_t(vv[z]) & 0xFFFFu;
 #pragma unroll
-                    for (int z = 0; z < DPL; ++z) {
-                        // one wide product (the multiply pipe is the bound), its low
-                        // 16 bits summed separately on the ALU pipe
-                        const int64_t prod = int64_t(pq[u]) * vv[z];
-                        f[u][z] += prod;
-                        r[u][z] += uint32_t(prod) & 0xFFFFu;
+                    for (int u = 0; u < PA_QW; ++u) {
+                        fh[u][z] += pq[u] * vh;
+                        fl[u][z] += (uint32_t(pq[u]) * vl) >> 16;
                     }
+                }
             }
         }
         __syncthreads();  // chunk c and Ps consumed
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
 #pragma unroll
             for (int z = 0; z < DPL; ++z) {
                 const uint32_t j = jl + z;
-                if (j < dh) pf_put_limbs(planes + size_t(t) * ldp + h * dh + j, plane, (f[u][z] - int64_t(r[u][z])) >> 16, wide);
+                if (j < dh) pf_put_limbs(planes + size_t(t) * ldp + h * dh + j, plane, int64_t(fh[u][z]) + fl[u][z], wide);
             }
         }
     }

@@ -183,7 +183,19 @@ int main() {
         printf("ldg  LDG.128 x8 unroll                : %7.1f GB/s\n", bytes / ms / 1e6);
     }
     struct Cfg { uint32_t S, D, W; };
-    std::vector<Cfg> cfgs = {{8192, 2, 8}, {8192, 3, 8}, {16384, 2, 4}, {16384, 1, 8}, {4096, 4, 8},
+    {  // L2-resident source: the same ring over a 48 MB buffer streamed repeatedly
+        const size_t small = size_t(48) << 20;
+        for (Cfg c : std::vector<Cfg>{{6144, 3, 8}, {8192, 2, 8}, {6144, 4, 8}, {4096, 4, 8}}) {
+            size_t smem = size_t(c.W) * c.D * c.S + c.W * c.D * 8 + 6144;
+            CK(cudaFuncSetAttribute(ring_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            CK(cudaFuncSetAttribute(ring_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            float m0 = time_it([&] { ring_kernel<false><<<sms, c.W * 32, smem>>>(buf, small, c.S, c.D, sink); });
+            float m1 = time_it([&] { ring_kernel<true><<<sms, c.W * 32, smem>>>(buf, small, c.S, c.D, sink); });
+            printf("L2 ring S=%5u D=%u warps=%2u (%3zu KB/SM) : copy %7.1f GB/s   +dp4a %7.1f GB/s\n", c.S, c.D, c.W,
+                   size_t(c.W) * c.D * c.S / 1024, small / m0 / 1e6, small / m1 / 1e6);
+        }
+    }
+    std::vector<Cfg> cfgs = {{6144, 3, 8}, {8192, 2, 8}, {8192, 3, 8}, {16384, 2, 4}, {16384, 1, 8}, {4096, 4, 8},
                              {8192, 2, 12}, {16384, 2, 6}, {32768, 1, 6}, {4096, 2, 16}, {8192, 1, 16}};
     for (auto c : cfgs) {
         size_t smem = size_t(c.W) * c.D * c.S + c.W * c.D * 8 + 6144;
