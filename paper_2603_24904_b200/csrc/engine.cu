@@ -630,6 +630,8 @@ PkArgs pk_args(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     a.kv_layer_stride = size_t(m.H) * m.cfg.max_ctx * m.dh;
     // CTAs per head: split the head's dims over the SMs the heads leave idle
     a.attn_parts = std::max(1u, std::min(s.grid / m.H, std::max(1u, m.dh / 8)));
+    if (const char* e = std::getenv("DIMG_ATTN_PARTS"))  // experiments: CTAs per head
+        a.attn_parts = std::max(1u, std::min(a.attn_parts, uint32_t(std::strtoul(e, nullptr, 0))));
     {
         auto log2_or = [](uint32_t x) { return x && !(x & (x - 1)) ? int32_t(__builtin_ctz(x)) : -1; };
         uint32_t dpp = (m.dh + a.attn_parts - 1) / a.attn_parts;
