@@ -202,7 +202,7 @@ def test_repeat_and_cached_vs_recompute(P, oracle):
     from oracle.pyoracle import Config
     cfg = P.ModelConfig(2, 16, 2, 32, 32, 64)
     m = P.gen_toy_model(7, cfg)
-    hashes = {P.generate_greedy(m, [3, 1, 4], 12).output_hash for _ in range(50)}
+    hashes = {P.generate_greedy(m, [3, 1, 4], 12).output_hash for _ in range(100)}
     assert len(hashes) == 1
     # KV-cached decode equals full recomputation (test_engine.cpp:113-126)
     m9 = P.gen_toy_model(9, cfg)
@@ -383,3 +383,27 @@ def test_tensor_core_prefill_and_batch_repeat(P, oracle, monkeypatch):
         res, path = P.generate_greedy_batch(m, prompts, 6)
         assert path == "tensor_cores"
         assert [r.token_ids for r in res] == want, rep
+
+
+def test_partition_invariance(P, golden_models, monkeypatch):
+    """The reference's thread/chunk invariance (proj/tests/test_engine.cpp:87-111,
+    test_kernels.cpp:79-97) on the GPU's own partitions: the attention split
+    into 1, 2 or 4 CTAs per head, the decode kernel vs the tensor-core prefill
+    vs the tensor-parallel shards -- identical tokens and logits every time,
+    100 repeats of the default path."""
+    g = golden_models["medium"]
+    m = _model_for(P, g)
+    want = g["tokens"]
+    for parts in ("1", "2", "4"):
+        monkeypatch.setenv("DIMG_ATTN_PARTS", parts)
+        for pf in ("1", "2"):
+            monkeypatch.setenv("DIMG_PREFILL", pf)
+            res = P.InferenceSession(m, keep_logits_cap=g["max_new"]).generate_greedy(g["prompt"], g["max_new"],
+                                                                                     keep_logits=True)
+            assert res.token_ids == want, (parts, pf)
+            assert _digest(P, res.logits) == g["logits_digest"], (parts, pf)
+    monkeypatch.delenv("DIMG_ATTN_PARTS")
+    monkeypatch.delenv("DIMG_PREFILL")
+    s = P.InferenceSession(m)
+    hashes = {s.generate_greedy(g["prompt"], g["max_new"]).output_hash.hex() for _ in range(100)}
+    assert hashes == {g["output_hash"]}
