@@ -95,3 +95,26 @@ def test_7b_c3_prefill_on_tensor_cores(P, golden_7b, model7b):
     assert res.output_hash.hex() == g["output_hash"]
     if g.get("logits_digest"):
         assert _digest(P, res.logits) == g["logits_digest"]
+
+
+def test_7b_c5_sharded_as_on_8_gpus(P, golden_7b, model7b):
+    """C5 as the 8-GPU run deals it (parallel.sequence_shard: 8 sequences per
+    rank, each rank one batch call; proj/tests/acceptance.cpp:92-127 deals
+    prompts to workers the same way): every shard with goldens, every
+    per-sequence hash equal to the oracle's single-sequence golden."""
+    from paper_2603_24904_b200.parallel import sequence_shard
+    have = {int(k[3:]) for k in golden_7b if k.startswith("c5_")}
+    if len(have) < 16:
+        pytest.skip("c5 goldens not generated")
+    checked = 0
+    for rank in range(8):
+        ids = sequence_shard(64, 8, rank)
+        if not set(ids) <= have:
+            continue
+        gs = [golden_7b[f"c5_{i}"] for i in ids]
+        prompts = [P.prompt_from_seed(g["prompt_seed"], g["config"][4], g["P"]) for g in gs]
+        res, path = P.generate_greedy_batch(model7b, prompts, gs[0]["max_new"])
+        assert path == "tensor_cores"
+        assert [r.output_hash.hex() for r in res] == [g["output_hash"] for g in gs], rank
+        checked += len(ids)
+    assert checked >= 16
