@@ -13,6 +13,7 @@
  */
 #include "dim_oracle.h"
 
+#include <stdio.h>
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>

@@ -11,7 +11,8 @@ import os
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdimg.so")
+# DIMG_LIB: an instrumented experiment build (tools/); the product is libdimg.so
+LIB_PATH = os.environ.get("DIMG_LIB") or os.path.join(HERE, "libdimg.so")
 
 u8p = C.POINTER(C.c_uint8)
 i8p = C.POINTER(C.c_int8)

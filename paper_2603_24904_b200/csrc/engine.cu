@@ -1700,6 +1700,13 @@ dimg_status dimg_session_trace(dimg_session* s, uint32_t n_steps, uint64_t* out,
     })
 }
 
+#ifdef DIMG_CHUNK_TRACE
+// Experiment build only: copies the per-chunk ring-wait log (g_ct) out.
+extern "C" int dimg_debug_chunk_trace(uint64_t* out) {
+    return cudaMemcpyFromSymbol(out, dimg::dev::g_ct, sizeof(dimg::dev::g_ct)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
 dimg_status dimg_session_trace_all(dimg_session* s, uint32_t n_steps, uint64_t* out, uint32_t cap) {
     // n decode steps with EVERY CTA stamping %globaltimer at the end of each
     // GEMV stage's prologue and chunk loop: out[(i * grid + cta) * 2 + 0/1]

@@ -374,7 +374,17 @@ __device__ __forceinline__ void fetch_issue(const Fetch& f, uint8_t* slot, uint6
     bulk_g2s(slot, fetch_src(f), fetch_bytes(f), bar);
 }
 
+#ifdef DIMG_CHUNK_TRACE
+// Experiment build only (tools/chunk_trace.py): warp 0 of every CTA logs
+// clock64 around each ring wait, plus stage markers.
+constexpr int CT_MAX = 4096;
+__device__ unsigned long long g_ct[148][CT_MAX][2];
+#endif
+
 struct Pipe {
+#ifdef DIMG_CHUNK_TRACE
+    uint32_t ctn;
+#endif
     uint8_t* slots;     // this warp's ring
     uint64_t* bars;
     uint32_t slot;      // slot of the next chunk to consume
@@ -385,7 +395,17 @@ struct Pipe {
 
 // Waits for the next chunk of this warp; returns its slot.
 __device__ __forceinline__ const uint8_t* pipe_wait(Pipe& p) {
+#ifdef DIMG_CHUNK_TRACE
+    const unsigned long long c0 = clock64();
     mbar_wait(&p.bars[p.slot], p.phase);
+    if (threadIdx.x == 0 && blockIdx.x < 148 && p.ctn < CT_MAX) {
+        g_ct[blockIdx.x][p.ctn][0] = c0;
+        g_ct[blockIdx.x][p.ctn][1] = clock64();
+        ++p.ctn;
+    }
+#else
+    mbar_wait(&p.bars[p.slot], p.phase);
+#endif
     return p.slots + p.slot * PK_SLOT;
 }
 
@@ -1463,6 +1483,9 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
     p.slot = 0;
     p.phase = 0;
     p.depth = depth;
+#ifdef DIMG_CHUNK_TRACE
+    p.ctn = 0;
+#endif
     p.f.step = 0;
     p.f.stage = 0;
     p.f.done = sc.n_steps == 0;
@@ -1498,6 +1521,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 tr[8] = clock64();
                 tr[0] = globaltimer();
             }
+#ifdef DIMG_CHUNK_TRACE
+            if (threadIdx.x == 0 && blockIdx.x < 148 && p.ctn < CT_MAX) {
+                g_ct[blockIdx.x][p.ctn][0] = clock64();
+                g_ct[blockIdx.x][p.ctn][1] = (1ull << 63) | (uint64_t(si) << 8) | 0;
+                ++p.ctn;
+            }
+#endif
             if (st.kind == SK_ATTN) {
                 const uint32_t np = a.attn_parts;
                 ++attn_epoch;
@@ -1548,6 +1578,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 // is done once this stage's inputs are complete
                 if (st.ssq_clear && blockIdx.x == 0 && threadIdx.x == 0) *st.ssq_clear = 0;
                 if (tr) tr[1] = globaltimer();
+#ifdef DIMG_CHUNK_TRACE
+                if (threadIdx.x == 0 && blockIdx.x < 148 && p.ctn < CT_MAX) {
+                    g_ct[blockIdx.x][p.ctn][0] = clock64();
+                    g_ct[blockIdx.x][p.ctn][1] = (1ull << 63) | (uint64_t(si) << 8) | 1;
+                    ++p.ctn;
+                }
+#endif
                 if (a.trace_all && threadIdx.x == 0 && nseq - 1 < a.trace_cap)
                     a.trace_all[(size_t(nseq - 1) * gridDim.x + blockIdx.x) * 2] = globaltimer();
                 GemvRT g_;
@@ -1574,6 +1611,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 if (L == 3) run_gemv<3>(sc, p, g_, planes, tag, best_v, best_i);
                 else run_gemv_wide(sc, p, g_, planes, tag, best_v, best_i);
                 if (tr) tr[2] = globaltimer();
+#ifdef DIMG_CHUNK_TRACE
+                if (threadIdx.x == 0 && blockIdx.x < 148 && p.ctn < CT_MAX) {
+                    g_ct[blockIdx.x][p.ctn][0] = clock64();
+                    g_ct[blockIdx.x][p.ctn][1] = (1ull << 63) | (uint64_t(si) << 8) | 2;
+                    ++p.ctn;
+                }
+#endif
                 if (a.trace_all && threadIdx.x == 0 && nseq - 1 < a.trace_cap)
                     a.trace_all[(size_t(nseq - 1) * gridDim.x + blockIdx.x) * 2 + 1] = globaltimer();
                 if (st.epi == EPI_ARGMAX) {
