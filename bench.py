@@ -79,30 +79,75 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def _pci_bus_id(cuda_index):
+    """PCI bus id of CUDA device `cuda_index` (NVML numbers GPUs differently
+    when CUDA_VISIBLE_DEVICES is set)."""
+    import ctypes
+    cu = ctypes.CDLL("libcuda.so.1")
+    cu.cuInit(0)
+    buf = ctypes.create_string_buffer(64)
+    if cu.cuDeviceGetPCIBusId(buf, 64, cuda_index) != 0:
+        return None
+    return buf.value.decode()
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML
+    every ~2 ms from a thread (a 35 ms decode region still gets ~15
+    samples); nvidia-smi (~50 ms per call) if NVML is unavailable."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, set of reason names)
+        self.source = None
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            bus = _pci_bus_id(index)
+            h = nv.nvmlDeviceGetHandleByPciBusId(bus) if bus else nv.nvmlDeviceGetHandleByIndex(index)
+            self._nv, self._h = nv, h
+            self._bits = [(nv.nvmlClocksEventReasonHwSlowdown, "hw_slowdown"),
+                          (nv.nvmlClocksEventReasonHwThermalSlowdown, "hw_thermal_slowdown"),
+                          (nv.nvmlClocksEventReasonSwThermalSlowdown, "sw_thermal_slowdown"),
+                          (nv.nvmlClocksEventReasonSwPowerCap, "sw_power_cap")]
+            self._max = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.source = "nvml"
+        except Exception:
+            self._nv = None
+            self.source = "nvidia-smi"
+
+    def _sample_nvml(self):
+        nv, h = self._nv, self._h
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.rows.append((float(sm), float(self._max), {n for b, n in self._bits if r & b}))
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True,
+                             text=True, timeout=5).stdout.strip()
+        if out:
+            r = [c.strip() for c in out.split(",")]
+            if r[1].replace(".", "").isdigit():
+                mx = float(r[2]) if r[2].replace(".", "").isdigit() else None
+                self.rows.append((float(r[1]), mx, {self.NAMES[i] for i in range(4)
+                                                    if len(r) > 5 + i and r[5 + i].lower() == "active"}))
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                self._sample_nvml() if self._nv else self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.05)
+            self._stop.wait(0.002 if self._nv else 0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -112,17 +157,20 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if not self.rows:  # the region was shorter than one sample: take one now
+            try:
+                self._sample_nvml() if self._nv else self._sample_smi()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
-        mx = max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = sorted(r[0] for r in self.rows)
+        mx = max((r[1] for r in self.rows if r[1]), default=None)
+        reasons = sorted(set().union(*(r[2] for r in self.rows)))
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows), "sm_mhz_min": sm[0], "source": self.source}
 
 
 # --------------------------------------------------------------------------

@@ -139,6 +139,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
+    return r;
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -419,7 +425,9 @@ __device__ __forceinline__ void pipe_release(const Sched& sc, Pipe& p) {
     __syncwarp();
     if (!p.f.done) {
         if ((threadIdx.x & 31) == 0) {
+#ifndef DIMG_EXP_NOFENCE
             fence_proxy_async();
+#endif
             fetch_issue(p.f, p.slots + sl * PK_SLOT, &p.bars[sl]);
         }
         fetch_advance(sc, p.f);
@@ -849,6 +857,7 @@ __device__ __forceinline__ void group_dot(const Sched& sc, Pipe& p, uint32_t Kp,
                                           int64_t& scale) {
     const int lane = threadIdx.x & 31;
     const uint32_t Kw = Kp / 4;
+    const uint32_t planes_s = L == 3 ? smem_u32(planes) : 0u;  // the 3-limb planes are in shared memory
     int32_t acc[PK_ROWS][L];
 #pragma unroll
     for (int r = 0; r < PK_ROWS; ++r)
@@ -861,7 +870,10 @@ __device__ __forceinline__ void group_dot(const Sched& sc, Pipe& p, uint32_t Kp,
         for (uint32_t c = lane * 16; c < w; c += 512) {
             uint4 xl[L];
 #pragma unroll
-            for (int k = 0; k < L; ++k) xl[k] = *reinterpret_cast<const uint4*>(planes + k * Kw + (k0 + c) / 4);
+            for (int k = 0; k < L; ++k) {
+                if constexpr (L == 3) xl[k] = lds128(planes_s + 4 * (k * Kw + (k0 + c) / 4));  // shared memory
+                else xl[k] = *reinterpret_cast<const uint4*>(planes + k * Kw + (k0 + c) / 4);  // wide: global scratch
+            }
 #pragma unroll
             for (int r = 0; r < PK_ROWS; ++r) {
                 const int4 wv = *reinterpret_cast<const int4*>(slot + r * w + c);

@@ -85,3 +85,30 @@ for k, v in tot.items():
     if v:
         a = np.array(v).mean(0) / ghz / 1e3
         print(f"  {k:6s} {a[0]:7.2f} {a[1]:7.2f} {a[2]:7.2f}")
+
+# per-chunk timeline of warp 0 in a few CTAs for the chosen layer: the gap
+# between one wait's end and the next wait's start is the chunk's compute
+# (+ release / epilogue at group ends)
+np.save("gpurun_out/ct_raw.npy", t)
+for cta in (0, 37, 74, 111):
+    ev = t[cta]
+    lines = []
+    inside = False
+    prev_end = None
+    for c0, c1 in ev:
+        c0 = int(c0); c1 = int(c1)
+        if c0 == 0:
+            break
+        if c1 >> 63:
+            si, kind = (c1 >> 8) & 0xFFFF, c1 & 0xFF
+            inside = si // 5 == layer
+            if inside:
+                lines.append(f"  [{names[si % 5]} marker {kind} @ {c0}]")
+            prev_end = c0 if kind == 1 else None
+            continue
+        if inside:
+            comp = (c0 - prev_end) if prev_end else -1
+            lines.append(f"    compute-before {comp:6d} clk  wait {c1 - c0:6d} clk")
+        prev_end = c1
+    print(f"CTA {cta}:")
+    print("\n".join(lines))
