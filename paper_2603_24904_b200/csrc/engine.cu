@@ -34,6 +34,7 @@
 #include "kernels/tc_gemm.cuh"
 #include "kernels/prefill.cuh"
 #include "kernels/pf_scores.cuh"
+#include "kernels/pf_pv.cuh"
 #include "kernels/batch.cuh"
 #include "kernels/blake3.cuh"
 #include "kernels/sample.cuh"
@@ -114,11 +115,13 @@ DevCtx& dev_ctx(int device) {
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(prop.sharedMemPerBlockOptin - fa.sharedSizeBytes)));
         };
-        set(pf_attn_kernel<1>);
-        set(pf_attn_kernel<2>);
-        set(pf_attn_kernel<4>);
-        set(pf_attn_kernel<8>);
+        set(pf_attn_kernel<1, false>);
+        set(pf_attn_kernel<2, false>);
+        set(pf_attn_kernel<4, false>);
+        set(pf_attn_kernel<8, false>);
+        set(pf_attn_kernel<4, true>);
         CK(cudaFuncSetAttribute(pf_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pf_scores_smem())));
+        CK(cudaFuncSetAttribute(pf_pv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pf_pv_smem())));
         set(bd_attn_kernel);
     }
     set_gemv_attrs<EPI_STORE, MODE_EMBED>();
@@ -454,6 +457,9 @@ struct PrefillWs {
     // split-K scratch possibly nonzero, so the next prefill re-zeroes it
     bool dirty = false;
     int8_t* kdig = nullptr;          // key digit planes [H][4][kdig_pad][128] (tensor-core scores, dh 128)
+    int8_t* vh = nullptr;            // V >> 16 planes [H][128 dims][kdig_pad positions] (tensor-core PV)
+    int32_t* fl = nullptr;           // sum_p floor(P vl / 2^16) [H][cap][128] (tensor-core PV)
+    CUtensorMap tm_vh;
     uint32_t* kd4 = nullptr;         // [layers]: some key of the layer needs the 4th digit
     uint32_t kdig_pad = 0;
     CUtensorMap tm_kdig;
@@ -777,6 +783,9 @@ void ensure_prefill_ws(dimg_session& s, uint32_t n) {
         w.kdig_pad = (w.cap + PS_M - 1) / PS_M * PS_M;
         w.kdig = s.mem.alloc<int8_t>(size_t(m.H) * PS_KD * w.kdig_pad * PS_DH);
         w.tm_kdig = tmap_bytes(w.kdig, PS_DH, size_t(m.H) * PS_KD * w.kdig_pad, PS_DH, PS_M);
+        w.vh = s.mem.alloc<int8_t>(size_t(m.H) * PV_M * w.kdig_pad);
+        w.tm_vh = tmap_bytes(w.vh, w.kdig_pad, size_t(m.H) * PV_M, w.kdig_pad, PV_M);
+        w.fl = s.mem.alloc<int32_t>(size_t(m.H) * w.cap * PV_M);
         if (!w.kd4) w.kd4 = s.mem.alloc<uint32_t>(m.L);
     }
     w.tm_ph_s = tmap_bytes(w.ph, m.F, size_t(3) * w.cap_pad, m.Kf, TG_BN_SMALL);
@@ -794,10 +803,10 @@ void ensure_prefill_ws(dimg_session& s, uint32_t n) {
 template <class... A>
 void launch_pf_attn(uint32_t dh, dim3 grid, size_t smem, cudaStream_t st, A... args) {
     const uint32_t dpl = (dh + 31) / 32;
-    if (dpl <= 1) launch_k(true, pf_attn_kernel<1>, grid, PA_THREADS, smem, st, args...);
-    else if (dpl <= 2) launch_k(true, pf_attn_kernel<2>, grid, PA_THREADS, smem, st, args...);
-    else if (dpl <= 4) launch_k(true, pf_attn_kernel<4>, grid, PA_THREADS, smem, st, args...);
-    else launch_k(true, pf_attn_kernel<8>, grid, PA_THREADS, smem, st, args...);  // dh <= 256 (tc_prefill_ok)
+    if (dpl <= 1) launch_k(true, pf_attn_kernel<1, false>, grid, PA_THREADS, smem, st, args..., (int32_t*)nullptr);
+    else if (dpl <= 2) launch_k(true, pf_attn_kernel<2, false>, grid, PA_THREADS, smem, st, args..., (int32_t*)nullptr);
+    else if (dpl <= 4) launch_k(true, pf_attn_kernel<4, false>, grid, PA_THREADS, smem, st, args..., (int32_t*)nullptr);
+    else launch_k(true, pf_attn_kernel<8, false>, grid, PA_THREADS, smem, st, args..., (int32_t*)nullptr);  // dh <= 256
 }
 
 // Positions 0..n-1 of the prompt through every layer on the tensor cores;
@@ -858,6 +867,10 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
     // DIMG_PF_KD4=1 forces the 4th key digit plane (tests of that path)
     const char* kd4_env = std::getenv("DIMG_PF_KD4");
     if (tc_scores) CK(cudaMemsetAsync(w.kd4, kd4_env && std::atoi(kd4_env) ? 1 : 0, size_t(m.L) * 4, st));
+    // PV's linear half on the tensor cores when dh = 128 (pf_pv.cuh);
+    // DIMG_PF_PV=0 keeps all of PV on the CUDA cores
+    const char* pv_env = std::getenv("DIMG_PF_PV");
+    const bool tc_pv = w.vh && dh == PV_M && (!pv_env || std::atoi(pv_env) != 0);
     for (uint32_t l = 0; l < m.L; ++l) {
         const auto& lw = m.layers[l];
         launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int64_t*)w.x, D, (const int64_t*)lw.attn_norm,
@@ -873,10 +886,24 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
             launch_k(true, pf_scores_kernel, dim3(H, (n + PS_Q - 1) / PS_Q), PS_THREADS, pf_scores_smem(), st,
                      w.tm_kdig, (const int64_t*)w.qkv, n, w.kdig_pad, D, m.inv_scale, w.strips, w.wide,
                      (const uint32_t*)(w.kd4 + l));
-        launch_pf_attn(dh, dim3(H, (n + PA_Q - 1) / PA_Q), asmem, st, (const int64_t*)w.qkv, n, D, dh,
-                       (const int32_t*)(s.kc32 + l * kv_layer), (const int32_t*)(s.vc32 + l * kv_layer),
-                       size_t(m.cfg.max_ctx) * dh, m.inv_scale, (const int64_t*)m.ctx->exp_lut, w.strips, w.pa,
-                       w.cap_pad, m.Kd, w.wide, tc_scores);
+        if (tc_pv) {
+            // PV's linear half on the tensor cores (pf_pv.cuh): vh planes, then
+            // softmax + the per-product half, then the MMAs + output planes
+            launch_k(true, pf_vh_kernel, dim3(H, (n + PV_KB - 1) / PV_KB), 256, 0, st,
+                     (const int32_t*)(s.vc32 + l * kv_layer), size_t(m.cfg.max_ctx) * dh, n, w.kdig_pad, w.vh, w.wide);
+            launch_k(true, pf_attn_kernel<4, true>, dim3(H, (n + PA_Q - 1) / PA_Q), PA_THREADS, asmem, st,
+                     (const int64_t*)w.qkv, n, D, dh, (const int32_t*)(s.kc32 + l * kv_layer),
+                     (const int32_t*)(s.vc32 + l * kv_layer), size_t(m.cfg.max_ctx) * dh, m.inv_scale,
+                     (const int64_t*)m.ctx->exp_lut, w.strips, w.pa, w.cap_pad, m.Kd, w.wide, tc_scores, w.fl);
+            launch_k(true, pf_pv_kernel, dim3(H, (n + PV_Q - 1) / PV_Q), PV_THREADS, pf_pv_smem(), st, w.tm_vh,
+                     (const int32_t*)w.strips, (const int32_t*)w.fl, (const int32_t*)(s.vc32 + l * kv_layer),
+                     size_t(m.cfg.max_ctx) * dh, n, w.pa, w.cap_pad, m.Kd, w.wide);
+        } else {
+            launch_pf_attn(dh, dim3(H, (n + PA_Q - 1) / PA_Q), asmem, st, (const int64_t*)w.qkv, n, D, dh,
+                           (const int32_t*)(s.kc32 + l * kv_layer), (const int32_t*)(s.vc32 + l * kv_layer),
+                           size_t(m.cfg.max_ctx) * dh, m.inv_scale, (const int64_t*)m.ctx->exp_lut, w.strips, w.pa,
+                           w.cap_pad, m.Kd, w.wide, tc_scores);
+        }
         gemm(lw.wo, w.tm_pa, TG_RESID, w.x, D);
         launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int64_t*)w.x, D, (const int64_t*)lw.ffn_norm,
                  int(lw.ffn_unit), (const int64_t*)m.ctx->seeds, w.pa, w.cap_pad, m.Kd, w.wide);

@@ -183,7 +183,10 @@ __device__ __forceinline__ void pa_cp_wait_all() { asm volatile("cp.async.wait_g
 // so a lane reads 16 bytes per position; V row-major). DPL = dims per lane in
 // PV (dh <= 32 DPL). Output: digit planes of the attention vector (WO's B
 // operand); values outside the fast representation set *wide.
-template <int DPL>
+// TCPV: only the per-product half sum_p floor(P vl / 2^16) here, written to
+// fl_out [H][n][dh]; pf_pv_kernel (pf_pv.cuh) adds the linear half on the
+// tensor cores and writes the planes.
+template <int DPL, bool TCPV>
 __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* __restrict__ qkv, uint32_t n,
                                                                 uint32_t D, uint32_t dh,
                                                                 const int32_t* __restrict__ K32,
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
                                                                 size_t head_stride, int64_t inv_scale,
                                                                 const int64_t* __restrict__ lut_g, int32_t* strips,
                                                                 uint8_t* planes, uint32_t rows_pad, uint32_t ldp,
-                                                                uint32_t* wide, bool scores_ready) {
+                                                                uint32_t* wide, bool scores_ready, int32_t* fl_out) {
     extern __shared__ __align__(16) uint8_t pa_smem[];
     __shared__ int64_t lut[257];
     const uint32_t h = blockIdx.x, q0 = blockIdx.y * PA_Q;
@@ -374,13 +377,28 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
                     const uint32_t vl = uint32_t(vv[z]) & 0xFFFFu;
 #pragma unroll
                     for (int u = 0; u < PA_QW; ++u) {
-                        fh[u][z] += pq[u] * vh;
+                        if constexpr (!TCPV) fh[u][z] += pq[u] * vh;
                         fl[u][z] += (uint32_t(pq[u]) * vl) >> 16;
                     }
                 }
             }
         }
         __syncthreads();  // chunk c and Ps consumed
+    }
+    if constexpr (TCPV) {
+        if (lane_on) {
+#pragma unroll
+            for (int u = 0; u < PA_QW; ++u) {
+                const uint32_t t = tw + u;
+                if (t >= n) break;
+                int32_t* dst = fl_out + (size_t(h) * n + t) * dh + jl;
+#pragma unroll
+                for (int z = 0; z < DPL; ++z)
+                    if (jl + z < dh) dst[z] = int32_t(fl[u][z]);
+            }
+        }
+        if (big) *wide = 1;
+        return;
     }
     if (lane_on) {
         const size_t plane = size_t(rows_pad) * ldp;

@@ -273,15 +273,22 @@ def test_dense_tokens_wide_rows_fall_back_exactly(P, oracle):
 
 # ---- tensor-core prefill (whole prompt per layer) ------------------------------
 
-@pytest.mark.parametrize("cfg6,plen,seed,kd4", [((2, 64, 2, 64, 64, 256), 200, 3, 0),
-                                                 ((2, 256, 2, 512, 300, 400), 300, 4, 0),
-                                                 ((2, 256, 2, 512, 300, 400), 300, 4, 1),
-                                                 ((3, 96, 3, 160, 77, 200), 40, 5, 0)])
-def test_tensor_core_prefill_matches_oracle(P, oracle, monkeypatch, cfg6, plen, seed, kd4):
-    """kd4=1 forces the tensor-core scores' 4th key digit plane (dh = 128)."""
+@pytest.mark.parametrize("cfg6,plen,seed,kd4,pv", [((2, 64, 2, 64, 64, 256), 200, 3, 0, 1),
+                                                    ((2, 256, 2, 512, 300, 400), 300, 4, 0, 1),
+                                                    ((2, 256, 2, 512, 300, 400), 300, 4, 1, 1),
+                                                    ((2, 256, 2, 512, 300, 400), 300, 4, 0, 0),
+                                                    ((1, 512, 4, 256, 300, 1024), 700, 6, 0, 1),
+                                                    ((1, 512, 4, 256, 300, 1024), 700, 6, 0, 0),
+                                                    ((2, 128, 1, 256, 64, 256), 130, 8, 0, 1),
+                                                    ((3, 96, 3, 160, 77, 200), 40, 5, 0, 1)])
+def test_tensor_core_prefill_matches_oracle(P, oracle, monkeypatch, cfg6, plen, seed, kd4, pv):
+    """kd4=1 forces the tensor-core scores' 4th key digit plane; pv=0 keeps
+    all of PV on the CUDA cores (dh = 128 shapes: pv=1 puts its linear half on
+    the tensor cores, pf_pv.cuh)."""
     from oracle.pyoracle import Config
     monkeypatch.setenv("DIMG_PREFILL", "1")
     monkeypatch.setenv("DIMG_PF_KD4", str(kd4))
+    monkeypatch.setenv("DIMG_PF_PV", str(pv))
     m = P.gen_toy_model(seed, P.ModelConfig(*cfg6))
     om = oracle.gen_toy(seed, Config(*cfg6))
     prompt = P.prompt_from_seed(seed + 100, cfg6[4], plen)
