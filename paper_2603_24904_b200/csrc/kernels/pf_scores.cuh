@@ -153,9 +153,13 @@ __global__ void __launch_bounds__(PS_THREADS, 1) pf_scores_kernel(const __grid_c
         const uint32_t tb = tmem + ((32 * (warp & 3)) << 16);
         {
             const int half = warp >> 2;
-            int64_t s[16];
+            // digit-pair sums grouped by their weight 2^(8k), k = i + d: at most
+            // three terms of |sum| < 2^21 each, so the groups are exact int32
+            int32_t g[PS_KD + PS_QD - 1][16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) s[e] = 0;
+            for (int k = 0; k < PS_KD + PS_QD - 1; ++k)
+#pragma unroll
+                for (int e = 0; e < 16; ++e) g[k][e] = 0;
 #pragma unroll
             for (int i = 0; i < PS_KD; ++i) {  // the three query digits of key digit i: one wait
                 if (i >= n_kd) break;
@@ -166,13 +170,20 @@ __global__ void __launch_bounds__(PS_THREADS, 1) pf_scores_kernel(const __grid_c
 #pragma unroll
                 for (int d = 0; d < PS_QD; ++d)
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) s[e] += int64_t(v[d][e]) << (8 * (i + d));
+                    for (int e = 0; e < 16; ++e) g[i + d][e] += v[d][e];
             }
+            // mul16(a, inv) with |a| = |dot >> 16| < 2^47 and 0 <= inv < 2^16
+            // (the usual dh): the product fits int64, one multiply
+            const bool small_inv = uint64_t(inv_scale) < (uint64_t(1) << 16);
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
                 const uint32_t qi = 16 * half + e, tq = q0 + qi;
                 if (tq < n && p <= tq) {
-                    const int64_t val = mul16(s[e] >> 16, inv_scale);
+                    int64_t s = 0;
+#pragma unroll
+                    for (int k = 0; k < PS_KD + PS_QD - 1; ++k) s += int64_t(g[k][e]) << (8 * k);
+                    const int64_t a = s >> 16;
+                    const int64_t val = small_inv ? (a * inv_scale) >> 16 : mul16(a, inv_scale);
                     big |= !fits_i32(val);
                     Sc[size_t(qi) * ld + p] = int32_t(val);
                 }

@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
                                                                 uint32_t* wide, bool scores_ready, int32_t* fl_out) {
     extern __shared__ __align__(16) uint8_t pa_smem[];
     __shared__ int64_t lut[257];
+    __shared__ int32_t lut32[258];  // [0] = e[0] (the cell-256 end), [1 + i] = e[i]
     const uint32_t h = blockIdx.x, q0 = blockIdx.y * PA_Q;
     const uint32_t npos = min(n, q0 + PA_Q);  // positions any query of this CTA sees
     const uint32_t ld = (n + 3) & ~3u, nq = dh / 4, chunk_q = PA_CH * nq;
@@ -205,7 +206,11 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
     int32_t* Ps = reinterpret_cast<int32_t*>(Q + size_t(PA_Q) * nq);  // [PA_Q][PA_CH]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     pdl_launch_dependents();
-    for (int i = threadIdx.x; i < 257; i += PA_THREADS) lut[i] = lut_g[i];  // constant: before the wait
+    for (int i = threadIdx.x; i < 257; i += PA_THREADS) {  // constant: before the wait
+        lut[i] = lut_g[i];
+        lut32[i + 1] = int32_t(lut_g[i]);
+    }
+    if (threadIdx.x == 0) lut32[0] = int32_t(lut_g[0]);
     pdl_wait();
     for (uint32_t i = threadIdx.x; i < PA_Q * nq && !scores_ready; i += PA_THREADS) {
         const uint32_t qi = i / nq, j = 4 * (i % nq);
@@ -298,17 +303,23 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
         if (t >= n) break;
         int32_t* R = Sw + size_t(u) * ld;
         const int32_t m = __reduce_max_sync(0xffffffffu, mx[u]);
+        // all in 32 bits: m - score < 2^32 (int32 scores), and the LUT
+        // weights and their interpolation (< 2^16 x 2^11) fit
         uint32_t tot = 0;  // <= 2^16 per weight, n <= 2560 positions
+        for (uint32_t p = lane; p <= t; p += 32) tot += exp_neg32(min(uint32_t(m - R[p]), uint32_t(8 * ONE)), lut32);
+        const uint32_t total = __reduce_add_sync(0xffffffffu, tot);
+        // floor(w 2^16 / total) <= 2^16: a float estimate within one of the
+        // quotient (three roundings of 2^-24), fixed by the exact remainder,
+        // which lies in (-total, 2 total) and so is exact as an int32 even
+        // though w 2^16 and q total wrap mod 2^32
+        const float scale = 65536.0f / float(total);
         for (uint32_t p = lane; p <= t; p += 32) {
-            const int64_t d = int64_t(m) - R[p];
-            tot += uint32_t(exp_neg(d > 8 * ONE ? 8 * ONE : d, lut));
-        }
-        const uint64_t total = __reduce_add_sync(0xffffffffu, tot);
-        const uint64_t inv = ~0ull / total;
-        for (uint32_t p = lane; p <= t; p += 32) {
-            const int64_t d = int64_t(m) - R[p];
-            const uint64_t w = uint64_t(exp_neg(d > 8 * ONE ? 8 * ONE : d, lut));
-            R[p] = int32_t(udiv_inv(w << 16, total, inv));  // <= 2^16
+            const uint32_t w = exp_neg32(min(uint32_t(m - R[p]), uint32_t(8 * ONE)), lut32);
+            uint32_t q = uint32_t(float(w) * scale);
+            const int32_t r = int32_t((w << 16) - q * total);
+            q -= r < 0;
+            q += r >= int32_t(total);
+            R[p] = int32_t(q);
         }
     }
 

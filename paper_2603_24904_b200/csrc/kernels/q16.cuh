@@ -118,6 +118,14 @@ __device__ __forceinline__ int64_t exp_neg(int64_t t, const int64_t* e) {
     return hi - (((hi - lo) * frac + 1024) >> 11);
 }
 
+// exp_neg on 32 bits for 0 <= t <= 8*ONE, with the table L[0] = e[0],
+// L[1 + i] = e[i] (e <= 2^16): cell 256 (t = 8*ONE) reads L[1] - L[0] = 0.
+__device__ __forceinline__ uint32_t exp_neg32(uint32_t t, const int32_t* L) {
+    const uint32_t cell = t >> 11, frac = t & 2047;
+    const int32_t hi = L[257 - cell], lo = L[256 - cell];
+    return uint32_t(hi - ((uint32_t(hi - lo) * frac + 1024) >> 11));
+}
+
 // floor(a / d) for a < 2^63, d >= 1, given inv = ~0ull / d (one division
 // shared by many quotients): umulhi(a, inv) is floor(a / d) or one less.
 __device__ __forceinline__ uint64_t udiv_inv(uint64_t a, uint64_t d, uint64_t inv) {

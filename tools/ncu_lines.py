@@ -54,10 +54,16 @@ def main():
     ap.add_argument("--top", type=int, default=40)
     ap.add_argument("--kernel", default=KERNEL, help="mangled kernel name (nvdisasm section)")
     ap.add_argument("--file", default="persistent.cuh", help="source file the line range refers to")
+    ap.add_argument("--select", default=None, help="ncu -k filter (regex) when the report holds several kernels")
     a = ap.parse_args()
-    txt = subprocess.run(["ncu", "-i", a.report, "--page", "source", "--csv", "--print-source", "sass"],
-                         check=True, capture_output=True, text=True).stdout
+    cmd = ["ncu", "-i", a.report, "--page", "source", "--csv", "--print-source", "sass"]
+    if a.select:
+        cmd += ["-k", "regex:" + a.select, "-c", "1"]
+    txt = subprocess.run(cmd, check=True, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
+    if rows and rows[0] and rows[0][0] == "Kernel Name":  # a multi-kernel report: its first section
+        end = next((i for i in range(1, len(rows)) if rows[i] and rows[i][0] == "Kernel Name"), len(rows))
+        rows = rows[:end]
     hdr = rows[1]
     ia, iss = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)")
     data = rows[2:]
