@@ -441,7 +441,7 @@ DevMat upload_mat(dimg_model& m, uint32_t rows, uint32_t K, const std::vector<Ro
 // Prefill workspace: all prompt tokens through a layer at once.
 struct PrefillWs {
     uint32_t cap = 0, cap_pad = 0;   // tokens
-    int64_t* x = nullptr;            // [cap][D] residual stream
+    int32_t* x = nullptr;            // [cap][D] residual stream (int32: clamped to +-2^24)
     int64_t* qkv = nullptr;          // [cap][3D] projections (q rotated in place)
     uint8_t* pa = nullptr;           // [3][cap_pad][Kd] limb planes of D-wide inputs
     uint8_t* ph = nullptr;           // [3][cap_pad][Kf] limb planes of the FFN hidden vector
@@ -766,7 +766,7 @@ void ensure_prefill_ws(dimg_session& s, uint32_t n) {
     const dimg_model& m = *s.m;
     w.cap = std::max(n, 128u);
     w.cap_pad = (w.cap + TG_BN - 1) / TG_BN * TG_BN;
-    w.x = s.mem.alloc<int64_t>(size_t(w.cap) * m.D);
+    w.x = s.mem.alloc<int32_t>(size_t(w.cap) * m.D);
     w.qkv = s.mem.alloc<int64_t>(size_t(w.cap) * 3 * m.D);
     w.pa = s.mem.alloc<uint8_t>(size_t(3) * w.cap_pad * m.Kd);
     w.ph = s.mem.alloc<uint8_t>(size_t(3) * w.cap_pad * m.Kf);
@@ -827,12 +827,12 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
     CK(cudaMemsetAsync(s.kvwide, 0, size_t(m.L) * H * 4, st));
     // every kernel of the chain by programmatic dependent launch (pdl_wait in each)
     launch_k(true, pf_embed_kernel, 1024, 256, 0, st, (const uint32_t*)s.tokens, n, (const int8_t*)m.embd,
-             (const int64_t*)m.embd_s, D, w.x);
+             (const int64_t*)m.embd_s, D, w.x, w.wide);
     // short prompts: 16-token tiles split over K (one split per CTA slot), as the decode batches
     const bool small = n <= uint32_t(TG_BN_SMALL);
     const uint32_t bn = small ? TG_BN_SMALL : TG_BN;
     const uint32_t sms = uint32_t(m.ctx->sm_count);
-    auto gemm = [&](const DevMat& W, const CUtensorMap& tb_big, uint32_t epi, int64_t* y, uint32_t ldy) {
+    auto gemm = [&](const DevMat& W, const CUtensorMap& tb_big, uint32_t epi, void* y, uint32_t ldy) {
         const CUtensorMap& tb = !small ? tb_big : (&tb_big == &w.tm_ph ? w.tm_ph_s : w.tm_pa_s);
         TgArgs a{};
         a.n_out = W.rows;
@@ -842,7 +842,8 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
         a.limb_rows = w.cap_pad;
         a.epi = epi;
         a.scales = W.s;
-        a.y = y;
+        if (epi == TG_RESID) a.x32 = static_cast<int32_t*>(y);  // the int32 residual stream
+        else a.y = static_cast<int64_t*>(y);
         a.ldy = ldy;
         a.planes = w.ph;
         a.limb_rows_out = w.cap_pad;
@@ -873,7 +874,7 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
     const bool tc_pv = w.vh && dh == PV_M && (!pv_env || std::atoi(pv_env) != 0);
     for (uint32_t l = 0; l < m.L; ++l) {
         const auto& lw = m.layers[l];
-        launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int64_t*)w.x, D, (const int64_t*)lw.attn_norm,
+        launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int32_t*)w.x, D, (const int64_t*)lw.attn_norm,
                  int(lw.attn_unit), (const int64_t*)m.ctx->seeds, w.pa, w.cap_pad, m.Kd, w.wide);
         gemm(lw.qkv, w.tm_pa, TG_STORE, w.qkv, 3 * D);
         const bool last = l + 1 == m.L;  // the last layer's output feeds only the lm_head
@@ -905,7 +906,7 @@ bool run_prefill_tc(dimg_session& s, uint32_t n) {
                            w.cap_pad, m.Kd, w.wide, tc_scores);
         }
         gemm(lw.wo, w.tm_pa, TG_RESID, w.x, D);
-        launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int64_t*)w.x, D, (const int64_t*)lw.ffn_norm,
+        launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int32_t*)w.x, D, (const int64_t*)lw.ffn_norm,
                  int(lw.ffn_unit), (const int64_t*)m.ctx->seeds, w.pa, w.cap_pad, m.Kd, w.wide);
         gemm(lw.gu, w.tm_pa, TG_SILU, nullptr, 0);
         gemm(lw.down, w.tm_ph, TG_RESID, w.x, D);
@@ -961,7 +962,8 @@ struct BatchRun {
     DevBuf mem;
     uint32_t B = 0, ctx = 0, nmax = 0, nmax_pad = 0, max_new = 0;
     uint32_t *tok = nullptr, *seq = nullptr, *pos = nullptr, *out = nullptr, *step = nullptr, *wide = nullptr;
-    int64_t *x = nullptr, *qkv = nullptr, *logits = nullptr;
+    int32_t* x = nullptr;  // residual stream, int32 (clamped to +-2^24)
+    int64_t *qkv = nullptr, *logits = nullptr;
     uint8_t *pa = nullptr, *ph = nullptr;
     int32_t *K32 = nullptr, *V32 = nullptr;
     size_t seq_stride = 0, layer_stride = 0;
@@ -1006,7 +1008,7 @@ void batch_alloc(BatchRun& r, dimg_model* m, uint32_t B, uint32_t ctx, uint32_t 
     r.out = r.mem.alloc<uint32_t>(size_t(B) * std::max(1u, max_new));
     r.step = r.mem.alloc<uint32_t>(1);
     r.wide = r.mem.alloc<uint32_t>(1);
-    r.x = r.mem.alloc<int64_t>(size_t(nmax) * m->D);
+    r.x = r.mem.alloc<int32_t>(size_t(nmax) * m->D);
     r.qkv = r.mem.alloc<int64_t>(size_t(nmax) * 3 * m->D);
     r.logits = r.mem.alloc<int64_t>(size_t(B) * m->V);
     r.pa = r.mem.alloc<uint8_t>(size_t(3) * r.nmax_pad * m->Kd);
@@ -1045,7 +1047,8 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
     cudaStream_t st = r.st;
     const uint32_t D = m.D, dh = m.dh, H = m.H;
     const BatchTok bt{r.tok, r.seq, r.pos};
-    launch_k(true, bd_embed_kernel, 1024, 256, 0, st, bt, n, (const int8_t*)m.embd, (const int64_t*)m.embd_s, D, r.x);
+    launch_k(true, bd_embed_kernel, 1024, 256, 0, st, bt, n, (const int8_t*)m.embd, (const int64_t*)m.embd_s, D, r.x,
+             r.wide);
     const bool small = n <= uint32_t(TG_BN_SMALL);
     const uint32_t bn = small ? TG_BN_SMALL : TG_BN;
     // split-K (DIMG_SPLITK=0 turns it off): 16-token tiles split whenever the
@@ -1055,7 +1058,7 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
     const char* sk = std::getenv("DIMG_SPLITK");
     const bool split_k = sk ? std::atoi(sk) != 0 : true;
     int sms = m.ctx->sm_count;
-    auto gemm = [&](const DevMat& W, const CUtensorMap& tb_big, uint32_t epi, int64_t* y, uint32_t ldy) {
+    auto gemm = [&](const DevMat& W, const CUtensorMap& tb_big, uint32_t epi, void* y, uint32_t ldy) {
         const bool in_h = &tb_big == &r.tm_ph;
         const CUtensorMap& tb = small ? (in_h ? r.tm_ph_s : r.tm_pa_s) : tb_big;
         TgArgs a{};
@@ -1066,7 +1069,8 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
         a.limb_rows = r.nmax_pad;
         a.epi = epi;
         a.scales = W.s;
-        a.y = y;
+        if (epi == TG_RESID) a.x32 = static_cast<int32_t*>(y);  // the int32 residual stream
+        else a.y = static_cast<int64_t*>(y);
         a.ldy = ldy;
         a.planes = r.ph;
         a.limb_rows_out = r.nmax_pad;
@@ -1084,10 +1088,10 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
     };
     auto norm = [&](const int64_t* g, int unit) {  // decode steps: a CTA cluster per token
         if (n <= 64u)
-            launch_k(true, bd_norm_cluster_kernel, n * BD_NCL, 256, 0, st, (const int64_t*)r.x, D, g, unit,
+            launch_k(true, bd_norm_cluster_kernel, n * BD_NCL, 256, 0, st, (const int32_t*)r.x, D, g, unit,
                      (const int64_t*)m.ctx->seeds, r.pa, r.nmax_pad, m.Kd, r.wide);
         else
-            launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int64_t*)r.x, D, g, unit,
+            launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int32_t*)r.x, D, g, unit,
                      (const int64_t*)m.ctx->seeds, r.pa, r.nmax_pad, m.Kd, r.wide);
     };
     const size_t asmem = bd_attn_smem(dh, r.ctx) + 8;

@@ -31,15 +31,19 @@ struct BatchTok {  // device arrays, one entry per token of the step
 };
 
 __global__ void bd_embed_kernel(BatchTok bt, uint32_t n, const int8_t* __restrict__ E,
-                                const int64_t* __restrict__ Es, uint32_t D, int64_t* __restrict__ x) {
+                                const int64_t* __restrict__ Es, uint32_t D, int32_t* __restrict__ x, uint32_t* wide) {
     pdl_launch_dependents();
     pdl_wait();
+    int bad = 0;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < size_t(n) * D;
          i += size_t(gridDim.x) * blockDim.x) {
         const uint32_t t = uint32_t(i / D), j = uint32_t(i % D);
         const uint32_t tk = bt.tok[t];
-        x[i] = int64_t(uint64_t(int64_t(E[size_t(tk) * D + j])) * uint64_t(Es[tk]));
+        const int64_t v = int64_t(uint64_t(int64_t(E[size_t(tk) * D + j])) * uint64_t(Es[tk]));
+        bad |= !fits_i32(v);  // the int32 residual stream (pf_embed_kernel)
+        x[i] = int32_t(v);
     }
+    if (bad) *wide = 1;
 }
 
 // RoPE (proj/src/kernels.cpp:70-82) and the KV append (:139-142) of token t
@@ -82,7 +86,7 @@ __global__ void bd_rope_kv_kernel(int64_t* __restrict__ qkv, BatchTok bt, uint32
 constexpr int BD_NCL = 4;
 
 __global__ void __cluster_dims__(BD_NCL, 1, 1) __launch_bounds__(256)
-    bd_norm_cluster_kernel(const int64_t* __restrict__ x, uint32_t K, const int64_t* __restrict__ gamma,
+    bd_norm_cluster_kernel(const int32_t* __restrict__ x, uint32_t K, const int64_t* __restrict__ gamma,
                            int gamma_unit, const int64_t* __restrict__ seeds, uint8_t* planes, uint32_t rows_pad,
                            uint32_t ldp, uint32_t* wide) {
     namespace cg = cooperative_groups;
@@ -94,7 +98,7 @@ __global__ void __cluster_dims__(BD_NCL, 1, 1) __launch_bounds__(256)
     pdl_wait();
     const uint32_t rank = cl.block_rank(), t = blockIdx.x / BD_NCL;
     const uint32_t per = (K + BD_NCL - 1) / BD_NCL, j0 = min(K, rank * per), j1 = min(K, j0 + per);
-    const int64_t* xr = x + size_t(t) * K;
+    const int32_t* xr = x + size_t(t) * K;
     constexpr int PER = 4;  // elements per thread in registers (K <= 4096)
     int64_t v[PER];
     u128 ss = 0;
@@ -104,7 +108,7 @@ __global__ void __cluster_dims__(BD_NCL, 1, 1) __launch_bounds__(256)
         v[u] = j < j1 ? xr[j] : 0;
         ss += mul_full(v[u], v[u]);
     }
-    for (uint32_t j = j0 + threadIdx.x + PER * 256; j < j1; j += 256) ss += mul_full(xr[j], xr[j]);
+    for (uint32_t j = j0 + threadIdx.x + PER * 256; j < j1; j += 256) ss += mul_full(int64_t(xr[j]), int64_t(xr[j]));
     ss = block_sum_u128(ss, red);
     if (threadIdx.x == 0) part = ss;
     cl.sync();
@@ -129,7 +133,7 @@ __global__ void __cluster_dims__(BD_NCL, 1, 1) __launch_bounds__(256)
         }
     }
     for (uint32_t j = j0 + threadIdx.x + PER * 256; j < j1; j += 256) {
-        int64_t o = mul16(xr[j], r);
+        int64_t o = mul16(int64_t(xr[j]), r);
         if (!gamma_unit) o = mul16(o, gamma[j]);
         pf_put_limbs(pr + j, plane, o, wide);
     }

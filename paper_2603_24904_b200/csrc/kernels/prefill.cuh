@@ -20,16 +20,23 @@
 namespace dimg::dev {
 
 // x[t] = embed_token(tok[t]) (proj/src/engine.cpp:10-19)
+// The residual stream is int32 in the prefill and batch paths: every residual
+// epilogue clamps it to +-2^24; an embedding value outside int32 (a model
+// with huge embedding scales) sets *wide and the exact path takes over.
 __global__ void pf_embed_kernel(const uint32_t* __restrict__ tok, uint32_t n, const int8_t* __restrict__ E,
-                                const int64_t* __restrict__ Es, uint32_t D, int64_t* __restrict__ x) {
+                                const int64_t* __restrict__ Es, uint32_t D, int32_t* __restrict__ x, uint32_t* wide) {
     pdl_launch_dependents();
     pdl_wait();
+    int bad = 0;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < size_t(n) * D;
          i += size_t(gridDim.x) * blockDim.x) {
         const uint32_t t = uint32_t(i / D), j = uint32_t(i % D);
         const uint32_t tk = tok[t];
-        x[i] = int64_t(uint64_t(int64_t(E[size_t(tk) * D + j])) * uint64_t(Es[tk]));
+        const int64_t v = int64_t(uint64_t(int64_t(E[size_t(tk) * D + j])) * uint64_t(Es[tk]));
+        bad |= !fits_i32(v);
+        x[i] = int32_t(v);
     }
+    if (bad) *wide = 1;
 }
 
 __device__ __forceinline__ void pf_put_limbs(uint8_t* p, size_t plane, int64_t v, uint32_t* wide) {
@@ -41,7 +48,7 @@ __device__ __forceinline__ void pf_put_limbs(uint8_t* p, size_t plane, int64_t v
 // is loaded once into registers (all loads in flight together).
 constexpr int PN_PER = 16;  // elements per thread held in registers (K <= 4096 with 256 threads)
 
-__global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int64_t* __restrict__ x, uint32_t K,
+__global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int32_t* __restrict__ x, uint32_t K,
                                                             const int64_t* __restrict__ gamma, int gamma_unit,
                                                             const int64_t* __restrict__ seeds, uint8_t* planes,
                                                             uint32_t rows_pad, uint32_t ldp, uint32_t* wide) {
@@ -50,7 +57,7 @@ __global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int64_t* __res
     pdl_launch_dependents();
     pdl_wait();
     const uint32_t t = blockIdx.x;
-    const int64_t* xr = x + size_t(t) * K;
+    const int32_t* xr = x + size_t(t) * K;
     int64_t v[PN_PER];
 #pragma unroll
     for (int u = 0; u < PN_PER; ++u) {
@@ -60,7 +67,7 @@ __global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int64_t* __res
     u128 ss = 0;
 #pragma unroll
     for (int u = 0; u < PN_PER; ++u) ss += mul_full(v[u], v[u]);
-    for (uint32_t j = threadIdx.x + PN_PER * 256; j < K; j += 256) ss += mul_full(xr[j], xr[j]);
+    for (uint32_t j = threadIdx.x + PN_PER * 256; j < K; j += 256) ss += mul_full(int64_t(xr[j]), int64_t(xr[j]));
     ss = block_sum_u128(ss, red);
     if (threadIdx.x == 0) {
         // usual case: the sum fits 63 bits and one u64 division is exact
@@ -82,7 +89,7 @@ __global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int64_t* __res
         }
     }
     for (uint32_t j = threadIdx.x + PN_PER * 256; j < K; j += 256) {
-        int64_t o = mul16(xr[j], r);
+        int64_t o = mul16(int64_t(xr[j]), r);
         if (!gamma_unit) o = mul16(o, gamma[j]);
         pf_put_limbs(pr + j, plane, o, wide);
     }

@@ -77,7 +77,8 @@ struct TgArgs {
     uint32_t a_rows;     // rows per K block of the K-block-major A operand (n_out padded to 128)
     uint32_t epi;
     const int64_t* scales;  // [n_out]
-    int64_t* y;             // STORE: y[t][n]; RESID: x[t][n] updated; SILU: h[t][n / 2]
+    int64_t* y;             // STORE: y[t][n]; SILU: h[t][n / 2]
+    int32_t* x32;           // RESID: the residual stream x[t][n] updated (|x| <= 2^24 after the clamp)
     uint32_t ldy;           // row stride of y (elements)
     // SILU: also the three limb planes of h for the next GEMM, [3][limb_rows_out][ldp] bytes
     uint8_t* planes;
@@ -464,19 +465,23 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
                     // RESID: all 16 residual loads in flight before the first store
                     // (the compiler may not hoist a load above a possibly aliasing store)
                     if (a.epi == TG_RESID) {
-                        int64_t yold[16];
+                        int32_t xold[16];
 #pragma unroll
                         for (int jj = 0; jj < 16; ++jj) {
                             const uint32_t t = t0 + c0 + jj;
-                            yold[jj] = nv && t < a.n_tok ? a.y[size_t(t) * a.ldy + n] : 0;
+                            xold[jj] = nv && t < a.n_tok ? a.x32[size_t(t) * a.ldy + n] : 0;
                         }
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) val[jj] = add_clamp(yold[jj], val[jj]);
-                    }
+                        for (int jj = 0; jj < 16; ++jj) {
+                            const uint32_t t = t0 + c0 + jj;
+                            if (nv && t < a.n_tok) a.x32[size_t(t) * a.ldy + n] = int32_t(add_clamp(xold[jj], val[jj]));
+                        }
+                    } else {
 #pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) {
-                        const uint32_t t = t0 + c0 + jj;
-                        if (nv && t < a.n_tok) a.y[size_t(t) * a.ldy + n] = val[jj];
+                        for (int jj = 0; jj < 16; ++jj) {
+                            const uint32_t t = t0 + c0 + jj;
+                            if (nv && t < a.n_tok) a.y[size_t(t) * a.ldy + n] = val[jj];
+                        }
                     }
                 }
             }
