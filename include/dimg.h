@@ -246,10 +246,22 @@ dimg_status dimg_session_stats(dimg_session* s, uint64_t out[4]);
  *                  dimg_nccl_unique_id, distributed by the caller.
  *   DIMG_TP_LOCAL  all tp_size shards on `device` in this process, the sums
  *                  done by kernels (testing the sharded kernels on one GPU).
+ *   (both: a chain of per-stage GEMV kernels + collectives per step)
+ *   DIMG_TP_FUSED_IPC    this process is rank tp_rank; every rank runs the
+ *                  persistent decode kernel on its shard and the sums happen
+ *                  INSIDE it: the wo / w_down epilogues store their rows'
+ *                  partials straight into every peer's inbox over NVLink
+ *                  (peer memory from CUDA IPC handles) and poll their own.
+ *                  After create: dimg_tp_exchange_handle on every rank, the
+ *                  tp_size handles gathered by the caller, dimg_tp_connect.
+ *   DIMG_TP_FUSED_LOCAL  the same kernel program for all tp_size shards on
+ *                  `device`: one cooperative launch whose CTAs are split
+ *                  between the ranks, exchanging through device memory (the
+ *                  one-GPU test of the fused path; tp_size <= 8).
  * tp_size must divide n_heads. keep_logits_cap: logits vectors a generate
- * call may return. */
+ * call may return (not with DIMG_TP_FUSED_IPC). */
 typedef struct dimg_tp dimg_tp;
-typedef enum { DIMG_TP_LOCAL = 0, DIMG_TP_NCCL = 1 } dimg_tp_backend;
+typedef enum { DIMG_TP_LOCAL = 0, DIMG_TP_NCCL = 1, DIMG_TP_FUSED_LOCAL = 2, DIMG_TP_FUSED_IPC = 3 } dimg_tp_backend;
 dimg_status dimg_nccl_unique_id(uint8_t id[128]);
 dimg_status dimg_tp_create(int device, const dimg_model_desc* desc, int backend, int tp_rank, int tp_size,
                            const uint8_t nccl_id[128], uint32_t keep_logits_cap, dimg_tp** out);
@@ -267,6 +279,11 @@ dimg_status dimg_tp_stream(dimg_tp* t, void** stream);
 /* Device bytes of this process's shards; kernel launches + collectives per
  * decode step (after the first generation). */
 dimg_status dimg_tp_info(dimg_tp* t, uint64_t* weight_bytes, uint64_t* launches_per_step);
+/* DIMG_TP_FUSED_IPC: this rank's exchange-block handle (a cudaIpcMemHandle_t,
+ * 64 bytes), and the group's handles in rank order (tp_size x 64 bytes) to
+ * map the peers' blocks; generation needs a connected group. */
+dimg_status dimg_tp_exchange_handle(dimg_tp* t, uint8_t handle[64]);
+dimg_status dimg_tp_connect(dimg_tp* t, const uint8_t* handles);
 
 /* ---- operator-level exports (host buffers in/out) for unit parity with
  *      proj/src/kernels.cpp; they run the engine's own device kernels. ---- */

@@ -117,6 +117,8 @@ def _load():
         "dimg_tp_tokens": ([vp, u32p, C.c_uint32], C.c_int),
         "dimg_tp_stream": ([vp, pp], C.c_int),
         "dimg_tp_info": ([vp, u64p, u64p], C.c_int),
+        "dimg_tp_exchange_handle": ([vp, u8p], C.c_int),
+        "dimg_tp_connect": ([vp, u8p], C.c_int),
         "dimg_op_dense": ([C.c_int, C.POINTER(QTensor), i64p, i64p], C.c_int),
         "dimg_op_dense_tokens": ([C.c_int, C.POINTER(QTensor), i64p, C.c_uint32, i64p], C.c_int),
         "dimg_blake3_device": ([C.c_int, vp, C.c_size_t, u8p, C.POINTER(C.c_float)], C.c_int),

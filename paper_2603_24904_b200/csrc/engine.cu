@@ -132,10 +132,16 @@ DevCtx& dev_ctx(int device) {
     set_gemv_attrs<EPI_RAW, MODE_PLAIN>();
     CK(cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(attn_op_scratch_bytes(8192))));
-    cudaFuncAttributes fa;
+    // dynamic shared memory of the persistent kernels: what the larger
+    // static footprint of the two leaves (the tensor-parallel group kernel
+    // also holds its rank's arguments)
+    cudaFuncAttributes fa, fg;
     CK(cudaFuncGetAttributes(&fa, decode_persistent_kernel));
-    c.smem_optin = int(prop.sharedMemPerBlockOptin) - int(fa.sharedSizeBytes);
+    CK(cudaFuncGetAttributes(&fg, decode_persistent_group_kernel));
+    c.smem_optin = int(prop.sharedMemPerBlockOptin) - int(std::max(fa.sharedSizeBytes, fg.sharedSizeBytes));
     CK(cudaFuncSetAttribute(decode_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            c.smem_optin));
+    CK(cudaFuncSetAttribute(decode_persistent_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             c.smem_optin));
     CK(cudaDeviceSynchronize());  // the tables above landed before any non-blocking stream reads them
     c.device = device;
@@ -499,8 +505,9 @@ struct dimg_session {
     uint32_t grid = 0, planes_bytes = 0, ring_depth = 2, wide_stride = 0;
     uint32_t* wide_planes = nullptr;
     size_t smem = 0;
+    bool own_stream = true;  // false: a tensor-parallel group's shared stream
     ~dimg_session() {
-        if (stream) cudaStreamDestroy(stream);
+        if (stream && own_stream) cudaStreamDestroy(stream);
     }
 };
 
@@ -577,6 +584,7 @@ std::vector<PkStage> step_program(const dimg_session& s) {
             wo.resid_embed = 1;  // layer 0: the residual input is the token's embedding
         }
         wo.no_barrier = (skip & 8) ? 1 : 0;
+        wo.tp_sum = 1;  // row-parallel under tensor parallelism: inbox buffer 0
         p.push_back(wo);
         PkStage gu = gemv_stage(lw.gu, MODE_NORM, EPI_SILU, s.x, lw.ffn_norm, s.h, lw.ffn_unit);
         gu.xw_in = xa;
@@ -588,6 +596,7 @@ std::vector<PkStage> step_program(const dimg_session& s) {
         dn.xw_in = xa;
         dn.xw_out = xb;
         dn.no_barrier = (skip & 8) ? 1 : 0;
+        dn.tp_sum = 2;  // inbox buffer 1
         p.push_back(dn);
     }
     PkStage head = gemv_stage(m.head, MODE_NORM, EPI_ARGMAX, s.x, m.final_norm, s.logits, m.final_unit);
@@ -628,14 +637,14 @@ PkArgs pk_args(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     t.scores = s.scores;
     t.out = s.att;
     t.ctl = s.ctl;
-    t.H = m.H;
+    t.H = m.Hl;  // this rank's heads (all of them on one GPU)
     t.dh = m.dh;
     t.max_ctx = m.cfg.max_ctx;
     t.inv_scale = m.inv_scale;
     t.exp_lut = m.ctx->exp_lut;
-    a.kv_layer_stride = size_t(m.H) * m.cfg.max_ctx * m.dh;
+    a.kv_layer_stride = size_t(m.Hl) * m.cfg.max_ctx * m.dh;
     // CTAs per head: split the head's dims over the SMs the heads leave idle
-    a.attn_parts = std::max(1u, std::min(s.grid / m.H, std::max(1u, m.dh / 8)));
+    a.attn_parts = std::max(1u, std::min(s.grid / m.Hl, std::max(1u, m.dh / 8)));
     if (const char* e = std::getenv("DIMG_ATTN_PARTS"))  // experiments: CTAs per head
         a.attn_parts = std::max(1u, std::min(a.attn_parts, uint32_t(std::strtoul(e, nullptr, 0))));
     {
@@ -669,7 +678,7 @@ void launch_pk(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     // tags of the attention score exchange: unique per attention stage, never 0
     const uint64_t n_attn = uint64_t(n_steps) * s.m->L;
     if (uint64_t(s.attn_tag) + n_attn + 2 > 0xFFFFFFFFull) {
-        CK(cudaMemsetAsync(s.xg, 0, size_t(s.m->H) * s.m->cfg.max_ctx * 16, s.stream));
+        CK(cudaMemsetAsync(s.xg, 0, size_t(s.m->Hl) * s.m->cfg.max_ctx * 16, s.stream));
         CK(cudaMemsetAsync(s.parts_w, 0, size_t(64) * s.grid, s.stream));
         s.attn_tag = 0;
     }
@@ -708,7 +717,7 @@ void ensure_keep(dimg_session& s, uint32_t need) {
     if (need <= s.keep_cap) return;
     CK(cudaStreamSynchronize(s.stream));
     void* p = nullptr;
-    CK(cudaMalloc(&p, size_t(need + 1) * s.m->V * sizeof(int64_t)));
+    CK(cudaMalloc(&p, size_t(need + 1) * s.m->Vl * sizeof(int64_t)));
     s.mem.ptrs.push_back(p);
     s.logits = static_cast<int64_t*>(p);
     s.keep_cap = need;
@@ -1376,26 +1385,11 @@ dimg_model* model_upload(int device, const dimg_model_desc* d, int tp_rank, int 
         return m.release();
     }
 }
-}  // namespace
-
-extern "C" {
-
-dimg_status dimg_model_free(dimg_model* m) {
-    DIMG_API_GUARD({
-        if (m) {
-            cudaSetDevice(m->device);
-            delete m;
-        }
-    })
-}
-
-dimg_status dimg_model_bytes_on_device(const dimg_model* m, uint64_t* bytes) {
-    DIMG_API_GUARD(*bytes = m->mem.bytes)
-}
-
-dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_session** out) {
-    DIMG_API_GUARD({
-        if (m->rowmajor) fail(DIMG_EINVAL, "session: a tensor-parallel shard generates through dimg_tp");
+// A session on model m (or on one tensor-parallel shard of it: the local
+// heads, FFN rows and vocab rows; the sizes below are the shard's), with
+// `grid` CTAs for the persistent kernel (0: one per SM).
+dimg_session* session_new(dimg_model* m, uint32_t keep_logits_cap, uint32_t grid) {
+    {
         CK(cudaSetDevice(m->device));
         auto s = std::make_unique<dimg_session>();
         s->m = m;
@@ -1404,37 +1398,37 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         s->x = s->mem.alloc<int64_t>(m->D);
         s->x32 = s->mem.alloc<int32_t>(m->Kd);
         CK(cudaMemsetAsync(s->x32, 0, size_t(m->Kd) * 4, s->stream));
-        s->qkv = s->mem.alloc<int64_t>(3 * size_t(m->D));
-        s->att = s->mem.alloc<int64_t>(m->D);
-        s->h = s->mem.alloc<int64_t>(m->F);
-        size_t kv = size_t(m->L) * m->H * ctx * m->dh;
+        s->qkv = s->mem.alloc<int64_t>(3 * size_t(m->Dl));
+        s->att = s->mem.alloc<int64_t>(m->Dl);
+        s->h = s->mem.alloc<int64_t>(m->Fl);
+        size_t kv = size_t(m->L) * m->Hl * ctx * m->dh;
         s->kc = s->mem.alloc<int64_t>(kv);
         s->vc = s->mem.alloc<int64_t>(kv);
-        s->scores = s->mem.alloc<int64_t>(size_t(m->H) * ctx);
+        s->scores = s->mem.alloc<int64_t>(size_t(m->Hl) * ctx);
         s->keep_cap = keep_logits_cap;
-        s->logits = s->mem.alloc<int64_t>(size_t(keep_logits_cap + 1) * m->V);
+        s->logits = s->mem.alloc<int64_t>(size_t(keep_logits_cap + 1) * m->Vl);
         s->tokens = s->mem.alloc<uint32_t>(ctx + 1);
         s->ctl = s->mem.alloc<Ctl>(1);
         s->bar = s->mem.alloc<unsigned int>(64);
-        s->xg = s->mem.alloc<unsigned long long>(size_t(m->H) * ctx * 2);
-        s->qkv_x = s->mem.alloc<unsigned long long>(size_t(3) * m->D * 2);
+        s->xg = s->mem.alloc<unsigned long long>(size_t(m->Hl) * ctx * 2);
+        s->qkv_x = s->mem.alloc<unsigned long long>(size_t(3) * m->Dl * 2);
         s->xwords = s->mem.alloc<uint32_t>(size_t(2) * m->Kd);
         CK(cudaMemsetAsync(s->xwords, 0, size_t(8) * m->Kd, s->stream));
-        CK(cudaMemsetAsync(s->qkv_x, 0, size_t(3) * m->D * 16, s->stream));
-        CK(cudaMemsetAsync(s->xg, 0, size_t(m->H) * ctx * 16, s->stream));
+        CK(cudaMemsetAsync(s->qkv_x, 0, size_t(3) * m->Dl * 16, s->stream));
+        CK(cudaMemsetAsync(s->xg, 0, size_t(m->Hl) * ctx * 16, s->stream));
         s->kc32 = s->mem.alloc<int32_t>(kv);
         s->vc32 = s->mem.alloc<int32_t>(kv);
-        s->kvwide = s->mem.alloc<uint32_t>(size_t(m->L) * m->H);
-        CK(cudaMemsetAsync(s->kvwide, 0, size_t(m->L) * m->H * 4, s->stream));
+        s->kvwide = s->mem.alloc<uint32_t>(size_t(m->L) * m->Hl);
+        CK(cudaMemsetAsync(s->kvwide, 0, size_t(m->L) * m->Hl * 4, s->stream));
         // one CTA per SM; shared memory = weight ring + limb planes + row accumulators
-        s->grid = uint32_t(m->ctx->sm_count);
+        s->grid = grid ? grid : uint32_t(m->ctx->sm_count);
         s->parts = s->mem.alloc<ArgPart>(s->grid);
         s->parts_w = s->mem.alloc<unsigned long long>(size_t(8) * s->grid);
         CK(cudaMemsetAsync(s->parts_w, 0, size_t(64) * s->grid, s->stream));
-        s->words_att = s->mem.alloc<uint32_t>(m->Kd);
-        s->words_h = s->mem.alloc<uint32_t>(m->Kf);
-        CK(cudaMemsetAsync(s->words_att, 0, size_t(4) * m->Kd, s->stream));
-        CK(cudaMemsetAsync(s->words_h, 0, size_t(4) * m->Kf, s->stream));
+        s->words_att = s->mem.alloc<uint32_t>(pad16(m->Dl));
+        s->words_h = s->mem.alloc<uint32_t>(pad16(m->Fl));
+        CK(cudaMemsetAsync(s->words_att, 0, size_t(4) * pad16(m->Dl), s->stream));
+        CK(cudaMemsetAsync(s->words_h, 0, size_t(4) * pad16(m->Fl), s->stream));
         s->ssq = s->mem.alloc<unsigned long long>(2 * size_t(m->L));
         s->host_stages = step_program(*s);
         // shared staging: rmsnorm = the int64 vector + 3 planes (11 Kp bytes);
@@ -1474,7 +1468,32 @@ dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_se
         CK(cudaMemsetAsync(s->ctl, 0, sizeof(Ctl), s->stream));
         CK(cudaMemsetAsync(s->tokens, 0, (ctx + 1) * 4, s->stream));
         CK(cudaStreamSynchronize(s->stream));
-        *out = s.release();
+        return s.release();
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+dimg_status dimg_model_free(dimg_model* m) {
+    DIMG_API_GUARD({
+        if (m) {
+            cudaSetDevice(m->device);
+            delete m;
+        }
+    })
+}
+
+dimg_status dimg_model_bytes_on_device(const dimg_model* m, uint64_t* bytes) {
+    DIMG_API_GUARD(*bytes = m->mem.bytes)
+}
+
+dimg_status dimg_session_create(dimg_model* m, uint32_t keep_logits_cap, dimg_session** out) {
+    DIMG_API_GUARD({
+        if (m->tp_size > 1 || m->rowmajor)
+            fail(DIMG_EINVAL, "session: a tensor-parallel shard generates through dimg_tp");
+        *out = session_new(m, keep_logits_cap, 0);
     })
 }
 

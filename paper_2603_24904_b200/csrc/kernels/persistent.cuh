@@ -60,6 +60,7 @@ struct PkStage {
     const uint32_t* in_words; // MODE_PLAIN: the input as tagged limb words (nullptr: build from x)
     uint32_t* out_words;      // EPI_SILU / attention: publish y as tagged limb words
     uint32_t no_barrier;      // 1: the next stage consumes tagged words, no grid barrier after this one
+    uint32_t tp_sum;          // EPI_RESID, tensor parallel: 1 + inbox buffer (WO 1, w_down 2); 0 none
     int32_t* x32_out;         // EPI_RESID: the clamped x also as int32 (|x| <= 2^24)
     const int32_t* x32_in;    // MODE_NORM after a RESID stage: read that copy (16 KB, not 32)
     // Residual stream as tagged words (no grid barrier after a RESID stage):
@@ -112,7 +113,20 @@ struct PkArgs {
     int32_t* vc32;
     uint32_t* kvwide;         // [L][H] some cached K/V value of the head needs more than 32 bits
     unsigned long long* trace_all;  // optional: [stage_seq][grid][2] every CTA's prologue end / chunk-loop end
+    // Tensor parallel: this launch is rank tp_rank of tp_g,
+    // holding its heads / FFN rows / vocab rows (vocab_off = its first vocab
+    // row). The row-parallel stages' (WO, w_down) pre-scale accumulators are
+    // summed across the ranks inside their epilogues: each CTA stores its rows'
+    // partials straight into every peer's inbox (tagged words, peer memory over
+    // NVLink or, for the one-device group, plain device memory) and polls its
+    // own inbox for the peers' partials of the same rows; the lm_head's per-CTA
+    // (max, index) partials go to every rank the same way. tp_g <= 1: none of it.
+    uint32_t tp_g, tp_rank, vocab_off;
+    unsigned long long* tp_in[8];     // every rank's inbox [2 (WO | down)][tp_g][d_model][2]
+    unsigned long long* tp_parts[8];  // every rank's lm_head slots [2][tp_g * grid][4]
 };
+
+constexpr int PK_TP_MAX = 8;
 
 // Scheduling constants, held in registers (never address kernel params or
 // shared structs from hot code: local memory goes through L1, which each
@@ -220,6 +234,14 @@ __device__ __forceinline__ void st_tagged2(unsigned long long* p, uint64_t a, ui
 __device__ __forceinline__ void ld_tagged2(const unsigned long long* p, uint64_t& a, uint64_t& b) {
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
+// The same at system scope: words another GPU stores into this one's memory
+// (or this one into a peer's) over NVLink.
+__device__ __forceinline__ void st_tagged2_sys(unsigned long long* p, uint64_t a, uint64_t b) {
+    asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_tagged2_sys(const unsigned long long* p, uint64_t& a, uint64_t& b) {
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
 
 // Limb word of a MODE_PLAIN input element: bytes 0-2 = the three low limb
 // bytes, byte 3 = wide bit (needs more than 3 limbs) << 7 | 7-bit stage tag.
@@ -297,14 +319,16 @@ __device__ __forceinline__ void copy_g2s(void* dst, const void* src, uint32_t by
 
 // Grid barrier #k (monotonic counter). Returns false if the wait timed out
 // (a hung peer): the caller then unwinds instead of hanging the GPU.
-__device__ __forceinline__ bool grid_sync(unsigned int* bar, Ctl* ctl, uint32_t k) {
+// vg: the CTAs of this rank (gridDim.x, or the rank's share of a one-device
+// tensor-parallel launch).
+__device__ __forceinline__ bool grid_sync(unsigned int* bar, Ctl* ctl, uint32_t k, uint32_t vg) {
     __shared__ int ok;
     __syncthreads();
     if (threadIdx.x == 0) {
         ok = 1;
         __threadfence();
         atomicAdd(bar, 1u);
-        const uint32_t target = (k + 1) * gridDim.x;
+        const uint32_t target = (k + 1) * vg;
         uint64_t t0 = globaltimer();
         while (ld_acquire(bar) < target) {
             if (*((volatile uint32_t*)&ctl->err) & 4u) { ok = 0; break; }
@@ -319,9 +343,10 @@ __device__ __forceinline__ bool grid_sync(unsigned int* bar, Ctl* ctl, uint32_t 
     return ok != 0;
 }
 
-__device__ __forceinline__ void cta_range(uint32_t n, uint32_t& lo, uint32_t& hi) {
-    lo = uint32_t(uint64_t(n) * blockIdx.x / gridDim.x);
-    hi = uint32_t(uint64_t(n) * (blockIdx.x + 1) / gridDim.x);
+// CTA vb of vg: its share of n units.
+__device__ __forceinline__ void cta_range(uint32_t n, uint32_t& lo, uint32_t& hi, uint32_t vb, uint32_t vg) {
+    lo = uint32_t(uint64_t(n) * vb / vg);
+    hi = uint32_t(uint64_t(n) * (vb + 1) / vg);
 }
 
 __device__ __forceinline__ uint32_t stages_in_step(const Sched& sc, uint32_t step) {
@@ -921,16 +946,58 @@ struct GemvRT {
     Ctl* ctl;
     unsigned long long* ytag; // EPI_STORE: tagged word pairs of y
     uint64_t tg;              // their tag << 32
+    uint32_t vb, vg;          // this CTA of the rank's vg
+    uint32_t row_off;         // EPI_ARGMAX: vocab index of row 0 (tensor parallel: the rank's slice)
+    uint32_t tp_buf, tp_tag;  // EPI_RESID, tensor parallel: 1 + inbox buffer (0: single GPU), exchange tag
 };
+
+// Tensor parallel: row `row`'s pre-scale accumulator summed over the tp_g
+// ranks (wrapping u64 adds: order-free, so every rank gets the same bits).
+// This rank's partial goes into slot [buf][tp_rank][row] of every peer's
+// inbox as two tagged words; the peers' partials of the same row arrive in
+// this rank's inbox the same way (they stream the same row groups in the same
+// order, so the wait is the ranks' skew). A peer that never publishes trips
+// the 4 s timeout: ctl->err bit 2, the launch fails instead of hanging.
+__device__ __forceinline__ uint64_t tp_sum_row(const PkArgs& a, uint32_t buf, uint32_t tag, uint32_t row,
+                                               uint32_t rows, uint64_t mine, Ctl* ctl) {
+    const uint32_t G = a.tp_g, me = a.tp_rank;
+    const uint64_t tg = uint64_t(tag) << 32;
+    const size_t out = ((size_t(buf) * G + me) * rows + row) * 2;
+#pragma unroll
+    for (uint32_t q = 0; q < PK_TP_MAX; ++q)
+        if (q < G && q != me) st_tagged2_sys(a.tp_in[q] + out, tg | uint32_t(mine), tg | uint32_t(mine >> 32));
+    uint64_t sum = mine;
+#pragma unroll
+    for (uint32_t q = 0; q < PK_TP_MAX; ++q) {
+        if (q >= G || q == me) continue;
+        const unsigned long long* w = a.tp_in[me] + ((size_t(buf) * G + q) * rows + row) * 2;
+        uint64_t lo, hi;
+        uint64_t g0 = 0;
+        for (uint32_t spins = 1;; ++spins) {
+            ld_tagged2_sys(w, lo, hi);
+            if (uint32_t(lo >> 32) == tag && uint32_t(hi >> 32) == tag) break;
+            if ((spins & 1023) == 0) {
+                const uint64_t now = globaltimer();
+                if (!g0) g0 = now;
+                if ((*((volatile uint32_t*)&ctl->err) & 4u) || now - g0 > 4000000000ull) {
+                    atomicOr(&ctl->err, 4u);
+                    break;
+                }
+            }
+        }
+        sum += (hi << 32) | (lo & 0xFFFFFFFFull);
+    }
+    return sum;
+}
 
 // All of this CTA's row groups of a GEMV stage, epilogues fused.
 template <int L>
-__device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT& g_,
+__device__ __forceinline__ void run_gemv(const PkArgs& a, const Sched& sc, Pipe& p, const GemvRT& g_,
                                          const uint32_t* planes, uint32_t tag, int64_t& best_v,
                                          uint32_t& best_i) {
     const int lane = threadIdx.x & 31;
     uint32_t g_lo, g_hi;
-    cta_range(g_.n_groups, g_lo, g_hi);
+    cta_range(g_.n_groups, g_lo, g_hi, g_.vb, g_.vg);
     for (uint32_t g = g_lo + (threadIdx.x >> 5); g < g_hi; g += PK_WARPS) {
         const uint32_t r0 = g * PK_ROWS;
         int64_t resid = 0, scale = 0;  // residual issued now, consumed after the dot product
@@ -942,6 +1009,16 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
         }
         uint64_t v[PK_ROWS];
         group_dot<L>(sc, p, g_.Kp, g_.n_segs, planes, v, scale);
+        if (g_.tp_buf && lane < PK_ROWS && r0 + lane < g_.rows) {
+            // the row-parallel partials -> the full pre-scale sum (kernels.cpp:18-30 on the whole row)
+            uint64_t mine = v[0];
+#pragma unroll
+            for (int r = 1; r < PK_ROWS; ++r) mine = lane == r ? v[r] : mine;
+            const uint64_t tot = tp_sum_row(a, g_.tp_buf - 1, g_.tp_tag, r0 + lane, g_.rows, mine, g_.ctl);
+#pragma unroll
+            for (int r = 0; r < PK_ROWS; ++r)
+                if (lane == r) v[r] = tot;
+        }
         uint64_t sq = 0;
         if (g_.epi == EPI_SILU) {
             // rows (2i, 2i+1) = (gate_i, up_i): lanes 0,1 finish pairs 0,1
@@ -974,11 +1051,11 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
                 if (g_.x32) g_.x32[row] = int32_t(x);
                 if (g_.xw_out) st_word(g_.xw_out + row, x_word(x, g_.tag6_out));
                 sq = uint64_t(x * x);  // |x| <= 2^24: x^2 < 2^49, 8192 rows < 2^62
-            } else {  // EPI_ARGMAX
+            } else {  // EPI_ARGMAX (vocab row = the rank's first row + row)
                 g_.lrow[row] = val;
-                if (better(val, row, best_v, best_i)) {
+                if (better(val, g_.row_off + row, best_v, best_i)) {
                     best_v = val;
-                    best_i = row;
+                    best_i = g_.row_off + row;
                 }
             }
         }
@@ -991,9 +1068,10 @@ __device__ __forceinline__ void run_gemv(const Sched& sc, Pipe& p, const GemvRT&
 }
 
 // The 8-limb instantiation only runs on out-of-range activations: out of line.
-__device__ __forceinline__ void run_gemv_wide(const Sched& sc, Pipe& p, const GemvRT& g_, const uint32_t* planes,
-                                           uint32_t tag, int64_t& best_v, uint32_t& best_i) {
-    run_gemv<8>(sc, p, g_, planes, tag, best_v, best_i);
+__device__ __forceinline__ void run_gemv_wide(const PkArgs& a, const Sched& sc, Pipe& p, const GemvRT& g_,
+                                              const uint32_t* planes, uint32_t tag, int64_t& best_v,
+                                              uint32_t& best_i) {
+    run_gemv<8>(a, sc, p, g_, planes, tag, best_v, best_i);
 }
 
 // ---- attention, positions split across the head's CTAs ---------------------------
@@ -1448,13 +1526,15 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
 
 // ---- the kernel -------------------------------------------------------------------
 
-__global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const PkArgs a) {
+// The kernel body for CTA vb of the vg CTAs of one rank (a single-GPU
+// launch: blockIdx.x of gridDim.x).
+__device__ __forceinline__ void pk_run(const PkArgs& a, const uint32_t vb, const uint32_t vg) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t depth = a.ring_depth;
     uint8_t* slots = smem;                                                // [warps][depth][SLOT]
     uint8_t* stage_mem = smem + size_t(PK_WARPS) * depth * PK_SLOT;       // planes_bytes
     uint64_t* bars = reinterpret_cast<uint64_t*>(stage_mem + a.planes_bytes);  // [warps][depth]
-    uint32_t* wide_planes = a.wide_planes + size_t(blockIdx.x) * a.wide_stride;  // 8-limb planes (rare)
+    uint32_t* wide_planes = a.wide_planes + size_t(vb) * a.wide_stride;  // 8-limb planes (rare)
     FetchInfo* s_fi = reinterpret_cast<FetchInfo*>(bars + PK_WARPS * PK_MAX_DEPTH);   // [n_layer_stages + 1]
     __shared__ u128 red[32];
     __shared__ int64_t s_bv[PK_WARPS];
@@ -1470,7 +1550,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
         const PkStage* st = a.stages + i;
         FetchInfo fi{};
         if (st->kind == SK_GEMV) {
-            cta_range(st->n_groups, fi.g_lo, fi.g_hi);
+            cta_range(st->n_groups, fi.g_lo, fi.g_hi, vb, vg);
             fi.W = st->W;
             fi.n_segs = st->n_segs;
             fi.Kp = st->Kp;
@@ -1527,7 +1607,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
             if (threadIdx.x < kStWords)
                 next_word = reinterpret_cast<const uint32_t*>(sc.stages + (si + 1 < nst ? si + 1 : 0))[threadIdx.x];
             unsigned long long* tr =
-                a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nseq < a.trace_cap ? a.trace + 32 * nseq : nullptr;
+                a.trace && vb == 0 && threadIdx.x == 0 && nseq < a.trace_cap ? a.trace + 32 * nseq : nullptr;
             ++nseq;
             if (tr) {
                 tr[8] = clock64();
@@ -1543,7 +1623,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
             if (st.kind == SK_ATTN) {
                 const uint32_t np = a.attn_parts;
                 ++attn_epoch;
-                for (uint32_t c = blockIdx.x; c < a.attn.H * np; c += gridDim.x)
+                for (uint32_t c = vb; c < a.attn.H * np; c += vg)
                     if (!attn_split(a, st.layer, c / np, c % np, np, pos, attn_epoch,
                                     reinterpret_cast<int64_t*>(stage_mem), red, st.out_words, s_lut,
                                     tr && c == 0 ? tr : nullptr))
@@ -1557,7 +1637,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                                        wide_planes, ctl);
                     if (L < 0) return;
                     if (L == PLAIN_WIDE) {  // grid-uniform: the int64 vector is visible after the barrier
-                        if (!grid_sync(a.bar, ctl, nbar++)) return;
+                        if (!grid_sync(a.bar, ctl, nbar++, vg)) return;
                         L = planes_from_x(st.K, st.Kp, st.x, planes, wide_planes, ctl, true);
                     }
                 } else {
@@ -1566,7 +1646,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                     // could lag behind their next writers). The embedding is
                     // written by the CTA holding group 0.
                     uint32_t glo, ghi;
-                    cta_range(st.n_groups, glo, ghi);
+                    cta_range(st.n_groups, glo, ghi, vb, vg);
                     int64_t* xb = reinterpret_cast<int64_t*>(stage_mem);
                     planes = reinterpret_cast<uint32_t*>(xb + st.Kp);
                     L = 3;
@@ -1588,7 +1668,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 if (L == 8) planes = wide_planes;  // out-of-range inputs: 8 planes in the global scratch
                 // the sum the previous stages' prologues consumed: every reader
                 // is done once this stage's inputs are complete
-                if (st.ssq_clear && blockIdx.x == 0 && threadIdx.x == 0) *st.ssq_clear = 0;
+                if (st.ssq_clear && vb == 0 && threadIdx.x == 0) *st.ssq_clear = 0;
                 if (tr) tr[1] = globaltimer();
 #ifdef DIMG_CHUNK_TRACE
                 if (threadIdx.x == 0 && blockIdx.x < 148 && p.ctn < CT_MAX) {
@@ -1598,7 +1678,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 }
 #endif
                 if (a.trace_all && threadIdx.x == 0 && nseq - 1 < a.trace_cap)
-                    a.trace_all[(size_t(nseq - 1) * gridDim.x + blockIdx.x) * 2] = globaltimer();
+                    a.trace_all[(size_t(nseq - 1) * vg + vb) * 2] = globaltimer();
                 GemvRT g_;
                 g_.epi = st.epi; g_.rows = st.rows; g_.Kp = st.Kp; g_.n_groups = st.n_groups;
                 g_.n_segs = st.n_segs; g_.tag7 = tag7_of(a.tag_base + attn_epoch); g_.y = st.y;
@@ -1614,14 +1694,19 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 g_.es = st.resid_embed ? a.embd_scales[token] : 0;
                 g_.ctl = ctl;
                 g_.ytag = st.ytag;
+                g_.vb = vb;
+                g_.vg = vg;
+                g_.row_off = a.vocab_off;
+                g_.tp_buf = a.tp_g > 1 ? st.tp_sum : 0u;
+                g_.tp_tag = a.tag_base + attn_epoch;
                 g_.tg = uint64_t(a.tag_base + attn_epoch + 1) << 32;  // the coming attention stage's tag
                 if (st.epi == EPI_ARGMAX) {
                     uint32_t slot = pos - logit_base;
                     slot = slot < keep_cap ? slot : keep_cap;
                     g_.lrow = st.y + size_t(slot) * st.rows;
                 }
-                if (L == 3) run_gemv<3>(sc, p, g_, planes, tag, best_v, best_i);
-                else run_gemv_wide(sc, p, g_, planes, tag, best_v, best_i);
+                if (L == 3) run_gemv<3>(a, sc, p, g_, planes, tag, best_v, best_i);
+                else run_gemv_wide(a, sc, p, g_, planes, tag, best_v, best_i);
                 if (tr) tr[2] = globaltimer();
 #ifdef DIMG_CHUNK_TRACE
                 if (threadIdx.x == 0 && blockIdx.x < 148 && p.ctn < CT_MAX) {
@@ -1631,7 +1716,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                 }
 #endif
                 if (a.trace_all && threadIdx.x == 0 && nseq - 1 < a.trace_cap)
-                    a.trace_all[(size_t(nseq - 1) * gridDim.x + blockIdx.x) * 2 + 1] = globaltimer();
+                    a.trace_all[(size_t(nseq - 1) * vg + vb) * 2 + 1] = globaltimer();
                 if (st.epi == EPI_ARGMAX) {
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
@@ -1644,11 +1729,21 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
                     if (threadIdx.x == 0) {
                         for (int w2 = 1; w2 < PK_WARPS; ++w2)
                             if (better(s_bv[w2], s_bi[w2], best_v, best_i)) { best_v = s_bv[w2]; best_i = s_bi[w2]; }
-                        a.parts[blockIdx.x].v = best_v;
-                        a.parts[blockIdx.x].idx = best_i;
-                        if (a.parts_w) {  // tagged copy: the next token needs no grid barrier
-                            const uint64_t tg = uint64_t(a.tag_base + attn_epoch) << 32;
-                            unsigned long long* pw = a.parts_w + (size_t(step & 1) * gridDim.x + blockIdx.x) * 4;
+                        a.parts[vb].v = best_v;
+                        a.parts[vb].idx = best_i;
+                        const uint64_t tg = uint64_t(a.tag_base + attn_epoch) << 32;
+                        if (a.tp_g > 1) {
+                            // tensor parallel: this CTA's pair into slot tp_rank * vg + vb of every rank
+                            const size_t o = (size_t(step & 1) * a.tp_g * vg + size_t(a.tp_rank) * vg + vb) * 4;
+#pragma unroll
+                            for (uint32_t q = 0; q < PK_TP_MAX; ++q)
+                                if (q < a.tp_g) {
+                                    st_tagged2_sys(a.tp_parts[q] + o, tg | uint32_t(uint64_t(best_v)),
+                                                   tg | uint32_t(uint64_t(best_v) >> 32));
+                                    st_tagged2_sys(a.tp_parts[q] + o + 2, tg | best_i, tg);
+                                }
+                        } else if (a.parts_w) {  // tagged copy: the next token needs no grid barrier
+                            unsigned long long* pw = a.parts_w + (size_t(step & 1) * vg + vb) * 4;
                             st_tagged2(pw, tg | uint32_t(uint64_t(best_v)), tg | uint32_t(uint64_t(best_v) >> 32));
                             st_tagged2(pw + 2, tg | best_i, tg);
                         }
@@ -1660,23 +1755,30 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
             if (threadIdx.x < kStWords) reinterpret_cast<uint32_t*>(&s_st[cur ^ 1])[threadIdx.x] = next_word;
             cur ^= 1;
             if (st.no_barrier) __syncthreads();  // the next descriptor is complete before anyone reads it
-            else if (!grid_sync(a.bar, ctl, nbar++)) return;
+            else if (!grid_sync(a.bar, ctl, nbar++, vg)) return;
         }
         if (step >= sc.n_prefill) {
             // every CTA reduces the lm_head partials itself (no extra barrier)
             int64_t bv = INT64_MIN;
             uint32_t bi = 0xFFFFFFFFu;
             const uint32_t ptag = a.tag_base + attn_epoch;
-            for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+            const bool tp = a.tp_g > 1;
+            const uint32_t n_parts = tp ? a.tp_g * vg : vg;  // every rank's CTAs
+            for (uint32_t b = threadIdx.x; b < n_parts; b += blockDim.x) {
                 int64_t v;
                 uint32_t i;
                 if (a.parts_w) {
-                    const unsigned long long* pw = a.parts_w + (size_t(step & 1) * gridDim.x + b) * 4;
+                    const unsigned long long* pw = a.parts_w + (size_t(step & 1) * n_parts + b) * 4;
                     uint64_t w0, w1, w2, w3;
                     uint32_t spins = 0;
                     for (;;) {
-                        ld_tagged2(pw, w0, w1);
-                        ld_tagged2(pw + 2, w2, w3);
+                        if (tp) {
+                            ld_tagged2_sys(pw, w0, w1);
+                            ld_tagged2_sys(pw + 2, w2, w3);
+                        } else {
+                            ld_tagged2(pw, w0, w1);
+                            ld_tagged2(pw + 2, w2, w3);
+                        }
                         if (uint32_t(w0 >> 32) == ptag && uint32_t(w1 >> 32) == ptag && uint32_t(w2 >> 32) == ptag) break;
                         if ((++spins & 1023) == 0 && (*((volatile uint32_t*)&ctl->err) & 4u)) break;
                         if ((spins & 0xFFFFF) == 0) atomicOr(&ctl->err, 4u);  // ~seconds: give up
@@ -1701,13 +1803,33 @@ __global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const 
             for (int w2 = 0; w2 < PK_WARPS; ++w2)
                 if (better(s_bv[w2], s_bi[w2], bv, bi)) { bv = s_bv[w2]; bi = s_bi[w2]; }
             token = bi;
-            if (blockIdx.x == 0 && threadIdx.x == 0) a.tokens[pos + 1] = token;
+            if (vb == 0 && threadIdx.x == 0) a.tokens[pos + 1] = token;
         } else {
             token = a.tokens[pos + 1];
         }
         ++pos;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->pos = pos;
+    if (vb == 0 && threadIdx.x == 0) ctl->pos = pos;
+}
+
+__global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_kernel(const PkArgs a) {
+    pk_run(a, blockIdx.x, gridDim.x);
+}
+
+// A tensor-parallel group on ONE device (the in-process backend that tests
+// the sharded program without more GPUs): one cooperative launch of
+// g x vg CTAs, CTAs [r vg, (r + 1) vg) running rank r with its own arguments
+// (copied to shared memory), so ranks that wait on one another are
+// co-resident by construction.
+__global__ void __launch_bounds__(PK_THREADS, 1) decode_persistent_group_kernel(const PkArgs* __restrict__ ranks,
+                                                                               uint32_t vg) {
+    __shared__ __align__(16) PkArgs s_a;
+    const uint32_t r = blockIdx.x / vg;
+    constexpr int kWords = sizeof(PkArgs) / 4;
+    for (int i = threadIdx.x; i < kWords; i += PK_THREADS)
+        reinterpret_cast<uint32_t*>(&s_a)[i] = reinterpret_cast<const uint32_t*>(ranks + r)[i];
+    __syncthreads();
+    pk_run(s_a, blockIdx.x - r * vg, vg);
 }
 
 }  // namespace dimg::dev

@@ -21,6 +21,19 @@
 // Each step (all ranks on this process) is captured once as a CUDA graph
 // (with and without the lm_head) and replayed; positions and tokens live in
 // device memory, as for the single-GPU engine.
+//
+// The fused backends run the single-GPU persistent decode kernel on each
+// rank's shard instead (one launch per generation), with the two
+// all-reduces per layer and the argmax gather done inside it over peer
+// memory (kernels/persistent.cuh tp_sum_row; no collective library):
+//   DIMG_TP_FUSED_IPC    one process per GPU; each rank allocates one
+//                  exchange block (inbox [2][g][D][2] + lm_head slots
+//                  [2][g * grid][4], tagged 8-byte words) and maps its
+//                  peers' with CUDA IPC handles the caller distributes.
+//   DIMG_TP_FUSED_LOCAL  every shard on one device; one cooperative launch
+//                  of g x (SMs / g) CTAs, each CTA running its rank's
+//                  arguments (decode_persistent_group_kernel), so ranks that
+//                  wait on each other are resident together by construction.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -83,6 +96,11 @@ struct TpRank {
     std::vector<GemvArgs> qkv_a, wo_a, gu_a, dn_a;
     std::vector<AttnArgs> at_a;
     GemvArgs head_a{};
+    // fused backends: the shard's persistent-kernel session and its
+    // exchange block (released before the model: declared after it)
+    dimg_session* s = nullptr;
+    unsigned long long* xch = nullptr;
+    ~TpRank() { delete s; }
 };
 
 }  // namespace
@@ -103,7 +121,15 @@ struct dimg_tp {
     uint32_t n_prompt = 0, max_new = 0, len = 0;
     cudaGraphExec_t graph_head = nullptr, graph_prompt = nullptr;
     uint64_t launches_per_step = 0;
+    // fused backends
+    bool fused = false, connected = false;
+    uint32_t vg = 0;                          // CTAs per rank
+    size_t inbox_elems = 0, slot_elems = 0;   // u64 words of the exchange block's two parts
+    std::vector<unsigned long long*> xch;     // every rank's exchange block (own or peer-mapped)
+    std::vector<void*> ipc_open;              // mapped peer blocks
+    PkArgs* d_args = nullptr;                 // FUSED_LOCAL: the ranks' kernel arguments
     ~dimg_tp() {
+        for (void* p : ipc_open) cudaIpcCloseMemHandle(p);
         if (graph_head) cudaGraphExecDestroy(graph_head);
         if (graph_prompt) cudaGraphExecDestroy(graph_prompt);
         if (comm) nccl_api().comm_destroy(comm);
@@ -357,6 +383,87 @@ void tp_gather_logits(dimg_tp& t, int64_t* out) {
     CK(cudaStreamSynchronize(t.st));
 }
 
+// ---- fused backends --------------------------------------------------------------
+
+void tpf_require_connected(const dimg_tp& t) {
+    if (t.fused && !t.connected) fail(DIMG_ELOGIC, "tp: dimg_tp_connect the group before generating");
+}
+
+// One persistent launch of n_steps forward steps (the first n_prefill
+// without the lm_head) on every rank of this process.
+void tpf_launch(dimg_tp& t, uint32_t n_steps, uint32_t n_prefill) {
+    if (n_steps == 0) return;
+    tpf_require_connected(t);
+    const uint64_t n_attn = uint64_t(n_steps) * t.L;
+    std::vector<PkArgs> args;
+    for (auto& rp : t.ranks) {
+        dimg_session& s = *rp->s;
+        const dimg_model& m = *rp->m;
+        if (uint64_t(s.attn_tag) + n_attn + 2 > 0xFFFFFFFFull) {
+            // tags restart at 0: every buffer that holds tagged words is
+            // cleared. Across processes a peer may already be writing this
+            // rank's inbox for the next launch, so only the one-device group
+            // can do that safely.
+            if (t.backend == DIMG_TP_FUSED_IPC)
+                fail(DIMG_ELOGIC, "tp: exchange tag space exhausted (2^32 attention stages); recreate the group");
+            CK(cudaMemsetAsync(s.xg, 0, size_t(m.Hl) * m.cfg.max_ctx * 16, t.st));
+            CK(cudaMemsetAsync(rp->xch, 0, (t.inbox_elems + t.slot_elems) * 8, t.st));
+            s.attn_tag = 0;
+        }
+        PkArgs a = pk_args(s, s.stages, n_layer_stages(s), n_steps, n_prefill);
+        a.tag_base = s.attn_tag;
+        s.attn_tag += uint32_t(n_attn);
+        a.tp_g = t.g;
+        a.tp_rank = uint32_t(m.tp_rank);
+        a.vocab_off = m.v0;
+        for (uint32_t q = 0; q < t.g; ++q) {
+            a.tp_in[q] = t.xch[q];
+            a.tp_parts[q] = t.xch[q] + t.inbox_elems;
+        }
+        a.parts_w = a.tp_parts[a.tp_rank];
+        CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned int), t.st));
+        CK(cudaMemsetAsync(s.ssq, 0, size_t(2) * m.L * sizeof(unsigned long long), t.st));
+        args.push_back(a);
+    }
+    const dimg_session& s0 = *t.ranks[0]->s;
+    if (t.backend == DIMG_TP_FUSED_LOCAL) {
+        CK(cudaMemcpyAsync(t.d_args, args.data(), args.size() * sizeof(PkArgs), cudaMemcpyHostToDevice, t.st));
+        const PkArgs* d = t.d_args;
+        uint32_t vg = t.vg;
+        void* params[] = {&d, &vg};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(decode_persistent_group_kernel), dim3(t.g * t.vg),
+                                       dim3(PK_THREADS), params, s0.smem, t.st));
+    } else {
+        void* params[] = {&args[0]};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(decode_persistent_kernel), dim3(t.vg),
+                                       dim3(PK_THREADS), params, s0.smem, t.st));
+    }
+}
+
+void tpf_begin(dimg_tp& t, const uint32_t* prompt, uint32_t p, uint32_t n, bool keep) {
+    tpf_require_connected(t);
+    if (keep && t.backend == DIMG_TP_FUSED_IPC)
+        fail(DIMG_EINVAL, "tp: keep_logits is not available with DIMG_TP_FUSED_IPC (each process holds its vocab slice)");
+    for (auto& rp : t.ranks) begin(*rp->s, prompt, p, n, keep);
+    t.n_prompt = p;
+    t.max_new = n;
+    t.len = 0;
+}
+
+void tpf_check_err(dimg_tp& t) {
+    for (auto& rp : t.ranks) check_ctl_err(*rp->s);
+}
+
+// The kept logits [max_new][V]: every rank's vocab slice (one device).
+void tpf_gather_logits(dimg_tp& t, int64_t* out) {
+    for (auto& rp : t.ranks)
+        CK(cudaMemcpy2DAsync(out + rp->m->v0, size_t(t.V) * 8, rp->s->logits, size_t(rp->m->Vl) * 8,
+                             size_t(rp->m->Vl) * 8, t.max_new, cudaMemcpyDeviceToHost, t.st));
+    CK(cudaStreamSynchronize(t.st));
+}
+
+const uint32_t* tp_tokens_dev(const dimg_tp& t) { return t.fused ? t.ranks[0]->s->tokens : t.ranks[0]->tokens; }
+
 }  // namespace
 
 extern "C" {
@@ -373,16 +480,20 @@ dimg_status dimg_nccl_unique_id(uint8_t id[128]) {
 dimg_status dimg_tp_create(int device, const dimg_model_desc* desc, int backend, int tp_rank, int tp_size,
                            const uint8_t nccl_id[128], uint32_t keep_logits_cap, dimg_tp** out) {
     DIMG_API_GUARD({
-        if (backend != DIMG_TP_LOCAL && backend != DIMG_TP_NCCL) fail(DIMG_EINVAL, "tp: unknown backend");
+        if (backend < DIMG_TP_LOCAL || backend > DIMG_TP_FUSED_IPC) fail(DIMG_EINVAL, "tp: unknown backend");
+        const bool fused = backend == DIMG_TP_FUSED_LOCAL || backend == DIMG_TP_FUSED_IPC;
+        const bool multi = backend == DIMG_TP_NCCL || backend == DIMG_TP_FUSED_IPC;  // one rank per process
         if (tp_size < 1 || tp_size > 64) fail(DIMG_EINVAL, "tp: tp_size in 1..64");
-        if (backend == DIMG_TP_NCCL && (tp_rank < 0 || tp_rank >= tp_size))
+        if (fused && tp_size > PK_TP_MAX) fail(DIMG_EINVAL, "tp: the fused backends take tp_size <= 8");
+        if (multi && (tp_rank < 0 || tp_rank >= tp_size))
             fail(DIMG_EINVAL, "tp: rank outside 0..tp_size-1");
         if (backend == DIMG_TP_NCCL && !nccl_id) fail(DIMG_EINVAL, "tp: the NCCL backend needs the unique id");
         auto t = std::make_unique<dimg_tp>();
         t->backend = backend;
         t->device = device;
         t->g = uint32_t(tp_size);
-        t->rank = backend == DIMG_TP_NCCL ? tp_rank : 0;
+        t->rank = multi ? tp_rank : 0;
+        t->fused = fused;
         t->ctx = &dev_ctx(device);
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking));
@@ -396,13 +507,35 @@ dimg_status dimg_tp_create(int device, const dimg_model_desc* desc, int backend,
             t->parts = t->mem.alloc<int64_t>(size_t(t->g) * t->D);
         }
         t->pairs = t->mem.alloc<unsigned long long>(2 * size_t(t->g));
-        const int lo = backend == DIMG_TP_LOCAL ? 0 : tp_rank, hi = backend == DIMG_TP_LOCAL ? tp_size : tp_rank + 1;
+        const int lo = multi ? tp_rank : 0, hi = multi ? tp_rank + 1 : tp_size;
+        if (fused) {
+            t->vg = backend == DIMG_TP_FUSED_LOCAL ? uint32_t(t->ctx->sm_count) / t->g : uint32_t(t->ctx->sm_count);
+            if (t->vg == 0) fail(DIMG_EINVAL, "tp: more ranks than SMs");
+            t->inbox_elems = size_t(2) * t->g * t->D * 2;
+            t->slot_elems = size_t(2) * t->g * t->vg * 4;
+            t->xch.assign(t->g, nullptr);
+            if (backend == DIMG_TP_FUSED_LOCAL) t->d_args = t->mem.alloc<PkArgs>(t->g);
+        }
         for (int r = lo; r < hi; ++r) {
             auto rk = std::make_unique<TpRank>();
-            rk->m.reset(model_upload(device, desc, r, tp_size, true));
-            tp_build_rank(*t, *rk);
+            // fused: the persistent kernel's blocked layout and a session per
+            // shard (sharing the group's stream); else the row-major GEMV layout
+            rk->m.reset(model_upload(device, desc, r, tp_size, !fused));
+            if (fused) {
+                rk->s = session_new(rk->m.get(), keep_logits_cap, t->vg);
+                CK(cudaStreamDestroy(rk->s->stream));
+                rk->s->stream = t->st;
+                rk->s->own_stream = false;
+                rk->xch = t->mem.alloc<unsigned long long>(t->inbox_elems + t->slot_elems);
+                CK(cudaMemset(rk->xch, 0, (t->inbox_elems + t->slot_elems) * 8));
+                t->xch[r] = rk->xch;
+            } else {
+                tp_build_rank(*t, *rk);
+            }
             t->ranks.push_back(std::move(rk));
         }
+        t->connected = backend != DIMG_TP_FUSED_IPC || tp_size == 1;
+        if (fused) t->launches_per_step = 1;  // at most: one launch runs all the steps of a call
         if (backend == DIMG_TP_NCCL) {
             ncclUniqueId u;
             std::memcpy(&u, nccl_id, 128);
@@ -428,15 +561,25 @@ dimg_status dimg_tp_generate_greedy(dimg_tp* t, const uint32_t* prompt, uint32_t
     // run_generation (proj/src/engine.cpp:31-54) on the sharded model; every
     // rank ends with the same tokens
     DIMG_API_GUARD({
-        tp_begin(*t, prompt, n_prompt, max_new, logits_out != nullptr);
+        if (t->fused) tpf_begin(*t, prompt, n_prompt, max_new, logits_out != nullptr);
+        else tp_begin(*t, prompt, n_prompt, max_new, logits_out != nullptr);
         g_generations.fetch_add(1, std::memory_order_relaxed);
         if (max_new > 0) {
-            tp_generate(*t);
-            CK(cudaMemcpyAsync(tokens_out, t->ranks[0]->tokens + n_prompt, size_t(max_new) * 4,
+            if (t->fused) {
+                tpf_launch(*t, n_prompt - 1 + max_new, n_prompt - 1);
+                t->len = n_prompt - 1 + max_new;
+            } else {
+                tp_generate(*t);
+            }
+            CK(cudaMemcpyAsync(tokens_out, tp_tokens_dev(*t) + n_prompt, size_t(max_new) * 4,
                                cudaMemcpyDeviceToHost, t->st));
         }
-        tp_check_err(*t);
-        if (logits_out && max_new > 0) tp_gather_logits(*t, logits_out);
+        if (t->fused) tpf_check_err(*t);
+        else tp_check_err(*t);
+        if (logits_out && max_new > 0) {
+            if (t->fused) tpf_gather_logits(*t, logits_out);
+            else tp_gather_logits(*t, logits_out);
+        }
         if (hash_out) {
             auto d = b3::hash(tokens_out, size_t(max_new) * 4, 1);
             std::memcpy(hash_out, d.data(), 32);
@@ -449,28 +592,35 @@ dimg_status dimg_tp_time_decode(dimg_tp* t, const uint32_t* prompt, uint32_t n_p
     // the prompt steps untimed, then n_steps lm_head steps between CUDA
     // events on the group's stream (tokens: dimg_tp_tokens)
     DIMG_API_GUARD({
-        tp_begin(*t, prompt, n_prompt, n_steps, false);
-        tp_run_steps(*t, false, n_prompt - 1);
-        tp_ensure_graph(*t, true);  // instantiated outside the timed region
+        if (t->fused) {
+            tpf_begin(*t, prompt, n_prompt, n_steps, false);
+            tpf_launch(*t, n_prompt - 1, n_prompt - 1);  // the prompt positions, untimed
+        } else {
+            tp_begin(*t, prompt, n_prompt, n_steps, false);
+            tp_run_steps(*t, false, n_prompt - 1);
+            tp_ensure_graph(*t, true);  // instantiated outside the timed region
+        }
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         CK(cudaStreamSynchronize(t->st));
         CK(cudaEventRecord(e0, t->st));
-        tp_run_steps(*t, true, n_steps);
+        if (t->fused) tpf_launch(*t, n_steps, 0);
+        else tp_run_steps(*t, true, n_steps);
         CK(cudaEventRecord(e1, t->st));
         CK(cudaEventSynchronize(e1));
         CK(cudaEventElapsedTime(ms, e0, e1));
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         t->len = n_prompt - 1 + n_steps;
-        tp_check_err(*t);
+        if (t->fused) tpf_check_err(*t);
+        else tp_check_err(*t);
     })
 }
 
 dimg_status dimg_tp_tokens(dimg_tp* t, uint32_t* out, uint32_t n_generated) {
     DIMG_API_GUARD({
-        CK(cudaMemcpyAsync(out, t->ranks[0]->tokens + t->n_prompt, size_t(n_generated) * 4, cudaMemcpyDeviceToHost,
+        CK(cudaMemcpyAsync(out, tp_tokens_dev(*t) + t->n_prompt, size_t(n_generated) * 4, cudaMemcpyDeviceToHost,
                            t->st));
         CK(cudaStreamSynchronize(t->st));
     })
@@ -485,6 +635,36 @@ dimg_status dimg_tp_info(dimg_tp* t, uint64_t* weight_bytes, uint64_t* launches_
         for (auto& rp : t->ranks) b += rp->m->mem.bytes;
         if (weight_bytes) *weight_bytes = b;
         if (launches_per_step) *launches_per_step = t->launches_per_step;
+    })
+}
+
+dimg_status dimg_tp_exchange_handle(dimg_tp* t, uint8_t handle[64]) {
+    DIMG_API_GUARD({
+        if (t->backend != DIMG_TP_FUSED_IPC) fail(DIMG_EINVAL, "tp: exchange handles belong to DIMG_TP_FUSED_IPC");
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+        CK(cudaSetDevice(t->device));
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, t->ranks[0]->xch));
+        std::memcpy(handle, &h, 64);
+    })
+}
+
+dimg_status dimg_tp_connect(dimg_tp* t, const uint8_t* handles) {
+    // maps every peer's exchange block (NVLink peer access enabled lazily)
+    DIMG_API_GUARD({
+        if (t->backend != DIMG_TP_FUSED_IPC) fail(DIMG_EINVAL, "tp: dimg_tp_connect belongs to DIMG_TP_FUSED_IPC");
+        if (t->connected) fail(DIMG_ELOGIC, "tp: already connected");
+        CK(cudaSetDevice(t->device));
+        for (uint32_t q = 0; q < t->g; ++q) {
+            if (int(q) == t->rank) continue;
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, handles + size_t(q) * 64, 64);
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            t->ipc_open.push_back(p);
+            t->xch[q] = static_cast<unsigned long long*>(p);
+        }
+        t->connected = true;
     })
 }
 

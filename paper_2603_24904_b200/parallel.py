@@ -16,10 +16,17 @@
 and its gloo tests (tests/test_parallel.py); the device shards are cut by
 dimg_model_upload with the same balanced blocks.
 
-`TensorParallel` runs the sharded model on the GPU (dimg_tp_*): backend
-"nccl" = this process is one rank (one process per GPU, NCCL all-reduce of
-the pre-scale accumulators); backend "local" = all shards on one device in
-this process (the sums done by kernels), for testing on one GPU.
+`TensorParallel` runs the sharded model on the GPU (dimg_tp_*):
+  - "fused-ipc": this process is one rank (one process per GPU); its shard
+    runs the persistent decode kernel, and the WO / w_down epilogues store
+    their rows' pre-scale partials straight into every peer's inbox over
+    NVLink (CUDA IPC peer memory, `connect_group`) and poll their own: the
+    all-reduce is fused into the GEMV, no collective call per layer;
+  - "fused": the same kernel program for all shards on one device (one
+    cooperative launch split between the ranks) -- the one-GPU test of it;
+  - "nccl": one process per GPU, per-stage GEMV kernels and an NCCL
+    all-reduce of the pre-scale accumulators (the collective-library
+    baseline); "local": that chain for all shards on one device.
 """
 from __future__ import annotations
 
@@ -117,7 +124,11 @@ def pick_argmax(candidates) -> int:
     return int(best[1])
 
 
-BACKENDS = {"local": 0, "nccl": 1}
+# "local" / "nccl": per-stage GEMV kernels + collectives (NCCL between
+# processes); "fused" / "fused-ipc": the persistent decode kernel on every
+# shard with the sums inside it (one device / one process per GPU over CUDA
+# IPC peer memory), include/dimg.h dimg_tp_backend.
+BACKENDS = {"local": 0, "nccl": 1, "fused": 2, "fused-ipc": 3}
 
 
 def nccl_unique_id() -> bytes:
@@ -171,6 +182,26 @@ class TensorParallel:
         out = np.zeros(max(1, n), np.uint32)
         check(lib.dimg_tp_tokens(self._h, ptr(out, u32p), n))
         return [int(t) for t in out[:n]]
+
+    def exchange_handle(self) -> bytes:
+        """fused-ipc: this rank's exchange-block handle (64 bytes)."""
+        h = (C.c_uint8 * 64)()
+        check(lib.dimg_tp_exchange_handle(self._h, h))
+        return bytes(h)
+
+    def connect(self, handles) -> None:
+        """fused-ipc: map the peers' exchange blocks (handles in rank order)."""
+        if len(handles) != self.tp_size or any(len(h) != 64 for h in handles):
+            raise ValueError("connect: one 64-byte handle per rank")
+        buf = (C.c_uint8 * (64 * self.tp_size))(*b"".join(handles))
+        check(lib.dimg_tp_connect(self._h, buf))
+
+    def connect_group(self, group=None) -> None:
+        """fused-ipc: exchange the handles over torch.distributed and connect."""
+        import torch.distributed as dist
+        hs = [None] * self.tp_size
+        dist.all_gather_object(hs, self.exchange_handle(), group=group)
+        self.connect(hs)
 
     def info(self):
         b, n = C.c_uint64(), C.c_uint64()

@@ -1,8 +1,12 @@
 """Tensor parallelism on the GPU (BASELINE config C4).
 
-The sharded kernels run through dimg_tp with the "local" backend: all
-tp_size shards on cuda:0, the cross-rank sums of the pre-scale accumulators
-done by kernels (no kernel waits on another). Every generation must equal
+The sharded kernels run through dimg_tp on one GPU: the "local" backend
+(per-stage kernels for all tp_size shards on cuda:0, the cross-rank sums of
+the pre-scale accumulators done by kernels, no kernel waiting on another) and
+the "fused" backend (the persistent decode kernel of every shard in ONE
+cooperative launch, CTAs split between the ranks, the sums exchanged inside
+the WO / w_down epilogues through each rank's inbox -- the program the
+"fused-ipc" backend runs with one process per GPU over peer memory). Every generation must equal
 the REFERENCE's goldens -- tokens, BLAKE3 output hash and every kept logit
 -- at every tensor-parallel degree (proj/src/kernels.cpp:18-50: the int64
 accumulator sum is order-free). The NCCL backend's code path (all-reduce,
@@ -26,12 +30,16 @@ def _degrees(H):
     return [g for g in (1, 2, 3, 4, 8) if H % g == 0]
 
 
+BACKENDS = ["local", "fused"]
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
 @pytest.mark.parametrize("name", [n for n in SMALL if n not in ("micro_s9", "micro_s123456789")])
-def test_tp_generation_matches_reference(P, golden_models, name):
+def test_tp_generation_matches_reference(P, golden_models, name, backend):
     g = golden_models[name]
     m = _model_for(P, g)
     for deg in _degrees(g["config"][2]):
-        tp = P.TensorParallel(m, deg, backend="local", keep_logits_cap=g["max_new"])
+        tp = P.TensorParallel(m, deg, backend=backend, keep_logits_cap=g["max_new"])
         res = tp.generate_greedy(g["prompt"], g["max_new"], keep_logits=True)
         assert res.token_ids == g["tokens"], deg
         assert res.output_hash.hex() == g["output_hash"], deg
@@ -41,16 +49,18 @@ def test_tp_generation_matches_reference(P, golden_models, name):
         tp.close()
 
 
-def test_tp_wild_model_takes_the_wide_path(P, golden_models):
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_tp_wild_model_takes_the_wide_path(P, golden_models, backend):
     """wild_b's activations need the 8-limb GEMV path on every shard."""
     g = golden_models["wild_b"]
     m = _model_for(P, g)
     for deg in (2, 4, 8):
-        res = P.TensorParallel(m, deg).generate_greedy(g["prompt"], g["max_new"])
+        res = P.TensorParallel(m, deg, backend=backend).generate_greedy(g["prompt"], g["max_new"])
         assert res.output_hash.hex() == g["output_hash"], deg
 
 
-def test_tp_uneven_ffn_and_vocab_splits(P, oracle):
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_tp_uneven_ffn_and_vocab_splits(P, oracle, backend):
     """d_ffn and vocab not divisible by the degree (balanced blocks)."""
     from oracle.pyoracle import Config
     cfg6 = (2, 96, 6, 101, 77, 64)
@@ -59,7 +69,7 @@ def test_tp_uneven_ffn_and_vocab_splits(P, oracle):
     prompt = P.prompt_from_seed(6, cfg6[4], 9)
     toks, h, lg = oracle.generate_greedy(om, prompt, 7, keep_logits=True)
     for deg in (2, 3, 6):
-        res = P.TensorParallel(m, deg, keep_logits_cap=7).generate_greedy(prompt, 7, keep_logits=True)
+        res = P.TensorParallel(m, deg, backend=backend, keep_logits_cap=7).generate_greedy(prompt, 7, keep_logits=True)
         assert res.token_ids == [int(t) for t in toks] and res.output_hash.hex() == h, deg
         assert np.array_equal(np.stack(res.logits), lg), deg
 
@@ -74,6 +84,40 @@ def test_tp_nccl_backend_world_one(P, golden_models):
     assert res.output_hash.hex() == g["output_hash"]
     assert _digest(P, res.logits) == g["logits_digest"]
     tp.close()
+
+
+def test_tp_fused_repeat_and_timing(P, golden_models):
+    """The fused group 100x on one group (tags keep advancing across
+    launches, inboxes are reused), then the timed-decode entry point."""
+    g = golden_models["medium"]
+    m = _model_for(P, g)
+    tp = P.TensorParallel(m, 2, backend="fused")
+    for _ in range(100):
+        assert tp.generate_greedy(g["prompt"], g["max_new"]).output_hash.hex() == g["output_hash"]
+    ms = tp.time_decode(g["prompt"], g["max_new"])
+    assert ms > 0 and tp.tokens(g["max_new"]) == g["tokens"]
+    assert tp.info()["launches_per_step"] == 1
+    tp.close()
+
+
+def test_tp_fused_ipc_world_one(P, golden_models):
+    """The one-process-per-GPU fused backend's API at world size 1 (nothing
+    to map: the group is connected at creation)."""
+    g = golden_models["medium"]
+    m = _model_for(P, g)
+    tp = P.TensorParallel(m, 1, backend="fused-ipc", rank=0)
+    assert len(tp.exchange_handle()) == 64
+    with pytest.raises(P.LogicError):
+        tp.connect([tp.exchange_handle()])  # already connected
+    assert tp.generate_greedy(g["prompt"], g["max_new"]).output_hash.hex() == g["output_hash"]
+    with pytest.raises(P.InvalidArgument):
+        tp.generate_greedy(g["prompt"], 2, keep_logits=True)  # each process holds only its vocab slice
+    tp.close()
+    # a two-rank group is not usable before connect
+    tp2 = P.TensorParallel(m, 2, backend="fused-ipc", rank=0)
+    with pytest.raises(P.LogicError):
+        tp2.generate_greedy(g["prompt"], 2)
+    tp2.close()
 
 
 def test_tp_errors(P):
@@ -101,9 +145,10 @@ def model7b(P, golden_7b):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("backend", BACKENDS)
 @pytest.mark.parametrize("deg", [2, 4, 8])
-def test_tp_7b_c2_and_c4(P, golden_7b, model7b, deg):
-    tp = P.TensorParallel(model7b, deg, keep_logits_cap=128)
+def test_tp_7b_c2_and_c4(P, golden_7b, model7b, deg, backend):
+    tp = P.TensorParallel(model7b, deg, backend=backend, keep_logits_cap=128)
     g = golden_7b["c2"]
     prompt = P.prompt_from_seed(g["prompt_seed"], g["config"][4], g["P"])
     res = tp.generate_greedy(prompt, g["max_new"], keep_logits=True)
