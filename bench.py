@@ -11,15 +11,23 @@ A step is one greedy decode token: one full forward of the 32-layer model
   N = 1   the persistent decode kernel (one launch for all K steps).
   N > 1   (torchrun, one process per GPU) TENSOR PARALLEL decode of the same
           single sequence (BASELINE configs[3]): each rank holds
-          1/N of every matrix, the pre-scale WO / w_down accumulators are
-          NCCL all-reduced (uint64 sum), the lm_head argmax pairs all-gathered;
+          1/N of every matrix and runs the persistent decode kernel on it;
+          the pre-scale WO / w_down accumulators (uint64 sums) and the
+          lm_head argmax pairs are exchanged INSIDE that kernel over NVLink
+          peer memory (backend "fused-ipc": CUDA IPC handles gathered over
+          torch.distributed, no collective call per layer);
           value = K / max-over-ranks time (strong scaling: the work per token
           is fixed, each GPU streams 1/N of it). The tokens are checked
           against the C2 golden. Extra keys at N > 1:
+            tp_nccl  the same decode with per-stage GEMVs + NCCL all-reduce
+                     (the collective-library baseline)
             c5  every rank generates its 8 C5 sequences through the batch
                 call (seqs 8r .. 8r+7), per-sequence hashes vs the goldens
             dp  every rank decodes its own sequence with the single-GPU
                 kernel (weak-scaling replicas, the N = 1 kernel's aggregate)
+          At N = 1, tp_one_gpu: the fused group program for g = 2, 4, 8 with
+          all g shards on this one GPU (one cooperative launch, ranks share
+          its HBM and SMs): the in-kernel exchange's cost, not a scaling figure.
 
 Keys beyond the base contract:
   e2e           the same metric through the reference-shaped C-ABI call
@@ -425,6 +433,27 @@ def blake3_leg(P, mf, dev, peak_gbs):
         return {"workload": "BLAKE3", "unavailable": str(e)}
 
 
+def tp_one_gpu(P, mf, prompt, gold, steps):
+    """The fused tensor-parallel program for g = 2, 4, 8 with every shard on
+    this one GPU (backend "fused": one cooperative launch, the g ranks' CTAs
+    share its SMs and HBM and exchange through device memory). Per-token time
+    against the single-GPU kernel = the cost of the in-kernel exchange and of
+    the narrower per-rank grids -- not a multi-GPU scaling number."""
+    out = {"workload": "C2 decode, fused TP program, all g shards on one GPU", "steps": steps}
+    try:
+        for g in (2, 4, 8):
+            tp = P.TensorParallel(mf, g, backend="fused")
+            tp.time_decode(prompt, 8)
+            ms = tp.time_decode(prompt, steps)
+            toks = tp.tokens(steps)
+            n = min(len(toks), len(gold.get("tokens", [])))
+            out[f"g{g}"] = {"ms_per_step": ms / steps, "tokens_match_c2_golden": toks[:n] == gold["tokens"][:n]}
+            tp.close()
+    except Exception as e:  # reported, not fatal to the headline
+        out["error"] = repr(e)
+    return out
+
+
 def run_ours(args, rank, world, local):
     import paper_2603_24904_b200 as P
     dist = None
@@ -479,33 +508,34 @@ def run_ours(args, rank, world, local):
             e2e_call = "dimg_generate_greedy(prompt 16 -> 128 tokens, BLAKE3 on host)"
             extra = {}
         else:
-            # tensor parallel: rank 0 makes the NCCL id, torch.distributed carries it
-            obj = [P.nccl_unique_id() if rank == 0 else None]
-            if dist is not None:
-                dist.broadcast_object_list(obj, src=0)
-            tp = P.TensorParallel(mf, world, backend="nccl", rank=rank, nccl_id=obj[0], device=dev)
-            tp.time_decode(prompt, args.warmup)  # warm: graphs captured, NCCL channels up
+            # tensor parallel, fused: every rank's persistent kernel exchanges
+            # the partial sums over peer memory (handles via torch.distributed)
+            tp = P.TensorParallel(mf, world, backend="fused-ipc", rank=rank, device=dev)
+            if world > 1:
+                tp.connect_group()
+            tp.time_decode(prompt, args.warmup)  # warm
             barrier()
             with ClockSampler(dev) as clk:
                 ms = tp.time_decode(prompt, args.warmup + args.steps)
                 ms_w = tp.time_decode(prompt, args.warmup)
             barrier()
-            # the K steps after W warm ones: difference of two CUDA-event timed runs
+            # the K steps after W warm ones: difference of two CUDA-event timed launches
             ms = max(ms - ms_w, 1e-6)
             toks = tp.tokens(args.warmup + args.steps)
             info = tp.info()
-            gpu_launches = info["launches_per_step"] * args.steps
-            kernel = "per-stage GEMVs + NCCL all-reduce (per decode step, per GPU)"
+            gpu_launches = 2  # the two timed persistent launches (all their steps inside)
+            kernel = "decode_persistent_kernel on the rank's shard, WO/w_down sums exchanged in-kernel (per step, per GPU)"
             tp.generate_greedy(prompt, 128)  # warm
             barrier()
             t1 = time.perf_counter()
             for _ in range(3):
                 res = tp.generate_greedy(prompt, 128)
             e2e_s = (time.perf_counter() - t1) / 3
-            e2e_call = "dimg_tp_generate_greedy(prompt 16 -> 128 tokens, BLAKE3 on host), NCCL tp"
+            e2e_call = "dimg_tp_generate_greedy(prompt 16 -> 128 tokens, BLAKE3 on host), fused-ipc tp"
             tp.close()
-            extra = {"nccl": {"backend": "nccl", "ranks": world, "rank0_comm_init": "ncclCommInitRank",
-                              "weight_bytes_per_rank": info["weight_bytes"]}}
+            extra = {"tp_group": {"backend": "fused-ipc", "ranks": world, "exchange": "CUDA IPC peer memory, in-kernel",
+                                  "handles_gathered_over": "torch.distributed (nccl process group)",
+                                  "weight_bytes_per_rank": info["weight_bytes"]}}
     ms_max = allreduce(ms, dist.ReduceOp.MAX if dist else None)
     e2e_s = allreduce(e2e_s, dist.ReduceOp.MAX if dist else None)
     per_step_ms = ms_max / args.steps
@@ -555,6 +585,26 @@ def run_ours(args, rank, world, local):
         dms = allreduce(sess.time_decode(args.steps), dist.ReduceOp.MAX)
         dp = {"workload": f"{world} independent batch-1 sequences, one per GPU (persistent kernel)",
               "tokens_per_s": world * args.steps / (dms / 1e3), "ms_per_step": dms / args.steps}
+    tp_nccl = tp_one = None
+    if world > 1 and legs:
+        # the collective-library baseline of the same TP decode: per-stage
+        # GEMVs + ncclAllReduce (rank 0 makes the NCCL id)
+        obj = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        tpn = P.TensorParallel(mf, world, backend="nccl", rank=rank, nccl_id=obj[0], device=dev)
+        tpn.time_decode(prompt, args.warmup)
+        barrier()
+        nms = tpn.time_decode(prompt, args.warmup + args.steps) - tpn.time_decode(prompt, args.warmup)
+        nms = allreduce(max(nms, 1e-6), dist.ReduceOp.MAX)
+        ntok = tpn.tokens(args.warmup + args.steps)
+        nn = min(len(ntok), len(gold.get("tokens", [])))
+        tp_nccl = {"workload": f"C4/C2 tensor parallel tp{world}: per-stage GEMVs + ncclAllReduce",
+                   "tokens_per_s": args.steps / (nms / 1e3), "ms_per_step": nms / args.steps,
+                   "launches_per_step": tpn.info()["launches_per_step"], "nccl_comm_init": "ncclCommInitRank",
+                   "tokens_match_c2_golden": ntok[:nn] == gold["tokens"][:nn] if nn else None}
+        tpn.close()
+    if world == 1 and rank == 0 and legs:
+        tp_one = tp_one_gpu(P, mf, prompt, gold, args.steps)
 
     if rank == 0:
         line = {
@@ -577,6 +627,8 @@ def run_ours(args, rank, world, local):
             "batch": batch if world == 1 else None,
             "c5": c5,
             "dp": dp,
+            "tp_nccl": tp_nccl,
+            "tp_one_gpu": tp_one,
             "blake3": blake3,
             "tokens_head": toks[:8],
         }
