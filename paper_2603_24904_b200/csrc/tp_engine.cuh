@@ -385,6 +385,15 @@ void tp_gather_logits(dimg_tp& t, int64_t* out) {
 
 // ---- fused backends --------------------------------------------------------------
 
+// Experiment knob (tools/tp_fused_probe.py --solo): DIMG_TP_SOLO=1 runs a
+// DIMG_TP_FUSED_IPC rank alone, WITHOUT the exchange (tp_g forced to 1): the
+// per-GPU cost of a g-way shard on a whole GPU, minus the peer latency. Its
+// tokens are wrong by construction (partial sums); never a product path.
+bool tp_solo() {
+    const char* e = std::getenv("DIMG_TP_SOLO");
+    return e && std::atoi(e) != 0;
+}
+
 void tpf_require_connected(const dimg_tp& t) {
     if (t.fused && !t.connected) fail(DIMG_ELOGIC, "tp: dimg_tp_connect the group before generating");
 }
@@ -421,6 +430,10 @@ void tpf_launch(dimg_tp& t, uint32_t n_steps, uint32_t n_prefill) {
             a.tp_parts[q] = t.xch[q] + t.inbox_elems;
         }
         a.parts_w = a.tp_parts[a.tp_rank];
+        if (t.backend == DIMG_TP_FUSED_IPC && tp_solo()) {  // timing experiment only (see tp_solo)
+            a.tp_g = 1;
+            a.parts_w = t.xch[t.rank] + t.inbox_elems;
+        }
         CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned int), t.st));
         CK(cudaMemsetAsync(s.ssq, 0, size_t(2) * m.L * sizeof(unsigned long long), t.st));
         args.push_back(a);
@@ -534,7 +547,7 @@ dimg_status dimg_tp_create(int device, const dimg_model_desc* desc, int backend,
             }
             t->ranks.push_back(std::move(rk));
         }
-        t->connected = backend != DIMG_TP_FUSED_IPC || tp_size == 1;
+        t->connected = backend != DIMG_TP_FUSED_IPC || tp_size == 1 || tp_solo();
         if (fused) t->launches_per_step = 1;  // at most: one launch runs all the steps of a call
         if (backend == DIMG_TP_NCCL) {
             ncclUniqueId u;
