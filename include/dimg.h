@@ -124,6 +124,9 @@ dimg_status dimg_rtab_load(const char* path, uint8_t* out, size_t cap, size_t* n
 /* The 257-entry exp LUT (q16.cpp:70-79) and 64 Q48 inv-sqrt seeds (:28-43). */
 dimg_status dimg_exp_lut(int64_t out[257]);
 dimg_status dimg_invsqrt_seeds(int64_t out[64]);
+/* inv_sqrt_q16 (proj/src/q16.cpp:56-68) as the device kernels compute it
+ * (kernels/q16.cuh), on the host: parity checks of its 64-bit fast path. */
+dimg_status dimg_inv_sqrt_q16(int64_t x, int64_t* out);
 
 /* Host model container: the canonical DIM1 bytes (ModelFile::bytes) plus
  * views into them (proj/include/dim/model.hpp:50-60). */

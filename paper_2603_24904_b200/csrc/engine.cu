@@ -1485,6 +1485,26 @@ dimg_status dimg_model_free(dimg_model* m) {
     })
 }
 
+dimg_status dimg_inv_sqrt_q16(int64_t x, int64_t* out) {
+    // the device kernels' inv_sqrt_q16 (kernels/q16.cuh: the 64-bit Newton
+    // path, else int128), run on the host -- for its parity test
+    DIMG_API_GUARD({
+        if (x <= 0) fail(DIMG_EDOMAIN, "inv_sqrt_q16: input must be positive");
+        const int b = 63 - __builtin_clzll(uint64_t(x));
+        int64_t r = inv_sqrt_q16_u64(x, b, invsqrt_seed(b));
+        if (r < 0) {
+            __int128 y = invsqrt_seed(b);
+            for (int it = 0; it < 3; ++it) {
+                __int128 t = (y * y) >> 48;
+                __int128 u = (__int128(x) * t) >> 16;
+                y = (y * ((__int128(3) << 48) - u)) >> 49;
+            }
+            r = int64_t((y + (__int128(1) << 31)) >> 32);
+        }
+        *out = r;
+    })
+}
+
 dimg_status dimg_model_bytes_on_device(const dimg_model* m, uint64_t* bytes) {
     DIMG_API_GUARD(*bytes = m->mem.bytes)
 }

@@ -583,7 +583,7 @@ __device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_un
         // products are 32 x 32 bits throughout.
         if (threadIdx.x == 0) {
             const uint64_t ss = uint64_t(ld_cg64(reinterpret_cast<const int64_t*>(ssq_in)));
-            const int64_t ms = int64_t((ss / K) >> 16);
+            const int64_t ms = int64_t(((K & (K - 1)) ? ss / K : ss >> (__ffs(K) - 1)) >> 16);
             s_r = inv_sqrt_q16(ms + 1, seeds);  // ms >= 0: ms + 1 > 0
         }
         int32_t* xs32 = reinterpret_cast<int32_t*>(xb);
@@ -812,7 +812,7 @@ __device__ __noinline__ int prologue_norm_words(uint32_t K, uint32_t Kp, bool ga
     if (threadIdx.x == 0) {
         uint64_t t = 0;
         for (int w = 0; w < PK_WARPS; ++w) t += s_ss[w];
-        const int64_t ms = int64_t((t / K) >> 16);
+        const int64_t ms = int64_t(((K & (K - 1)) ? t / K : t >> (__ffs(K) - 1)) >> 16);  // d_model 2^k: a shift
         s_r2 = inv_sqrt_q16(ms + 1, seeds);  // ms >= 0: ms + 1 > 0
     }
     __syncthreads();

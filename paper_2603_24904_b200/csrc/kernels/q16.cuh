@@ -94,10 +94,49 @@ __device__ __forceinline__ int64_t add_clamp(int64_t a, int64_t b) {
     return s > ACT_CLAMP ? ACT_CLAMP : (s < -ACT_CLAMP ? -ACT_CLAMP : s);
 }
 
+// floor(a b / 2^s) for 0 < s < 64; *ok cleared if the quotient needs more
+// than 64 bits.
+__host__ __device__ __forceinline__ uint64_t mul_shr_u64(uint64_t a, uint64_t b, int s, bool* ok) {
+#ifdef __CUDA_ARCH__
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+#else
+    const unsigned __int128 p = (unsigned __int128)a * b;
+    const uint64_t lo = uint64_t(p), hi = uint64_t(p >> 64);
+#endif
+    if (hi >> s) *ok = false;
+    return (lo >> s) | (hi << (64 - s));
+}
+
+// The same three Newton steps on 64-bit words: for x >= 16 every quantity
+// is non-negative and bounded -- the octave seed y0 = 2^(56 - b/2 - 1/4) is
+// within 2^(+-1/4) of 2^56 / sqrt(x), so y <= 2^54.3, t = y^2 >> 48 < 2^61,
+// u = x t >> 16 < 2^48.6 < 3 * 2^48, and y (3 * 2^48 - u) < 2^105 -- so each
+// int128 product of the reference is one exact 64 x 64 -> 128-bit product
+// whose shifted quotient fits 64 bits, and the floors agree (no negative
+// values). Returns -1 where that does not hold (x < 16, u >= 3 * 2^48, a
+// quotient above 2^64), and the caller takes the int128 path. tests/test_host.py checks it against
+// the oracle's int128 routine over every octave.
+__host__ __device__ __forceinline__ int64_t inv_sqrt_q16_u64(int64_t x, int b, int64_t seed) {
+    if (b < 4 || seed <= 0) return -1;
+    const uint64_t three = uint64_t(3) << 48;
+    uint64_t y = uint64_t(seed);
+    bool ok = true;
+    for (int it = 0; it < 3; ++it) {
+        const uint64_t t = mul_shr_u64(y, y, 48, &ok);
+        const uint64_t u = mul_shr_u64(uint64_t(x), t, 16, &ok);
+        if (u >= three) return -1;
+        y = mul_shr_u64(y, three - u, 49, &ok);
+    }
+    if (!ok || (y >> 62)) return -1;
+    return int64_t((y + (uint64_t(1) << 31)) >> 32);
+}
+
 // inv_sqrt_q16: octave seed (host-built Q48 table) + three Newton steps at
 // Q48 in int128, rounded to Q16 (proj/src/q16.cpp:56-68). x > 0.
 __device__ __noinline__ int64_t inv_sqrt_q16(int64_t x, const int64_t* seeds) {
     int b = 63 - __clzll(x);
+    const int64_t f = inv_sqrt_q16_u64(x, b, seeds[b]);
+    if (f >= 0) return f;
     i128 y = seeds[b];
     const i128 three = i128(3) << 48;
 #pragma unroll

@@ -219,3 +219,21 @@ def test_rtab_save_load_roundtrip(tmp_path):
         P.load_rope_tables(str(tmp_path / "missing.rtab"))
     with pytest.raises(P.errors.IOFailure):
         P.save_rope_tables(t, str(tmp_path / "no" / "dir.rtab"))
+
+
+def test_inv_sqrt_fast_path_matches_oracle(P, oracle):
+    """The kernels' inv_sqrt_q16 (64-bit Newton steps where every product
+    provably fits, the int128 steps otherwise; kernels/q16.cuh) against the
+    oracle's int128 restatement of q16.cpp:56-68: every octave's ends, a
+    spread inside each octave, and all x < 2^14."""
+    from paper_2603_24904_b200._lib import lib
+    rng = np.random.default_rng(5)
+    xs = set(range(1, 1 << 14))
+    for b in range(63):
+        lo, hi = 1 << b, (1 << (b + 1)) - 1
+        xs.update({lo, lo + 1, hi, hi - 1, (lo + hi) // 2})
+        xs.update(int(v) for v in rng.integers(lo, hi, size=64, endpoint=True, dtype=np.uint64))
+    out = C.c_int64()
+    for x in sorted(v for v in xs if v > 0):
+        assert lib.dimg_inv_sqrt_q16(x, C.byref(out)) == 0
+        assert out.value == oracle.lib.orc_inv_sqrt(x), x
