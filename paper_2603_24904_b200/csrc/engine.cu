@@ -1067,6 +1067,12 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
     const char* sk = std::getenv("DIMG_SPLITK");
     const bool split_k = sk ? std::atoi(sk) != 0 : true;
     int sms = m.ctx->sm_count;
+    // DIMG_BD_SKIP (timing experiments only; results are wrong): bit 0 skips
+    // the norms, 1 RoPE/KV, 2 attention -- what each launch chain costs
+    static const uint32_t skip = [] {
+        const char* e = std::getenv("DIMG_BD_SKIP");
+        return e ? uint32_t(std::strtoul(e, nullptr, 0)) : 0u;
+    }();
     auto gemm = [&](const DevMat& W, const CUtensorMap& tb_big, uint32_t epi, void* y, uint32_t ldy) {
         const bool in_h = &tb_big == &r.tm_ph;
         const CUtensorMap& tb = small ? (in_h ? r.tm_ph_s : r.tm_pa_s) : tb_big;
@@ -1095,7 +1101,7 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
         a.tile_cnt = r.tile_cnt;
         launch_limb_gemm(W.tmap, tb, a, st, bn, true);
     };
-    auto norm = [&](const int64_t* g, int unit) {  // decode steps: a CTA cluster per token
+    auto norm_ = [&](const int64_t* g, int unit) {  // decode steps: a CTA cluster per token
         if (n <= 64u)
             launch_k(true, bd_norm_cluster_kernel, n * BD_NCL, 256, 0, st, (const int32_t*)r.x, D, g, unit,
                      (const int64_t*)m.ctx->seeds, r.pa, r.nmax_pad, m.Kd, r.wide);
@@ -1104,15 +1110,18 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
                      (const int64_t*)m.ctx->seeds, r.pa, r.nmax_pad, m.Kd, r.wide);
     };
     const size_t asmem = bd_attn_smem(dh, r.ctx) + 8;
+    auto norm = [&](const int64_t* g, int unit) {
+        if (!(skip & 1)) norm_(g, unit);
+    };
     for (uint32_t l = 0; l < m.L; ++l) {
         const auto& lw = m.layers[l];
         norm(lw.attn_norm, lw.attn_unit);
         gemm(lw.qkv, r.tm_pa, TG_STORE, r.qkv, 3 * D);
-        launch_k(true, bd_rope_kv_kernel, dim3(n, H), dh / 2, 0, st, r.qkv, bt, D, dh, (const int64_t*)m.rope_cos,
+        if (!(skip & 2)) launch_k(true, bd_rope_kv_kernel, dim3(n, H), dh / 2, 0, st, r.qkv, bt, D, dh, (const int64_t*)m.rope_cos,
                  (const int64_t*)m.rope_sin, r.K32 + l * r.layer_stride, r.V32 + l * r.layer_stride, r.seq_stride,
                  r.ctx, r.wide);
         if (l + 1 == m.L && !logits) break;  // prompt positions only feed the KV caches
-        launch_k(true, bd_attn_kernel, dim3(H, n), BD_THREADS, asmem, st, (const int64_t*)r.qkv, bt, D, dh,
+        if (!(skip & 4)) launch_k(true, bd_attn_kernel, dim3(H, n), BD_THREADS, asmem, st, (const int64_t*)r.qkv, bt, D, dh,
                  (const int32_t*)(r.K32 + l * r.layer_stride), (const int32_t*)(r.V32 + l * r.layer_stride),
                  r.seq_stride, r.ctx, m.inv_scale, (const int64_t*)m.ctx->exp_lut, r.pa, r.nmax_pad, m.Kd, r.wide);
         gemm(lw.wo, r.tm_pa, TG_RESID, r.x, D);

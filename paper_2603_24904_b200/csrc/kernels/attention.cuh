@@ -67,6 +67,54 @@ __device__ __forceinline__ void softmax_strip_inl(int64_t* S, uint32_t n, const 
     __syncthreads();
 }
 
+// softmax_q16 over S[0..n) in place (proj/src/kernels.cpp:90-107), the same
+// arithmetic as softmax_strip with fewer round trips: the int64 max as two
+// 32-bit REDUX steps, the weights (<= 2^16 each, n <= 2^19) summed in 32 bits
+// per warp, and the per-element division (w << 16) / total as a multiply by
+// floor((2^64 - 1) / total) plus one exact correction step.
+__device__ __forceinline__ void softmax_strip_fast(int64_t* S, uint32_t n, const int64_t* lut, u128* red) {
+    if (n > (1u << 19)) {  // the 32-bit warp sums could overflow: the plain version
+        softmax_strip_inl(S, n, lut, red);
+        return;
+    }
+    int64_t* smax = reinterpret_cast<int64_t*>(red);           // [8]
+    uint32_t* ssum = reinterpret_cast<uint32_t*>(smax + 8);    // [8]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t m = INT64_MIN;
+#pragma unroll 1
+    for (uint32_t t = threadIdx.x; t < n; t += ATTN_THREADS) m = S[t] > m ? S[t] : m;
+    const int32_t mh = __reduce_max_sync(0xffffffffu, int32_t(uint64_t(m) >> 32));
+    const uint32_t ml = __reduce_max_sync(0xffffffffu, int32_t(uint64_t(m) >> 32) == mh ? uint32_t(m) : 0u);
+    if (lane == 0) smax[warp] = int64_t((uint64_t(uint32_t(mh)) << 32) | ml);
+    __syncthreads();
+    m = smax[0];
+#pragma unroll
+    for (int w = 1; w < ATTN_THREADS / 32; ++w) m = smax[w] > m ? smax[w] : m;
+    uint32_t tot = 0;
+#pragma unroll 1
+    for (uint32_t t = threadIdx.x; t < n; t += ATTN_THREADS) {
+        const int64_t d = wrap_sub(m, S[t]);
+        const int64_t w = exp_neg(d > 8 * ONE ? 8 * ONE : d, lut);
+        S[t] = w;
+        tot += uint32_t(w);
+    }
+    tot = __reduce_add_sync(0xffffffffu, tot);
+    if (lane == 0) ssum[warp] = tot;
+    __syncthreads();
+    uint64_t total = 0;
+#pragma unroll
+    for (int w = 0; w < ATTN_THREADS / 32; ++w) total += ssum[w];
+    const uint64_t inv = ~0ull / total;
+#pragma unroll 1
+    for (uint32_t t = threadIdx.x; t < n; t += ATTN_THREADS) {
+        const uint64_t a = uint64_t(S[t]) << 16;
+        uint64_t q = __umul64hi(a, inv);  // floor(a / total) or one less
+        q += (a - q * total) >= total;
+        S[t] = int64_t(q);
+    }
+    __syncthreads();
+}
+
 __device__ __noinline__ void softmax_strip(int64_t* S, uint32_t n, const int64_t* lut, u128* red) {
     softmax_strip_inl(S, n, lut, red);
 }

@@ -143,7 +143,7 @@ __global__ void __cluster_dims__(BD_NCL, 1, 1) __launch_bounds__(256)
 constexpr int BD_THREADS = 256;
 
 __host__ __device__ constexpr size_t bd_attn_smem(uint32_t dh, uint32_t ctx) {
-    return size_t(ctx) * 8 + size_t(dh) * 4 + size_t(BD_THREADS) * 8;
+    return size_t(ctx) * 8 + size_t(dh) * 4 + size_t(BD_THREADS) * 8 * 4;
 }
 
 // attention_step (proj/src/kernels.cpp:117-177) of token t against positions
@@ -167,13 +167,95 @@ __global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __re
     const uint32_t b = bt.seq[t], T = bt.pos[t] + 1;
     int64_t* S = reinterpret_cast<int64_t*>(bd_smem);              // [ctx]
     int32_t* q = reinterpret_cast<int32_t*>(S + ctx);              // [dh]
-    uint64_t* part = reinterpret_cast<uint64_t*>(q + dh + (dh & 1));  // [BD_THREADS]
+    uint64_t* part = reinterpret_cast<uint64_t*>(q + dh + (dh & 1));  // [4 * BD_THREADS]
     for (uint32_t j = threadIdx.x; j < dh; j += BD_THREADS) q[j] = int32_t(qkv[size_t(t) * 3 * D + size_t(h) * dh + j]);
     __syncthreads();
     const int32_t* Kh = K32 + size_t(b) * seq_stride + size_t(h) * ctx * dh;
     const int32_t* Vh = V32 + size_t(b) * seq_stride + size_t(h) * ctx * dh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int big = 0;
+    const size_t plane = size_t(rows_pad) * ldp;
+    if ((dh & 3) == 0 && dh <= 512) {
+        // The decode kernel's layout (persistent.cuh attn_split), so a step
+        // costs a few memory round trips instead of one per position group:
+        // scores -- an octet of lanes per position, 64 positions' K rows in
+        // flight per pass, each lane 4 dims of every 32; the int64 sums are
+        // exact (|q| < 2^23, |k| < 2^31, dh <= 512).
+        const uint32_t oc = threadIdx.x >> 3, e = threadIdx.x & 7;
+        constexpr uint32_t NOCT = BD_THREADS / 8;
+        for (uint32_t b0 = 0; b0 < T; b0 += 2 * NOCT) {
+            const uint32_t ta = b0 + oc, tb = ta + NOCT;
+            int64_t da = 0, db = 0;
+            for (uint32_t c0 = 0; c0 < dh; c0 += 128) {
+                int4 ka[4], kb[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t j = c0 + 4 * e + 32 * u;
+                    ka[u] = (j < dh && ta < T) ? *reinterpret_cast<const int4*>(Kh + size_t(ta) * dh + j) : make_int4(0, 0, 0, 0);
+                    kb[u] = (j < dh && tb < T) ? *reinterpret_cast<const int4*>(Kh + size_t(tb) * dh + j) : make_int4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t j = c0 + 4 * e + 32 * u;
+                    const int4 qq = j < dh ? *reinterpret_cast<const int4*>(q + j) : make_int4(0, 0, 0, 0);
+                    da += int64_t(qq.x) * ka[u].x + int64_t(qq.y) * ka[u].y + int64_t(qq.z) * ka[u].z +
+                          int64_t(qq.w) * ka[u].w;
+                    db += int64_t(qq.x) * kb[u].x + int64_t(qq.y) * kb[u].y + int64_t(qq.z) * kb[u].z +
+                          int64_t(qq.w) * kb[u].w;
+                }
+            }
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                da += __shfl_xor_sync(0xffffffffu, da, o);
+                db += __shfl_xor_sync(0xffffffffu, db, o);
+            }
+            if (e == 0) {
+                if (ta < T) S[ta] = mul16(da >> 16, inv_scale);
+                if (tb < T) S[tb] = mul16(db >> 16, inv_scale);
+            }
+        }
+        __syncthreads();
+        softmax_strip_fast(S, T, lut, red);  // ends with a barrier
+        // PV: thread = (4-dim quad, position slice), 8 V rows in flight;
+        // p <= 2^16 and |v| < 2^31: floor(p v / 2^16) is one exact 64-bit
+        // product (mul16_prob's int32 case)
+        const uint32_t nq = dh / 4, slices = BD_THREADS / nq;
+        const uint32_t jq = threadIdx.x % nq, sl = threadIdx.x / nq;
+        int64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        if (sl < slices) {
+            constexpr int U = 8;
+            for (uint32_t p = sl; p < T; p += U * slices) {
+                int4 vv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t tt = p + u * slices;
+                    vv[u] = tt < T ? *reinterpret_cast<const int4*>(Vh + size_t(tt) * dh + 4 * jq) : make_int4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t tt = p + u * slices;
+                    const int64_t pr = tt < T ? S[tt] : 0;
+                    a0 += (pr * vv[u].x) >> 16;
+                    a1 += (pr * vv[u].y) >> 16;
+                    a2 += (pr * vv[u].z) >> 16;
+                    a3 += (pr * vv[u].w) >> 16;
+                }
+            }
+        }
+        part[4 * threadIdx.x + 0] = uint64_t(a0);
+        part[4 * threadIdx.x + 1] = uint64_t(a1);
+        part[4 * threadIdx.x + 2] = uint64_t(a2);
+        part[4 * threadIdx.x + 3] = uint64_t(a3);
+        __syncthreads();
+        for (uint32_t jj = threadIdx.x; jj < dh; jj += BD_THREADS) {
+            const uint32_t qd = jj >> 2, z = jj & 3;
+            uint64_t sum = 0;
+            for (uint32_t s2 = 0; s2 < slices; ++s2) sum += part[4 * (s2 * nq + qd) + z];
+            if (!put_sdigits(planes + size_t(t) * ldp + h * dh + jj, plane, int64_t(sum))) big = 1;
+        }
+        if (big) *wide = 1;
+        return;
+    }
     // four positions per warp per pass, their row loads in flight together
     for (uint32_t p0 = 4 * warp; p0 < T; p0 += 4 * (BD_THREADS / 32)) {
         int64_t d[4] = {0, 0, 0, 0};
@@ -215,7 +297,6 @@ __global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __re
     }
     part[threadIdx.x] = acc;
     __syncthreads();
-    const size_t plane = size_t(rows_pad) * ldp;
     for (uint32_t jj = threadIdx.x; jj < dh; jj += BD_THREADS) {
         uint64_t sum = 0;
         if (dh <= BD_THREADS) {
