@@ -1117,13 +1117,15 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
         const auto& lw = m.layers[l];
         norm(lw.attn_norm, lw.attn_unit);
         gemm(lw.qkv, r.tm_pa, TG_STORE, r.qkv, 3 * D);
-        if (!(skip & 2)) launch_k(true, bd_rope_kv_kernel, dim3(n, H), dh / 2, 0, st, r.qkv, bt, D, dh, (const int64_t*)m.rope_cos,
+        // decode steps: RoPE + the KV append run inside the attention kernel
+        if (!(skip & 2) && !logits) launch_k(true, bd_rope_kv_kernel, dim3(n, H), dh / 2, 0, st, r.qkv, bt, D, dh, (const int64_t*)m.rope_cos,
                  (const int64_t*)m.rope_sin, r.K32 + l * r.layer_stride, r.V32 + l * r.layer_stride, r.seq_stride,
                  r.ctx, r.wide);
         if (l + 1 == m.L && !logits) break;  // prompt positions only feed the KV caches
         if (!(skip & 4)) launch_k(true, bd_attn_kernel, dim3(H, n), BD_THREADS, asmem, st, (const int64_t*)r.qkv, bt, D, dh,
-                 (const int32_t*)(r.K32 + l * r.layer_stride), (const int32_t*)(r.V32 + l * r.layer_stride),
-                 r.seq_stride, r.ctx, m.inv_scale, (const int64_t*)m.ctx->exp_lut, r.pa, r.nmax_pad, m.Kd, r.wide);
+                 r.K32 + l * r.layer_stride, r.V32 + l * r.layer_stride, r.seq_stride, r.ctx, m.inv_scale,
+                 (const int64_t*)m.ctx->exp_lut, r.pa, r.nmax_pad, m.Kd, r.wide,
+                 logits ? (const int64_t*)m.rope_cos : nullptr, logits ? (const int64_t*)m.rope_sin : nullptr);
         gemm(lw.wo, r.tm_pa, TG_RESID, r.x, D);
         norm(lw.ffn_norm, lw.ffn_unit);
         gemm(lw.gu, r.tm_pa, TG_SILU, nullptr, 0);

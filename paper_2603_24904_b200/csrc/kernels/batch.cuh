@@ -90,7 +90,6 @@ __global__ void __cluster_dims__(BD_NCL, 1, 1) __launch_bounds__(256)
                            int gamma_unit, const int64_t* __restrict__ seeds, uint8_t* planes, uint32_t rows_pad,
                            uint32_t ldp, uint32_t* wide) {
     namespace cg = cooperative_groups;
-    __shared__ u128 red[32];
     __shared__ u128 part;
     __shared__ int64_t s_r;
     cg::cluster_group cl = cg::this_cluster();
@@ -101,21 +100,48 @@ __global__ void __cluster_dims__(BD_NCL, 1, 1) __launch_bounds__(256)
     const int32_t* xr = x + size_t(t) * K;
     constexpr int PER = 4;  // elements per thread in registers (K <= 4096)
     int64_t v[PER];
-    u128 ss = 0;
+    // x^2 < 2^62 (int32 x) in three 21-bit chunks: per thread <= 8 elements
+    // (K <= 8192), so every warp total is < 2^29 -- one REDUX per chunk
+    uint32_t c0 = 0, c1 = 0, c2 = 0;
+    const auto add_sq = [&](int64_t x) {
+        const uint64_t q2 = uint64_t(x * x);
+        c0 += uint32_t(q2) & 0x1FFFFFu;
+        c1 += uint32_t(q2 >> 21) & 0x1FFFFFu;
+        c2 += uint32_t(q2 >> 42);
+    };
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
         const uint32_t j = j0 + threadIdx.x + u * 256;
         v[u] = j < j1 ? xr[j] : 0;
-        ss += mul_full(v[u], v[u]);
+        add_sq(v[u]);
     }
-    for (uint32_t j = j0 + threadIdx.x + PER * 256; j < j1; j += 256) ss += mul_full(int64_t(xr[j]), int64_t(xr[j]));
-    ss = block_sum_u128(ss, red);
-    if (threadIdx.x == 0) part = ss;
+    for (uint32_t j = j0 + threadIdx.x + PER * 256; j < j1; j += 256) add_sq(int64_t(xr[j]));
+    __shared__ uint32_t s_c[8][3];
+    c0 = __reduce_add_sync(0xffffffffu, c0);
+    c1 = __reduce_add_sync(0xffffffffu, c1);
+    c2 = __reduce_add_sync(0xffffffffu, c2);
+    if ((threadIdx.x & 31) == 0) {
+        s_c[threadIdx.x >> 5][0] = c0;
+        s_c[threadIdx.x >> 5][1] = c1;
+        s_c[threadIdx.x >> 5][2] = c2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t t0 = 0, t1 = 0, t2 = 0;
+        for (int w = 0; w < 8; ++w) {
+            t0 += s_c[w][0];
+            t1 += s_c[w][1];
+            t2 += s_c[w][2];
+        }
+        part = u128(t0) + (u128(t1) << 21) + (u128(t2) << 42);
+    }
     cl.sync();
     if (threadIdx.x == 0) {
         u128 tot = 0;
         for (uint32_t r = 0; r < BD_NCL; ++r) tot += *cl.map_shared_rank(&part, r);
-        const int64_t ms = (tot >> 63) == 0 ? int64_t((uint64_t(tot) / K) >> 16) : int64_t((i128(tot) / i128(K)) >> 16);
+        const int64_t ms = (tot >> 63) != 0          ? int64_t((i128(tot) / i128(K)) >> 16)
+                           : (K & (K - 1)) == 0       ? int64_t((uint64_t(tot) >> (__ffs(K) - 1)) >> 16)
+                                                      : int64_t((uint64_t(tot) / K) >> 16);
         s_r = ms + 1 > 0 ? inv_sqrt_q16(ms + 1, seeds) : 0;
         if (ms + 1 <= 0) *wide = 1;  // the reference throws (domain_error): the exact path reports it
     }
@@ -151,12 +177,17 @@ __host__ __device__ constexpr size_t bd_attn_smem(uint32_t dh, uint32_t ctx) {
 // warp per position, lanes over 4-dim quads), the softmax of softmax_q16 over
 // the strip in shared memory, the per-product floor of mul16(p, v).
 // grid (H, n); writes the limb planes of the attention vector, row t.
+// rc != nullptr (decode steps: one token per sequence, so no other CTA
+// reads this (sequence, head) row): the CTA also does bd_rope_kv_kernel's
+// work for its head first -- RoPE of q and k, the K/V append -- one launch
+// per layer fewer.
 __global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __restrict__ qkv, BatchTok bt,
-                                                             uint32_t D, uint32_t dh, const int32_t* __restrict__ K32,
-                                                             const int32_t* __restrict__ V32, size_t seq_stride,
-                                                             uint32_t ctx, int64_t inv_scale,
+                                                             uint32_t D, uint32_t dh, int32_t* K32, int32_t* V32,
+                                                             size_t seq_stride, uint32_t ctx, int64_t inv_scale,
                                                              const int64_t* __restrict__ lut_g, uint8_t* planes,
-                                                             uint32_t rows_pad, uint32_t ldp, uint32_t* wide) {
+                                                             uint32_t rows_pad, uint32_t ldp, uint32_t* wide,
+                                                             const int64_t* __restrict__ rc,
+                                                             const int64_t* __restrict__ rs) {
     extern __shared__ __align__(16) uint8_t bd_smem[];
     __shared__ int64_t lut[257];
     __shared__ u128 red[32];
@@ -168,10 +199,40 @@ __global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __re
     int64_t* S = reinterpret_cast<int64_t*>(bd_smem);              // [ctx]
     int32_t* q = reinterpret_cast<int32_t*>(S + ctx);              // [dh]
     uint64_t* part = reinterpret_cast<uint64_t*>(q + dh + (dh & 1));  // [4 * BD_THREADS]
-    for (uint32_t j = threadIdx.x; j < dh; j += BD_THREADS) q[j] = int32_t(qkv[size_t(t) * 3 * D + size_t(h) * dh + j]);
-    __syncthreads();
     const int32_t* Kh = K32 + size_t(b) * seq_stride + size_t(h) * ctx * dh;
     const int32_t* Vh = V32 + size_t(b) * seq_stride + size_t(h) * ctx * dh;
+    const int64_t* qr = qkv + size_t(t) * 3 * D + size_t(h) * dh;
+    if (rc) {
+        // RoPE (kernels.cpp:70-82) of q and k at position T - 1, the K/V append
+        // (:139-142); the same values and range checks as bd_rope_kv_kernel
+        const uint32_t half = dh / 2, p = T - 1;
+        const int64_t* kr = qr + D;
+        const int64_t* vr = qr + 2 * D;
+        int32_t* Kw = K32 + size_t(b) * seq_stride + (size_t(h) * ctx + p) * dh;
+        int32_t* Vw = V32 + size_t(b) * seq_stride + (size_t(h) * ctx + p) * dh;
+        const auto b23 = [](int64_t a) { return a >= -(int64_t(1) << 23) && a < (int64_t(1) << 23); };
+        int bad = 0;
+        for (uint32_t i = threadIdx.x; i < half; i += BD_THREADS) {
+            const int64_t c = rc[size_t(p) * half + i], sn = rs[size_t(p) * half + i];
+            int64_t q0, q1, k0, k1;
+            rope_pair(qr[i], qr[i + half], c, sn, q0, q1);
+            rope_pair(kr[i], kr[i + half], c, sn, k0, k1);
+            q[i] = int32_t(q0);
+            q[i + half] = int32_t(q1);
+            Kw[i] = int32_t(k0);
+            Kw[i + half] = int32_t(k1);
+            bad |= !fits_i32(k0) || !fits_i32(k1) || !b23(q0) || !b23(q1);
+        }
+        for (uint32_t j = threadIdx.x; j < dh; j += BD_THREADS) {
+            const int64_t v = vr[j];
+            Vw[j] = int32_t(v);
+            bad |= !fits_i32(v);
+        }
+        if (bad) *wide = 1;
+    } else {
+        for (uint32_t j = threadIdx.x; j < dh; j += BD_THREADS) q[j] = int32_t(qr[j]);
+    }
+    __syncthreads();  // q, and this CTA's appended K/V row, before they are read
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int big = 0;
     const size_t plane = size_t(rows_pad) * ldp;
