@@ -255,7 +255,7 @@ void launch_limb_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs
     int dev = 0, sms = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const uint32_t items = gemm_tiles(a, bn) * std::max(1u, a.ksplit);
+    const uint32_t items = gemm_tiles(a, bn) * (a.streamk ? a.n_kblk : std::max(1u, a.ksplit));
     const uint32_t per_sm = bn == TG_BN_SMALL ? 2u : 1u;
     const uint32_t grid = std::min<uint32_t>(items, per_sm * uint32_t(sms));
     if (bn == TG_BN_SMALL)
@@ -1066,6 +1066,8 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
     // traffic (tools/gemm_bench.cu: 30 -> 22 us at 64 tokens)
     const char* sk = std::getenv("DIMG_SPLITK");
     const bool split_k = sk ? std::atoi(sk) != 0 : true;
+    const char* skv = std::getenv("DIMG_STREAMK");
+    const bool streamk = skv ? std::atoi(skv) != 0 : false;
     int sms = m.ctx->sm_count;
     // DIMG_BD_SKIP (timing experiments only; results are wrong): bit 0 skips
     // the norms, 1 RoPE/KV, 2 attention -- what each launch chain costs
@@ -1097,6 +1099,12 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
                    : a.n_kblk >= 64 ? std::min(4u, pick_ksplit(gemm_tiles(a, bn), a.n_kblk, uint32_t(sms)))
                                     : 1;
         if (size_t(gemm_tiles(a, bn)) * TG_L * bn * TG_BM > r.partial_elems) a.ksplit = 1;
+        // DIMG_STREAMK=1 (experiment, off): stream-K for the decode steps --
+        // every CTA the same number of weight K blocks (gate/up's 172 tiles
+        // on 296 CTA slots), but nearly every tile then goes through the
+        // red.add partial sums: C5 B=8 0.381 s vs 0.334 s, B=64 equal
+        a.streamk = small && streamk && split_k &&
+                    size_t(gemm_tiles(a, bn)) * TG_L * bn * TG_BM <= r.partial_elems ? 1u : 0u;
         a.partial = r.partial;
         a.tile_cnt = r.tile_cnt;
         launch_limb_gemm(W.tmap, tb, a, st, bn, true);

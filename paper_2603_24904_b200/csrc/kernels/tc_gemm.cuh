@@ -91,6 +91,12 @@ struct TgArgs {
     // is the unsplit int32 accumulator, so no overflow), the last one to
     // finish reads it once, zeroes it and runs the epilogue.
     uint32_t ksplit;
+    // stream-K instead (streamk != 0; ksplit ignored): CTA c of G takes the
+    // contiguous run [c T / G, (c + 1) T / G) of the T = tiles x n_kblk K
+    // blocks in tile order, so every CTA streams the same number of weight
+    // bytes (+-1 block) whatever the tile count; a tile shared by several
+    // CTAs is finished like a split-K tile by the last piece to arrive.
+    uint32_t streamk;
     int32_t* partial;       // [tiles][3][BN][128], zero between launches (the last CTA resets)
     uint32_t* tile_cnt;     // [tiles], zero between launches (the last CTA resets)
     // tile order: 0 = feature tiles fastest (concurrent CTAs share the token
@@ -236,6 +242,32 @@ __device__ __forceinline__ void tg_tile(uint32_t tile, uint32_t n_mt, uint32_t n
     }
 }
 
+// One CTA's work, in the same order for the producer, the MMA issuer and the
+// epilogue: items (tile, K split) strided over the grid, or with stream-K one
+// contiguous run of K blocks cut at tile boundaries into pieces. `pieces` =
+// how many CTAs contribute to the tile (1: no partial sums).
+struct TgIter {
+    uint32_t item, g, g1, nk, ksplit, n_items, n_tiles, G;
+    bool sk;
+    __device__ __forceinline__ TgIter(const TgArgs& a, uint32_t tiles) {
+        nk = a.n_kblk;
+        n_tiles = tiles;
+        G = gridDim.x;
+        sk = a.streamk != 0;
+        ksplit = a.ksplit ? a.ksplit : 1;
+        n_items = tiles * ksplit;
+        item = blockIdx.x;
+        const uint64_t T = uint64_t(tiles) * nk;
+        g = uint32_t(T * blockIdx.x / G);
+        g1 = uint32_t(T * (blockIdx.x + 1) / G);
+    }
+    // the CTA whose run holds K block b: the largest c with c T / G <= b
+    __device__ __forceinline__ uint32_t cta_of(uint64_t b) const {
+        return uint32_t(((b + 1) * G - 1) / (uint64_t(n_tiles) * nk));
+    }
+    __device__ __forceinline__ bool next(uint32_t& tile, uint32_t& kb0, uint32_t& kb1, uint32_t& pieces);
+};
+
 // work item -> (tile, K-block range)
 __device__ __forceinline__ void tg_item(uint32_t item, uint32_t ksplit, uint32_t n_kblk, uint32_t& tile,
                                         uint32_t& ks, uint32_t& kb0, uint32_t& kb1) {
@@ -243,6 +275,24 @@ __device__ __forceinline__ void tg_item(uint32_t item, uint32_t ksplit, uint32_t
     ks = item % ksplit;
     kb0 = uint32_t(uint64_t(n_kblk) * ks / ksplit);
     kb1 = uint32_t(uint64_t(n_kblk) * (ks + 1) / ksplit);
+}
+
+__device__ __forceinline__ bool TgIter::next(uint32_t& tile, uint32_t& kb0, uint32_t& kb1, uint32_t& pieces) {
+    if (sk) {
+        if (g >= g1) return false;
+        tile = g / nk;
+        kb0 = g - tile * nk;
+        kb1 = min(nk, kb0 + (g1 - g));
+        g += kb1 - kb0;
+        pieces = cta_of(uint64_t(tile + 1) * nk - 1) - cta_of(uint64_t(tile) * nk) + 1;
+        return true;
+    }
+    if (item >= n_items) return false;
+    uint32_t ks;
+    tg_item(item, ksplit, nk, tile, ks, kb0, kb1);
+    pieces = ksplit;
+    item += G;
+    return true;
 }
 
 template <int BN>
@@ -262,8 +312,7 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
     if (threadIdx.x == 0) tr[0] = tg_now();
 #endif
     const uint32_t n_mt = (a.n_out + TG_BM - 1) / TG_BM, n_tt = (a.n_tok + BN - 1) / BN;
-    const uint32_t ksplit = a.ksplit ? a.ksplit : 1;
-    const uint32_t n_items = n_mt * n_tt * ksplit;
+    const uint32_t n_tiles = n_mt * n_tt;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S::STAGES; ++s) {
@@ -297,9 +346,9 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
         // constant: the first ring of A tiles streams in while the previous
         // kernel (which writes the B planes) finishes.
         uint32_t it = 0;
-        for (uint32_t item = blockIdx.x; item < n_items && it < S::STAGES; item += gridDim.x) {
-            uint32_t tile, ks, kb0, kb1, n0, t0;
-            tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
+        TgIter w0(a, n_tiles);
+        uint32_t tile, kb0, kb1, pieces, n0, t0;
+        while (it < S::STAGES && w0.next(tile, kb0, kb1, pieces)) {
             tg_tile<BN>(tile, n_mt, n_tt, a.token_fast, n0, t0);
             for (uint32_t kb = kb0; kb < kb1 && it < S::STAGES; ++kb, ++it) {
                 tg_expect_tx_w(&full[it], S::STAGE_BYTES);
@@ -312,9 +361,8 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
         if (lane == 0) tr[2] = tg_now();
 #endif
         it = 0;
-        for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-            uint32_t tile, ks, kb0, kb1, n0, t0;
-            tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
+        TgIter w1(a, n_tiles);
+        while (w1.next(tile, kb0, kb1, pieces)) {
             tg_tile<BN>(tile, n_mt, n_tt, a.token_fast, n0, t0);
             for (uint32_t kb = kb0; kb < kb1; ++kb, ++it) {
                 const uint32_t s = it % S::STAGES;
@@ -336,9 +384,9 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
     } else if (warp == 1) {
         // MMA issuer (whole warp, one elected lane issues)
         uint32_t it = 0, j = 0;
-        for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++j) {
-            uint32_t tile, ks, kb0, kb1;
-            tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
+        TgIter w(a, n_tiles);
+        uint32_t tile, kb0, kb1, pieces;
+        for (; w.next(tile, kb0, kb1, pieces); ++j) {
             const uint32_t b = j % S::NB;
             if (j >= S::NB) tg_mbar_wait(&acc_empty[b], ((j / S::NB) & 1) ^ 1);  // epilogue drained set b
             tg_fence_after();
@@ -373,9 +421,9 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
         const uint32_t c_first = 16 * ((warp - 2) / 4);  // this warp's first 16-column chunk
         const uint32_t fl = 32 * q + lane;  // feature within the tile
         uint32_t j = 0;
-        for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x, ++j) {
-            uint32_t tile, ks, kb0, kb1, n0, t0;
-            tg_item(item, ksplit, a.n_kblk, tile, ks, kb0, kb1);
+        TgIter w(a, n_tiles);
+        uint32_t tile, kb0, kb1, pieces, n0, t0;
+        for (; w.next(tile, kb0, kb1, pieces); ++j) {
             tg_tile<BN>(tile, n_mt, n_tt, a.token_fast, n0, t0);
             const uint32_t b = j % S::NB;
             const uint32_t n = n0 + fl;
@@ -383,9 +431,9 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
             tg_mbar_wait(&acc_full[b], (j / S::NB) & 1);
             tg_fence_after();
             const uint32_t tbase = tmem + ((32 * q) << 16) + b * S::ACC;
-            int32_t* part = ksplit > 1 ? a.partial + size_t(tile) * (TG_L * BN * TG_BM) : nullptr;
+            int32_t* part = pieces > 1 ? a.partial + size_t(tile) * (TG_L * BN * TG_BM) : nullptr;
             bool last = true;
-            if (ksplit > 1) {
+            if (pieces > 1) {
                 // this split's partials added into the tile accumulator (fire and forget)
                 for (uint32_t c0 = c_first; c0 < BN; c0 += 16 * NH) {
                     int32_t d[TG_L][16];
@@ -405,7 +453,7 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
                 if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tg_smem_u32(&acc_empty[b])) : "memory");
                 __threadfence();
                 asm volatile("bar.sync 1, %0;" ::"n"(32 * S::EPI_WARPS) : "memory");
-                if (threadIdx.x == 64) s_last = atomicAdd(a.tile_cnt + tile, 1u) == ksplit - 1;
+                if (threadIdx.x == 64) s_last = atomicAdd(a.tile_cnt + tile, 1u) == pieces - 1;
                 asm volatile("bar.sync 1, %0;" ::"n"(32 * S::EPI_WARPS) : "memory");
                 last = s_last != 0;
                 if (last) {
@@ -417,7 +465,7 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
             const int64_t sc = nv ? a.scales[n] : 0;
             for (uint32_t c0 = c_first; c0 < BN; c0 += 16 * NH) {
                 int32_t d[TG_L][16];
-                if (ksplit > 1) {
+                if (pieces > 1) {
                     // the summed accumulator: 48 independent loads, then zero it for the next launch
 #pragma unroll
                     for (int l = 0; l < TG_L; ++l)
