@@ -643,8 +643,11 @@ PkArgs pk_args(dimg_session& s, const PkStage* stages, uint32_t n_layer_stages, 
     t.inv_scale = m.inv_scale;
     t.exp_lut = m.ctx->exp_lut;
     a.kv_layer_stride = size_t(m.Hl) * m.cfg.max_ctx * m.dh;
-    // CTAs per head: split the head's dims over the SMs the heads leave idle
-    a.attn_parts = std::max(1u, std::min(s.grid / m.Hl, std::max(1u, m.dh / 8)));
+    // CTAs per head: split the head's dims over the SMs the heads leave idle,
+    // at most 4 (measured best at 7B for the whole model and for its
+    // tensor-parallel shards: 16 parts per head cost a TP-8 rank 911 vs 852
+    // us/token, tools/tp_fused_probe.py --solo with DIMG_ATTN_PARTS)
+    a.attn_parts = std::max(1u, std::min({s.grid / m.Hl, std::max(1u, m.dh / 8), 4u}));
     if (const char* e = std::getenv("DIMG_ATTN_PARTS"))  // experiments: CTAs per head
         a.attn_parts = std::max(1u, std::min(a.attn_parts, uint32_t(std::strtoul(e, nullptr, 0))));
     {
