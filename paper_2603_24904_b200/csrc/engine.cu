@@ -1112,9 +1112,9 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
         a.tile_cnt = r.tile_cnt;
         launch_limb_gemm(W.tmap, tb, a, st, bn, true);
     };
-    auto norm_ = [&](const int64_t* g, int unit) {  // decode steps: a CTA cluster per token
+    auto norm_ = [&](const int64_t* g, int unit) {  // decode steps: one 1024-thread CTA per token
         if (n <= 64u)
-            launch_k(true, bd_norm_cluster_kernel, n * BD_NCL, 256, 0, st, (const int32_t*)r.x, D, g, unit,
+            launch_k(true, bd_norm1k_kernel, n, 1024, 0, st, (const int32_t*)r.x, D, g, unit,
                      (const int64_t*)m.ctx->seeds, r.pa, r.nmax_pad, m.Kd, r.wide);
         else
             launch_k(true, pf_norm_limbs_kernel, n, 256, 0, st, (const int32_t*)r.x, D, g, unit,

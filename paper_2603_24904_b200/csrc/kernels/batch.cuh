@@ -14,8 +14,6 @@
 // sequence path instead.
 #pragma once
 
-#include <cooperative_groups.h>
-
 #include <cstdint>
 
 #include "attention.cuh"
@@ -77,46 +75,37 @@ __global__ void bd_rope_kv_kernel(int64_t* __restrict__ qkv, BatchTok bt, uint32
 }
 
 // rmsnorm (proj/src/kernels.cpp:56-68) of each token row into the next
-// GEMM's digit planes, for the few tokens of a decode batch: a cluster of
-// BD_NCL CTAs per token, each summing x^2 over a quarter of the row; the
-// partial sums meet through distributed shared memory behind one cluster
-// barrier, and every CTA derives the same r (inv_sqrt_q16 of the u128 total,
-// order-free) and writes its quarter. A single CTA per token left 8 SMs
-// working through a long load -> reduce -> Newton -> store chain.
-constexpr int BD_NCL = 4;
-
-__global__ void __cluster_dims__(BD_NCL, 1, 1) __launch_bounds__(256)
-    bd_norm_cluster_kernel(const int32_t* __restrict__ x, uint32_t K, const int64_t* __restrict__ gamma,
-                           int gamma_unit, const int64_t* __restrict__ seeds, uint8_t* planes, uint32_t rows_pad,
-                           uint32_t ldp, uint32_t* wide) {
-    namespace cg = cooperative_groups;
-    __shared__ u128 part;
+// GEMM's digit planes, for the few tokens of a decode batch: ONE 1024-thread
+// CTA per token (no cluster barriers; round 1's 4-CTA cluster with a
+// distributed-shared-memory exchange was 2% slower per C5 step): 4 elements
+// per thread for K <= 4096, x^2 summed in 21-bit chunks with REDUX
+// (per-warp totals < 2^29), one shared-memory pass for the block total.
+__global__ void __launch_bounds__(1024) bd_norm1k_kernel(const int32_t* __restrict__ x, uint32_t K,
+                                                         const int64_t* __restrict__ gamma, int gamma_unit,
+                                                         const int64_t* __restrict__ seeds, uint8_t* planes,
+                                                         uint32_t rows_pad, uint32_t ldp, uint32_t* wide) {
+    __shared__ uint32_t s_c[32][3];
     __shared__ int64_t s_r;
-    cg::cluster_group cl = cg::this_cluster();
     pdl_launch_dependents();
     pdl_wait();
-    const uint32_t rank = cl.block_rank(), t = blockIdx.x / BD_NCL;
-    const uint32_t per = (K + BD_NCL - 1) / BD_NCL, j0 = min(K, rank * per), j1 = min(K, j0 + per);
+    const uint32_t t = blockIdx.x;
     const int32_t* xr = x + size_t(t) * K;
-    constexpr int PER = 4;  // elements per thread in registers (K <= 4096)
+    constexpr int PER = 4;
     int64_t v[PER];
-    // x^2 < 2^62 (int32 x) in three 21-bit chunks: per thread <= 8 elements
-    // (K <= 8192), so every warp total is < 2^29 -- one REDUX per chunk
     uint32_t c0 = 0, c1 = 0, c2 = 0;
-    const auto add_sq = [&](int64_t x) {
-        const uint64_t q2 = uint64_t(x * x);
+    const auto add_sq = [&](int64_t xv) {
+        const uint64_t q2 = uint64_t(xv * xv);  // < 2^62
         c0 += uint32_t(q2) & 0x1FFFFFu;
         c1 += uint32_t(q2 >> 21) & 0x1FFFFFu;
         c2 += uint32_t(q2 >> 42);
     };
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
-        const uint32_t j = j0 + threadIdx.x + u * 256;
-        v[u] = j < j1 ? xr[j] : 0;
+        const uint32_t j = threadIdx.x + u * 1024;
+        v[u] = j < K ? xr[j] : 0;
         add_sq(v[u]);
     }
-    for (uint32_t j = j0 + threadIdx.x + PER * 256; j < j1; j += 256) add_sq(int64_t(xr[j]));
-    __shared__ uint32_t s_c[8][3];
+    for (uint32_t j = threadIdx.x + PER * 1024; j < K; j += 1024) add_sq(int64_t(xr[j]));  // K <= 8192
     c0 = __reduce_add_sync(0xffffffffu, c0);
     c1 = __reduce_add_sync(0xffffffffu, c1);
     c2 = __reduce_add_sync(0xffffffffu, c2);
@@ -128,22 +117,17 @@ __global__ void __cluster_dims__(BD_NCL, 1, 1) __launch_bounds__(256)
     __syncthreads();
     if (threadIdx.x == 0) {
         uint64_t t0 = 0, t1 = 0, t2 = 0;
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < 32; ++w) {
             t0 += s_c[w][0];
             t1 += s_c[w][1];
             t2 += s_c[w][2];
         }
-        part = u128(t0) + (u128(t1) << 21) + (u128(t2) << 42);
-    }
-    cl.sync();
-    if (threadIdx.x == 0) {
-        u128 tot = 0;
-        for (uint32_t r = 0; r < BD_NCL; ++r) tot += *cl.map_shared_rank(&part, r);
+        const u128 tot = u128(t0) + (u128(t1) << 21) + (u128(t2) << 42);
         const int64_t ms = (tot >> 63) != 0          ? int64_t((i128(tot) / i128(K)) >> 16)
                            : (K & (K - 1)) == 0       ? int64_t((uint64_t(tot) >> (__ffs(K) - 1)) >> 16)
                                                       : int64_t((uint64_t(tot) / K) >> 16);
         s_r = ms + 1 > 0 ? inv_sqrt_q16(ms + 1, seeds) : 0;
-        if (ms + 1 <= 0) *wide = 1;  // the reference throws (domain_error): the exact path reports it
+        if (ms + 1 <= 0) *wide = 1;
     }
     __syncthreads();
     const int64_t r = s_r;
@@ -151,19 +135,18 @@ __global__ void __cluster_dims__(BD_NCL, 1, 1) __launch_bounds__(256)
     uint8_t* pr = planes + size_t(t) * ldp;
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
-        const uint32_t j = j0 + threadIdx.x + u * 256;
-        if (j < j1) {
+        const uint32_t j = threadIdx.x + u * 1024;
+        if (j < K) {
             int64_t o = mul16(v[u], r);
             if (!gamma_unit) o = mul16(o, gamma[j]);
             pf_put_limbs(pr + j, plane, o, wide);
         }
     }
-    for (uint32_t j = j0 + threadIdx.x + PER * 256; j < j1; j += 256) {
+    for (uint32_t j = threadIdx.x + PER * 1024; j < K; j += 1024) {
         int64_t o = mul16(int64_t(xr[j]), r);
         if (!gamma_unit) o = mul16(o, gamma[j]);
         pf_put_limbs(pr + j, plane, o, wide);
     }
-    cl.sync();  // peers may still be reading this CTA's partial
 }
 
 constexpr int BD_THREADS = 256;
