@@ -1145,7 +1145,7 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
     if (logits) {
         norm(m.final_norm, m.final_unit);
         gemm(m.head, r.tm_pa, TG_STORE, r.logits, m.V);
-        launch_k(true, bd_argmax_kernel, n, 256, 0, st, (const int64_t*)r.logits, m.V, r.tok, r.pos,
+        launch_k(true, bd_argmax_kernel, n, 1024, 0, st, (const int64_t*)r.logits, m.V, r.tok, r.pos,
                  (const uint32_t*)r.seq, r.out, r.max_new, r.step);
         launch_k(true, bd_step_kernel, 1, 1, 0, st, r.step);
     }

@@ -357,22 +357,36 @@ __global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __re
 // Greedy selection per token row of the logits (proj/src/engine.cpp:113-120:
 // largest value, lowest index on ties); feeds the next step: tok[t] = the
 // choice, pos[t] += 1, and the choice is recorded at out[seq][step].
-__global__ void __launch_bounds__(256) bd_argmax_kernel(const int64_t* __restrict__ logits, uint32_t V,
-                                                        uint32_t* tok, uint32_t* pos, const uint32_t* seq,
-                                                        uint32_t* out, uint32_t max_new, uint32_t* step) {
-    __shared__ int64_t sv[8];
-    __shared__ uint32_t si[8];
+__global__ void __launch_bounds__(1024) bd_argmax_kernel(const int64_t* __restrict__ logits, uint32_t V,
+                                                         uint32_t* tok, uint32_t* pos, const uint32_t* seq,
+                                                         uint32_t* out, uint32_t max_new, uint32_t* step) {
+    __shared__ int64_t sv[32];
+    __shared__ uint32_t si[32];
     pdl_launch_dependents();
     pdl_wait();
     const uint32_t t = blockIdx.x;
     const int64_t* row = logits + size_t(t) * V;
     int64_t bv = INT64_MIN;
     uint32_t bi = 0xFFFFFFFFu;
-    for (uint32_t i = threadIdx.x; i < V; i += blockDim.x)
-        if (better(row[i], i, bv, bi)) {
-            bv = row[i];
-            bi = i;
+    // 8 loads in flight per thread: the row (256 KB at 32000 vocab) is a few
+    // memory round trips, not one per element
+    constexpr int U = 8;
+    for (uint32_t i0 = threadIdx.x; i0 < V; i0 += U * blockDim.x) {
+        int64_t vals[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t i = i0 + u * blockDim.x;
+            vals[u] = i < V ? row[i] : INT64_MIN;
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t i = i0 + u * blockDim.x;
+            if (i < V && better(vals[u], i, bv, bi)) {
+                bv = vals[u];
+                bi = i;
+            }
+        }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -388,7 +402,7 @@ __global__ void __launch_bounds__(256) bd_argmax_kernel(const int64_t* __restric
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < 8; ++w)
+        for (uint32_t w = 1; w < blockDim.x / 32; ++w)
             if (better(sv[w], si[w], bv, bi)) {
                 bv = sv[w];
                 bi = si[w];
