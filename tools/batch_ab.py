@@ -25,8 +25,14 @@ for B in (8, 64):
     ok = sum(res[i].output_hash.hex() == gold[f"c5_{i}"]["output_hash"] for i in range(B) if f"c5_{i}" in gold)
     print(f"B={B} {best:.4f} s {B * 128 / best:.0f} tok/s golden {ok} {path}")
 '''
-knob, vals = sys.argv[1], sys.argv[2:]
-for rnd in range(2):
-    for v in vals:
-        o = subprocess.run([sys.executable, "-c", CHILD], env=dict(os.environ, **{knob: v}), capture_output=True, text=True)
-        print(f"{knob}={v}: " + (" | ".join(o.stdout.strip().splitlines()) or o.stderr[-800:]), flush=True)
+def main():
+    knob, vals = sys.argv[1], sys.argv[2:]
+    for rnd in range(2):
+        for v in vals:
+            o = subprocess.run([sys.executable, "-c", CHILD], env=dict(os.environ, **{knob: v}), capture_output=True,
+                               text=True)
+            print(f"{knob}={v}: " + (" | ".join(o.stdout.strip().splitlines()) or o.stderr[-800:]), flush=True)
+
+
+if __name__ == "__main__":
+    main()
