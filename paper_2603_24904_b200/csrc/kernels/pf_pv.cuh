@@ -2,8 +2,10 @@
 // half on the tensor cores, exact:
 //   out(t, j) = sum_p floor(P(t, p) V(p, j) / 2^16)
 //             = sum_p P vh  +  sum_p floor(P vl / 2^16),   V = vh 2^16 + vl, vl in [0, 2^16).
-// The second sum is per-product arithmetic and stays on the CUDA cores
-// (pf_attn_kernel<_, true> writes it to a scratch); the first is a plain
+// The second sum F is per-product arithmetic and stays on the CUDA cores:
+// pf_attn_kernel<_, true> writes only U = sum_p ((P V mod 2^32) >> 16), which
+// is congruent to T + F modulo 2^16 (T = the first sum); as 0 <= F < sum_p P
+// <= 2^16, F = (U - T) mod 2^16 exactly (epilogue). The first is a plain
 // integer GEMM over the positions, done here with tcgen05.mma kind::i8:
 //   A = vh as ONE signed byte digit per (dim, position) -- exact while
 //       |V| < 2^23, else *wide and the engine reruns on the exact path;
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(256) pf_vh_kernel(const int32_t* __restrict__ 
 
 // grid (H, ceil(n / 32)); vmap: the vh planes [H * 128 rows][n_pad bytes];
 // strips: the probabilities [H][n rounded to 32][ld] (pf_attn_kernel); fl:
-// sum_p floor(P vl / 2^16) [H][n][128]; out: the attention vector's three
+// U = sum_p ((P V mod 2^32) >> 16) [H][n][128]; out: the attention vector's three
 // signed digit planes (WO's B operand).
 __global__ void __launch_bounds__(PV_THREADS, 1) pf_pv_kernel(const __grid_constant__ CUtensorMap vmap,
                                                               const int32_t* __restrict__ strips,
@@ -177,7 +179,11 @@ __global__ void __launch_bounds__(PV_THREADS, 1) pf_pv_kernel(const __grid_const
             if (tq >= n) break;
             int64_t v;
             if (tq == 0) v = V32[size_t(h) * head_stride + j];  // P(0, 0) = 2^16: the output is V(0)
-            else v = int64_t(d0[e]) + 256 * int64_t(d1[e]) + fl[(size_t(h) * n + tq) * PV_M + j];
+            else {
+                const int64_t T = int64_t(d0[e]) + 256 * int64_t(d1[e]);  // sum_p P vh
+                const uint32_t U = uint32_t(fl[(size_t(h) * n + tq) * PV_M + j]);
+                v = T + int64_t((U - uint32_t(T)) & 0xFFFFu);  // + sum_p floor(P vl / 2^16)
+            }
             if (!put_sdigits(planes + size_t(tq) * ldp + h * PV_M + j, plane, v)) big = 1;
         }
     }

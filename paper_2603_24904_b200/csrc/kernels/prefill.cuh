@@ -153,10 +153,10 @@ constexpr int PA_CH = 64;       // cached positions per K / V chunk
 constexpr int PA_THREADS = 256;
 static_assert(PA_Q == PA_QW * PA_THREADS / 32, "every warp owns PA_QW queries");
 
-// shared memory: K/V chunk double buffer + the CTA's queries + one chunk of
-// probabilities ([query][position])
+// shared memory: K/V chunk double buffer + the CTA's queries + a double
+// buffer of probability chunks ([query][position])
 __host__ __device__ constexpr size_t pf_attn_smem(uint32_t dh) {
-    return 2 * size_t(PA_CH) * dh * 4 + size_t(PA_Q) * dh * 4 + size_t(PA_CH) * PA_Q * 4;
+    return 2 * size_t(PA_CH) * dh * 4 + size_t(PA_Q) * dh * 4 + 2 * size_t(PA_CH) * PA_Q * 4;
 }
 // global score / probability strips, [H][n rounded to PA_Q][ld] int32
 __host__ __device__ constexpr size_t pf_attn_strip_elems(uint32_t H, uint32_t n) {
@@ -190,9 +190,12 @@ __device__ __forceinline__ void pa_cp_wait_all() { asm volatile("cp.async.wait_g
 // so a lane reads 16 bytes per position; V row-major). DPL = dims per lane in
 // PV (dh <= 32 DPL). Output: digit planes of the attention vector (WO's B
 // operand); values outside the fast representation set *wide.
-// TCPV: only the per-product half sum_p floor(P vl / 2^16) here, written to
-// fl_out [H][n][dh]; pf_pv_kernel (pf_pv.cuh) adds the linear half on the
-// tensor cores and writes the planes.
+// TCPV: only the per-product half here, and only modulo 2^16: fl_out
+// [H][n][dh] gets U = sum_p ((P v_p mod 2^32) >> 16) = sum_p ((P vh_p +
+// floor(P vl_p / 2^16)) mod 2^16) -- one IMAD + one LEA.HI per product, no
+// vl mask. pf_pv_kernel (pf_pv.cuh) computes the linear half T = sum_p P vh_p
+// on the tensor cores; F = sum_p floor(P vl_p / 2^16) < sum_p P <= 2^16, so
+// F = (U - T) mod 2^16 exactly, and the output is T + F.
 template <int DPL, bool TCPV>
 __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* __restrict__ qkv, uint32_t n,
                                                                 uint32_t D, uint32_t dh,
@@ -328,6 +331,11 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
             q += r >= int32_t(total);
             R[p] = int32_t(q);
         }
+        // the positions after t that the warp's PV loop reads for this row
+        // (up to its last query) must hold probability 0: the probability
+        // chunks are copied into shared memory unmasked
+        const uint32_t pe = min(npos, tw + PA_QW);
+        if (t + 1 + lane < pe) R[t + 1 + lane] = 0;
     }
 
     // ---- PV (kernels.cpp:153-159): lane owns dims lane * DPL ... + DPL - 1
@@ -353,17 +361,27 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
         }
         pa_cp_commit();
     };
+    // this chunk's probabilities, [query][position], copied with V: every
+    // position a warp reads is <= its last query and < npos, and holds 0
+    // past each row's own query (softmax pass); rows of queries >= n are
+    // never used
+    auto load_p = [&](uint32_t c, int32_t* dst) {
+        const uint32_t c0 = c * PA_CH;
+        for (uint32_t i = threadIdx.x; i < PA_Q * (PA_CH / 4); i += PA_THREADS) {
+            const uint32_t qi = i / (PA_CH / 4), p = c0 + 4 * (i % (PA_CH / 4));
+            const bool ok = p < ld;  // ld % 4 == 0: the 16 bytes lie inside the row
+            pa_cp16(dst + qi * PA_CH + (p - c0), Sc + size_t(qi) * ld + (ok ? p : 0), ok);
+        }
+    };
     __syncthreads();  // every row's probabilities written (global, same CTA)
+    load_p(0, Ps);
     load_v(0, KV);
     for (uint32_t c = 0; c < nch; ++c) {
         const int4* cur = KV + (c & 1) * chunk_q;
+        const int32_t* Pc = Ps + (c & 1) * (PA_Q * PA_CH);
         const uint32_t c0 = c * PA_CH;
-        // this chunk's probabilities, [query][position] (0 past each query)
-        for (uint32_t i = threadIdx.x; i < PA_CH * PA_Q; i += PA_THREADS) {
-            const uint32_t qi = i / PA_CH, pp = i % PA_CH, t = q0 + qi, p = c0 + pp;
-            Ps[i] = (t < n && p <= t) ? Sc[size_t(qi) * ld + p] : 0;
-        }
         if (c + 1 < nch) {
+            load_p(c + 1, Ps + ((c + 1) & 1) * (PA_Q * PA_CH));
             load_v(c + 1, KV + ((c + 1) & 1) * chunk_q);
             pa_cp_wait_prev();
         } else {
@@ -377,7 +395,7 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
             for (uint32_t pp = 0; pp < pend; ++pp) {
                 int32_t pq[PA_QW];
 #pragma unroll
-                for (int u = 0; u < PA_QW; ++u) pq[u] = Ps[(PA_QW * warp + u) * PA_CH + pp];  // broadcast
+                for (int u = 0; u < PA_QW; ++u) pq[u] = Pc[(PA_QW * warp + u) * PA_CH + pp];  // broadcast
                 int32_t vv[DPL];
                 if constexpr (DPL >= 4) {
 #pragma unroll
@@ -391,12 +409,19 @@ __global__ void __launch_bounds__(PA_THREADS, 2) pf_attn_kernel(const int64_t* _
                 }
 #pragma unroll
                 for (int z = 0; z < DPL; ++z) {
-                    const int32_t vh = vv[z] >> 16;
-                    const uint32_t vl = uint32_t(vv[z]) & 0xFFFFu;
+                    if constexpr (TCPV) {
+                        // (P v mod 2^32) >> 16 = (P vh + floor(P vl / 2^16)) mod 2^16
+                        const uint32_t vu = uint32_t(vv[z]);
 #pragma unroll
-                    for (int u = 0; u < PA_QW; ++u) {
-                        if constexpr (!TCPV) fh[u][z] += pq[u] * vh;
-                        fl[u][z] += (uint32_t(pq[u]) * vl) >> 16;
+                        for (int u = 0; u < PA_QW; ++u) fl[u][z] += (uint32_t(pq[u]) * vu) >> 16;
+                    } else {
+                        const int32_t vh = vv[z] >> 16;
+                        const uint32_t vl = uint32_t(vv[z]) & 0xFFFFu;
+#pragma unroll
+                        for (int u = 0; u < PA_QW; ++u) {
+                            fh[u][z] += pq[u] * vh;
+                            fl[u][z] += (uint32_t(pq[u]) * vl) >> 16;
+                        }
                     }
                 }
             }

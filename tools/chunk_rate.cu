@@ -41,6 +41,20 @@ __device__ __forceinline__ void mma_s8(int (&c)[4], uint32_t a0, uint32_t a1, ui
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ void mma_su(int (&c)[4], uint4 a, uint2 b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y));
+}
+__device__ __forceinline__ void mma_ss2(int (&c)[4], uint4 a, uint2 b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y));
+}
+constexpr int PSTR = 4096 + 64;  // plane stride (bytes): 16 words mod 32 -> conflict-free LDS.64
+
 // mode 0: DP4A (the decode kernel's loop); mode 1: mma.sync
 template <int MODE>
 __global__ void __launch_bounds__(256, 1) rate(unsigned long long* out, int* sink) {
@@ -48,7 +62,7 @@ __global__ void __launch_bounds__(256, 1) rate(unsigned long long* out, int* sin
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint8_t* chunk = sm + warp * CH;           // this warp's weight chunk
     uint8_t* planes = sm + 8 * CH;             // 3 x 4096 B limb planes (shared by all warps)
-    for (int i = threadIdx.x; i < 8 * CH + 3 * 4096; i += 256) sm[i] = uint8_t(i * 131 + 7);
+    for (int i = threadIdx.x; i < 8 * CH + 3 * PSTR; i += 256) sm[i] = uint8_t(i * 131 + 7);
     __syncthreads();
     const uint32_t cs = static_cast<uint32_t>(__cvta_generic_to_shared(chunk));
     const uint32_t ps = static_cast<uint32_t>(__cvta_generic_to_shared(planes));
@@ -100,6 +114,28 @@ __global__ void __launch_bounds__(256, 1) rate(unsigned long long* out, int* sin
 #pragma unroll
             for (int q = 0; q < 4; ++q) sum += c[q][0] ^ c[q][1] ^ c[q][2] ^ c[q][3];
         }
+    } else if constexpr (MODE >= 3) {
+        // the 4-row group kept: A = 4 rows x 4 K-quarters of a 128-byte block
+        // (one LDS.128 fragment), B = (quarter, limb) columns; pair MMA for
+        // limbs 0/1 (u8), single MMA for limb 2 (s8); the diagonal is used.
+        constexpr int NS = MODE - 1;  // independent accumulator sets (2, 3, 4)
+        const int g = lane >> 2, t = lane & 3;
+        const uint32_t bp_off = (g & 1) * PSTR + (g >> 1) * 32 + 8 * t;
+        const uint32_t bs_off = 2 * PSTR + (g & 3) * 32 + 8 * t;
+        for (int r = 0; r < REP; ++r) {
+            int cp[NS][4] = {}, cq[NS][4] = {};
+            const uint32_t pb = ps + (r & 1) * 1536;
+#pragma unroll
+            for (int kb = 0; kb < 12; ++kb) {
+                const uint4 a = lds128(cs + kb * 512 + lane * 16);
+                const uint2 bp = lds64(pb + kb * 128 + bp_off);
+                const uint2 bq = lds64(pb + kb * 128 + bs_off);
+                mma_su(cp[kb % NS], a, bp);
+                mma_ss2(cq[kb % NS], a, bq);
+            }
+#pragma unroll
+            for (int q = 0; q < NS; ++q) sum += cp[q][0] ^ cp[q][1] ^ cp[q][2] ^ cp[q][3] ^ cq[q][0] ^ cq[q][3];
+        }
     } else {
         // A = weights (16 rows x 32 B per mma, one LDS.128 fragment), B = limbs
         // (N = 8, 3 real columns: lanes 0-11): 12 mma per chunk, 4 accumulators
@@ -131,10 +167,10 @@ int main() {
     int* sink;
     cudaMalloc(&d, 148 * 8 * 8);
     cudaMalloc(&sink, 4);
-    const int smem = 8 * CH + 3 * 4096;
+    const int smem = 8 * CH + 3 * PSTR;
     unsigned long long h[148 * 8];
-    for (int mode = 0; mode < 3; ++mode) {
-        auto k = mode == 0 ? rate<0> : mode == 1 ? rate<1> : rate<2>;
+    for (int mode = 0; mode < 6; ++mode) {
+        auto k = mode == 0 ? rate<0> : mode == 1 ? rate<1> : mode == 2 ? rate<2> : mode == 3 ? rate<3> : mode == 4 ? rate<4> : rate<5>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         for (int it = 0; it < 2; ++it) {
             cudaEvent_t e0, e1;
@@ -153,7 +189,7 @@ int main() {
             const double clk_per_chunk = avg / REP;
             const double bytes = 148.0 * 8 * REP * CH;
             printf("%s: %.0f clk per 6 KB chunk per warp (8 warps/SM), %.2f TB/s of weights GPU-wide (%.3f ms) %s\n",
-                   mode == 0 ? "dp4a         " : mode == 1 ? "mma B=weights" : "mma A=weights", clk_per_chunk, bytes / (ms * 1e-3) / 1e12, ms,
+                   mode == 0 ? "dp4a         " : mode == 1 ? "mma B=weights" : mode == 2 ? "mma A=weights" : mode == 3 ? "diag4 acc2   " : mode == 4 ? "diag4 acc3   " : "diag4 acc4   ", clk_per_chunk, bytes / (ms * 1e-3) / 1e12, ms,
                    cudaGetErrorString(cudaGetLastError()));
         }
     }
