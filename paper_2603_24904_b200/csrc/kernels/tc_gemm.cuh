@@ -97,7 +97,7 @@ struct TgArgs {
     // bytes (+-1 block) whatever the tile count; a tile shared by several
     // CTAs is finished like a split-K tile by the last piece to arrive.
     uint32_t streamk;
-    int32_t* partial;       // [tiles][3][BN][128], zero between launches (the last CTA resets)
+    int32_t* partial;       // [tiles][3][BN / 2][128] int64 token-pair sums, zero between launches (the last CTA resets)
     uint32_t* tile_cnt;     // [tiles], zero between launches (the last CTA resets)
     // tile order: 0 = feature tiles fastest (concurrent CTAs share the token
     // tile; weights re-read per token tile), 1 = token tiles fastest
@@ -431,10 +431,17 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
             tg_mbar_wait(&acc_full[b], (j / S::NB) & 1);
             tg_fence_after();
             const uint32_t tbase = tmem + ((32 * q) << 16) + b * S::ACC;
-            int32_t* part = pieces > 1 ? a.partial + size_t(tile) * (TG_L * BN * TG_BM) : nullptr;
+            // split-K accumulator of the tile: int32 sums of token pairs (2c, 2c + 1)
+            // packed into one int64 word lo + 2^32 hi -- a 64-bit add sums both
+            // exactly (each total fits int32), halving the atomics
+            unsigned long long* part =
+                pieces > 1 ? reinterpret_cast<unsigned long long*>(a.partial) + size_t(tile) * (TG_L * (BN / 2) * TG_BM)
+                           : nullptr;
             bool last = true;
             if (pieces > 1) {
-                // this split's partials added into the tile accumulator (fire and forget)
+                // this split's partials added into the tile accumulator (fire and
+                // forget); token columns past the batch are skipped (never read)
+                const uint32_t nvalid = a.n_tok - t0;
                 for (uint32_t c0 = c_first; c0 < BN; c0 += 16 * NH) {
                     int32_t d[TG_L][16];
 #pragma unroll
@@ -443,10 +450,11 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
 #pragma unroll
                     for (int l = 0; l < TG_L; ++l)
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj)
-                            asm volatile("red.global.add.s32 [%0], %1;" ::"l"(part + (size_t(l) * BN + c0 + jj) * TG_BM + fl),
-                                         "r"(d[l][jj])
-                                         : "memory");
+                        for (int jj = 0; jj < 16; jj += 2)
+                            if (c0 + jj < nvalid)
+                                asm volatile("red.global.add.u64 [%0], %1;" ::"l"(part + (size_t(l) * (BN / 2) + (c0 + jj) / 2) * TG_BM + fl),
+                                             "l"(uint64_t(int64_t(d[l][jj])) + (uint64_t(uint32_t(d[l][jj + 1])) << 32))
+                                             : "memory");
                 }
                 tg_fence_before();
                 __syncwarp();
@@ -466,15 +474,21 @@ __global__ void __launch_bounds__(TgShape<BN>::THREADS, TgShape<BN>::MIN_BLOCKS)
             for (uint32_t c0 = c_first; c0 < BN; c0 += 16 * NH) {
                 int32_t d[TG_L][16];
                 if (pieces > 1) {
-                    // the summed accumulator: 48 independent loads, then zero it for the next launch
+                    // the summed accumulator: 24 independent loads, then zero it for the next launch
+                    unsigned long long sp[TG_L][8];
 #pragma unroll
                     for (int l = 0; l < TG_L; ++l)
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) d[l][jj] = __ldcg(part + (size_t(l) * BN + c0 + jj) * TG_BM + fl);
+                        for (int jp = 0; jp < 8; ++jp) sp[l][jp] = __ldcg(part + (size_t(l) * (BN / 2) + c0 / 2 + jp) * TG_BM + fl);
 #pragma unroll
                     for (int l = 0; l < TG_L; ++l)
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) __stcg(part + (size_t(l) * BN + c0 + jj) * TG_BM + fl, 0);
+                        for (int jp = 0; jp < 8; ++jp) {
+                            __stcg(part + (size_t(l) * (BN / 2) + c0 / 2 + jp) * TG_BM + fl, 0ull);
+                            const int32_t lo = int32_t(uint32_t(sp[l][jp]));  // exact: the total fits int32
+                            d[l][2 * jp] = lo;
+                            d[l][2 * jp + 1] = int32_t(uint32_t((sp[l][jp] - uint64_t(int64_t(lo))) >> 32));
+                        }
                 } else {
 #pragma unroll
                     for (int l = 0; l < TG_L; ++l) tg_ld16(tbase + l * BN + c0, d[l]);
