@@ -237,3 +237,31 @@ def test_inv_sqrt_fast_path_matches_oracle(P, oracle):
     for x in sorted(v for v in xs if v > 0):
         assert lib.dimg_inv_sqrt_q16(x, C.byref(out)) == 0
         assert out.value == oracle.lib.orc_inv_sqrt(x), x
+
+
+def test_pv_remainder_mod_2_16_identity():
+    """The tensor-core prefill PV (pf_attn_kernel<_, true> + pf_pv_kernel)
+    recovers sum_p floor(P_p v_p / 2^16) (proj/src/kernels.cpp:153-159 after
+    the mul16 of each product) from T = sum_p P_p vh_p (tensor cores) and
+    U = sum_p ((P_p v_p mod 2^32) >> 16) (CUDA cores, no vl mask) as
+    T + ((U - T) mod 2^16): exact because F = sum_p floor(P_p vl_p / 2^16)
+    lies in [0, sum_p P_p) and sum_p P_p <= 2^16. Checked here on random and
+    extreme rows, including |v| up to 2^23 and one-hot probabilities."""
+    rng = np.random.default_rng(5)
+    cases = []
+    for n in (1, 2, 7, 64, 300, 2048):
+        w = rng.integers(1, 1 << 16, n, dtype=np.int64)
+        P = (w << 16) // w.sum()  # floor(w 2^16 / total): sums to <= 2^16
+        for lim in (1 << 8, 1 << 16, 1 << 23):
+            cases.append((P, rng.integers(-lim, lim, n, dtype=np.int64)))
+    onehot = np.zeros(5, np.int64)
+    onehot[2] = (1 << 16) - 1
+    cases.append((onehot, np.array([-(1 << 23)] * 5, np.int64)))
+    cases.append((np.full(4, 1 << 14, np.int64), np.array([(1 << 23) - 1, -(1 << 23), 65535, -1], np.int64)))
+    for P, v in cases:
+        assert P.sum() <= 1 << 16
+        want = int(((P * v) >> 16).sum())  # floor per product
+        vh = v >> 16
+        T = int((P * vh).sum())
+        U = int((((P * v) & 0xFFFFFFFF) >> 16).sum())
+        assert T + ((U - T) & 0xFFFF) == want
