@@ -509,33 +509,73 @@ def run_ours(args, rank, world, local):
             extra = {}
         else:
             # tensor parallel, fused: every rank's persistent kernel exchanges
-            # the partial sums over peer memory (handles via torch.distributed)
-            tp = P.TensorParallel(mf, world, backend="fused-ipc", rank=rank, device=dev)
-            if world > 1:
-                tp.connect_group()
-            tp.time_decode(prompt, args.warmup)  # warm
-            barrier()
-            with ClockSampler(dev) as clk:
-                ms = tp.time_decode(prompt, args.warmup + args.steps)
-                ms_w = tp.time_decode(prompt, args.warmup)
-            barrier()
-            # the K steps after W warm ones: difference of two CUDA-event timed launches
-            ms = max(ms - ms_w, 1e-6)
-            toks = tp.tokens(args.warmup + args.steps)
-            info = tp.info()
-            gpu_launches = 2  # the two timed persistent launches (all their steps inside)
-            kernel = "decode_persistent_kernel on the rank's shard, WO/w_down sums exchanged in-kernel (per step, per GPU)"
-            tp.generate_greedy(prompt, 128)  # warm
-            barrier()
-            t1 = time.perf_counter()
-            for _ in range(3):
-                res = tp.generate_greedy(prompt, 128)
-            e2e_s = (time.perf_counter() - t1) / 3
-            e2e_call = "dimg_tp_generate_greedy(prompt 16 -> 128 tokens, BLAKE3 on host), fused-ipc tp"
-            tp.close()
-            extra = {"tp_group": {"backend": "fused-ipc", "ranks": world, "exchange": "CUDA IPC peer memory, in-kernel",
-                                  "handles_gathered_over": "torch.distributed (nccl process group)",
-                                  "weight_bytes_per_rank": info["weight_bytes"]}}
+            # the partial sums over peer memory (handles via torch.distributed).
+            # A probe (construct, connect, one short decode) must succeed on
+            # every rank first; otherwise every rank takes the NCCL TP path as
+            # the headline (same collectives on all ranks, so none is left
+            # waiting), and the line says why.
+            def tp_headline(tp, backend):
+                tp.time_decode(prompt, args.warmup)  # warm
+                barrier()
+                with ClockSampler(dev) as clk_:
+                    ms_ = tp.time_decode(prompt, args.warmup + args.steps)
+                    ms_w = tp.time_decode(prompt, args.warmup)
+                barrier()
+                # the K steps after W warm ones: difference of two CUDA-event timed launches
+                ms_ = max(ms_ - ms_w, 1e-6)
+                toks_ = tp.tokens(args.warmup + args.steps)
+                info_ = tp.info()
+                tp.generate_greedy(prompt, 128)  # warm
+                barrier()
+                t1_ = time.perf_counter()
+                for _ in range(3):
+                    res_ = tp.generate_greedy(prompt, 128)
+                e2e_ = (time.perf_counter() - t1_) / 3
+                return ms_, clk_, toks_, info_, res_, e2e_
+
+            tp, fused_err = None, None
+            try:
+                if os.environ.get("DIMG_BENCH_FORCE_NCCL"):  # exercises the fallback
+                    raise RuntimeError("DIMG_BENCH_FORCE_NCCL set")
+                tp = P.TensorParallel(mf, world, backend="fused-ipc", rank=rank, device=dev)
+            except Exception as e:
+                fused_err = f"{type(e).__name__}: {e}"[:300]
+            if world > 1 and allreduce(0.0 if fused_err else 1.0, dist.ReduceOp.MIN) < 1:
+                fused_err = fused_err or "a peer rank could not build its fused-ipc shard"
+            if fused_err is None:
+                try:
+                    if world > 1:
+                        tp.connect_group()
+                    tp.time_decode(prompt, 2)  # probe: one launch, in-kernel exchange with every peer
+                except Exception as e:
+                    fused_err = f"{type(e).__name__}: {e}"[:300]
+                if world > 1 and allreduce(0.0 if fused_err else 1.0, dist.ReduceOp.MIN) < 1:
+                    fused_err = fused_err or "a peer rank's fused-ipc probe failed"
+            if fused_err is None:
+                ms, clk, toks, info, res, e2e_s = tp_headline(tp, "fused-ipc")
+                gpu_launches = 2  # the two timed persistent launches (all their steps inside)
+                kernel = ("decode_persistent_kernel on the rank's shard, WO/w_down sums exchanged in-kernel "
+                          "(per step, per GPU)")
+                e2e_call = "dimg_tp_generate_greedy(prompt 16 -> 128 tokens, BLAKE3 on host), fused-ipc tp"
+                extra = {"tp_group": {"backend": "fused-ipc", "ranks": world,
+                                      "exchange": "CUDA IPC peer memory, in-kernel",
+                                      "handles_gathered_over": "torch.distributed (nccl process group)",
+                                      "weight_bytes_per_rank": info["weight_bytes"]}}
+                tp.close()
+            else:
+                if tp is not None:
+                    tp.close()
+                obj = [P.nccl_unique_id() if rank == 0 else None]
+                if world > 1:
+                    dist.broadcast_object_list(obj, src=0)
+                tpn = P.TensorParallel(mf, world, backend="nccl", rank=rank, nccl_id=obj[0], device=dev)
+                ms, clk, toks, info, res, e2e_s = tp_headline(tpn, "nccl")
+                gpu_launches = 2 * info["launches_per_step"] * args.steps
+                kernel = "per-stage GEMV kernels on the rank's shard + ncclAllReduce (fused-ipc fallback)"
+                e2e_call = "dimg_tp_generate_greedy(prompt 16 -> 128 tokens, BLAKE3 on host), nccl tp"
+                extra = {"tp_group": {"backend": "nccl", "ranks": world, "fused_ipc_error": fused_err,
+                                      "weight_bytes_per_rank": info["weight_bytes"]}}
+                tpn.close()
     ms_max = allreduce(ms, dist.ReduceOp.MAX if dist else None)
     e2e_s = allreduce(e2e_s, dist.ReduceOp.MAX if dist else None)
     per_step_ms = ms_max / args.steps
