@@ -258,7 +258,7 @@ def run_reference(args, rank, world):
     cfg = Config(*CFG7B)
     threads = os.cpu_count() or 1
     if not Reference.available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdimref.so not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libdimref.so not built"})
         return 0
     ref = Reference()
     t0 = time.time()
@@ -284,7 +284,7 @@ def run_reference(args, rank, world):
                              **host_cpu()),
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -673,13 +673,27 @@ def run_ours(args, rank, world, local):
             "tokens_head": toks[:8],
         }
         line.update(extra)
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist is not None:
         dist.destroy_process_group()
     return 0
 
 
+_JSON_FD = None
+
+
+def emit(line):
+    """The one JSON line, on the process's original stdout."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _JSON_FD
+    # everything but the JSON line goes to stderr: libraries print to fd 1
+    # (NCCL's version banner at communicator init, for one)
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=128)
