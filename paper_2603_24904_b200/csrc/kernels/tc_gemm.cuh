@@ -54,6 +54,11 @@ struct TgShape {
 #define TG_RING_SMALL (100 * 1024)
 #endif
     static constexpr int RING = BN >= 64 ? 200 * 1024 : TG_RING_SMALL;
+    // 16-token tiles: the register bound that lets one of these CTAs share an
+    // SM with the previous kernel's CTAs (PDL) -- 3 -> <= 113 registers
+#ifndef TG_SMALL_MINB
+#define TG_SMALL_MINB 2
+#endif
     static constexpr int STAGES = RING / STAGE_BYTES;
     static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;  // + alignment slack
     static constexpr int ACC = TG_L * BN;  // TMEM columns of one tile's accumulators
@@ -63,7 +68,7 @@ struct TgShape {
     // is then not exposed behind a short tile list), 4 for 16-token tiles
     static constexpr int EPI_WARPS = BN >= 64 ? 8 : 4;
     static constexpr int THREADS = 64 + 32 * EPI_WARPS;
-    static constexpr int MIN_BLOCKS = BN >= 64 ? 1 : 2;
+    static constexpr int MIN_BLOCKS = BN >= 64 ? 1 : TG_SMALL_MINB;
     static constexpr uint32_t TMEM_COLS = NB * ACC <= 128 ? 128 : NB * ACC <= 256 ? 256 : 512;
 };
 
