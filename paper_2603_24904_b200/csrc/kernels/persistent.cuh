@@ -473,6 +473,25 @@ __device__ __forceinline__ void pipe_release(const Sched& sc, Pipe& p) {
 // probes): planes straight from x.
 constexpr int PLAIN_WIDE = 9;
 
+// mul16(x, r) = (x r) >> 16 (proj/src/q16.cpp) for |x|, r <= 2^24 (the
+// residual stream after the clamp and the rmsnorm factor): one IMAD.WIDE and
+// one funnel shift give the low 32 bits of the result (its three limb bytes);
+// fits &= the result lies in [-2^23, 2^23), i.e. x r in [-2^39, 2^39).
+__device__ __forceinline__ uint32_t norm_lo32(int32_t x, int32_t r, int& fits) {
+    int64_t p;
+    asm("mul.wide.s32 %0, %1, %2;" : "=l"(p) : "r"(x), "r"(r));
+    const int32_t hi = int32_t(p >> 32);
+    fits &= uint32_t((hi >> 7) + 1) <= 1u;
+    return __funnelshift_r(uint32_t(p), uint32_t(hi), 16);
+}
+
+// Bytes 0, 1, 2 of four elements -> one word per limb plane.
+__device__ __forceinline__ void put_planes3(uint32_t* planes, uint32_t Kw, uint32_t w, const uint32_t (&lo)[4]) {
+    planes[w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0040), __byte_perm(lo[2], lo[3], 0x0040), 0x5410);
+    planes[Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0051), __byte_perm(lo[2], lo[3], 0x0051), 0x5410);
+    planes[2 * Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0062), __byte_perm(lo[2], lo[3], 0x0062), 0x5410);
+}
+
 // 8-limb planes go to the CTA's global scratch (wplanes): shared memory only
 // holds the usual 3.
 __device__ __noinline__ int planes_from_x(uint32_t K, uint32_t Kp, const int64_t* x, uint32_t* splanes,
@@ -599,14 +618,8 @@ __device__ __noinline__ int prologue_norm(uint32_t K, uint32_t Kp, bool gamma_un
             const int32_t xs[4] = {e4.x, e4.y, e4.z, e4.w};
             uint32_t lo[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int64_t v = 4 * w + e < K ? (int64_t(xs[e]) * int32_t(r_inv)) >> 16 : 0;
-                fits &= uint64_t(v + (int64_t(1) << 23)) < (uint64_t(1) << 24);
-                lo[e] = uint32_t(v);
-            }
-            planes[w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0040), __byte_perm(lo[2], lo[3], 0x0040), 0x5410);
-            planes[Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0051), __byte_perm(lo[2], lo[3], 0x0051), 0x5410);
-            planes[2 * Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0062), __byte_perm(lo[2], lo[3], 0x0062), 0x5410);
+            for (int e = 0; e < 4; ++e) lo[e] = norm_lo32(4 * w + e < K ? xs[e] : 0, int32_t(r_inv), fits);
+            put_planes3(planes, Kw, w, lo);
         }
         fits = __syncthreads_and(fits);
         if (tr) tr[7] = clock64();
@@ -820,22 +833,32 @@ __device__ __noinline__ int prologue_norm_words(uint32_t K, uint32_t Kp, bool ga
     const int64_t r_inv = s_r2;  // <= 2^24: 32 x 32-bit products
     int fits = 1;
     const int64_t* gk = gamma_unit ? nullptr : gamma;  // mul16(v, ONE) == v: unit gains skipped
+    if (!gk) {  // unit gains: 32-bit limbs straight from the product (block-uniform branch)
 #pragma unroll 1
-    for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
-        const int4 e4 = *reinterpret_cast<const int4*>(xs32 + 4 * w);
-        const int32_t xs[4] = {e4.x, e4.y, e4.z, e4.w};  // padding slots hold 0
-        uint32_t lo[4];
+        for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
+            const int4 e4 = *reinterpret_cast<const int4*>(xs32 + 4 * w);
+            const int32_t xs[4] = {e4.x, e4.y, e4.z, e4.w};  // padding slots hold 0
+            uint32_t lo[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const uint32_t j = 4 * w + e;
-            int64_t v = (int64_t(xs[e]) * int32_t(r_inv)) >> 16;
-            if (gk && j < K) v = mul16(v, ld_cg64(gk + j));
-            fits &= uint64_t(v + (int64_t(1) << 23)) < (uint64_t(1) << 24);
-            lo[e] = uint32_t(v);
+            for (int e = 0; e < 4; ++e) lo[e] = norm_lo32(xs[e], int32_t(r_inv), fits);
+            put_planes3(planes, Kw, w, lo);
         }
-        planes[w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0040), __byte_perm(lo[2], lo[3], 0x0040), 0x5410);
-        planes[Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0051), __byte_perm(lo[2], lo[3], 0x0051), 0x5410);
-        planes[2 * Kw + w] = __byte_perm(__byte_perm(lo[0], lo[1], 0x0062), __byte_perm(lo[2], lo[3], 0x0062), 0x5410);
+    } else {
+#pragma unroll 1
+        for (uint32_t w = threadIdx.x; w < Kw; w += blockDim.x) {
+            const int4 e4 = *reinterpret_cast<const int4*>(xs32 + 4 * w);
+            const int32_t xs[4] = {e4.x, e4.y, e4.z, e4.w};  // padding slots hold 0
+            uint32_t lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t j = 4 * w + e;
+                int64_t v = (int64_t(xs[e]) * int32_t(r_inv)) >> 16;
+                if (j < K) v = mul16(v, ld_cg64(gk + j));
+                fits &= uint64_t(v + (int64_t(1) << 23)) < (uint64_t(1) << 24);
+                lo[e] = uint32_t(v);
+            }
+            put_planes3(planes, Kw, w, lo);
+        }
     }
     fits = __syncthreads_and(fits);
     if (tr) tr[7] = clock64();
