@@ -915,7 +915,7 @@ __device__ __forceinline__ void group_dot(const Sched& sc, Pipe& p, uint32_t Kp,
         const uint8_t* slot = pipe_wait(p);
         const uint32_t w = s + 1 < n_segs ? PK_SEG : Kp - (n_segs - 1) * PK_SEG;
         const uint32_t k0 = s * PK_SEG;
-        for (uint32_t c = lane * 16; c < w; c += 512) {
+        auto pass = [&](uint32_t c) {
             uint4 xl[L];
 #pragma unroll
             for (int k = 0; k < L; ++k) {
@@ -937,6 +937,12 @@ __device__ __forceinline__ void group_dot(const Sched& sc, Pipe& p, uint32_t Kp,
                 acc[r][L - 1] = dp4a_ss(wv.z, xl[L - 1].z, acc[r][L - 1]);
                 acc[r][L - 1] = dp4a_ss(wv.w, xl[L - 1].w, acc[r][L - 1]);
             }
+        };
+        if (L == 3 && w == PK_SEG) {  // full segment: a fixed trip count, no loop branches
+#pragma unroll
+            for (int i = 0; i < PK_SEG / 512; ++i) pass(lane * 16 + 512 * i);
+        } else {
+            for (uint32_t c = lane * 16; c < w; c += 512) pass(c);
         }
         if (s + 1 == n_segs)  // lane r < 4 takes row r's scale from the chunk tail
             scale = lane < PK_ROWS ? *reinterpret_cast<const int64_t*>(slot + PK_ROWS * w + 8 * lane) : 0;
