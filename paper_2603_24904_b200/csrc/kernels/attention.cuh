@@ -104,13 +104,31 @@ __device__ __forceinline__ void softmax_strip_fast(int64_t* S, uint32_t n, const
     uint64_t total = 0;
 #pragma unroll
     for (int w = 0; w < ATTN_THREADS / 32; ++w) total += ssum[w];
-    const uint64_t inv = ~0ull / total;
+    if (total < (uint64_t(1) << 30)) {
+        // floor(w 2^16 / total), w <= 2^16: a float estimate within one of the
+        // quotient (three roundings of 2^-24 on a quotient <= 2^16), fixed by
+        // the exact remainder, which lies in (-total, 2 total) and so is an
+        // exact int32 although w 2^16 and q total wrap (no 64-bit division)
+        const uint32_t tot32 = uint32_t(total);
+        const float scale = 65536.0f / float(tot32);
 #pragma unroll 1
-    for (uint32_t t = threadIdx.x; t < n; t += ATTN_THREADS) {
-        const uint64_t a = uint64_t(S[t]) << 16;
-        uint64_t q = __umul64hi(a, inv);  // floor(a / total) or one less
-        q += (a - q * total) >= total;
-        S[t] = int64_t(q);
+        for (uint32_t t = threadIdx.x; t < n; t += ATTN_THREADS) {
+            const uint32_t w = uint32_t(S[t]);
+            uint32_t q = uint32_t(float(w) * scale);
+            const int32_t r = int32_t((w << 16) - q * tot32);
+            q -= r < 0;
+            q += r >= int32_t(tot32);
+            S[t] = int64_t(q);
+        }
+    } else {
+        const uint64_t inv = ~0ull / total;
+#pragma unroll 1
+        for (uint32_t t = threadIdx.x; t < n; t += ATTN_THREADS) {
+            const uint64_t a = uint64_t(S[t]) << 16;
+            uint64_t q = __umul64hi(a, inv);  // floor(a / total) or one less
+            q += (a - q * total) >= total;
+            S[t] = int64_t(q);
+        }
     }
     __syncthreads();
 }

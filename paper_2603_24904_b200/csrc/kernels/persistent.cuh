@@ -1485,7 +1485,22 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
     ASTAMP(19);
     __syncthreads();
     ASTAMP(20);
-    if (threadIdx.x < nd) {
+    if (!wide && pv_shape && nd * 8 == ATTN_THREADS && (slices & 7) == 0) {
+        // eight lanes per output dim, each summing every eighth slice, then a
+        // 3-step shuffle tree (instead of one lane walking all the slices)
+        const uint32_t j = threadIdx.x >> 3, g = threadIdx.x & 7, qd = j >> 2, z = j & 3;
+        uint64_t sum = 0;
+#pragma unroll 4
+        for (uint32_t s2 = g; s2 < slices; s2 += 8) sum += part[4 * (s2 * nquads + qd) + z];
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+        if (g == 0) {
+            const uint32_t o = h * dh + d0 + j;
+            A.attn.out[o] = int64_t(sum);
+            st_word(out_words + o, limb_word(int64_t(sum), tag7_of(A.tag_base + epoch)));
+        }
+    } else if (threadIdx.x < nd) {
         uint64_t sum = 0;
         if (!wide && pv_shape) {
             const uint32_t qd = threadIdx.x >> 2, z = threadIdx.x & 3;
