@@ -242,10 +242,10 @@ __global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __re
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t j = c0 + 4 * e + 32 * u;
                     const int4 qq = j < dh ? *reinterpret_cast<const int4*>(q + j) : make_int4(0, 0, 0, 0);
-                    da += int64_t(qq.x) * ka[u].x + int64_t(qq.y) * ka[u].y + int64_t(qq.z) * ka[u].z +
-                          int64_t(qq.w) * ka[u].w;
-                    db += int64_t(qq.x) * kb[u].x + int64_t(qq.y) * kb[u].y + int64_t(qq.z) * kb[u].z +
-                          int64_t(qq.w) * kb[u].w;
+                    da += mulw(qq.x, ka[u].x) + mulw(qq.y, ka[u].y) + mulw(qq.z, ka[u].z) +
+                          mulw(qq.w, ka[u].w);
+                    db += mulw(qq.x, kb[u].x) + mulw(qq.y, kb[u].y) + mulw(qq.z, kb[u].z) +
+                          mulw(qq.w, kb[u].w);
                 }
             }
 #pragma unroll
@@ -279,10 +279,10 @@ __global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __re
                 for (int u = 0; u < U; ++u) {
                     const uint32_t tt = p + u * slices;
                     const int64_t pr = tt < T ? S[tt] : 0;
-                    a0 += (pr * vv[u].x) >> 16;
-                    a1 += (pr * vv[u].y) >> 16;
-                    a2 += (pr * vv[u].z) >> 16;
-                    a3 += (pr * vv[u].w) >> 16;
+                    a0 += mulw(int32_t(pr), vv[u].x) >> 16;  // pr <= 2^16
+                    a1 += mulw(int32_t(pr), vv[u].y) >> 16;
+                    a2 += mulw(int32_t(pr), vv[u].z) >> 16;
+                    a3 += mulw(int32_t(pr), vv[u].w) >> 16;
                 }
             }
         }

@@ -56,6 +56,14 @@ __device__ __forceinline__ int64_t mul_shr(int64_t a, int64_t b) {
     return int64_t((lo >> k) | (hi << (64 - k)));
 }
 
+// int64(a) * b for int32 operands as one IMAD.WIDE (in some contexts the
+// compiler emits a 64 x 64-bit multiply for the C++ expression).
+__device__ __forceinline__ int64_t mulw(int32_t a, int32_t b) {
+    int64_t p;
+    asm("mul.wide.s32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+    return p;
+}
+
 // Full signed 64x64 -> 128-bit product.
 __device__ __forceinline__ u128 mul_full(int64_t a, int64_t b) {
     return (u128(uint64_t(__mul64hi(a, b))) << 64) | uint64_t(a * b);
