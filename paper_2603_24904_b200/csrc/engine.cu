@@ -122,7 +122,8 @@ DevCtx& dev_ctx(int device) {
         set(pf_attn_kernel<4, true>);
         CK(cudaFuncSetAttribute(pf_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pf_scores_smem())));
         CK(cudaFuncSetAttribute(pf_pv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pf_pv_smem())));
-        set(bd_attn_kernel);
+        set(bd_attn_kernel<false>);
+        set(bd_attn_kernel<true>);
     }
     set_gemv_attrs<EPI_STORE, MODE_EMBED>();
     set_gemv_attrs<EPI_RESID, MODE_PLAIN>();
@@ -1133,7 +1134,7 @@ void batch_step(BatchRun& r, uint32_t n, bool logits) {
                  (const int64_t*)m.rope_sin, r.K32 + l * r.layer_stride, r.V32 + l * r.layer_stride, r.seq_stride,
                  r.ctx, r.wide);
         if (l + 1 == m.L && !logits) break;  // prompt positions only feed the KV caches
-        if (!(skip & 4)) launch_k(true, bd_attn_kernel, dim3(H, n), BD_THREADS, asmem, st, (const int64_t*)r.qkv, bt, D, dh,
+        if (!(skip & 4)) launch_k(true, small ? bd_attn_kernel<true> : bd_attn_kernel<false>, dim3(H, n), BD_THREADS, asmem, st, (const int64_t*)r.qkv, bt, D, dh,
                  r.K32 + l * r.layer_stride, r.V32 + l * r.layer_stride, r.seq_stride, r.ctx, m.inv_scale,
                  (const int64_t*)m.ctx->exp_lut, r.pa, r.nmax_pad, m.Kd, r.wide,
                  logits ? (const int64_t*)m.rope_cos : nullptr, logits ? (const int64_t*)m.rope_sin : nullptr);

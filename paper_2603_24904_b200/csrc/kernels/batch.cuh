@@ -164,6 +164,10 @@ __host__ __device__ constexpr size_t bd_attn_smem(uint32_t dh, uint32_t ctx) {
 // reads this (sequence, head) row): the CTA also does bd_rope_kv_kernel's
 // work for its head first -- RoPE of q and k, the K/V append -- one launch
 // per layer fewer.
+// KDB (decode steps of <= 16 sequences): the next pass's K rows load while
+// this pass's products run (+1% at 8 sequences; its registers cost the
+// 64-sequence steps occupancy, so those use the plain loop).
+template <bool KDB>
 __global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __restrict__ qkv, BatchTok bt,
                                                              uint32_t D, uint32_t dh, int32_t* K32, int32_t* V32,
                                                              size_t seq_stride, uint32_t ctx, int64_t inv_scale,
@@ -227,6 +231,46 @@ __global__ void __launch_bounds__(BD_THREADS) bd_attn_kernel(const int64_t* __re
         // exact (|q| < 2^23, |k| < 2^31, dh <= 512).
         const uint32_t oc = threadIdx.x >> 3, e = threadIdx.x & 7;
         constexpr uint32_t NOCT = BD_THREADS / 8;
+        if (KDB && dh <= 128) {
+            // one 128-dim pass per position: the next pass's K rows are loaded
+            // while this pass's products run
+            int4 ka[4], kb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t j = 4 * e + 32 * u;
+                ka[u] = (j < dh && oc < T) ? *reinterpret_cast<const int4*>(Kh + size_t(oc) * dh + j) : make_int4(0, 0, 0, 0);
+                kb[u] = (j < dh && oc + NOCT < T) ? *reinterpret_cast<const int4*>(Kh + size_t(oc + NOCT) * dh + j) : make_int4(0, 0, 0, 0);
+            }
+            for (uint32_t b0 = 0; b0 < T; b0 += 2 * NOCT) {
+                const uint32_t ta = b0 + oc, tb = ta + NOCT, na = ta + 2 * NOCT, nb = tb + 2 * NOCT;
+                int4 ka2[4], kb2[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t j = 4 * e + 32 * u;
+                    ka2[u] = (j < dh && na < T) ? *reinterpret_cast<const int4*>(Kh + size_t(na) * dh + j) : make_int4(0, 0, 0, 0);
+                    kb2[u] = (j < dh && nb < T) ? *reinterpret_cast<const int4*>(Kh + size_t(nb) * dh + j) : make_int4(0, 0, 0, 0);
+                }
+                int64_t da = 0, db = 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t j = 4 * e + 32 * u;
+                    const int4 qq = j < dh ? *reinterpret_cast<const int4*>(q + j) : make_int4(0, 0, 0, 0);
+                    da += mulw(qq.x, ka[u].x) + mulw(qq.y, ka[u].y) + mulw(qq.z, ka[u].z) + mulw(qq.w, ka[u].w);
+                    db += mulw(qq.x, kb[u].x) + mulw(qq.y, kb[u].y) + mulw(qq.z, kb[u].z) + mulw(qq.w, kb[u].w);
+                }
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) {
+                    da += __shfl_xor_sync(0xffffffffu, da, o);
+                    db += __shfl_xor_sync(0xffffffffu, db, o);
+                }
+                if (e == 0) {
+                    if (ta < T) S[ta] = mul16(da >> 16, inv_scale);
+                    if (tb < T) S[tb] = mul16(db >> 16, inv_scale);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) ka[u] = ka2[u], kb[u] = kb2[u];
+            }
+        } else
         for (uint32_t b0 = 0; b0 < T; b0 += 2 * NOCT) {
             const uint32_t ta = b0 + oc, tb = ta + NOCT;
             int64_t da = 0, db = 0;
