@@ -976,6 +976,7 @@ struct GemvRT {
     unsigned long long* ytag; // EPI_STORE: tagged word pairs of y
     uint64_t tg;              // their tag << 32
     uint32_t vb, vg;          // this CTA of the rank's vg
+    uint32_t g_lo, g_hi;      // its row groups (cta_range, precomputed per stage at launch)
     uint32_t row_off;         // EPI_ARGMAX: vocab index of row 0 (tensor parallel: the rank's slice)
     uint32_t tp_buf, tp_tag;  // EPI_RESID, tensor parallel: 1 + inbox buffer (0: single GPU), exchange tag
 };
@@ -1025,8 +1026,7 @@ __device__ __forceinline__ void run_gemv(const PkArgs& a, const Sched& sc, Pipe&
                                          const uint32_t* planes, uint32_t tag, int64_t& best_v,
                                          uint32_t& best_i) {
     const int lane = threadIdx.x & 31;
-    uint32_t g_lo, g_hi;
-    cta_range(g_.n_groups, g_lo, g_hi, g_.vb, g_.vg);
+    const uint32_t g_lo = g_.g_lo, g_hi = g_.g_hi;
     for (uint32_t g = g_lo + (threadIdx.x >> 5); g < g_hi; g += PK_WARPS) {
         const uint32_t r0 = g * PK_ROWS;
         int64_t resid = 0, scale = 0;  // residual issued now, consumed after the dot product
@@ -1641,8 +1641,7 @@ __device__ __forceinline__ void pk_run(const PkArgs& a, const uint32_t vb, const
                     // without rows here must not read x / the sums at all (it
                     // could lag behind their next writers). The embedding is
                     // written by the CTA holding group 0.
-                    uint32_t glo, ghi;
-                    cta_range(st.n_groups, glo, ghi, vb, vg);
+                    const uint32_t glo = s_fi[si].g_lo, ghi = s_fi[si].g_hi;  // cta_range at launch
                     int64_t* xb = reinterpret_cast<int64_t*>(stage_mem);
                     planes = reinterpret_cast<uint32_t*>(xb + st.Kp);
                     L = 3;
@@ -1692,6 +1691,8 @@ __device__ __forceinline__ void pk_run(const PkArgs& a, const uint32_t vb, const
                 g_.ytag = st.ytag;
                 g_.vb = vb;
                 g_.vg = vg;
+                g_.g_lo = s_fi[si].g_lo;
+                g_.g_hi = s_fi[si].g_hi;
                 g_.row_off = a.vocab_off;
                 g_.tp_buf = a.tp_g > 1 ? st.tp_sum : 0u;
                 g_.tp_tag = a.tag_base + attn_epoch;
