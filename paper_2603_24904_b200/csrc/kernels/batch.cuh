@@ -115,19 +115,24 @@ __global__ void __launch_bounds__(1024) bd_norm1k_kernel(const int32_t* __restri
         s_c[threadIdx.x >> 5][2] = c2;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t t0 = 0, t1 = 0, t2 = 0;
-        for (int w = 0; w < 32; ++w) {
-            t0 += s_c[w][0];
-            t1 += s_c[w][1];
-            t2 += s_c[w][2];
-        }
+    if (threadIdx.x < 32) {
+        // warp 0 adds the 32 warp totals (< 2^29 each) as 16-bit halves, so
+        // every 32-bit REDUX sum stays exact
+        const auto add32 = [](uint32_t v) {
+            return uint64_t(__reduce_add_sync(0xffffffffu, v & 0xFFFFu)) +
+                   (uint64_t(__reduce_add_sync(0xffffffffu, v >> 16)) << 16);
+        };
+        const uint64_t t0 = add32(s_c[threadIdx.x][0]);
+        const uint64_t t1 = add32(s_c[threadIdx.x][1]);
+        const uint64_t t2 = add32(s_c[threadIdx.x][2]);
         const u128 tot = u128(t0) + (u128(t1) << 21) + (u128(t2) << 42);
         const int64_t ms = (tot >> 63) != 0          ? int64_t((i128(tot) / i128(K)) >> 16)
                            : (K & (K - 1)) == 0       ? int64_t((uint64_t(tot) >> (__ffs(K) - 1)) >> 16)
                                                       : int64_t((uint64_t(tot) / K) >> 16);
-        s_r = ms + 1 > 0 ? inv_sqrt_q16(ms + 1, seeds) : 0;
-        if (ms + 1 <= 0) *wide = 1;
+        if (threadIdx.x == 0) {
+            s_r = ms + 1 > 0 ? inv_sqrt_q16(ms + 1, seeds) : 0;
+            if (ms + 1 <= 0) *wide = 1;
+        }
     }
     __syncthreads();
     const int64_t r = s_r;
