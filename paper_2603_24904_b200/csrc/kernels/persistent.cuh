@@ -581,8 +581,9 @@ __device__ __noinline__ int prologue_plain(uint32_t K, uint32_t Kp, const int64_
             planes[2 * Kw + w] = __byte_perm(__byte_perm(v.x, v.y, 0x0062), __byte_perm(v.z, v.w, 0x0062), 0x5410);
         }
     }
-    if (!__syncthreads_and(ok)) return -1;
-    return __syncthreads_or(wide) ? PLAIN_WIDE : 3;
+    const int f = __syncthreads_or((ok ? 0 : 2) | (wide ? 1 : 0));  // one barrier for both decisions
+    if (f & 2) return -1;
+    return (f & 1) ? PLAIN_WIDE : 3;
 }
 
 // rmsnorm input: the residual stream (or the embedded token on layer 0)
@@ -817,11 +818,10 @@ __device__ __noinline__ int prologue_norm_words(uint32_t K, uint32_t Kp, bool ga
         }
     }
     if (*((volatile uint32_t*)&ctl->err) & 4u) ok = 0;
-    if (!__syncthreads_and(ok)) return -1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     if ((threadIdx.x & 31) == 0) s_ss[threadIdx.x >> 5] = ss;
-    __syncthreads();
+    if (!__syncthreads_and(ok)) return -1;  // also publishes the warp sums
     if (threadIdx.x == 0) {
         uint64_t t = 0;
         for (int w = 0; w < PK_WARPS; ++w) t += s_ss[w];
