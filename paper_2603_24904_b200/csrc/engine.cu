@@ -272,7 +272,7 @@ void launch_limb_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const TgArgs
 // ---------------------------------------------------------------------------
 // Every dense matrix is stored "row-group blocked" for the persistent
 // kernel: rows padded to a multiple of 4, K padded to 16, then chunk
-// (group g, K-segment s) = rows 4g..4g+3 x columns [2048 s, 2048 s + w) laid
+// (group g, K-segment s) = rows 4g..4g+3 x columns [PK_SEG s, PK_SEG s + w) laid
 // out contiguously, so one cp.async.bulk moves one chunk. q/k/v are one
 // matrix (3D rows); gate/up are interleaved (gate_i row 2i, up_i row 2i+1) so
 // a row group holds whole (gate, up) pairs for the silu*up epilogue.

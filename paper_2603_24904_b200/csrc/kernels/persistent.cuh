@@ -10,11 +10,12 @@
 // private shared-memory ring with cp.async.bulk (TMA bulk copies, mbarrier
 // completion) while it waits at a barrier or builds the next input vector.
 // The weight stream runs continuously across stage, layer and token
-// boundaries. (tools/microbench.cu: this ring shape -- 8 KB chunks, 2 deep,
-// 8 warps, 128 KB/SM -- streams 7.3 TB/s on a B200 with the DP4A work on.)
+// boundaries. (tools/microbench.cu: rings of 4-8 KB chunks, 8 warps,
+// 128-192 KB/SM stream ~7 TB/s on a B200 with the DP4A work on; in the
+// kernel 4 KB chunks, as many per warp as shared memory leaves, measured best.)
 //
 // Weight layout in HBM ("row-group blocked", built at upload): each matrix is
-// cut into groups of 4 rows and K-segments of <= 2048 bytes; chunk (group,
+// cut into groups of 4 rows and K-segments of <= PK_SEG bytes; chunk (group,
 // segment) is one contiguous 4 x seg block = one bulk copy. CTAs own
 // contiguous balanced group ranges; warp w of a CTA owns groups w, w+8, ...
 // and walks all K-segments of a group, so its per-limb int32 partial sums stay
@@ -38,8 +39,14 @@ namespace dimg::dev {
 
 constexpr int PK_THREADS = 256;
 constexpr int PK_WARPS = PK_THREADS / 32;
-constexpr int PK_MAX_DEPTH = 6;         // chunks in flight per warp (runtime depth <= this)
-constexpr int PK_SEG = 1536;            // K-segment width (bytes)
+#ifndef DIMG_PK_MAX_DEPTH
+#define DIMG_PK_MAX_DEPTH 6
+#endif
+constexpr int PK_MAX_DEPTH = DIMG_PK_MAX_DEPTH;  // chunks in flight per warp (runtime depth <= this)
+#ifndef DIMG_PK_SEG
+#define DIMG_PK_SEG 1024
+#endif
+constexpr int PK_SEG = DIMG_PK_SEG;     // K-segment width (bytes; a multiple of 512)
 constexpr int PK_ROWS = 4;              // rows per group
 constexpr int PK_SCALES = PK_ROWS * 8;             // the group's 4 int64 row scales
 constexpr int PK_SLOT = PK_ROWS * PK_SEG + PK_SCALES;  // chunk bytes incl. trailing scales

@@ -27,16 +27,17 @@ for _ in range(5):
 print(json.dumps(out))
 '''
 
-libs = sys.argv[1:3]
-rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-res = {lib: [] for lib in libs}
-for r in range(rounds):
-    for lib in libs:
-        env = dict(os.environ, DIMG_LIB=os.path.abspath(lib))
-        o = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
-        if o.returncode:
-            print(lib, o.stderr[-2000:])
-            sys.exit(1)
-        res[lib] += json.loads(o.stdout.strip().splitlines()[-1])
-for lib, v in res.items():
-    print(f"{lib}: median {statistics.median(v):.1f} us/token  min {min(v):.1f}  max {max(v):.1f}  (n={len(v)})")
+if __name__ == "__main__":
+    libs = sys.argv[1:3]
+    rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    res = {lib: [] for lib in libs}
+    for r in range(rounds):
+        for lib in libs:
+            env = dict(os.environ, DIMG_LIB=os.path.abspath(lib))
+            o = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
+            if o.returncode:
+                print(lib, o.stderr[-2000:])
+                sys.exit(1)
+            res[lib] += json.loads(o.stdout.strip().splitlines()[-1])
+    for lib, v in res.items():
+        print(f"{lib}: median {statistics.median(v):.1f} us/token  min {min(v):.1f}  max {max(v):.1f}  (n={len(v)})")
