@@ -955,6 +955,18 @@ __device__ __forceinline__ void group_dot(const Sched& sc, Pipe& p, uint32_t Kp,
             scale = lane < PK_ROWS ? *reinterpret_cast<const int64_t*>(slot + PK_ROWS * w + 8 * lane) : 0;
         pipe_release(sc, p);
     }
+#ifndef DIMG_EXP_SHFL_REDUCE
+    // per-limb warp totals with REDUX: exact in int32 (|sum| <= K * 128 * 255
+    // < 2^31 for K <= 65536, the same bound the per-limb accumulation has),
+    // then every lane recombines the limbs (wrapping, as the reference's int64)
+#pragma unroll
+    for (int r = 0; r < PK_ROWS; ++r) {
+        uint64_t v = 0;
+#pragma unroll
+        for (int k = 0; k < L; ++k) v += uint64_t(int64_t(__reduce_add_sync(0xffffffffu, acc[r][k]))) << (8 * k);
+        out[r] = v;
+    }
+#else
 #pragma unroll
     for (int r = 0; r < PK_ROWS; ++r) {
         uint64_t v = 0;
@@ -963,6 +975,7 @@ __device__ __forceinline__ void group_dot(const Sched& sc, Pipe& p, uint32_t Kp,
         out[r] = v;
     }
     reduce4(out);
+#endif
 }
 
 // Everything the GEMV loop needs, by value (registers).
