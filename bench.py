@@ -570,7 +570,7 @@ def run_ours(args, rank, world, local):
                     dist.broadcast_object_list(obj, src=0)
                 tpn = P.TensorParallel(mf, world, backend="nccl", rank=rank, nccl_id=obj[0], device=dev)
                 ms, clk, toks, info, res, e2e_s = tp_headline(tpn, "nccl")
-                gpu_launches = 2 * info["launches_per_step"] * args.steps
+                gpu_launches = info["launches_per_step"] * (2 * args.warmup + args.steps)  # the two timed calls
                 kernel = "per-stage GEMV kernels on the rank's shard + ncclAllReduce (fused-ipc fallback)"
                 e2e_call = "dimg_tp_generate_greedy(prompt 16 -> 128 tokens, BLAKE3 on host), nccl tp"
                 extra = {"tp_group": {"backend": "nccl", "ranks": world, "fused_ipc_error": fused_err,
