@@ -64,14 +64,51 @@ __global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int32_t* __res
         const uint32_t j = threadIdx.x + u * 256;
         v[u] = j < K ? xr[j] : 0;
     }
-    u128 ss = 0;
+    // |x| <= 2^24 (every row after a residual clamp): x^2 < 2^48 summed in
+    // 21-bit chunks with REDUX, as bd_norm1k_kernel; otherwise (an embedding
+    // row beyond 2^24) the 128-bit sums
+    int small = 1;
 #pragma unroll
-    for (int u = 0; u < PN_PER; ++u) ss += mul_full(v[u], v[u]);
-    for (uint32_t j = threadIdx.x + PN_PER * 256; j < K; j += 256) ss += mul_full(int64_t(xr[j]), int64_t(xr[j]));
-    ss = block_sum_u128(ss, red);
+    for (int u = 0; u < PN_PER; ++u) small &= v[u] >= -(int64_t(1) << 24) && v[u] <= (int64_t(1) << 24);
+    small = __syncthreads_and(small && K <= PN_PER * 256);
+    u128 ss = 0;
+    if (small) {
+        uint32_t c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+        for (int u = 0; u < PN_PER; ++u) {
+            const uint64_t q2 = uint64_t(mulw(int32_t(v[u]), int32_t(v[u])));
+            c0 += uint32_t(q2) & 0x1FFFFFu;
+            c1 += uint32_t(q2 >> 21) & 0x1FFFFFu;
+            c2 += uint32_t(q2 >> 42);
+        }
+        // per-warp sums < 32 * 16 * 2^21 = 2^30: exact 32-bit REDUX
+        c0 = __reduce_add_sync(0xffffffffu, c0);
+        c1 = __reduce_add_sync(0xffffffffu, c1);
+        c2 = __reduce_add_sync(0xffffffffu, c2);
+        uint64_t* sw = reinterpret_cast<uint64_t*>(red);  // [8 warps][3]
+        if ((threadIdx.x & 31) == 0) {
+            sw[3 * (threadIdx.x >> 5)] = c0;
+            sw[3 * (threadIdx.x >> 5) + 1] = c1;
+            sw[3 * (threadIdx.x >> 5) + 2] = c2;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t t0 = 0, t1 = 0, t2 = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) t0 += sw[3 * w], t1 += sw[3 * w + 1], t2 += sw[3 * w + 2];
+            ss = u128(t0) + (u128(t1) << 21) + (u128(t2) << 42);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < PN_PER; ++u) ss += mul_full(v[u], v[u]);
+        for (uint32_t j = threadIdx.x + PN_PER * 256; j < K; j += 256) ss += mul_full(int64_t(xr[j]), int64_t(xr[j]));
+        ss = block_sum_u128(ss, red);
+    }
     if (threadIdx.x == 0) {
         // usual case: the sum fits 63 bits and one u64 division is exact
-        const int64_t ms = (ss >> 63) == 0 ? int64_t((uint64_t(ss) / K) >> 16) : int64_t((i128(ss) / i128(K)) >> 16);
+        const int64_t ms = (ss >> 63) != 0       ? int64_t((i128(ss) / i128(K)) >> 16)
+                           : (K & (K - 1)) == 0 ? int64_t((uint64_t(ss) >> (__ffs(K) - 1)) >> 16)
+                                                : int64_t((uint64_t(ss) / K) >> 16);
         s_r = ms + 1 > 0 ? inv_sqrt_q16(ms + 1, seeds) : 0;
         if (ms + 1 <= 0) *wide = 1;  // the reference throws (domain_error): the exact path reports it
     }
@@ -79,11 +116,12 @@ __global__ void __launch_bounds__(256) pf_norm_limbs_kernel(const int32_t* __res
     const int64_t r = s_r;
     const size_t plane = size_t(rows_pad) * ldp;
     uint8_t* pr = planes + size_t(t) * ldp;
+    const bool r32 = small && r >= 0 && r <= (int64_t(1) << 24);  // mul16(x, r) as one IMAD.WIDE
 #pragma unroll
     for (int u = 0; u < PN_PER; ++u) {
         const uint32_t j = threadIdx.x + u * 256;
         if (j < K) {
-            int64_t o = mul16(v[u], r);
+            int64_t o = r32 ? mulw(int32_t(v[u]), int32_t(r)) >> 16 : mul16(v[u], r);
             if (!gamma_unit) o = mul16(o, gamma[j]);
             pf_put_limbs(pr + j, plane, o, wide);
         }
