@@ -1286,6 +1286,32 @@ __device__ __forceinline__ bool attn_split(const PkArgs& A, uint32_t layer, uint
         const unsigned long long* W = A.qkv_x;
         const uint64_t tagq = uint32_t(A.tag_base + epoch);
         int ok = 1;
+        if (3 * dh <= 2 * ATTN_THREADS) {
+            // at most two words per thread: both loads in flight per retry
+            const uint32_t i0 = threadIdx.x, i1 = threadIdx.x + ATTN_THREADS;
+            const bool h0 = i0 < 3 * dh, h1 = i1 < 3 * dh;
+            const size_t r0 = size_t(i0 / dh) * D + size_t(h) * dh + (i0 % dh);
+            const size_t r1 = size_t(i1 / dh) * D + size_t(h) * dh + (i1 % dh);
+            uint64_t lo0 = tagq << 32, hi0 = tagq << 32, lo1 = tagq << 32, hi1 = tagq << 32;
+            uint32_t spins = 0;
+            uint64_t g0 = 0;
+            for (;;) {
+                if (h0) ld_tagged2(W + 2 * r0, lo0, hi0);
+                if (h1) ld_tagged2(W + 2 * r1, lo1, hi1);
+                if ((lo0 >> 32) == tagq && (hi0 >> 32) == tagq && (lo1 >> 32) == tagq && (hi1 >> 32) == tagq) break;
+                if ((++spins & 1023) == 0) {
+                    const uint64_t now = globaltimer();
+                    if (!g0) g0 = now;
+                    if ((*((volatile uint32_t*)&A.ctl->err) & 4u) || now - g0 > 4000000000ull) {
+                        atomicOr(&A.ctl->err, 4u);
+                        ok = 0;
+                        break;
+                    }
+                }
+            }
+            if (h0) qkv_s[i0] = int64_t((hi0 << 32) | (lo0 & 0xFFFFFFFFull));
+            if (h1) qkv_s[i1] = int64_t((hi1 << 32) | (lo1 & 0xFFFFFFFFull));
+        } else
 #pragma unroll 1
         for (uint32_t i = threadIdx.x; i < 3 * dh && ok; i += ATTN_THREADS) {
             const uint32_t which = i / dh, j = i - which * dh;
